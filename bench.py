@@ -1,0 +1,353 @@
+#!/usr/bin/env python
+"""Benchmark: iHDG element-DOF updates/s per sweep (BASELINE.json metric).
+
+Workload: BASELINE config 5 (2D convection-diffusion, 2048^2 quads, p=6,
+m=3 -> 616.6 M volume DOFs, kappa=1e-3 by default, backward Euler dt = h/p),
+the largest configuration and the one the metric's 1/2/4/8-GPU clause is
+quoted on.  One bench "step" = one iHDG-II sweep over every element
+(gather -> lifted local solve -> write -> stopping-norm partials), i.e. one
+launch of the fused sweep kernel.  The state (4.9 GB per buffer) is far
+larger than L2 (126 MB), so no explicit flush is needed.
+
+Multi-GPU (torchrun): weak scaling by default -- each rank owns a 2048 x 2048
+strip of a 2048 x (2048 N) mesh on [0,1] x [0,N], with a halo
+exchange of the boundary layers (NCCL send/recv) and an all-gather of the
+norm partials every sweep; ``--scaling strong`` splits the 2048^2 mesh.
+
+``--impl reference`` times the CPU oracle's C/OpenMP sweep (the reference's
+`_sweep_cy` role: LU solve per element, -O3 -fopenmp) on a bounded sample of
+the same workload, with all host threads.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+BYTES_PER_DOF = 24  # read u^k, read s, write u^{k+1} (fp64), SURVEY.md 8d
+
+
+def _peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return float(d.get("hbm_gbs", 6650.0)), "measured"
+    return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip()
+                if out:
+                    self.rows.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        if self._t:
+            self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if len(r) > 3 + i and r[3 + i] == "Active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def _dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def _workload(args, world):
+    from paper_1711_01175_b200.basis import build_operators
+    from paper_1711_01175_b200.mesh import build_mesh
+    from paper_1711_01175_b200.workloads import make_config
+
+    wl = make_config(5, seed=args.seed, kappa=args.kappa, cells=args.cells)
+    n = wl.mesh.cells[0]
+    if world > 1 and args.scaling == "weak":
+        mesh = build_mesh(2, [n, n * world], (np.zeros(2), np.array([1.0, float(world)])))
+        wl.mesh = mesh
+        wl.ops = build_operators(wl.ops.p, 2, mesh.h)
+    return wl
+
+
+def _cpu_sample(args, threads):
+    """Oracle C/OpenMP sweep on a strip of the config-5 mesh (same h, p, kappa)."""
+    from oracle.ihdg_oracle import OracleProblem, OracleSolver
+
+    n = args.cells or 2048
+    rows = args.cpu_rows
+    h = 1.0 / n
+    p = args.order
+    prob = OracleProblem("cd", 2, beta=np.array([1.0, 1.0]), kappa=args.kappa)
+    S = OracleSolver(prob, [n, rows], p, box=(np.zeros(2), np.array([1.0, rows * h])), dt=h / p)
+    rng = np.random.default_rng(args.seed)
+    u = rng.normal(size=(S.nel, S.nv))
+    rhs = S.rhs_static(u)
+    data = S.c_sweep_data()
+    out = np.empty_like(u)
+    S.c_sweep(data, u, rhs, out, threads)  # warm-up
+    times = []
+    for _ in range(args.cpu_reps):
+        t0 = time.perf_counter()
+        S.c_sweep(data, u, rhs, out, threads)
+        times.append(time.perf_counter() - t0)
+        u, out = out, u
+    best = min(times)
+    dofs = S.nel * S.nv
+    return dofs / best, f"{S.nel} elements ({n}x{rows} strip of config 5, p={p}, m=3), best of {len(times)} sweeps", best
+
+
+def run_reference(args):
+    rank, world, _ = _dist_env()
+    if rank != 0:
+        return
+    import os as _os
+
+    threads = len(_os.sched_getaffinity(0))
+    val, sample, _ = _cpu_sample(args, threads)
+    unit = "element-DOF updates/s"
+    line = {
+        "metric": "iHDG element-DOF updates/sec per sweep (config 5: 2D CD 2048^2 p=6)",
+        "value": val, "unit": unit, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": None, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic (seeded Fourier initial data)", "impl": "reference",
+        "config": {"workload": f"config5: 2D convection-diffusion 2048^2 quads p=6 kappa={args.kappa:g} "
+                               "BE dt=h/p; CPU sample", "parallelism": "openmp"},
+        "cpu_baseline": {"value": val, "unit": unit, "cores": threads, "kind": "port", "sample": sample},
+        "e2e": {"value": val, "unit": unit, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args):
+    import torch
+
+    rank, world, local = _dist_env()
+    torch.cuda.set_device(local)
+    group = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        group = dist.group.WORLD
+    from paper_1711_01175_b200 import _native as N
+    from paper_1711_01175_b200.partition import strip_range
+    from paper_1711_01175_b200.solver import DeviceSolver, DistributedSweeper
+
+    wl = _workload(args, world)
+    mesh = wl.mesh
+    nlay = mesh.cells[1]
+    layers = strip_range(nlay, rank, world)
+    t_setup = time.perf_counter()
+    sv = DeviceSolver(mesh, wl.problem, wl.ops, dt=wl.dt, layers=layers, max_iters=20000)
+    for name, fld in wl.initial.items():
+        sv.set_state_component(fld, sv.spec.labels.index(name))
+    sv.begin_step()
+    torch.cuda.synchronize()
+    setup_s = time.perf_counter() - t_setup
+    dofs_rank = sv.nloc * sv.nv
+    dofs_total = mesh.n_elements * sv.nv
+    dsw = DistributedSweeper(sv, rank, world, group) if world > 1 else None
+    # a large tolerance-free run: status stays RUNNING for K+W sweeps
+    sv.reset_state(tol=0.0, max_iters=args.steps + args.warmup + 10)
+    a = sv.sweep_args("volume", finalize=1 if world == 1 else 0)
+
+    def one():
+        if dsw is None:
+            sv.sweep_once(a=a)
+        else:
+            dsw.sweep(a)
+
+    for _ in range(args.warmup):
+        one()
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize()
+        e0.record(sv.stream)
+        for _ in range(args.steps):
+            one()
+        e1.record(sv.stream)
+        torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    if world > 1:
+        t = torch.tensor([ms], device=sv.device)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms = float(t.item())
+    ms_step = ms / args.steps
+    value = dofs_total * args.steps / (ms / 1e3)
+    # kernel-only time of the sweep launches (single rank: the step IS one launch)
+    sweep_ms = ms_step
+    if world > 1:
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+        acc = 0.0
+        for _ in range(min(args.steps, 5)):
+            sv.u[sv.cur]  # noqa
+            ev[0].record(sv.stream)
+            aa = sv.sweep_args("volume", finalize=0)
+            aa.u_old, aa.u_new = sv.u[sv.cur].data_ptr(), sv.u[1 - sv.cur].data_ptr()
+            N.check(sv.L.ihdg_sweep(__import__("ctypes").byref(aa), sv._sptr), "ihdg_sweep")
+            ev[1].record(sv.stream)
+            torch.cuda.synchronize()
+            acc += ev[0].elapsed_time(ev[1])
+            sv.cur = 1 - sv.cur
+        sweep_ms = acc / min(args.steps, 5)
+    peak, peak_kind = _peaks()
+    achieved = BYTES_PER_DOF * dofs_rank / (sweep_ms / 1e3) / 1e9
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tp):
+        try:
+            with open(tp) as f:
+                traffic = json.load(f).get("bytes_per_launch")
+        except Exception:
+            traffic = None
+    # ---- time to converge (one BE step per kappa in --ttc, from the same u^m) ----
+    ttc = {}
+    if args.ttc_steps > 0 and world == 1:
+        for kap in args.ttc_kappas:
+            from paper_1711_01175_b200.workloads import make_config
+
+            w2 = make_config(5, seed=args.seed, kappa=kap, cells=args.cells)
+            s2 = DeviceSolver(w2.mesh, w2.problem, w2.ops, dt=w2.dt, max_iters=20000) if kap != args.kappa else sv
+            s2.zero_state()
+            for name, fld in w2.initial.items():
+                s2.set_state_component(fld, s2.spec.labels.index(name))
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            iters = []
+            for _ in range(args.ttc_steps):
+                s2.begin_step()
+                r = s2.iterate(tol=1e-10, max_iters=20000, norm="volume", batch=32)
+                iters.append(r.iterations)
+                if r.status != "converged":
+                    break
+            torch.cuda.synchronize()
+            ttc[f"kappa={kap:g}"] = {"seconds": time.perf_counter() - t0, "steps": len(iters),
+                                     "sweeps_per_step": iters}
+            if s2 is not sv:
+                del s2
+                torch.cuda.empty_cache()
+    # ---- e2e: one BE step through the public API from pinned host buffers ----
+    e2e = None
+    if args.e2e and world == 1:
+        nloc, nv = sv.nloc, sv.nv
+        host_in = torch.empty((nloc, nv), dtype=torch.float64, pin_memory=True)
+        host_out = torch.empty((nloc, nv), dtype=torch.float64, pin_memory=True)
+        host_in.copy_(sv.interior())
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        sv.interior().copy_(host_in, non_blocking=True)
+        sv.begin_step()
+        r = sv.iterate(tol=1e-10, max_iters=20000, norm="volume", batch=32)
+        host_out.copy_(sv.interior(), non_blocking=True)
+        torch.cuda.synchronize()
+        dt_e2e = time.perf_counter() - t0
+        e2e = {"value": dofs_total * r.iterations / dt_e2e, "unit": "element-DOF updates/s",
+               "h2d_bytes_per_step": int(nloc * nv * 8), "d2h_bytes_per_step": int(nloc * nv * 8),
+               "sweeps": r.iterations, "seconds": dt_e2e,
+               "what": "one backward-Euler step via DeviceSolver (upload u^m, RHS, iterate to 1e-10, download)"}
+    cpu = None
+    if rank == 0 and world == 1 and args.cpu_baseline:
+        threads = len(os.sched_getaffinity(0))
+        v, sample, _ = _cpu_sample(args, threads)
+        cpu = {"value": v, "unit": "element-DOF updates/s", "cores": threads, "kind": "port", "sample": sample}
+    if rank == 0:
+        line = {
+            "metric": "iHDG element-DOF updates/sec per sweep (config 5: 2D CD 2048^2 p=6)",
+            "value": value, "unit": "element-DOF updates/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+            "scaling": "weak" if (world == 1 or args.scaling == "weak") else "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded Fourier initial data)",
+            "config": {"workload": f"config5: 2D convection-diffusion {mesh.cells[0]}x{mesh.cells[1]} quads "
+                                   f"p={wl.ops.p} m=3 kappa={args.kappa:g} BE dt=h/p; step = one sweep",
+                       "dofs": int(dofs_total), "elements": int(mesh.n_elements),
+                       "parallelism": f"strip{world}", "l2": "state 4.9 GB/GPU >> 126 MB L2 (no flush needed)"},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
+                         "bytes_per_dof": BYTES_PER_DOF, "kernel_ms": sweep_ms},
+            "clocks": clk.summary(),
+            "gpu_launches": args.steps * (1 if world == 1 else 2),
+            "setup_seconds": setup_s,
+            "time_to_converge": ttc or None,
+            "e2e": e2e,
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--kappa", type=float, default=1e-3)
+    ap.add_argument("--cells", type=int, default=None)
+    ap.add_argument("--order", type=int, default=6)
+    ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"])
+    ap.add_argument("--ttc-steps", type=int, default=5)
+    ap.add_argument("--ttc-kappas", type=float, nargs="*", default=[1e-3])
+    ap.add_argument("--no-e2e", dest="e2e", action="store_false")
+    ap.add_argument("--no-cpu", dest="cpu_baseline", action="store_false")
+    ap.add_argument("--cpu-rows", type=int, default=64)
+    ap.add_argument("--cpu-reps", type=int, default=3)
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "ours":
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

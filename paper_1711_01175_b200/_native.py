@@ -1,0 +1,145 @@
+"""ctypes binding of libihdg_cuda.so (include/ihdg.h).
+
+There is no CPU fallback: if the shared library is missing or cannot be
+loaded, every product entry point raises ``NativeUnavailable``.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+__all__ = ["NativeUnavailable", "lib", "Geom", "IterState", "AssemblyArgs", "ClassApplyArgs",
+           "FieldArgs", "QuadArgs", "SweepArgs", "FinalizeArgs", "TraceArgs", "check",
+           "LIB_PATH", "STATUS_NAMES"]
+
+LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libihdg_cuda.so")
+
+IHDG_OK = 0
+RUNNING, CONVERGED, DIVERGED, NAN, MAXITER = 0, 1, 2, 3, 4
+STATUS_NAMES = {RUNNING: "running", CONVERGED: "converged", DIVERGED: "diverged",
+                NAN: "diverged", MAXITER: "max-iter"}
+NORM_VOLUME, NORM_TRACE = 0, 1
+
+_p = C.c_void_p
+_i32 = C.c_int32
+_i64 = C.c_int64
+_f64 = C.c_double
+
+
+class NativeUnavailable(RuntimeError):
+    pass
+
+
+class Geom(C.Structure):
+    _fields_ = [("dim", _i32), ("order", _i32), ("ncomp", _i32), ("pad0", _i32),
+                ("cells", _i64 * 3), ("periodic", _i32 * 3), ("pad1", _i32),
+                ("layer_begin", _i64), ("layer_end", _i64)]
+
+
+class IterState(C.Structure):
+    _fields_ = [("status", _i32), ("iters", _i32), ("max_iters", _i32), ("ticket", C.c_uint32),
+                ("tol", _f64), ("first_norm", _f64), ("last_norm", _f64),
+                ("diverge_factor", _f64)]
+
+
+class AssemblyArgs(C.Structure):
+    _fields_ = [("dim", _i32), ("order", _i32), ("ncomp", _i32), ("n_class", _i32),
+                ("n_ops", _i32), ("n_terms", _i32), ("nr", _i32), ("pad0", _i32),
+                ("ops1d", _p), ("op_ncols", _p), ("terms", _p), ("coefs", _p),
+                ("A", _p), ("Ainv", _p), ("AinvT", _p), ("B", _p), ("R", _p),
+                ("LT", _p), ("PT", _p), ("min_pivot", _p)]
+
+
+class ClassApplyArgs(C.Structure):
+    _fields_ = [("g", Geom), ("opT", _p), ("class_of_mask", _p), ("inp", _p), ("out", _p),
+                ("in_stride", _i64), ("in_offset", _i32), ("ncols", _i32), ("in_ghost", _i32),
+                ("out_ghost", _i32), ("accumulate", _i32), ("pad0", _i32)]
+
+
+class FieldArgs(C.Structure):
+    _fields_ = [("g", Geom), ("lo", _f64 * 3), ("h", _f64 * 3), ("ref1d", _p), ("params", _p),
+                ("out", _p), ("out_stride", _i64), ("out_offset", _i32), ("out_ghost", _i32),
+                ("npts1d", _i32), ("kind", _i32), ("nmodes", _i32), ("pad0", _i32)]
+
+
+class QuadArgs(C.Structure):
+    _fields_ = [("g", Geom), ("Bq", _p), ("fq", _p), ("out", _p), ("out_stride", _i64),
+                ("out_offset", _i32), ("nq", _i32), ("jac", _f64)]
+
+
+class SweepArgs(C.Structure):
+    _fields_ = [("g", Geom), ("u_old", _p), ("u_new", _p), ("s", _p), ("LT", _p),
+                ("class_of_mask", _p), ("chol1d", _p), ("tile_partials", _p), ("state", _p),
+                ("norm_hist", _p), ("face_w", (_f64 * 4) * 6), ("comp_w", _f64 * 4),
+                ("out_w", (_f64 * 4) * 6), ("jac", _f64), ("jac_face", _f64 * 3),
+                ("coupled", _i32 * 6), ("out_face", _i32 * 6), ("norm_kind", _i32),
+                ("finalize", _i32), ("tile_offset", _i64)]
+
+
+class FinalizeArgs(C.Structure):
+    _fields_ = [("tile_partials", _p), ("n_tiles", _i64), ("state", _p), ("norm_hist", _p)]
+
+
+class TraceArgs(C.Structure):
+    _fields_ = [("g", Geom), ("u", _p), ("trace", _p), ("w_int_own", (_f64 * 4) * 3),
+                ("w_int_nbr", (_f64 * 4) * 3), ("w_lo", (_f64 * 4) * 3), ("w_hi", (_f64 * 4) * 3)]
+
+
+_STRUCTS = [Geom, IterState, AssemblyArgs, ClassApplyArgs, FieldArgs, QuadArgs, SweepArgs,
+            FinalizeArgs, TraceArgs]
+
+# exported symbol -> (restype, argtypes)
+SIGNATURES = {
+    "ihdg_abi_version": (_i32, []),
+    "ihdg_struct_size": (_i64, [_i32]),
+    "ihdg_last_error": (C.c_char_p, []),
+    "ihdg_supported": (_i32, [_i32, _i32, _i32]),
+    "ihdg_tile_elems": (_i32, [_i32, _i32, _i32]),
+    "ihdg_tile_count": (_i64, [C.POINTER(Geom)]),
+    "ihdg_assemble": (_i32, [C.POINTER(AssemblyArgs), _p]),
+    "ihdg_class_apply": (_i32, [C.POINTER(ClassApplyArgs), _p]),
+    "ihdg_eval_field": (_i32, [C.POINTER(FieldArgs), _p]),
+    "ihdg_quad_project": (_i32, [C.POINTER(QuadArgs), _p]),
+    "ihdg_sweep": (_i32, [C.POINTER(SweepArgs), _p]),
+    "ihdg_finalize": (_i32, [C.POINTER(FinalizeArgs), _p]),
+    "ihdg_extract_trace": (_i32, [C.POINTER(TraceArgs), _p]),
+    "ihdg_copy_state": (_i32, [C.POINTER(Geom), _p, _p, _p]),
+    "ihdg_iterate": (_i32, [C.POINTER(SweepArgs), _p, _p, _i32, _p, C.POINTER(IterState),
+                            C.POINTER(_i64)]),
+}
+
+_lib = None
+
+
+def lib():
+    """Load libihdg_cuda.so once; raise NativeUnavailable if it is missing."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise NativeUnavailable(
+            f"{LIB_PATH} is not built; run `python -c 'import __graft_entry__ as g; g.build()'` "
+            "(there is no CPU fallback for the iHDG sweep)")
+    try:
+        L = C.CDLL(LIB_PATH)
+    except OSError as exc:  # pragma: no cover - depends on the box
+        raise NativeUnavailable(f"cannot load {LIB_PATH}: {exc}") from exc
+    for name, (res, args) in SIGNATURES.items():
+        fn = getattr(L, name)
+        fn.restype = res
+        fn.argtypes = args
+    if L.ihdg_abi_version() != 1:
+        raise NativeUnavailable("libihdg_cuda.so ABI version mismatch")
+    for i, st in enumerate(_STRUCTS):
+        if L.ihdg_struct_size(i) != C.sizeof(st):
+            raise NativeUnavailable(f"ABI struct size mismatch for {st.__name__}: "
+                                    f"C {L.ihdg_struct_size(i)} vs ctypes {C.sizeof(st)}")
+    _lib = L
+    return L
+
+
+def check(rc: int, what: str) -> None:
+    if rc != IHDG_OK:
+        msg = lib().ihdg_last_error().decode(errors="replace")
+        raise RuntimeError(f"{what} failed ({rc}): {msg}")

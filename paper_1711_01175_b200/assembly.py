@@ -1,0 +1,421 @@
+"""Element-local iHDG-II operators as Kronecker term lists (host side of K1).
+
+On an affine axis-aligned element every bilinear form of the substituted
+iHDG-II local solvers is a sum of tensor products of 1D reference matrices:
+
+    mass       (phi_j, phi_i)_K            = J  * (M1 x M1 x M1)
+    Q_a[i, j]  (phi_j, d_a phi_i)_K        = Jf_a * (M1 .. S1^T(axis a) .. M1)
+    face mass  <phi_j, phi_i>_{face (a,s)} = Jf_a * (M1 .. E_s(axis a) .. M1)
+    coupling   <q_face, phi_i>_{face (a,s)}= Jf_a * (M1 .. e_s(axis a) .. M1)
+
+with J = prod h/2, Jf_a = J / (h_a/2), S1[i,j] = int l_i l_j', E_s the endpoint
+projector and e_s the endpoint column.  This module writes down, per PDE,
+which coefficient multiplies which tensor product (the physics); the device
+kernel K1 (``ihdg_assemble``) evaluates the entries, inverts A and forms
+L = A^-1 B, P = A^-1 R.
+
+Derivations (n = owner outward normal of face f = (a, s), sgn = +-1):
+
+transport
+    A = -sum_a beta_a Q_a + sum_{beta.n>0} (beta.n) Mf [+ (c + 1/dt) M]
+    B_f = |beta.n| Bf on inflow faces; neighbour scalar q = u^k_nbr.
+
+convection-diffusion, unknowns (sigma, u),
+    u_hat = (q_own + q_nbr)/alpha,  q_X = sigma_X.n_X + (alpha + beta.n_X)/2 u_X
+    alpha = sqrt((beta.n)^2 + 4), tau = (alpha - beta.n)/2, c+ = (alpha+beta.n)/2
+    interior face:  (s_a,s_a) += Mf/alpha        (s_a,u) += sgn c+/alpha Mf
+                    (u,s_a)  += sgn(1-tau/alpha) Mf
+                    (u,u)    += (beta.n + tau - tau c+/alpha) Mf
+                    B: s_a row -sgn/alpha Bf, u row tau/alpha Bf
+    Dirichlet face (u_hat = g_D = 0): (u,s_a) += sgn Mf, (u,u) += (beta.n+tau) Mf
+    neighbour scalar q = -sgn sigma_a,nbr + tau u_nbr.
+
+shallow water, unknowns (phi, u, v),
+    phi_hat = (q_own + q_nbr)/2, q_X = phi_X + sqrt(Phi) theta_X.n_X
+    interior face:  (phi,phi) += sqrt(Phi)/2 Mf   (phi,th_a) += Phi sgn/2 Mf
+                    (th_a,phi) += Phi sgn/2 Mf    (th_a,th_a) += Phi sqrt(Phi)/2 Mf
+                    B: phi row sqrt(Phi)/2 Bf, th_a row -Phi sgn/2 Bf
+    wall face (mirror state): phi_hat = phi + sqrt(Phi) theta.n
+                    (th_a,phi) += Phi sgn Mf      (th_a,th_a) += Phi sqrt(Phi) Mf
+    Coriolis f and friction gamma implicit.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from .basis import ElementOperators
+from .pde import ConvectionDiffusionProblem, ShallowWaterProblem, TransportProblem
+
+__all__ = ["OperatorSpec", "build_spec", "OPS"]
+
+# 1D operator table indices
+MASS, CONV, CONVT, E0, E1, C0, C1 = range(7)
+OPS = {"mass": MASS, "conv": CONV, "convT": CONVT, "E0": E0, "E1": E1, "c0": C0, "c1": C1}
+A_T, B_T, R_T = 0, 1, 2
+
+
+@dataclass
+class OperatorSpec:
+    """Everything the device needs to assemble and sweep one problem."""
+
+    dim: int
+    order: int
+    ncomp: int
+    labels: tuple
+    n_class: int
+    class_masks: list           # boundary mask of each class
+    class_of_mask: np.ndarray   # (64,) int32
+    ops1d: np.ndarray           # (7, N1, N1)
+    op_ncols: np.ndarray        # (7,) int32
+    terms: np.ndarray           # (nt, 8) int32
+    coefs: np.ndarray           # (nt,)
+    nr: int                     # R columns
+    time_comp0: int             # first component with a time derivative
+    n_time_comp: int
+    forcing_comp: int           # component row receiving (f, v)
+    face_w: np.ndarray          # (6, 4)
+    coupled: np.ndarray         # (6,) int32
+    out_face: np.ndarray        # (6,) int32 (trace norm faces)
+    out_w: np.ndarray           # (6, 4)
+    comp_w: np.ndarray          # (4,)
+    trace_w: dict               # int_own, int_nbr, lo, hi : (3, 4)
+    jac: float
+    jac_face: np.ndarray        # (3,)
+    periodic: tuple
+    boundary_rhs: list = field(default_factory=list)
+
+    @property
+    def n1(self):
+        return self.order + 1
+
+    @property
+    def n_nodes(self):
+        return self.n1 ** self.dim
+
+    @property
+    def nv(self):
+        return self.ncomp * self.n_nodes
+
+    @property
+    def kin(self):
+        return 2 * self.dim * self.n1 ** (self.dim - 1)
+
+
+class _Terms:
+    def __init__(self, dim):
+        self.dim = dim
+        self.rows = []
+        self.coefs = []
+
+    def add(self, cls, target, rc, cb, axis_ops, coef):
+        if coef == 0.0:
+            return
+        ops = list(axis_ops) + [MASS] * (3 - len(axis_ops))
+        self.rows.append([cls, target, rc, cb, ops[0], ops[1], ops[2], 0])
+        self.coefs.append(float(coef))
+
+    def vol(self, cls, target, rc, cb, coef, axis=None, op=None):
+        ops = [MASS] * self.dim
+        if axis is not None:
+            ops[axis] = op
+        self.add(cls, target, rc, cb, ops, coef)
+
+
+def _ops_table(ops: ElementOperators) -> tuple[np.ndarray, np.ndarray]:
+    n1 = ops.n1
+    T = np.zeros((7, n1, n1))
+    T[MASS] = ops.mass1d
+    T[CONV] = ops.conv1d
+    T[CONVT] = ops.conv1d.T
+    T[E0][0, 0] = 1.0
+    T[E1][n1 - 1, n1 - 1] = 1.0
+    T[C0][0, 0] = 1.0
+    T[C1][n1 - 1, 0] = 1.0
+    ncols = np.array([n1, n1, n1, n1, n1, 1, 1], dtype=np.int32)
+    return T, ncols
+
+
+def _class_masks(mesh) -> list[int]:
+    """Boundary masks (bit 2a+s = face (a,s) on the physical boundary) that occur."""
+    per_axis = []
+    for a in range(mesh.dim):
+        lo, hi = 1 << (2 * a), 1 << (2 * a + 1)
+        n = mesh.cells[a]
+        if mesh.periodic[a]:
+            pats = [0]
+        elif n == 1:
+            pats = [lo | hi]
+        elif n == 2:
+            pats = [lo, hi]
+        else:
+            pats = [0, lo, hi]
+        per_axis.append(pats)
+    masks = [0]
+    for pats in per_axis:
+        masks = [m | p for m in masks for p in pats]
+    return sorted(set(masks))
+
+
+def build_spec(mesh, problem, ops: ElementOperators, dt=None, norm="auto") -> OperatorSpec:
+    d = mesh.dim
+    if ops.dim != d:
+        raise ValueError("ops.dim != mesh.dim")
+    if not np.allclose(ops.h, mesh.h, rtol=1e-14, atol=0.0):
+        raise ValueError("ops.h does not match mesh.h")
+    h = mesh.h
+    J = float(np.prod(h / 2.0))
+    Jf = np.array([float(np.prod([h[b] / 2.0 for b in range(d) if b != a])) for a in range(d)])
+    jac_face = np.zeros(3)
+    jac_face[:d] = Jf
+    T, ncols = _ops_table(ops)
+    terms = _Terms(d)
+    face_w = np.zeros((6, 4))
+    coupled = np.zeros(6, dtype=np.int32)
+    out_face = np.zeros(6, dtype=np.int32)
+    out_w = np.zeros((6, 4))
+    comp_w = np.zeros(4)
+    tw = {k: np.zeros((3, 4)) for k in ("int_own", "int_nbr", "lo", "hi")}
+    inv_dt = 0.0 if dt is None else 1.0 / float(dt)
+
+    def E(s):
+        return E1 if s else E0
+
+    def Cc(s):
+        return C1 if s else C0
+
+    if isinstance(problem, TransportProblem):
+        beta = problem.beta_const(d)
+        if beta is None:
+            raise NotImplementedError("device path needs a constant beta (shared operator)")
+        m = 1
+        masks = [0]
+        class_of_mask = np.zeros(64, dtype=np.int32)
+        cls = 0
+        for a in range(d):
+            terms.vol(cls, A_T, 0, 0, -beta[a] * Jf[a], axis=a, op=CONVT)
+        terms.vol(cls, A_T, 0, 0, (problem.reaction + inv_dt) * J)
+        for f in range(2 * d):
+            a, s = divmod(f, 2)
+            sgn = 1.0 if s else -1.0
+            bn = beta[a] * sgn
+            if bn > 0:
+                terms.vol(cls, A_T, 0, 0, bn * Jf[a], axis=a, op=E(s))
+                out_face[f] = 1
+                out_w[f, 0] = 1.0
+            elif bn < 0:
+                terms.vol(cls, B_T, 0, f, -bn * Jf[a], axis=a, op=Cc(s))
+                coupled[f] = 1
+                face_w[f, 0] = 1.0
+        for a in range(d):
+            if beta[a] > 0:
+                tw["int_own"][a, 0] = 1.0
+            elif beta[a] < 0:
+                tw["int_nbr"][a, 0] = 1.0
+            else:
+                tw["int_own"][a, 0] = tw["int_nbr"][a, 0] = 0.5
+            tw["lo"][a, 0] = 1.0 if -beta[a] >= 0 else 0.0  # outflow: u_hat = u^-, inflow: g = 0
+            tw["hi"][a, 0] = 1.0 if beta[a] >= 0 else 0.0
+        if dt is not None:
+            terms.vol(cls, R_T, 0, 0, J * inv_dt)
+        nr = ops.n_nodes if dt is not None else 0
+        tc0, ntc, fcomp = 0, 1, 0
+        comp_w[0] = 1.0
+        if problem.inflow is not None:
+            raise NotImplementedError("non-zero inflow data is not wired to the device path yet")
+        labels = ("u",)
+    elif isinstance(problem, ConvectionDiffusionProblem):
+        beta = problem.beta_const(d)
+        if beta is None:
+            raise NotImplementedError("device path needs a constant beta (shared operator)")
+        if problem.dirichlet is not None:
+            raise NotImplementedError("non-zero Dirichlet data is not wired to the device path yet")
+        m = d + 1
+        U = d
+        masks = _class_masks(mesh)
+        class_of_mask = np.zeros(64, dtype=np.int32)
+        for ci, mk in enumerate(masks):
+            class_of_mask[mk] = ci
+        kinv = 1.0 / problem.kappa
+        for ci, mk in enumerate(masks):
+            for a in range(d):
+                terms.vol(ci, A_T, a, a, kinv * J)
+                terms.vol(ci, A_T, a, U, -Jf[a], axis=a, op=CONVT)
+                terms.vol(ci, A_T, U, a, -Jf[a], axis=a, op=CONVT)
+                terms.vol(ci, A_T, U, U, -beta[a] * Jf[a], axis=a, op=CONVT)
+            terms.vol(ci, A_T, U, U, (problem.nu + inv_dt) * J)
+            for f in range(2 * d):
+                a, s = divmod(f, 2)
+                sgn = 1.0 if s else -1.0
+                bn = beta[a] * sgn
+                alpha = np.sqrt(bn * bn + 4.0)
+                tau = 0.5 * (alpha - bn)
+                cp = 0.5 * (alpha + bn)
+                if mk & (1 << f):
+                    terms.vol(ci, A_T, U, a, sgn * Jf[a], axis=a, op=E(s))
+                    terms.vol(ci, A_T, U, U, (bn + tau) * Jf[a], axis=a, op=E(s))
+                else:
+                    terms.vol(ci, A_T, a, a, Jf[a] / alpha, axis=a, op=E(s))
+                    terms.vol(ci, A_T, a, U, sgn * cp / alpha * Jf[a], axis=a, op=E(s))
+                    terms.vol(ci, A_T, U, a, sgn * (1.0 - tau / alpha) * Jf[a], axis=a, op=E(s))
+                    terms.vol(ci, A_T, U, U, (bn + tau - tau * cp / alpha) * Jf[a], axis=a, op=E(s))
+                    terms.vol(ci, B_T, a, f, -sgn / alpha * Jf[a], axis=a, op=Cc(s))
+                    terms.vol(ci, B_T, U, f, tau / alpha * Jf[a], axis=a, op=Cc(s))
+            if dt is not None:
+                terms.vol(ci, R_T, U, 0, J * inv_dt)
+        for f in range(2 * d):
+            a, s = divmod(f, 2)
+            sgn = 1.0 if s else -1.0
+            bn = beta[a] * sgn
+            alpha = np.sqrt(bn * bn + 4.0)
+            face_w[f, a] = -sgn
+            face_w[f, U] = 0.5 * (alpha - bn)
+            coupled[f] = 1
+        for a in range(d):
+            alpha = np.sqrt(beta[a] ** 2 + 4.0)
+            tw["int_own"][a, a] = 1.0 / alpha
+            tw["int_own"][a, U] = 0.5 * (alpha + beta[a]) / alpha
+            tw["int_nbr"][a, a] = -1.0 / alpha
+            tw["int_nbr"][a, U] = 0.5 * (alpha - beta[a]) / alpha
+        nr = ops.n_nodes if dt is not None else 0
+        tc0, ntc, fcomp = U, 1, U
+        comp_w[:m] = 1.0
+        labels = problem.labels(d)
+    elif isinstance(problem, ShallowWaterProblem):
+        if d != 2:
+            raise ValueError("shallow water is 2D")
+        if dt is None:
+            raise ValueError("shallow water needs a time step (backward Euler)")
+        if problem.beta_cor != 0.0:
+            raise NotImplementedError("variable Coriolis parameter (beta_cor != 0) not on the device path")
+        if any(t != 0.0 for t in problem.tau):
+            raise NotImplementedError("wind stress forcing not on the device path")
+        m = 3
+        P = float(problem.Phi)
+        sP = np.sqrt(P)
+        fc = float(problem.f0)
+        masks = _class_masks(mesh)
+        class_of_mask = np.zeros(64, dtype=np.int32)
+        for ci, mk in enumerate(masks):
+            class_of_mask[mk] = ci
+        for ci, mk in enumerate(masks):
+            terms.vol(ci, A_T, 0, 0, J * inv_dt)
+            for a in range(2):
+                th = 1 + a
+                terms.vol(ci, A_T, 0, th, -P * Jf[a], axis=a, op=CONVT)
+                terms.vol(ci, A_T, th, 0, -P * Jf[a], axis=a, op=CONVT)
+                terms.vol(ci, A_T, th, th, (P * inv_dt + problem.gamma * P) * J)
+            terms.vol(ci, A_T, 1, 2, -fc * P * J)
+            terms.vol(ci, A_T, 2, 1, fc * P * J)
+            for f in range(4):
+                a, s = divmod(f, 2)
+                sgn = 1.0 if s else -1.0
+                th = 1 + a
+                if mk & (1 << f):  # reflective wall
+                    terms.vol(ci, A_T, th, 0, P * sgn * Jf[a], axis=a, op=E(s))
+                    terms.vol(ci, A_T, th, th, P * sP * Jf[a], axis=a, op=E(s))
+                else:
+                    terms.vol(ci, A_T, 0, 0, 0.5 * sP * Jf[a], axis=a, op=E(s))
+                    terms.vol(ci, A_T, 0, th, 0.5 * P * sgn * Jf[a], axis=a, op=E(s))
+                    terms.vol(ci, A_T, th, 0, 0.5 * P * sgn * Jf[a], axis=a, op=E(s))
+                    terms.vol(ci, A_T, th, th, 0.5 * P * sP * Jf[a], axis=a, op=E(s))
+                    terms.vol(ci, B_T, 0, f, 0.5 * sP * Jf[a], axis=a, op=Cc(s))
+                    terms.vol(ci, B_T, th, f, -0.5 * P * sgn * Jf[a], axis=a, op=Cc(s))
+            terms.vol(ci, R_T, 0, 0, J * inv_dt)
+            terms.vol(ci, R_T, 1, 1, P * J * inv_dt)
+            terms.vol(ci, R_T, 2, 2, P * J * inv_dt)
+        for f in range(4):
+            a, s = divmod(f, 2)
+            sgn = 1.0 if s else -1.0
+            face_w[f, 0] = 1.0
+            face_w[f, 1 + a] = -sP * sgn
+            coupled[f] = 1
+        for a in range(2):
+            tw["int_own"][a, 0] = 0.5
+            tw["int_own"][a, 1 + a] = 0.5 * sP
+            tw["int_nbr"][a, 0] = 0.5
+            tw["int_nbr"][a, 1 + a] = -0.5 * sP
+            tw["lo"][a, 0] = 1.0
+            tw["lo"][a, 1 + a] = -sP
+            tw["hi"][a, 0] = 1.0
+            tw["hi"][a, 1 + a] = sP
+        nr = 3 * ops.n_nodes
+        tc0, ntc, fcomp = 0, 3, 0
+        comp_w[:3] = 1.0
+        labels = problem.labels(d)
+    else:
+        raise TypeError(f"unsupported problem type {type(problem).__name__}")
+
+    terms_arr = np.asarray(terms.rows, dtype=np.int32).reshape(-1, 8)
+    return OperatorSpec(
+        dim=d, order=ops.p, ncomp=m, labels=tuple(labels), n_class=len(masks),
+        class_masks=list(masks), class_of_mask=class_of_mask, ops1d=T, op_ncols=ncols,
+        terms=terms_arr, coefs=np.asarray(terms.coefs, dtype=float), nr=nr,
+        time_comp0=tc0, n_time_comp=ntc, forcing_comp=fcomp, face_w=face_w, coupled=coupled,
+        out_face=out_face, out_w=out_w, comp_w=comp_w, trace_w=tw, jac=J, jac_face=jac_face,
+        periodic=tuple(mesh.periodic))
+
+
+def evaluate_terms(spec: OperatorSpec):
+    """Host evaluation of the term list -> (A, B, R) per class.
+
+    Mirror of the first stage of K1 (k_assemble_build), used by the CPU tests
+    to check the physics against the oracle without a GPU.  Not on the
+    product path.
+    """
+    d, n1 = spec.dim, spec.n1
+    npn, nv, nf, kin = spec.n_nodes, spec.nv, n1 ** (d - 1), spec.kin
+    A = np.zeros((spec.n_class, nv, nv))
+    B = np.zeros((spec.n_class, nv, kin))
+    R = np.zeros((spec.n_class, nv, max(spec.nr, 1)))
+    for row, coef in zip(spec.terms, spec.coefs):
+        cls, target, rc, cb = (int(x) for x in row[:4])
+        mats = []
+        for a in range(d):
+            op = spec.ops1d[row[4 + a]]
+            mats.append(op[:, : spec.op_ncols[row[4 + a]]])
+        K = np.ones((1, 1))
+        for mtx in mats:
+            K = np.kron(mtx, K)
+        K = coef * K
+        if target == A_T:
+            A[cls, rc * npn:(rc + 1) * npn, cb * npn:(cb + 1) * npn] += K
+        elif target == B_T:
+            B[cls, rc * npn:(rc + 1) * npn, cb * nf:(cb + 1) * nf] += K
+        else:
+            R[cls, rc * npn:(rc + 1) * npn, cb * npn:(cb + 1) * npn] += K
+    return A, B, R
+
+
+def face_node_indices(dim: int, n1: int, f: int) -> np.ndarray:
+    """Volume node index of each node of local face f (tangential axes
+    increasing, the smallest fastest: mesh.py:166-187).  Mirrors
+    ihdg::face_node_vidx in csrc/ihdg_common.cuh."""
+    a, s = divmod(f, 2)
+    out = []
+    for n in range(n1 ** (dim - 1)):
+        v, mul, rem = 0, 1, n
+        for b in range(dim):
+            if b == a:
+                ib = n1 - 1 if s else 0
+            else:
+                ib = rem % n1
+                rem //= n1
+            v += ib * mul
+            mul *= n1
+        out.append(v)
+    return np.array(out, dtype=np.int64)
+
+
+def neighbor_coupling(spec: OperatorSpec, B: np.ndarray, f: int) -> np.ndarray:
+    """(NV x NV) map neighbour iterate-k volume state -> RHS of face f:
+    B[:, face block f] @ (q extraction with face_w from the neighbour's
+    opposite face).  Host mirror of the gather in k_sweep (tests only)."""
+    npn, nv, nf = spec.n_nodes, spec.nv, spec.n1 ** (spec.dim - 1)
+    W = np.zeros((nf, nv))
+    idx = face_node_indices(spec.dim, spec.n1, f ^ 1)
+    for c in range(spec.ncomp):
+        W[np.arange(nf), c * npn + idx] = spec.face_w[f, c]
+    return B[:, f * nf:(f + 1) * nf] @ W

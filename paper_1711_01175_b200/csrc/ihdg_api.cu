@@ -1,0 +1,314 @@
+// extern "C" entry points of libihdg_cuda.so (declared in include/ihdg.h).
+#include <cstdio>
+#include <string>
+
+#include "ihdg_kernels.cuh"
+#include "ihdg_setup_kernels.cuh"
+
+using namespace ihdg;
+
+namespace {
+
+thread_local std::string g_err;
+
+int set_err(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+#define IHDG_CUDA_TRY(expr)                                                                  \
+  do {                                                                                       \
+    cudaError_t e_ = (expr);                                                                 \
+    if (e_ != cudaSuccess) return set_err(IHDG_ERR_CUDA, std::string(#expr) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+
+int check_launch(const char* what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return set_err(IHDG_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+  return IHDG_OK;
+}
+
+int num_sms() {
+  static int sms = 0;
+  if (sms == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (sms <= 0) sms = 148;
+  }
+  return sms;
+}
+
+// ---- per-instantiation launchers -----------------------------------------
+template <int D, int N1, int M>
+int launch_sweep(const ihdg_sweep_args* a, cudaStream_t st) {
+  using C = Cfg<D, N1, M>;
+  static int grid_max = 0;
+  const size_t smem = SweepSmem<D, N1, M>::bytes;
+  if (grid_max == 0) {
+    IHDG_CUDA_TRY(cudaFuncSetAttribute(k_sweep<D, N1, M>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int nb = 0;
+    IHDG_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_sweep<D, N1, M>, C::NT, smem));
+    if (nb < 1) return set_err(IHDG_ERR_UNSUPPORTED, "sweep kernel does not fit on an SM");
+    grid_max = nb * num_sms();
+  }
+  Geo geo;
+  geo.init(a->g, C::TE);
+  int64_t grid = geo.ntiles < grid_max ? geo.ntiles : grid_max;
+  if (grid < 1) grid = 1;
+  k_sweep<D, N1, M><<<(unsigned)grid, C::NT, smem, st>>>(*a);
+  return check_launch("k_sweep");
+}
+
+template <int D, int N1, int M>
+int launch_apply(const ihdg_class_apply_args* a, cudaStream_t st) {
+  using C = Cfg<D, N1, M>;
+  static int grid_max = 0;
+  const size_t smem = (size_t)C::NV * C::TE * sizeof(double);
+  if (a->ncols > C::NV) return set_err(IHDG_ERR_ARG, "class_apply: ncols > NV");
+  if (grid_max == 0) {
+    IHDG_CUDA_TRY(cudaFuncSetAttribute(k_class_apply<D, N1, M>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int nb = 0;
+    IHDG_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_class_apply<D, N1, M>, C::NT, smem));
+    if (nb < 1) nb = 1;
+    grid_max = nb * num_sms();
+  }
+  Geo geo;
+  geo.init(a->g, C::TE);
+  int64_t grid = geo.ntiles < grid_max ? geo.ntiles : grid_max;
+  if (grid < 1) return IHDG_OK;
+  k_class_apply<D, N1, M><<<(unsigned)grid, C::NT, smem, st>>>(*a);
+  return check_launch("k_class_apply");
+}
+
+template <int D, int N1, int M>
+int tile_elems() {
+  return Cfg<D, N1, M>::TE;
+}
+
+struct Entry {
+  int D, N1, M;
+  int (*sweep)(const ihdg_sweep_args*, cudaStream_t);
+  int (*apply)(const ihdg_class_apply_args*, cudaStream_t);
+  int (*te)();
+};
+
+#define IHDG_ENTRY(D, N1, M) {D, N1, M, launch_sweep<D, N1, M>, launch_apply<D, N1, M>, tile_elems<D, N1, M>},
+
+// Instantiated (dim, p+1, m): transport m=1; CD m=d+1; shallow water m=3 (2D).
+const Entry kEntries[] = {
+    IHDG_ENTRY(1, 2, 1) IHDG_ENTRY(1, 3, 1) IHDG_ENTRY(1, 4, 1) IHDG_ENTRY(1, 5, 1) IHDG_ENTRY(1, 6, 1)
+    IHDG_ENTRY(1, 7, 1)
+    IHDG_ENTRY(1, 2, 2) IHDG_ENTRY(1, 3, 2) IHDG_ENTRY(1, 4, 2) IHDG_ENTRY(1, 5, 2)
+    IHDG_ENTRY(2, 2, 1) IHDG_ENTRY(2, 3, 1) IHDG_ENTRY(2, 4, 1) IHDG_ENTRY(2, 5, 1) IHDG_ENTRY(2, 6, 1)
+    IHDG_ENTRY(2, 7, 1)
+    IHDG_ENTRY(2, 2, 3) IHDG_ENTRY(2, 3, 3) IHDG_ENTRY(2, 4, 3) IHDG_ENTRY(2, 5, 3) IHDG_ENTRY(2, 6, 3)
+    IHDG_ENTRY(2, 7, 3)
+    IHDG_ENTRY(3, 2, 1) IHDG_ENTRY(3, 3, 1) IHDG_ENTRY(3, 4, 1) IHDG_ENTRY(3, 5, 1)
+    IHDG_ENTRY(3, 2, 4) IHDG_ENTRY(3, 3, 4) IHDG_ENTRY(3, 4, 4)
+};
+
+const Entry* find_entry(int D, int order, int M) {
+  for (const Entry& e : kEntries)
+    if (e.D == D && e.N1 == order + 1 && e.M == M) return &e;
+  return nullptr;
+}
+
+int check_geom(const ihdg_geom& g) {
+  if (g.dim < 1 || g.dim > 3) return set_err(IHDG_ERR_ARG, "dim must be 1, 2 or 3");
+  if (g.order < 1 || g.order > 10) return set_err(IHDG_ERR_ARG, "order must be in 1..10");
+  if (g.ncomp < 1 || g.ncomp > IHDG_MAX_COMP) return set_err(IHDG_ERR_ARG, "ncomp must be in 1..4");
+  for (int a = 0; a < g.dim; ++a)
+    if (g.cells[a] < 1) return set_err(IHDG_ERR_ARG, "cell counts must be positive");
+  if (g.layer_begin < 0 || g.layer_end > g.cells[g.dim - 1] || g.layer_end <= g.layer_begin)
+    return set_err(IHDG_ERR_ARG, "bad layer range");
+  return IHDG_OK;
+}
+
+int64_t layer_size(const ihdg_geom& g) {
+  int64_t ls = 1;
+  for (int a = 0; a < g.dim - 1; ++a) ls *= g.cells[a];
+  return ls;
+}
+
+}  // namespace
+
+extern "C" {
+
+int ihdg_abi_version(void) { return IHDG_ABI_VERSION; }
+
+const char* ihdg_last_error(void) { return g_err.c_str(); }
+
+int64_t ihdg_struct_size(int32_t which) {
+  switch (which) {
+    case 0: return sizeof(ihdg_geom);
+    case 1: return sizeof(ihdg_iter_state);
+    case 2: return sizeof(ihdg_assembly_args);
+    case 3: return sizeof(ihdg_class_apply_args);
+    case 4: return sizeof(ihdg_field_args);
+    case 5: return sizeof(ihdg_quad_args);
+    case 6: return sizeof(ihdg_sweep_args);
+    case 7: return sizeof(ihdg_finalize_args);
+    case 8: return sizeof(ihdg_trace_args);
+    default: return -1;
+  }
+}
+
+int ihdg_supported(int32_t dim, int32_t order, int32_t ncomp) {
+  return find_entry(dim, order, ncomp) != nullptr ? 1 : 0;
+}
+
+int32_t ihdg_tile_elems(int32_t dim, int32_t order, int32_t ncomp) {
+  const Entry* e = find_entry(dim, order, ncomp);
+  return e ? e->te() : -1;
+}
+
+int64_t ihdg_tile_count(const ihdg_geom* g) {
+  if (g == nullptr || check_geom(*g) != IHDG_OK) return -1;
+  const Entry* e = find_entry(g->dim, g->order, g->ncomp);
+  if (e == nullptr) return -1;
+  Geo geo;
+  geo.init(*g, e->te());
+  return geo.ntiles;
+}
+
+int ihdg_assemble(const ihdg_assembly_args* a, void* stream) {
+  if (a == nullptr) return set_err(IHDG_ERR_ARG, "null args");
+  if (a->dim < 1 || a->dim > 3 || a->order < 1 || a->ncomp < 1 || a->n_class < 1)
+    return set_err(IHDG_ERR_ARG, "bad assembly dims");
+  cudaStream_t st = (cudaStream_t)stream;
+  AsmDims dm;
+  dm.D = a->dim;
+  dm.N1 = a->order + 1;
+  dm.NP = 1;
+  for (int i = 0; i < dm.D; ++i) dm.NP *= dm.N1;
+  dm.NF = dm.NP / dm.N1;
+  dm.NV = a->ncomp * dm.NP;
+  dm.KIN = 2 * dm.D * dm.NF;
+  dm.nr = a->nr;
+  int* perm = nullptr;
+  IHDG_CUDA_TRY(cudaMallocAsync((void**)&perm, sizeof(int) * dm.NV * a->n_class, st));
+  k_assemble_build<<<a->n_class, 256, 0, st>>>(*a, dm);
+  int rc = check_launch("k_assemble_build");
+  if (rc) return rc;
+  k_gauss_jordan<<<a->n_class, 512, 2 * dm.NV * sizeof(double), st>>>(*a, dm, perm);
+  rc = check_launch("k_gauss_jordan");
+  if (rc) return rc;
+  k_assemble_lift<<<a->n_class, 256, 0, st>>>(*a, dm);
+  rc = check_launch("k_assemble_lift");
+  if (rc) return rc;
+  IHDG_CUDA_TRY(cudaFreeAsync(perm, st));
+  return IHDG_OK;
+}
+
+int ihdg_class_apply(const ihdg_class_apply_args* a, void* stream) {
+  if (a == nullptr) return set_err(IHDG_ERR_ARG, "null args");
+  int rc = check_geom(a->g);
+  if (rc) return rc;
+  const Entry* e = find_entry(a->g.dim, a->g.order, a->g.ncomp);
+  if (e == nullptr) return set_err(IHDG_ERR_UNSUPPORTED, "no kernel instantiated for this (dim, order, ncomp)");
+  return e->apply(a, (cudaStream_t)stream);
+}
+
+int ihdg_eval_field(const ihdg_field_args* a, void* stream) {
+  if (a == nullptr) return set_err(IHDG_ERR_ARG, "null args");
+  int rc = check_geom(a->g);
+  if (rc) return rc;
+  Geo geo;
+  geo.init(a->g, 1);
+  int64_t npts = 1;
+  for (int i = 0; i < a->g.dim; ++i) npts *= a->npts1d;
+  int64_t total = geo.nloc * npts;
+  int64_t blocks = (total + 255) / 256;
+  if (blocks > 8 * num_sms() * 8) blocks = 8 * num_sms() * 8;
+  if (blocks < 1) return IHDG_OK;
+  k_eval_field<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(*a);
+  return check_launch("k_eval_field");
+}
+
+int ihdg_quad_project(const ihdg_quad_args* a, void* stream) {
+  if (a == nullptr) return set_err(IHDG_ERR_ARG, "null args");
+  int rc = check_geom(a->g);
+  if (rc) return rc;
+  Geo geo;
+  geo.init(a->g, 1);
+  int64_t np = 1;
+  for (int i = 0; i < a->g.dim; ++i) np *= (a->g.order + 1);
+  int64_t total = geo.nloc * np;
+  int64_t blocks = (total + 255) / 256;
+  if (blocks > 64 * num_sms()) blocks = 64 * num_sms();
+  if (blocks < 1) return IHDG_OK;
+  k_quad_project<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(*a);
+  return check_launch("k_quad_project");
+}
+
+int ihdg_sweep(const ihdg_sweep_args* a, void* stream) {
+  if (a == nullptr) return set_err(IHDG_ERR_ARG, "null args");
+  int rc = check_geom(a->g);
+  if (rc) return rc;
+  const Entry* e = find_entry(a->g.dim, a->g.order, a->g.ncomp);
+  if (e == nullptr) return set_err(IHDG_ERR_UNSUPPORTED, "no kernel instantiated for this (dim, order, ncomp)");
+  return e->sweep(a, (cudaStream_t)stream);
+}
+
+int ihdg_finalize(const ihdg_finalize_args* a, void* stream) {
+  if (a == nullptr) return set_err(IHDG_ERR_ARG, "null args");
+  k_finalize<<<1, 256, 0, (cudaStream_t)stream>>>(*a);
+  return check_launch("k_finalize");
+}
+
+int ihdg_extract_trace(const ihdg_trace_args* a, void* stream) {
+  if (a == nullptr) return set_err(IHDG_ERR_ARG, "null args");
+  int rc = check_geom(a->g);
+  if (rc) return rc;
+  if (a->g.layer_begin != 0 || a->g.layer_end != a->g.cells[a->g.dim - 1])
+    return set_err(IHDG_ERR_UNSUPPORTED, "trace extraction needs the whole mesh on one rank");
+  k_extract_trace<<<4 * num_sms(), 256, 0, (cudaStream_t)stream>>>(*a);
+  return check_launch("k_extract_trace");
+}
+
+int ihdg_copy_state(const ihdg_geom* g, const double* src, double* dst, void* stream) {
+  if (g == nullptr) return set_err(IHDG_ERR_ARG, "null args");
+  int rc = check_geom(*g);
+  if (rc) return rc;
+  int64_t np = 1;
+  for (int i = 0; i < g->dim; ++i) np *= (g->order + 1);
+  const int64_t ls = layer_size(*g);
+  const int64_t n = ((g->layer_end - g->layer_begin) * ls + 2 * ls) * g->ncomp * np;
+  IHDG_CUDA_TRY(cudaMemcpyAsync(dst, src, n * sizeof(double), cudaMemcpyDeviceToDevice, (cudaStream_t)stream));
+  return IHDG_OK;
+}
+
+int ihdg_iterate(const ihdg_sweep_args* a0, double* buf0, double* buf1, int32_t batch, void* stream,
+                 ihdg_iter_state* state_out, int64_t* n_launched) {
+  if (a0 == nullptr || buf0 == nullptr || buf1 == nullptr || state_out == nullptr)
+    return set_err(IHDG_ERR_ARG, "null args");
+  if (batch < 1) batch = 1;
+  int rc = check_geom(a0->g);
+  if (rc) return rc;
+  const Entry* e = find_entry(a0->g.dim, a0->g.order, a0->g.ncomp);
+  if (e == nullptr) return set_err(IHDG_ERR_UNSUPPORTED, "no kernel instantiated for this (dim, order, ncomp)");
+  static thread_local ihdg_iter_state* hs = nullptr;
+  if (hs == nullptr) IHDG_CUDA_TRY(cudaMallocHost((void**)&hs, sizeof(ihdg_iter_state)));
+  cudaStream_t st = (cudaStream_t)stream;
+  ihdg_sweep_args a = *a0;
+  a.finalize = 1;
+  int64_t launched = 0;
+  for (;;) {
+    for (int j = 0; j < batch; ++j) {
+      a.u_old = (launched & 1) ? buf1 : buf0;
+      a.u_new = (launched & 1) ? buf0 : buf1;
+      rc = e->sweep(&a, st);
+      if (rc) return rc;
+      ++launched;
+    }
+    IHDG_CUDA_TRY(cudaMemcpyAsync(hs, a.state, sizeof(ihdg_iter_state), cudaMemcpyDeviceToHost, st));
+    IHDG_CUDA_TRY(cudaStreamSynchronize(st));
+    if (hs->status != IHDG_RUNNING) break;
+  }
+  *state_out = *hs;
+  if (n_launched) *n_launched = launched;
+  return IHDG_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,381 @@
+// Generic iHDG-II kernels (any instantiated dim / order / ncomp).
+//
+// K2+K3  k_sweep        : fused gather -> lifted local solve -> write -> norm
+// K4     k_class_apply  : per-element class operator (s = A^-1 b, s = P u^m)
+// finalize_block        : fixed-order reduction of tile partials + stop rule
+#pragma once
+
+#include "ihdg_common.cuh"
+
+namespace ihdg {
+
+constexpr long long NO_NBR = -(1LL << 62);
+
+// Fixed-order (rank-count independent) reduction of the tile partials and the
+// stopping / divergence logic of `run`.
+// 256 virtual lanes, lane v sums tiles v, v+256, ... in order, then a fixed
+// binary tree.  Must be executed by every thread of one CTA.
+__device__ inline void finalize_block(const double* parts, int64_t n, ihdg_iter_state* st,
+                                      double* hist) {
+  __shared__ double red[256];
+  for (int v = threadIdx.x; v < 256; v += blockDim.x) {
+    double s = 0.0;
+    for (int64_t i = v; i < n; i += 256) s += __ldcg(parts + i);
+    red[v] = s;
+  }
+  __syncthreads();
+  for (int w = 128; w > 0; w >>= 1) {
+    for (int v = threadIdx.x; v < w; v += blockDim.x) red[v] += red[v + w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    const double norm = sqrt(red[0]);
+    const int it = st->iters + 1;
+    st->iters = it;
+    if (hist != nullptr && it <= st->max_iters) hist[it - 1] = norm;
+    if (it == 1) st->first_norm = norm;
+    st->last_norm = norm;
+    int status = IHDG_RUNNING;
+    if (!(norm == norm)) status = IHDG_NAN;
+    else if (norm < st->tol) status = IHDG_CONVERGED;
+    else if (it > 1 && norm > st->diverge_factor * st->first_norm) status = IHDG_DIVERGED;
+    else if (it >= st->max_iters) status = IHDG_MAXITER;
+    st->status = status;
+    st->ticket = 0u;
+    __threadfence();
+  }
+}
+
+template <int D, int N1, int M>
+struct SweepSmem {
+  using C = Cfg<D, N1, M>;
+  static constexpr size_t doubles = (size_t)C::KIN * C::TE + 2 * (size_t)C::TE * C::NV +
+                                    N1 * N1 + C::TE * (2 * D + 1);
+  static constexpr size_t bytes = doubles * sizeof(double);
+};
+
+// One iHDG-II sweep (Algorithm 1 lines 2-4) over a strip.
+// Each CTA walks tiles of TE consecutive elements of one layer:
+//   1. neighbour ids + boundary mask -> operator class
+//   2. q[k][t]: neighbour iterate-k face scalars (TraceSnapshot)
+//   3. u^{k+1} = s + L_class q  (apply_local in lifted form),
+//      threads own rows, L is read once per tile and reused over TE elements
+//   4. delta = u^{k+1} - u^k; mass-weighted (sum-factorised Cholesky of the
+//      1D mass) or trace norm -> one partial per tile in a fixed order.
+template <int D, int N1, int M>
+__global__ void __launch_bounds__(Cfg<D, N1, M>::NT)
+    k_sweep(const ihdg_sweep_args a) {
+  using C = Cfg<D, N1, M>;
+  constexpr int NP = C::NP, NV = C::NV, NF = C::NF, KIN = C::KIN;
+  constexpr int TE = C::TE, RP = C::RP, G = C::G, NT = C::NT, J = C::J;
+  constexpr int NFACE = 2 * D;
+
+  extern __shared__ __align__(16) double sm[];
+  double* q_s = sm;                 // [KIN][TE]
+  double* d_s = q_s + KIN * TE;     // [TE][NV]
+  double* t_s = d_s + TE * NV;      // [TE][NV]
+  double* c_s = t_s + TE * NV;      // [N1][N1]
+  double* pf_s = c_s + N1 * N1;     // [TE][NFACE+1]
+  __shared__ int fv_s[NFACE][NF];
+  __shared__ int cls_s[TE];
+  __shared__ long long nb_s[TE][NFACE];
+  __shared__ int uni_s;
+  __shared__ int last_s;
+
+  ihdg_iter_state* st = a.state;
+  if (st->status != IHDG_RUNNING) return;
+
+  Geo geo;
+  geo.init(a.g, TE);
+  const int tid = threadIdx.x;
+  for (int i = tid; i < NFACE * NF; i += NT) fv_s[i / NF][i % NF] = face_node_vidx(D, N1, i / NF, i % NF);
+  for (int i = tid; i < N1 * N1; i += NT) c_s[i] = a.chol1d[i];
+
+  const int64_t ls = geo.ls;
+  const double* __restrict__ uo = a.u_old + ls * NV;
+  double* __restrict__ un = a.u_new + ls * NV;
+  const double* __restrict__ sv = a.s;
+
+  for (int64_t tile = blockIdx.x; tile < geo.ntiles; tile += gridDim.x) {
+    int64_t e0;
+    int nt;
+    geo.tile_range(tile, TE, e0, nt);
+    __syncthreads();
+    if (tid < TE) {
+      const int t = tid;
+      if (t < nt) {
+        const int64_t e = e0 + t;
+        int64_t idx[3];
+        geo.multi_index(e, idx);
+        int mask = 0;
+        for (int f = 0; f < NFACE; ++f) {
+          int64_t nb;
+          if (geo.neighbor(e, idx, f, nb)) {
+            nb_s[t][f] = nb;
+          } else {
+            nb_s[t][f] = NO_NBR;
+            mask |= 1 << f;
+          }
+        }
+        cls_s[t] = a.class_of_mask[mask];
+      } else {
+        cls_s[t] = -1;
+      }
+    }
+    __syncthreads();
+    if (tid == 0) {
+      int u = 1;
+      for (int t = 1; t < nt; ++t) u &= (cls_s[t] == cls_s[0]);
+      uni_s = u;
+    }
+    // -- gather neighbour face scalars (iterate k) --------------------------
+    for (int i = tid; i < KIN * TE; i += NT) {
+      const int k = i / TE, t = i % TE;
+      const int f = k / NF, n = k % NF;
+      double v = 0.0;
+      if (t < nt && a.coupled[f]) {
+        const long long nb = nb_s[t][f];
+        if (nb != NO_NBR) {
+          const double* p = uo + nb * NV + fv_s[f ^ 1][n];
+#pragma unroll
+          for (int c = 0; c < M; ++c) v = fma(a.face_w[f][c], __ldg(p + c * NP), v);
+        }
+      }
+      q_s[i] = v;
+    }
+    __syncthreads();
+    // -- lifted local solve: rows x elements --------------------------------
+    const int r = tid % RP, gi = tid / RP;
+    for (int r0 = 0; r0 < NV; r0 += RP) {
+      const int rr = r0 + r;
+      const bool rv = rr < NV;
+      double acc[J];
+#pragma unroll
+      for (int j = 0; j < J; ++j) {
+        const int t = gi + j * G;
+        acc[j] = (rv && t < nt) ? __ldg(sv + (e0 + t) * NV + rr) : 0.0;
+      }
+      if (uni_s) {
+        const double* __restrict__ Lc = a.LT + (size_t)cls_s[0] * KIN * NV + (rv ? rr : 0);
+#pragma unroll 4
+        for (int k = 0; k < KIN; ++k) {
+          const double l = __ldg(Lc + (size_t)k * NV);
+#pragma unroll
+          for (int j = 0; j < J; ++j) acc[j] = fma(l, q_s[k * TE + gi + j * G], acc[j]);
+        }
+      } else if (rv) {
+#pragma unroll
+        for (int j = 0; j < J; ++j) {
+          const int t = gi + j * G;
+          if (t < nt) {
+            const double* __restrict__ Lc = a.LT + (size_t)cls_s[t] * KIN * NV + rr;
+            double s = acc[j];
+            for (int k = 0; k < KIN; ++k) s = fma(__ldg(Lc + (size_t)k * NV), q_s[k * TE + t], s);
+            acc[j] = s;
+          }
+        }
+      }
+      if (rv) {
+#pragma unroll
+        for (int j = 0; j < J; ++j) {
+          const int t = gi + j * G;
+          if (t < nt) {
+            const int64_t o = (e0 + t) * NV + rr;
+            un[o] = acc[j];
+            d_s[t * NV + rr] = acc[j] - __ldg(uo + o);
+          }
+        }
+      }
+    }
+    __syncthreads();
+    // -- stopping norm of the successive difference --------------------------
+    if (a.norm_kind == IHDG_NORM_VOLUME) {
+      // ||delta||_M^2 = J * sum_c w_c |(C^T (x) ... (x) C^T) delta_c|^2
+      double* src = d_s;
+      double* dst = t_s;
+      int mul = 1;
+      for (int ax = 0; ax < D; ++ax) {
+        for (int i = tid; i < nt * NV; i += NT) {
+          const int t = i / NV, rem = i % NV;
+          const int n = rem % NP;
+          const int ia = (n / mul) % N1;
+          const int base = t * NV + rem - ia * mul;
+          double v = 0.0;
+          for (int ip = ia; ip < N1; ++ip) v = fma(c_s[ip * N1 + ia], src[base + ip * mul], v);
+          dst[i] = v;
+        }
+        __syncthreads();
+        double* tmp = src;
+        src = dst;
+        dst = tmp;
+        mul *= N1;
+      }
+      const int warp = tid >> 5, lane = tid & 31;
+      for (int t = warp; t < nt; t += NT / 32) {
+        double s = 0.0;
+        for (int i = lane; i < NV; i += 32) {
+          const double v = src[t * NV + i];
+          s = fma(a.comp_w[i / NP] * v, v, s);
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+        if (lane == 0) pf_s[t * (NFACE + 1)] = a.jac * s;
+      }
+    } else {
+      // skeleton L2 norm of the trace update on the flagged (outflow) faces
+      for (int i = tid; i < nt * NFACE; i += NT) {
+        const int t = i / NFACE, f = i % NFACE;
+        double v = 0.0;
+        if (a.out_face[f]) {
+          double x[NF], y[NF];
+#pragma unroll
+          for (int n = 0; n < NF; ++n) {
+            double w = 0.0;
+#pragma unroll
+            for (int c = 0; c < M; ++c) w = fma(a.out_w[f][c], d_s[t * NV + c * NP + fv_s[f][n]], w);
+            x[n] = w;
+          }
+          int mul = 1;
+#pragma unroll
+          for (int ax = 0; ax < D - 1; ++ax) {
+#pragma unroll
+            for (int n = 0; n < NF; ++n) {
+              const int ia = (n / mul) % N1;
+              double w = 0.0;
+              for (int ip = ia; ip < N1; ++ip) w = fma(c_s[ip * N1 + ia], x[n + (ip - ia) * mul], w);
+              y[n] = w;
+            }
+#pragma unroll
+            for (int n = 0; n < NF; ++n) x[n] = y[n];
+            mul *= N1;
+          }
+#pragma unroll
+          for (int n = 0; n < NF; ++n) v = fma(x[n], x[n], v);
+          v *= a.jac_face[f >> 1];
+        }
+        pf_s[t * (NFACE + 1) + 1 + f] = v;
+      }
+      __syncthreads();
+      if (tid < nt) {
+        double s = 0.0;
+        for (int f = 0; f < NFACE; ++f) s += pf_s[tid * (NFACE + 1) + 1 + f];
+        pf_s[tid * (NFACE + 1)] = s;
+      }
+    }
+    __syncthreads();
+    if (tid == 0) {
+      double s = 0.0;
+      for (int t = 0; t < nt; ++t) s += pf_s[t * (NFACE + 1)];
+      a.tile_partials[tile] = s;
+    }
+  }
+
+  if (a.finalize) {
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) {
+      const unsigned tk = atomicAdd(&st->ticket, 1u);
+      last_s = (tk == gridDim.x - 1);
+    }
+    __syncthreads();
+    if (last_s) {
+      __threadfence();
+      finalize_block(a.tile_partials, geo.ntiles, st, a.norm_hist);
+    }
+  }
+}
+
+template <int D, int N1, int M>
+struct ApplySmem {
+  using C = Cfg<D, N1, M>;
+  static constexpr size_t bytes = (size_t)C::NV * C::TE * sizeof(double);
+};
+
+// out[e][r] (+)= sum_k opT[class(e)][k][r] * in[e][in_offset + k]
+template <int D, int N1, int M>
+__global__ void __launch_bounds__(Cfg<D, N1, M>::NT)
+    k_class_apply(const ihdg_class_apply_args a) {
+  using C = Cfg<D, N1, M>;
+  constexpr int NV = C::NV, TE = C::TE, RP = C::RP, G = C::G, NT = C::NT, J = C::J;
+  constexpr int NFACE = 2 * D;
+  extern __shared__ __align__(16) double sm[];
+  double* in_s = sm;  // [ncols][TE]
+  __shared__ int cls_s[TE];
+  __shared__ int uni_s;
+  Geo geo;
+  geo.init(a.g, TE);
+  const int tid = threadIdx.x;
+  const int ncols = a.ncols;
+  const double* in0 = a.in + (a.in_ghost ? geo.ls * a.in_stride : 0) + a.in_offset;
+  double* out0 = a.out + (a.out_ghost ? geo.ls * NV : 0);
+  for (int64_t tile = blockIdx.x; tile < geo.ntiles; tile += gridDim.x) {
+    int64_t e0;
+    int nt;
+    geo.tile_range(tile, TE, e0, nt);
+    __syncthreads();
+    if (tid < TE) {
+      const int t = tid;
+      if (t < nt) {
+        const int64_t e = e0 + t;
+        int64_t idx[3];
+        geo.multi_index(e, idx);
+        int mask = 0;
+        for (int f = 0; f < NFACE; ++f) {
+          int64_t nb;
+          if (!geo.neighbor(e, idx, f, nb)) mask |= 1 << f;
+        }
+        cls_s[t] = a.class_of_mask[mask];
+      } else {
+        cls_s[t] = -1;
+      }
+    }
+    for (int i = tid; i < ncols * TE; i += NT) {
+      const int k = i / TE, t = i % TE;
+      in_s[i] = (t < nt) ? in0[(e0 + t) * a.in_stride + k] : 0.0;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      int u = 1;
+      for (int t = 1; t < nt; ++t) u &= (cls_s[t] == cls_s[0]);
+      uni_s = u;
+    }
+    __syncthreads();
+    const int r = tid % RP, gi = tid / RP;
+    for (int r0 = 0; r0 < NV; r0 += RP) {
+      const int rr = r0 + r;
+      if (rr >= NV) continue;
+      double acc[J];
+#pragma unroll
+      for (int j = 0; j < J; ++j) {
+        const int t = gi + j * G;
+        acc[j] = (a.accumulate && t < nt) ? out0[(e0 + t) * NV + rr] : 0.0;
+      }
+      if (uni_s) {
+        const double* Op = a.opT + (size_t)cls_s[0] * ncols * NV + rr;
+        for (int k = 0; k < ncols; ++k) {
+          const double l = __ldg(Op + (size_t)k * NV);
+#pragma unroll
+          for (int j = 0; j < J; ++j) acc[j] = fma(l, in_s[k * TE + gi + j * G], acc[j]);
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < J; ++j) {
+          const int t = gi + j * G;
+          if (t < nt) {
+            const double* Op = a.opT + (size_t)cls_s[t] * ncols * NV + rr;
+            double s = acc[j];
+            for (int k = 0; k < ncols; ++k) s = fma(__ldg(Op + (size_t)k * NV), in_s[k * TE + t], s);
+            acc[j] = s;
+          }
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < J; ++j) {
+        const int t = gi + j * G;
+        if (t < nt) out0[(e0 + t) * NV + rr] = acc[j];
+      }
+    }
+  }
+}
+
+}  // namespace ihdg

@@ -1,0 +1,349 @@
+// Setup kernels: K1 assembly + Gauss-Jordan inversion, analytic field
+// evaluation, quadrature projection, trace extraction.
+#pragma once
+
+#include "ihdg_common.cuh"
+#include "ihdg_kernels.cuh"
+
+namespace ihdg {
+
+// ---------------------------------------------------------------------------
+// K1: Kronecker term-list assembly (one CTA per operator class).
+// A local matrix of the substituted iHDG-II weak form (SPEC.md:246-274,
+// PAPER.md:409-420, 714-727, 1067-1077) is a sum of tensor products of 1D
+// reference matrices (mass, convection, endpoint projectors) times
+// coefficients; the host (assembly.py) derives the term list, this kernel
+// evaluates the entries in fp64.
+// ---------------------------------------------------------------------------
+struct AsmDims {
+  int D, N1, NP, NV, NF, KIN, nr;
+};
+
+__global__ void k_assemble_build(const ihdg_assembly_args a, AsmDims dm) {
+  const int cls = blockIdx.x;
+  const int tid = threadIdx.x, nth = blockDim.x;
+  double* A = a.A + (size_t)cls * dm.NV * dm.NV;
+  double* B = a.B + (size_t)cls * dm.NV * dm.KIN;
+  double* R = a.R ? a.R + (size_t)cls * dm.NV * dm.nr : nullptr;
+  for (int i = tid; i < dm.NV * dm.NV; i += nth) A[i] = 0.0;
+  for (int i = tid; i < dm.NV * dm.KIN; i += nth) B[i] = 0.0;
+  if (R)
+    for (int i = tid; i < dm.NV * dm.nr; i += nth) R[i] = 0.0;
+  __syncthreads();
+  const int N1 = dm.N1;
+  for (int tm = 0; tm < a.n_terms; ++tm) {
+    const int* T = a.terms + 8 * tm;
+    if (T[0] != cls) continue;
+    const int target = T[1], rc = T[2], cb = T[3];
+    const double coef = a.coefs[tm];
+    int nc[3] = {1, 1, 1};
+    const double* op[3] = {nullptr, nullptr, nullptr};
+    int ncols = 1;
+    for (int ax = 0; ax < dm.D; ++ax) {
+      op[ax] = a.ops1d + (size_t)T[4 + ax] * N1 * N1;
+      nc[ax] = a.op_ncols[T[4 + ax]];
+      ncols *= nc[ax];
+    }
+    double* dst;
+    int ld, col0;
+    if (target == 0) {
+      dst = A; ld = dm.NV; col0 = cb * dm.NP;
+    } else if (target == 1) {
+      dst = B; ld = dm.KIN; col0 = cb * dm.NF;
+    } else {
+      dst = R; ld = dm.nr; col0 = cb * dm.NP;
+    }
+    if (dst == nullptr) continue;
+    for (int idx = tid; idx < dm.NP * ncols; idx += nth) {
+      int i = idx / ncols, j = idx % ncols;
+      double v = coef;
+      int ii = i, jj = j;
+      for (int ax = 0; ax < dm.D; ++ax) {
+        const int ia = ii % N1, ja = jj % nc[ax];
+        ii /= N1;
+        jj /= nc[ax];
+        v *= op[ax][ia * N1 + ja];
+      }
+      dst[(size_t)(rc * dm.NP + i) * ld + col0 + j] += v;
+    }
+    __syncthreads();
+  }
+}
+
+// In-place Gauss-Jordan inversion with partial pivoting (row swaps undone by
+// column swaps in reverse), one CTA per class, matrix in global memory.
+__global__ void k_gauss_jordan(const ihdg_assembly_args a, AsmDims dm, int* perm_ws) {
+  const int cls = blockIdx.x;
+  const int n = dm.NV;
+  const int tid = threadIdx.x, nth = blockDim.x;
+  double* M = a.Ainv + (size_t)cls * n * n;
+  const double* A = a.A + (size_t)cls * n * n;
+  int* perm = perm_ws + (size_t)cls * n;
+  extern __shared__ double gj_s[];
+  double* colk = gj_s;       // [n]
+  double* rowk = gj_s + n;   // [n]
+  __shared__ double bval[1024];
+  __shared__ int bidx[1024];
+  __shared__ double minpiv;
+  for (int i = tid; i < n * n; i += nth) M[i] = A[i];
+  if (tid == 0) minpiv = 1e300;
+  __syncthreads();
+  for (int k = 0; k < n; ++k) {
+    // pivot search: max |M[i][k]|, i >= k, ties -> smallest i
+    double bv = -1.0;
+    int bi = n;
+    for (int i = k + tid; i < n; i += nth) {
+      const double v = fabs(M[(size_t)i * n + k]);
+      if (v > bv) { bv = v; bi = i; }
+    }
+    bval[tid] = bv;
+    bidx[tid] = bi;
+    __syncthreads();
+    for (int w = nth / 2; w > 0; w >>= 1) {
+      if (tid < w) {
+        const double v2 = bval[tid + w];
+        const int i2 = bidx[tid + w];
+        if (v2 > bval[tid] || (v2 == bval[tid] && i2 < bidx[tid])) {
+          bval[tid] = v2;
+          bidx[tid] = i2;
+        }
+      }
+      __syncthreads();
+    }
+    const int p = bidx[0];
+    if (tid == 0) {
+      perm[k] = p;
+      if (bval[0] < minpiv) minpiv = bval[0];
+    }
+    if (p != k) {
+      for (int j = tid; j < n; j += nth) {
+        const double t = M[(size_t)k * n + j];
+        M[(size_t)k * n + j] = M[(size_t)p * n + j];
+        M[(size_t)p * n + j] = t;
+      }
+    }
+    __syncthreads();
+    const double piv = M[(size_t)k * n + k];
+    for (int j = tid; j < n; j += nth) {
+      rowk[j] = (j == k ? 1.0 : M[(size_t)k * n + j]) / piv;
+      colk[j] = M[(size_t)j * n + k];
+    }
+    __syncthreads();
+    for (int idx = tid; idx < n * n; idx += nth) {
+      const int i = idx / n, j = idx % n;
+      if (i == k) {
+        M[idx] = rowk[j];
+      } else {
+        const double base = (j == k) ? 0.0 : M[idx];
+        M[idx] = fma(-colk[i], rowk[j], base);
+      }
+    }
+    __syncthreads();
+  }
+  for (int k = n - 1; k >= 0; --k) {
+    const int p = perm[k];
+    if (p != k) {
+      for (int i = tid; i < n; i += nth) {
+        const double t = M[(size_t)i * n + k];
+        M[(size_t)i * n + k] = M[(size_t)i * n + p];
+        M[(size_t)i * n + p] = t;
+      }
+    }
+    __syncthreads();
+  }
+  if (tid == 0) a.min_pivot[cls] = minpiv;
+}
+
+// LT[c][k][r] = sum_j Ainv[r][j] B[j][k];  PT likewise with R;  AinvT.
+__global__ void k_assemble_lift(const ihdg_assembly_args a, AsmDims dm) {
+  const int cls = blockIdx.x;
+  const int n = dm.NV;
+  const double* Ai = a.Ainv + (size_t)cls * n * n;
+  const double* B = a.B + (size_t)cls * n * dm.KIN;
+  double* LT = a.LT + (size_t)cls * dm.KIN * n;
+  for (int idx = threadIdx.x; idx < dm.KIN * n; idx += blockDim.x) {
+    const int k = idx / n, r = idx % n;
+    double s = 0.0;
+    for (int j = 0; j < n; ++j) s = fma(Ai[(size_t)r * n + j], B[(size_t)j * dm.KIN + k], s);
+    LT[idx] = s;
+  }
+  if (a.PT && a.R && dm.nr > 0) {
+    const double* R = a.R + (size_t)cls * n * dm.nr;
+    double* PT = a.PT + (size_t)cls * dm.nr * n;
+    for (int idx = threadIdx.x; idx < dm.nr * n; idx += blockDim.x) {
+      const int k = idx / n, r = idx % n;
+      double s = 0.0;
+      for (int j = 0; j < n; ++j) s = fma(Ai[(size_t)r * n + j], R[(size_t)j * dm.nr + k], s);
+      PT[idx] = s;
+    }
+  }
+  if (a.AinvT) {
+    double* AT = a.AinvT + (size_t)cls * n * n;
+    for (int idx = threadIdx.x; idx < n * n; idx += blockDim.x) {
+      const int j = idx / n, r = idx % n;
+      AT[idx] = Ai[(size_t)r * n + j];
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Analytic fields at element tensor points (nodal interpolation = project,
+// SPEC.md:117-121; forcing at Gauss points for (f,v)_K).
+// ---------------------------------------------------------------------------
+__global__ void k_eval_field(const ihdg_field_args a) {
+  Geo geo;
+  geo.init(a.g, 1);
+  const int D = geo.D;
+  int npts = 1;
+  for (int ax = 0; ax < D; ++ax) npts *= a.npts1d;
+  const int64_t total = geo.nloc * npts;
+  double* out0 = a.out + (a.out_ghost ? geo.ls * a.out_stride : 0) + a.out_offset;
+  const int np = 2 + D;
+  for (int64_t gid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; gid < total;
+       gid += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t e = gid / npts;
+    int pt = (int)(gid % npts);
+    int64_t idx[3];
+    geo.multi_index(e, idx);
+    double x[3];
+    for (int ax = 0; ax < D; ++ax) {
+      const int ia = pt % a.npts1d;
+      pt /= a.npts1d;
+      // same rounding as mesh.py element_points: (lo + i h) + (0.5 h) (ref + 1)
+      const double orig = __dadd_rn(a.lo[ax], __dmul_rn((double)idx[ax], a.h[ax]));
+      x[ax] = __dadd_rn(orig, __dmul_rn(__dmul_rn(0.5, a.h[ax]), __dadd_rn(a.ref1d[ia], 1.0)));
+    }
+    double v = 0.0;
+    for (int m = 0; m < a.nmodes; ++m) {
+      const double* P = a.params + m * np;
+      if (a.kind == 0) {
+        double arg = P[1 + D];
+        for (int ax = 0; ax < D; ++ax) arg = fma(2.0 * M_PI * P[1 + ax], x[ax], arg);
+        v += P[0] * sin(arg);
+      } else {
+        double r2 = 0.0;
+        for (int ax = 0; ax < D; ++ax) {
+          const double dx = x[ax] - P[1 + ax];
+          r2 = fma(dx, dx, r2);
+        }
+        const double w = P[1 + D];
+        v += P[0] * exp(-r2 / (2.0 * w * w));
+      }
+    }
+    out0[e * a.out_stride + (gid % npts)] = v;
+  }
+}
+
+// b[e][i] = jac * sum_q prod_a Bq[i_a][q_a] fq[e][q]
+__global__ void k_quad_project(const ihdg_quad_args a) {
+  Geo geo;
+  geo.init(a.g, 1);
+  const int D = geo.D;
+  const int N1 = a.g.order + 1;
+  int NP = 1, NQ = 1;
+  for (int ax = 0; ax < D; ++ax) {
+    NP *= N1;
+    NQ *= a.nq;
+  }
+  const int64_t total = geo.nloc * NP;
+  for (int64_t gid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; gid < total;
+       gid += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t e = gid / NP;
+    const int i = (int)(gid % NP);
+    int ia[3] = {0, 0, 0};
+    int ii = i;
+    for (int ax = 0; ax < D; ++ax) {
+      ia[ax] = ii % N1;
+      ii /= N1;
+    }
+    const double* f = a.fq + e * NQ;
+    double s = 0.0;
+    for (int q = 0; q < NQ; ++q) {
+      int qq = q;
+      double w = 1.0;
+      for (int ax = 0; ax < D; ++ax) {
+        w *= a.Bq[ia[ax] * a.nq + qq % a.nq];
+        qq /= a.nq;
+      }
+      s = fma(w, f[q], s);
+    }
+    a.out[e * a.out_stride + a.out_offset + i] = a.jac * s;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Single-valued trace on every face in mesh.py order (mesh.py:89-125).
+// ---------------------------------------------------------------------------
+__global__ void k_extract_trace(const ihdg_trace_args a) {
+  Geo geo;
+  geo.init(a.g, 1);
+  const int D = geo.D;
+  const int N1 = a.g.order + 1;
+  const int M = a.g.ncomp;
+  int NP = 1, NF = 1;
+  for (int ax = 0; ax < D; ++ax) NP *= N1;
+  for (int ax = 0; ax < D - 1; ++ax) NF *= N1;
+  const int NV = M * NP;
+  // faces per axis
+  int64_t off[4] = {0, 0, 0, 0};
+  int64_t ntan[3], planes[3];
+  for (int ax = 0; ax < D; ++ax) {
+    ntan[ax] = 1;
+    for (int b = 0; b < D; ++b)
+      if (b != ax) ntan[ax] *= geo.c[b];
+    planes[ax] = geo.c[ax] + (geo.per[ax] ? 0 : 1);
+    off[ax + 1] = off[ax] + planes[ax] * ntan[ax];
+  }
+  const int64_t nfaces = off[D];
+  const double* u0 = a.u + geo.ls * NV;
+  for (int64_t gid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; gid < nfaces * NF;
+       gid += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t fid = gid / NF;
+    const int n = (int)(gid % NF);
+    int ax = 0;
+    while (fid >= off[ax + 1]) ++ax;
+    const int64_t lf = fid - off[ax];
+    const int64_t plane = lf / ntan[ax];
+    int64_t tl = lf % ntan[ax];
+    int64_t idx[3] = {0, 0, 0};
+    for (int b = 0; b < D; ++b) {
+      if (b == ax) continue;
+      idx[b] = tl % geo.c[b];
+      tl /= geo.c[b];
+    }
+    auto elem = [&](int64_t ia) {
+      int64_t e = 0;
+      for (int b = 0; b < D; ++b) e += (b == ax ? ia : idx[b]) * geo.stride[b];
+      return e;
+    };
+    const int f_hi = 2 * ax + 1, f_lo = 2 * ax;
+    double v = 0.0;
+    if (plane > 0 && plane < geo.c[ax]) {
+      const int64_t eo = elem(plane - 1), en = elem(plane);
+      const int vo = face_node_vidx(D, N1, f_hi, n), vn = face_node_vidx(D, N1, f_lo, n);
+      for (int c = 0; c < M; ++c)
+        v += a.w_int_own[ax][c] * u0[eo * NV + c * NP + vo] + a.w_int_nbr[ax][c] * u0[en * NV + c * NP + vn];
+    } else if (plane == 0 && geo.per[ax]) {
+      const int64_t eo = elem(geo.c[ax] - 1), en = elem(0);
+      const int vo = face_node_vidx(D, N1, f_hi, n), vn = face_node_vidx(D, N1, f_lo, n);
+      for (int c = 0; c < M; ++c)
+        v += a.w_int_own[ax][c] * u0[eo * NV + c * NP + vo] + a.w_int_nbr[ax][c] * u0[en * NV + c * NP + vn];
+    } else if (plane == 0) {
+      const int64_t eo = elem(0);
+      const int vo = face_node_vidx(D, N1, f_lo, n);
+      for (int c = 0; c < M; ++c) v += a.w_lo[ax][c] * u0[eo * NV + c * NP + vo];
+    } else {
+      const int64_t eo = elem(geo.c[ax] - 1);
+      const int vo = face_node_vidx(D, N1, f_hi, n);
+      for (int c = 0; c < M; ++c) v += a.w_hi[ax][c] * u0[eo * NV + c * NP + vo];
+    }
+    a.trace[gid] = v;
+  }
+}
+
+__global__ void k_finalize(const ihdg_finalize_args a) {
+  if (a.state->status != IHDG_RUNNING) return;  // later sweeps are no-ops
+  finalize_block(a.tile_partials, a.n_tiles, a.state, a.norm_hist);
+}
+
+}  // namespace ihdg

@@ -1,0 +1,387 @@
+"""Device-resident iHDG-II solver for one rank's strip of the mesh.
+
+PyTorch is used only as plumbing: it allocates device memory, provides the
+CUDA stream and (for several ranks) torch.distributed.  All arithmetic of the
+iteration runs in libihdg_cuda.so kernels (see include/ihdg.h).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import time
+from dataclasses import dataclass
+from typing import Optional
+
+import numpy as np
+
+from . import _native as N
+from .assembly import OperatorSpec, build_spec
+from .basis import ElementOperators
+from .pde import FourierModes, GaussianBump
+
+__all__ = ["DeviceSolver", "IterResult"]
+
+
+def _torch():
+    import torch
+
+    if not torch.cuda.is_available():
+        raise N.NativeUnavailable("no CUDA device: the iHDG sweep has no CPU fallback")
+    return torch
+
+
+def _ptr(t) -> int:
+    return 0 if t is None else int(t.data_ptr())
+
+
+@dataclass
+class IterResult:
+    iterations: int
+    status: str
+    norms: np.ndarray
+    first_norm: float
+    last_norm: float
+    launched: int
+    seconds: float
+
+
+class DeviceSolver:
+    """Factor-once local operators + ping-pong iterate buffers on one GPU.
+
+    ``layers`` = (begin, end) range of the slowest axis owned by this rank
+    (strip partition); default the whole mesh.
+    """
+
+    def __init__(self, mesh, problem, ops: ElementOperators, dt=None, layers=None,
+                 device=None, max_iters: int = 100000, spec: Optional[OperatorSpec] = None):
+        torch = _torch()
+        L = N.lib()
+        self.torch = torch
+        self.L = L
+        self.mesh, self.problem, self.ops, self.dt = mesh, problem, ops, dt
+        self.spec = spec if spec is not None else build_spec(mesh, problem, ops, dt)
+        sp = self.spec
+        d = mesh.dim
+        if not L.ihdg_supported(d, ops.p, sp.ncomp):
+            raise NotImplementedError(f"no sweep kernel for dim={d}, p={ops.p}, m={sp.ncomp}")
+        self.device = torch.device("cuda", torch.cuda.current_device() if device is None else device)
+        nlay = mesh.cells[d - 1]
+        lb, le = (0, nlay) if layers is None else (int(layers[0]), int(layers[1]))
+        self.layers = (lb, le)
+        g = N.Geom()
+        g.dim, g.order, g.ncomp = d, ops.p, sp.ncomp
+        for a in range(3):
+            g.cells[a] = mesh.cells[a] if a < d else 1
+            g.periodic[a] = int(mesh.periodic[a]) if a < d else 0
+        g.layer_begin, g.layer_end = lb, le
+        self.geom = g
+        self.ls = int(np.prod(mesh.cells[: d - 1])) if d > 1 else 1
+        self.nloc = (le - lb) * self.ls
+        self.nv = sp.nv
+        self.np_ = sp.n_nodes
+        self.ntiles = int(L.ihdg_tile_count(C.byref(g)))
+        if self.ntiles < 1:
+            raise RuntimeError("ihdg_tile_count failed")
+        self.max_iters = int(max_iters)
+        dev = self.device
+        f64 = torch.float64
+        with torch.cuda.device(dev):
+            self.stream = torch.cuda.current_stream(dev)
+            self._assemble()
+            npad = self.nloc + 2 * self.ls
+            self.u = [torch.zeros((npad, self.nv), dtype=f64, device=dev) for _ in range(2)]
+            self.cur = 0
+            self.s = torch.zeros((self.nloc, self.nv), dtype=f64, device=dev)
+            self.s_static = None
+            self.partials = torch.zeros(self.ntiles, dtype=f64, device=dev)
+            self.state_dev = torch.zeros(C.sizeof(N.IterState), dtype=torch.uint8, device=dev)
+            self.norm_hist = torch.zeros(self.max_iters, dtype=f64, device=dev)
+            self.chol = torch.as_tensor(ops.chol1d.copy(), dtype=f64, device=dev)
+            self.class_of_mask = torch.as_tensor(sp.class_of_mask, device=dev)
+
+    # -- setup -------------------------------------------------------------
+    @property
+    def _sptr(self):
+        return C.c_void_p(self.stream.cuda_stream)
+
+    def _assemble(self):
+        torch, sp, dev, f64 = self.torch, self.spec, self.device, self.torch.float64
+        nc, nv, kin, nr = sp.n_class, sp.nv, sp.kin, sp.nr
+        self._ops1d = torch.as_tensor(sp.ops1d, dtype=f64, device=dev).contiguous()
+        self._opn = torch.as_tensor(sp.op_ncols, device=dev)
+        self._terms = torch.as_tensor(sp.terms, device=dev).contiguous()
+        self._coefs = torch.as_tensor(sp.coefs, dtype=f64, device=dev)
+        self.A = torch.zeros((nc, nv, nv), dtype=f64, device=dev)
+        self.Ainv = torch.zeros_like(self.A)
+        self.AinvT = torch.zeros_like(self.A)
+        self.B = torch.zeros((nc, nv, kin), dtype=f64, device=dev)
+        self.R = torch.zeros((nc, nv, max(nr, 1)), dtype=f64, device=dev)
+        self.LT = torch.zeros((nc, kin, nv), dtype=f64, device=dev)
+        self.PT = torch.zeros((nc, max(nr, 1), nv), dtype=f64, device=dev)
+        self.min_pivot = torch.zeros(nc, dtype=f64, device=dev)
+        a = N.AssemblyArgs()
+        a.dim, a.order, a.ncomp, a.n_class = sp.dim, sp.order, sp.ncomp, nc
+        a.n_ops, a.n_terms, a.nr = sp.ops1d.shape[0], sp.terms.shape[0], nr
+        a.ops1d, a.op_ncols = _ptr(self._ops1d), _ptr(self._opn)
+        a.terms, a.coefs = _ptr(self._terms), _ptr(self._coefs)
+        a.A, a.Ainv, a.AinvT, a.B = _ptr(self.A), _ptr(self.Ainv), _ptr(self.AinvT), _ptr(self.B)
+        a.R = _ptr(self.R) if nr > 0 else 0
+        a.LT = _ptr(self.LT)
+        a.PT = _ptr(self.PT) if nr > 0 else 0
+        a.min_pivot = _ptr(self.min_pivot)
+        N.check(self.L.ihdg_assemble(C.byref(a), self._sptr), "ihdg_assemble")
+        piv = self.min_pivot.cpu().numpy()
+        scale = self.A.abs().amax(dim=(1, 2)).cpu().numpy()
+        bad = np.nonzero(~(piv > 1e-13 * scale))[0]
+        if bad.size:
+            c = int(bad[0])
+            raise np.linalg.LinAlgError(
+                f"singular local matrix in operator class {c} (boundary mask {sp.class_masks[c]}): "
+                f"min pivot {piv[c]:.3e}, max |A| {scale[c]:.3e}")
+
+    # -- state -------------------------------------------------------------
+    def interior(self, which=None):
+        t = self.u[self.cur if which is None else which]
+        return t[self.ls: self.ls + self.nloc]
+
+    def set_state(self, data) -> None:
+        """Host (nloc, m, Np) array (or device tensor) -> current iterate."""
+        torch = self.torch
+        t = self.interior()
+        src = torch.as_tensor(np.ascontiguousarray(data, dtype=np.float64)) if isinstance(data, np.ndarray) else data
+        t.copy_(src.reshape(self.nloc, self.nv), non_blocking=False)
+        self.u[self.cur][: self.ls].zero_()
+        self.u[self.cur][self.ls + self.nloc:].zero_()
+
+    def zero_state(self) -> None:
+        self.u[self.cur].zero_()
+
+    def get_state(self) -> np.ndarray:
+        return self.interior().reshape(self.nloc, self.spec.ncomp, self.np_).cpu().numpy()
+
+    def _field_args(self, field, ref1d_t, out, out_stride, out_offset, out_ghost):
+        a = N.FieldArgs()
+        a.g = self.geom
+        for i in range(self.mesh.dim):
+            a.lo[i] = float(self.mesh.lo[i])
+            a.h[i] = float(self.mesh.h[i])
+        params = self.torch.as_tensor(field.device_params(), dtype=self.torch.float64, device=self.device)
+        a.ref1d, a.params, a.out = _ptr(ref1d_t), _ptr(params), _ptr(out)
+        a.out_stride, a.out_offset, a.out_ghost = out_stride, out_offset, out_ghost
+        a.npts1d = ref1d_t.numel()
+        a.kind = 0 if isinstance(field, FourierModes) else 1
+        a.nmodes = params.shape[0]
+        return a, params
+
+    def set_state_component(self, field, comp: int) -> None:
+        """Nodal interpolation (project) of an analytic field into one component."""
+        torch = self.torch
+        if isinstance(field, (FourierModes, GaussianBump)):
+            ref = torch.as_tensor(self.ops.nodes, dtype=torch.float64, device=self.device)
+            a, keep = self._field_args(field, ref, self.u[self.cur], self.nv, comp * self.np_, 1)
+            N.check(self.L.ihdg_eval_field(C.byref(a), self._sptr), "ihdg_eval_field")
+            torch.cuda.current_stream(self.device).synchronize()
+        else:
+            pts = self._local_points(self.ops.nodes)
+            vals = np.asarray(field(pts.reshape(-1, self.mesh.dim)), dtype=float).reshape(self.nloc, self.np_)
+            self.interior().view(self.nloc, self.spec.ncomp, self.np_)[:, comp, :].copy_(
+                torch.as_tensor(vals, device=self.device))
+
+    def _local_points(self, ref):
+        pts = self.mesh.all_element_points([ref] * self.mesh.dim)
+        lb, le = self.layers
+        return pts[lb * self.ls: le * self.ls]
+
+    def set_forcing(self, forcing) -> None:
+        """Static RHS part s_f = A^-1 (f, v)_K."""
+        torch, sp, ops = self.torch, self.spec, self.ops
+        nq = ops.quad_points.size
+        d = self.mesh.dim
+        fq = torch.zeros((self.nloc, nq ** d), dtype=torch.float64, device=self.device)
+        if isinstance(forcing, (FourierModes, GaussianBump)):
+            ref = torch.as_tensor(ops.quad_points, dtype=torch.float64, device=self.device)
+            a, keep = self._field_args(forcing, ref, fq, nq ** d, 0, 0)
+            N.check(self.L.ihdg_eval_field(C.byref(a), self._sptr), "ihdg_eval_field")
+        else:
+            pts = self._local_points(ops.quad_points)
+            vals = np.asarray(forcing(pts.reshape(-1, d)), dtype=float).reshape(self.nloc, -1)
+            fq.copy_(torch.as_tensor(vals, device=self.device))
+        b = torch.zeros((self.nloc, self.nv), dtype=torch.float64, device=self.device)
+        Bq = torch.as_tensor(ops.quad_to_rhs, dtype=torch.float64, device=self.device).contiguous()
+        q = N.QuadArgs()
+        q.g = self.geom
+        q.Bq, q.fq, q.out = _ptr(Bq), _ptr(fq), _ptr(b)
+        q.out_stride, q.out_offset, q.nq, q.jac = self.nv, sp.forcing_comp * self.np_, nq, sp.jac
+        N.check(self.L.ihdg_quad_project(C.byref(q), self._sptr), "ihdg_quad_project")
+        self.s_static = torch.zeros((self.nloc, self.nv), dtype=torch.float64, device=self.device)
+        self._apply(self.AinvT, self.nv, b, self.nv, 0, 0, self.s_static, 0)
+        self.stream.synchronize()
+
+    def _apply(self, opT, ncols, inp, in_stride, in_offset, in_ghost, out, accumulate):
+        a = N.ClassApplyArgs()
+        a.g = self.geom
+        a.opT, a.class_of_mask, a.inp, a.out = _ptr(opT), _ptr(self.class_of_mask), _ptr(inp), _ptr(out)
+        a.in_stride, a.in_offset, a.ncols = in_stride, in_offset, ncols
+        a.in_ghost, a.out_ghost, a.accumulate = in_ghost, 0, accumulate
+        N.check(self.L.ihdg_class_apply(C.byref(a), self._sptr), "ihdg_class_apply")
+
+    def prepare_steady(self) -> None:
+        """s = A^-1 b (forcing) or 0."""
+        if self.s_static is None:
+            self.s.zero_()
+        else:
+            self.s.copy_(self.s_static)
+
+    def begin_step(self) -> None:
+        """Backward-Euler RHS of the next step from the current state u^m (K4)."""
+        sp = self.spec
+        if sp.nr == 0:
+            raise RuntimeError("problem was assembled without a time step")
+        if self.s_static is not None:
+            self.s.copy_(self.s_static)
+            acc = 1
+        else:
+            acc = 0
+        self._apply(self.PT, sp.nr, self.u[self.cur], self.nv, sp.time_comp0 * self.np_, 1, self.s, acc)
+
+    # -- iteration ---------------------------------------------------------
+    def sweep_args(self, norm: str, finalize: int = 1) -> N.SweepArgs:
+        sp = self.spec
+        a = N.SweepArgs()
+        a.g = self.geom
+        a.s, a.LT = _ptr(self.s), _ptr(self.LT)
+        a.class_of_mask, a.chol1d = _ptr(self.class_of_mask), _ptr(self.chol)
+        a.tile_partials, a.state, a.norm_hist = _ptr(self.partials), _ptr(self.state_dev), _ptr(self.norm_hist)
+        for f in range(6):
+            for c in range(4):
+                a.face_w[f][c] = float(sp.face_w[f, c])
+                a.out_w[f][c] = float(sp.out_w[f, c])
+            a.coupled[f] = int(sp.coupled[f])
+            a.out_face[f] = int(sp.out_face[f])
+        for c in range(4):
+            a.comp_w[c] = float(sp.comp_w[c])
+        a.jac = sp.jac
+        for i in range(3):
+            a.jac_face[i] = float(sp.jac_face[i])
+        a.norm_kind = N.NORM_TRACE if norm == "trace" else N.NORM_VOLUME
+        a.finalize = finalize
+        a.tile_offset = 0
+        return a
+
+    def reset_state(self, tol: float, max_iters: int, diverge_factor: float = 1e6) -> None:
+        st = N.IterState()
+        st.status, st.iters, st.max_iters, st.ticket = N.RUNNING, 0, min(int(max_iters), self.max_iters), 0
+        st.tol, st.first_norm, st.last_norm, st.diverge_factor = tol, 0.0, 0.0, diverge_factor
+        host = self.torch.frombuffer(bytearray(bytes(st)), dtype=self.torch.uint8)
+        self.state_dev.copy_(host)
+
+    def read_state(self) -> N.IterState:
+        raw = bytes(self.state_dev.cpu().numpy().tobytes())
+        return N.IterState.from_buffer_copy(raw)
+
+    def iterate(self, tol: float = 1e-10, max_iters: int = 10000, norm: str = "volume",
+                batch: int = 16) -> IterResult:
+        """Algorithm 1 from the current iterate until the
+        stopping rule holds; the latest iterate becomes current."""
+        self.reset_state(tol, max_iters)
+        a = self.sweep_args(norm, finalize=1)
+        out = N.IterState()
+        nl = C.c_int64(0)
+        b0, b1 = self.u[self.cur], self.u[1 - self.cur]
+        t0 = time.perf_counter()
+        N.check(self.L.ihdg_iterate(C.byref(a), _ptr(b0), _ptr(b1), int(batch), self._sptr,
+                                    C.byref(out), C.byref(nl)), "ihdg_iterate")
+        sec = time.perf_counter() - t0
+        self.cur = (self.cur + out.iters) % 2
+        it = out.iters
+        norms = self.norm_hist[:it].cpu().numpy().copy()
+        return IterResult(it, N.STATUS_NAMES[out.status], norms, out.first_norm, out.last_norm,
+                          int(nl.value), sec)
+
+    def sweep_once(self, norm: str = "volume", finalize: int = 1, a: Optional[N.SweepArgs] = None):
+        """One sweep from the current iterate (used by the bench and multi-rank driver)."""
+        if a is None:
+            a = self.sweep_args(norm, finalize)
+        a.u_old, a.u_new = _ptr(self.u[self.cur]), _ptr(self.u[1 - self.cur])
+        N.check(self.L.ihdg_sweep(C.byref(a), self._sptr), "ihdg_sweep")
+        self.cur = 1 - self.cur
+
+    # -- output ------------------------------------------------------------
+    def trace(self) -> np.ndarray:
+        """Single-valued trace (n_faces, 1, N_f) in mesh.py face order."""
+        if self.layers != (0, self.mesh.cells[self.mesh.dim - 1]):
+            raise NotImplementedError("trace of a partitioned mesh: gather the state first")
+        sp = self.spec
+        nf = sp.n1 ** (self.mesh.dim - 1)
+        out = self.torch.zeros((self.mesh.n_faces, nf), dtype=self.torch.float64, device=self.device)
+        a = N.TraceArgs()
+        a.g = self.geom
+        a.u, a.trace = _ptr(self.u[self.cur]), _ptr(out)
+        for ax in range(3):
+            for c in range(4):
+                a.w_int_own[ax][c] = float(sp.trace_w["int_own"][ax, c])
+                a.w_int_nbr[ax][c] = float(sp.trace_w["int_nbr"][ax, c])
+                a.w_lo[ax][c] = float(sp.trace_w["lo"][ax, c])
+                a.w_hi[ax][c] = float(sp.trace_w["hi"][ax, c])
+        N.check(self.L.ihdg_extract_trace(C.byref(a), self._sptr), "ihdg_extract_trace")
+        return out.cpu().numpy().reshape(self.mesh.n_faces, 1, nf)
+
+
+class DistributedSweeper:
+    """Strip-partitioned iHDG-II over torch.distributed ranks (one GPU each).
+
+    Per sweep: halo exchange of the boundary layers (NCCL send/recv over
+    NVLink), the fused sweep kernel with finalize off, an all-gather of the
+    tile partials, and the fixed-order finalize on every rank, so every rank
+    derives the same device-side convergence flag.
+    """
+
+    def __init__(self, solver: DeviceSolver, rank: int, world: int, group=None):
+        self.sv, self.rank, self.world, self.group = solver, rank, world, group
+        torch = solver.torch
+        self.ntiles_rank = solver.ntiles
+        self.global_partials = torch.zeros(self.ntiles_rank * world, dtype=torch.float64,
+                                           device=solver.device)
+        self.periodic_last = bool(solver.mesh.periodic[solver.mesh.dim - 1])
+        self.nlay = solver.layers[1] - solver.layers[0]
+
+    def _exchange(self):
+        from .partition import halo_exchange
+
+        sv = self.sv
+        halo_exchange(sv.u[sv.cur], sv.ls, self.nlay, self.rank, self.world, self.periodic_last,
+                      self.group)
+
+    def sweep(self, a: N.SweepArgs) -> None:
+        import torch.distributed as dist
+
+        sv = self.sv
+        self._exchange()
+        a.u_old, a.u_new = _ptr(sv.u[sv.cur]), _ptr(sv.u[1 - sv.cur])
+        N.check(sv.L.ihdg_sweep(C.byref(a), sv._sptr), "ihdg_sweep")
+        dist.all_gather_into_tensor(self.global_partials, sv.partials, group=self.group)
+        f = N.FinalizeArgs()
+        f.tile_partials, f.n_tiles = _ptr(self.global_partials), self.global_partials.numel()
+        f.state, f.norm_hist = _ptr(sv.state_dev), _ptr(sv.norm_hist)
+        N.check(sv.L.ihdg_finalize(C.byref(f), sv._sptr), "ihdg_finalize")
+        sv.cur = 1 - sv.cur
+
+    def iterate(self, tol=1e-10, max_iters=10000, norm="volume", batch=16) -> IterResult:
+        sv = self.sv
+        sv.reset_state(tol, max_iters)
+        a = sv.sweep_args(norm, finalize=0)
+        start = sv.cur
+        launched = 0
+        t0 = time.perf_counter()
+        while True:
+            for _ in range(batch):
+                self.sweep(a)
+                launched += 1
+            st = sv.read_state()
+            if st.status != N.RUNNING:
+                break
+        sec = time.perf_counter() - t0
+        sv.cur = (start + st.iters) % 2
+        norms = sv.norm_hist[: st.iters].cpu().numpy().copy()
+        return IterResult(st.iters, N.STATUS_NAMES[st.status], norms, st.first_norm, st.last_norm,
+                          launched, sec)

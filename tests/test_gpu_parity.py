@@ -1,0 +1,174 @@
+"""Parity of the sm_100a sweep (through the C-ABI) with the CPU oracle.
+
+Bar (BASELINE.json north_star): the same iteration count to convergence and
+volume / trace fields within 1e-10 relative L2 in fp64.
+"""
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+TOL_FIELD = 1e-10
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _gpu():
+    import torch
+
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    torch.cuda.set_device(0)
+
+
+def _wl(cfg, **kw):
+    from paper_1711_01175_b200.workloads import make_config
+
+    return make_config(cfg, seed=kw.pop("seed", 0), **kw)
+
+
+def _steady(wl, stop):
+    from paper_1711_01175_b200.iteration import IterationConfig, run
+    from tests.oracle_bridge import oracle_solver
+
+    rep = run(wl.mesh, wl.problem, wl.ops, IterationConfig(stop=stop, tol=1e-10))
+    S = oracle_solver(wl)
+    ref = S.run(norm="trace" if stop == "trace" else "volume", tol=1e-10)
+    return rep, S, ref
+
+
+def _unsteady(wl):
+    from paper_1711_01175_b200.iteration import IterationConfig, run_time_dependent
+    from tests.oracle_bridge import oracle_initial, oracle_solver
+
+    reps = run_time_dependent(wl.mesh, wl.problem, wl.ops, IterationConfig(tol=1e-10), wl.dt,
+                              n_steps=wl.n_steps, initial=wl.initial, keep_states=True)
+    S = oracle_solver(wl)
+    u_end, refs = S.run_time_dependent(oracle_initial(wl, S), wl.n_steps, tol=1e-10)
+    return reps, S, refs
+
+
+def test_config1_full_size_parity():
+    from tests.oracle_bridge import rel_l2
+
+    wl = _wl(1)
+    rep, S, ref = _steady(wl, "trace")
+    assert rep.status == ref["status"] == "converged"
+    assert rep.iterations == ref["iterations"] == 2 * 16  # 2N-1 layers + detection sweep
+    assert rel_l2(rep.state.data.reshape(S.nel, -1), ref["u"]) < TOL_FIELD
+    assert rel_l2(rep.trace, S.trace(ref["u"])) < TOL_FIELD
+    assert np.allclose(rep.successive_norms, ref["norms"], rtol=1e-8, atol=1e-300)
+
+
+def test_config1_volume_rule():
+    from tests.oracle_bridge import rel_l2
+
+    wl = _wl(1, seed=3)
+    rep, S, ref = _steady(wl, "successive")
+    assert rep.iterations == ref["iterations"]
+    assert rel_l2(rep.state.data.reshape(S.nel, -1), ref["u"]) < TOL_FIELD
+
+
+@pytest.mark.parametrize("cells,steps", [(16, 2), (24, 1)])
+def test_config2_reduced_parity(cells, steps):
+    from tests.oracle_bridge import rel_l2
+
+    wl = _wl(2, cells=cells, n_steps=steps)
+    reps, S, refs = _unsteady(wl)
+    assert [r.iterations for r in reps] == [r["iterations"] for r in refs]
+    assert all(r.status == "converged" for r in reps)
+    for r, o in zip(reps, refs):
+        assert rel_l2(r.state.data.reshape(S.nel, -1), o["u"]) < TOL_FIELD
+
+
+def test_config3_reduced_parity():
+    from tests.oracle_bridge import rel_l2
+
+    wl = _wl(3, cells=16, n_steps=2)
+    reps, S, refs = _unsteady(wl)
+    assert [r.iterations for r in reps] == [r["iterations"] for r in refs]
+    for r, o in zip(reps, refs):
+        assert rel_l2(r.state.data.reshape(S.nel, -1), o["u"]) < TOL_FIELD
+
+
+def test_config4_reduced_parity():
+    from tests.oracle_bridge import rel_l2
+
+    wl = _wl(4, cells=8)
+    rep, S, ref = _steady(wl, "successive")
+    assert rep.iterations == ref["iterations"] == 3 * 7 + 1 + 1
+    assert rel_l2(rep.state.data.reshape(S.nel, -1), ref["u"]) < TOL_FIELD
+    assert rel_l2(rep.trace, S.trace(ref["u"])) < TOL_FIELD
+
+
+@pytest.mark.parametrize("kappa", [1e-1, 1e-3])
+def test_config5_reduced_parity(kappa):
+    from tests.oracle_bridge import rel_l2
+
+    wl = _wl(5, cells=32, kappa=kappa, n_steps=1)
+    reps, S, refs = _unsteady(wl)
+    assert [r.iterations for r in reps] == [r["iterations"] for r in refs]
+    for r, o in zip(reps, refs):
+        assert rel_l2(r.state.data.reshape(S.nel, -1), o["u"]) < TOL_FIELD
+
+
+def test_device_assembly_matches_host_terms():
+    """K1 (device Kronecker assembly + Gauss-Jordan) vs numpy."""
+    from paper_1711_01175_b200.assembly import evaluate_terms
+    from paper_1711_01175_b200.solver import DeviceSolver
+
+    wl = _wl(5, cells=8, kappa=1e-1)
+    ds = DeviceSolver(wl.mesh, wl.problem, wl.ops, dt=wl.dt)
+    A, B, R = evaluate_terms(ds.spec)
+    Ad = ds.A.cpu().numpy()
+    assert np.max(np.abs(Ad - A)) <= 1e-14 * np.max(np.abs(A))
+    Ai = np.linalg.inv(A)
+    Aid = ds.Ainv.cpu().numpy()
+    assert np.max(np.abs(Aid - Ai)) <= 1e-10 * np.max(np.abs(Ai))
+    L = np.einsum("cij,cjk->cik", Ai, B)
+    assert np.max(np.abs(ds.LT.cpu().numpy().transpose(0, 2, 1) - L)) <= 1e-10 * np.max(np.abs(L))
+
+
+def test_zero_problem_one_iteration():
+    """f = 0, g = 0, zero initial guess -> 1 iteration, zero solution."""
+    from paper_1711_01175_b200.basis import build_operators
+    from paper_1711_01175_b200.iteration import IterationConfig, run
+    from paper_1711_01175_b200.mesh import build_mesh
+    from paper_1711_01175_b200.pde import TransportProblem
+
+    mesh = build_mesh(2, [8, 8])
+    rep = run(mesh, TransportProblem(beta=np.array([1.0, 1.0])), build_operators(2, 2, mesh.h),
+              IterationConfig())
+    assert rep.iterations == 1 and rep.status == "converged"
+    assert np.all(rep.state.data == 0.0)
+
+
+def test_repeat_is_bit_identical():
+    from paper_1711_01175_b200.iteration import IterationConfig, run
+
+    wl = _wl(1, seed=7)
+    r1 = run(wl.mesh, wl.problem, wl.ops, IterationConfig(stop="trace"))
+    r2 = run(wl.mesh, wl.problem, wl.ops, IterationConfig(stop="trace"))
+    assert r1.iterations == r2.iterations
+    assert np.array_equal(r1.state.data, r2.state.data)
+    assert np.array_equal(r1.successive_norms, r2.successive_norms)
+
+
+def test_max_iter_status():
+    from paper_1711_01175_b200.iteration import IterationConfig, run
+
+    wl = _wl(1)
+    rep = run(wl.mesh, wl.problem, wl.ops, IterationConfig(stop="trace", max_iters=5))
+    assert rep.status == "max-iter" and rep.iterations == 5
+
+
+def test_config4_full_size_layer_count():
+    """64^3: 3*63+1 = 190 layers (PAPER.md:1426 reports 190) + 1 detection sweep;
+    the last successive difference is exactly zero (bitwise fixed point)."""
+    from paper_1711_01175_b200.iteration import IterationConfig, run
+
+    wl = _wl(4)
+    rep = run(wl.mesh, wl.problem, wl.ops, IterationConfig(), return_trace=False)
+    assert rep.status == "converged"
+    assert rep.iterations == 191
+    assert rep.successive_norms[-1] == 0.0 and rep.successive_norms[-2] > 0.0
