@@ -248,6 +248,9 @@ int ihdg_class_apply(const ihdg_class_apply_args* a, void* stream);
 int ihdg_eval_field(const ihdg_field_args* a, void* stream);
 int ihdg_quad_project(const ihdg_quad_args* a, void* stream);
 int ihdg_sweep(const ihdg_sweep_args* a, void* stream);
+/* 1 if ihdg_sweep would use the streaming (TMA bulk-copy) kernel for these
+ * args, 0 if it falls back to the generic kernel */
+int ihdg_stream_variant(const ihdg_sweep_args* a);
 int ihdg_finalize(const ihdg_finalize_args* a, void* stream);
 int ihdg_extract_trace(const ihdg_trace_args* a, void* stream);
 /* copy the ghost-padded layer range between two buffers (initial guess) */

@@ -102,6 +102,7 @@ SIGNATURES = {
     "ihdg_eval_field": (_i32, [C.POINTER(FieldArgs), _p]),
     "ihdg_quad_project": (_i32, [C.POINTER(QuadArgs), _p]),
     "ihdg_sweep": (_i32, [C.POINTER(SweepArgs), _p]),
+    "ihdg_stream_variant": (_i32, [C.POINTER(SweepArgs)]),
     "ihdg_finalize": (_i32, [C.POINTER(FinalizeArgs), _p]),
     "ihdg_extract_trace": (_i32, [C.POINTER(TraceArgs), _p]),
     "ihdg_copy_state": (_i32, [C.POINTER(Geom), _p, _p, _p]),

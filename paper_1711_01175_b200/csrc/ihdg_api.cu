@@ -7,6 +7,8 @@
 
 using namespace ihdg;
 
+int ihdg_stream_launch(const ihdg_sweep_args* a, cudaStream_t st);
+
 namespace {
 
 thread_local std::string g_err;
@@ -242,13 +244,20 @@ int ihdg_quad_project(const ihdg_quad_args* a, void* stream) {
   return check_launch("k_quad_project");
 }
 
+static int do_sweep(const Entry* e, const ihdg_sweep_args* a, cudaStream_t st) {
+  const int rc = ihdg_stream_launch(a, st);
+  if (rc == 1) return IHDG_OK;
+  if (rc < 0) return check_launch("k_sweep_stream");
+  return e->sweep(a, st);
+}
+
 int ihdg_sweep(const ihdg_sweep_args* a, void* stream) {
   if (a == nullptr) return set_err(IHDG_ERR_ARG, "null args");
   int rc = check_geom(a->g);
   if (rc) return rc;
   const Entry* e = find_entry(a->g.dim, a->g.order, a->g.ncomp);
   if (e == nullptr) return set_err(IHDG_ERR_UNSUPPORTED, "no kernel instantiated for this (dim, order, ncomp)");
-  return e->sweep(a, (cudaStream_t)stream);
+  return do_sweep(e, a, (cudaStream_t)stream);
 }
 
 int ihdg_finalize(const ihdg_finalize_args* a, void* stream) {
@@ -298,7 +307,7 @@ int ihdg_iterate(const ihdg_sweep_args* a0, double* buf0, double* buf1, int32_t 
     for (int j = 0; j < batch; ++j) {
       a.u_old = (launched & 1) ? buf1 : buf0;
       a.u_new = (launched & 1) ? buf0 : buf1;
-      rc = e->sweep(&a, st);
+      rc = do_sweep(e, &a, st);
       if (rc) return rc;
       ++launched;
     }

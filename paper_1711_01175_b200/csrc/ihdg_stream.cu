@@ -1,0 +1,97 @@
+// Instantiations + dispatch of the streaming sweep (ihdg_stream.cuh).
+#include <cstdlib>
+#include <cstring>
+#include <string>
+
+#include "ihdg_stream.cuh"
+
+namespace ihdg {
+
+int stream_sms() {
+  static int sms = 0;
+  if (sms == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (sms <= 0) sms = 148;
+  }
+  return sms;
+}
+
+template <int D, int N1, int M, int NCF, int NWC, int E, int NS, int G>
+int launch_stream_t(const ihdg_sweep_args* a, cudaStream_t st) {
+  using C = SCfg<D, N1, M, NCF, NWC, E, NS, G>;
+  static_assert(E == Cfg<D, N1, M>::TE, "stream tile must equal the generic tile (tile partial count)");
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(k_sweep_stream<D, N1, M, NCF, NWC, E, NS, G>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::BYTES);
+    if (e != cudaSuccess) return -2;
+    configured = true;
+  }
+  Geo geo;
+  geo.init(a->g, E);
+  int64_t grid = geo.ntiles < stream_sms() ? geo.ntiles : stream_sms();
+  if (grid < 1) grid = 1;
+  k_sweep_stream<D, N1, M, NCF, NWC, E, NS, G><<<(unsigned)grid, C::NT, C::BYTES, st>>>(*a);
+  return cudaGetLastError() == cudaSuccess ? 0 : -2;
+}
+
+struct StreamEntry {
+  int D, N1, M, NCF, NWC, E, NV;
+  int (*launch)(const ihdg_sweep_args*, cudaStream_t);
+};
+
+#define IHDG_STREAM(D, N1, M, NCF, NWC, E, NS, G) \
+  {D, N1, M, NCF, NWC, E, M * Pow<N1, D>::v, launch_stream_t<D, N1, M, NCF, NWC, E, NS, G>},
+
+const StreamEntry kStream[] = {
+    IHDG_STREAM(2, 7, 3, 4, 2, 16, 3, 2)   // config 5: CD 2D p=6
+    IHDG_STREAM(2, 5, 3, 4, 2, 16, 4, 4)   // configs 2/3: CD / SW 2D p=4
+    IHDG_STREAM(3, 4, 1, 3, 1, 32, 3, 4)   // config 4: transport 3D p=3
+};
+
+// Returns the entry usable for these args, or nullptr (generic kernel).
+const StreamEntry* stream_entry(const ihdg_sweep_args* a) {
+  static int forced_generic = -1;
+  if (forced_generic < 0) {
+    const char* s = std::getenv("IHDG_SWEEP_IMPL");
+    forced_generic = (s != nullptr && std::strcmp(s, "generic") == 0) ? 1 : 0;
+  }
+  if (forced_generic) return nullptr;
+  if (a->norm_kind != IHDG_NORM_VOLUME) return nullptr;
+  const ihdg_geom& g = a->g;
+  int ncf = 0, maxw = 0;
+  for (int f = 0; f < 2 * g.dim; ++f) {
+    if (!a->coupled[f]) continue;
+    ++ncf;
+    int w = 0;
+    for (int c = 0; c < g.ncomp; ++c) w += a->face_w[f][c] != 0.0;
+    maxw = w > maxw ? w : maxw;
+  }
+  for (const StreamEntry& e : kStream) {
+    if (e.D != g.dim || e.N1 != g.order + 1 || e.M != g.ncomp) continue;
+    if (e.NCF != ncf || maxw > e.NWC) continue;
+    Geo geo;
+    geo.init(g, e.E);
+    if (geo.tile_len % e.E != 0) continue;                       // full tiles only
+    if ((geo.ls * e.NV * 8) % 16 != 0) continue;                  // ghost offset
+    if (((uintptr_t)a->u_old | (uintptr_t)a->u_new | (uintptr_t)a->s) % 16 != 0) continue;
+    return &e;
+  }
+  return nullptr;
+}
+
+}  // namespace ihdg
+
+// 1 if the streaming kernel is used for these args, 0 for the generic one.
+int ihdg_stream_variant(const ihdg_sweep_args* a) { return ihdg::stream_entry(a) != nullptr ? 1 : 0; }
+
+// Launch the streaming kernel if applicable. Returns 1 launched, 0 not
+// applicable, <0 on launch error.
+int ihdg_stream_launch(const ihdg_sweep_args* a, cudaStream_t st) {
+  const ihdg::StreamEntry* e = ihdg::stream_entry(a);
+  if (e == nullptr) return 0;
+  int rc = e->launch(a, st);
+  return rc == 0 ? 1 : rc;
+}
