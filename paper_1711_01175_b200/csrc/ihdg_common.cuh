@@ -104,6 +104,59 @@ struct Geo {
   }
 };
 
+// Per-tile neighbour geometry for tiles that lie inside one axis-0 row
+// (requires cells[0] % TE == 0).  Everything the sweep needs per element is
+// derived from the first element with integer compares; the int64 div/mod
+// of Geo::multi_index runs once per tile instead of once per element-face.
+struct TileInfo {
+  int64_t e0;       // first local element
+  int nt;           // elements in the tile
+  int i0;           // axis-0 index of the first element
+  int c0;           // cells along axis 0
+  int per0;         // axis 0 periodic
+  int has[6];       // face f (axis >= 1) has a neighbour (uniform over the tile)
+  int64_t off[6];   // neighbour element offset for faces of axis >= 1
+
+  __device__ void init(const Geo& g, int64_t tile, int TE) {
+    g.tile_range(tile, TE, e0, nt);
+    int64_t idx[3];
+    g.multi_index(e0, idx);
+    i0 = (int)idx[0];
+    c0 = (int)g.c[0];
+    per0 = g.per[0];
+    for (int f = 0; f < 6; ++f) {
+      has[f] = 0;
+      off[f] = 0;
+    }
+    for (int f = 2; f < 2 * g.D; ++f) {
+      int64_t nb;
+      has[f] = g.neighbor(e0, idx, f, nb) ? 1 : 0;
+      off[f] = has[f] ? nb - e0 : 0;
+    }
+  }
+  // missing-neighbour mask of tile element t
+  __device__ int mask(int t, int D) const {
+    int m = 0;
+    const int i = i0 + t;
+    if (!per0) {
+      if (i == 0) m |= 1;
+      if (i == c0 - 1) m |= 2;
+    }
+    for (int f = 2; f < 2 * D; ++f)
+      if (!has[f]) m |= 1 << f;
+    return m;
+  }
+  // local index of the neighbour of tile element t across face f (valid only
+  // when the mask bit is clear)
+  __device__ int64_t nbr(int t, int f) const {
+    const int64_t e = e0 + t;
+    if (f >= 2) return e + off[f];
+    const int i = i0 + t;
+    if (f == 0) return i > 0 ? e - 1 : e + (c0 - 1);
+    return i < c0 - 1 ? e + 1 : e - (c0 - 1);
+  }
+};
+
 // Volume index of node n of local face f (tangential axes increasing, the
 // smallest fastest: mesh.py:166-187 shared ordering; nodes lexicographic with
 // axis 0 fastest: mesh.py:155-164).

@@ -75,6 +75,7 @@ const StreamEntry* stream_entry(const ihdg_sweep_args* a) {
     Geo geo;
     geo.init(g, e.E);
     if (geo.tile_len % e.E != 0) continue;                       // full tiles only
+    if (g.cells[0] % e.E != 0) continue;                         // tiles inside one axis-0 row
     if ((geo.ls * e.NV * 8) % 16 != 0) continue;                  // ghost offset
     if (((uintptr_t)a->u_old | (uintptr_t)a->u_new | (uintptr_t)a->s) % 16 != 0) continue;
     return &e;

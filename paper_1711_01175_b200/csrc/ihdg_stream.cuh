@@ -196,9 +196,10 @@ __global__ void __launch_bounds__(SCfg<D, N1, M, NCF, NWC, E, NS, G>::NT, 1)
       double* sst = sm + stage * C::STAGE;
       double* ust = sst + TILE;
       double* hst = ust + TILE;
-      int64_t e0;
-      int nt;
-      geo.tile_range(tile, E, e0, nt);
+      TileInfo ti;
+      ti.init(geo, tile, E);
+      const int64_t e0 = ti.e0;
+      const int nt = ti.nt;
       if (lane == 0) {
         const uint32_t bytes = (uint32_t)(nt * NV * sizeof(double));
         mbar_arrive_expect_tx(&full_bar[stage], 2 * bytes);
@@ -211,12 +212,8 @@ __global__ void __launch_bounds__(SCfg<D, N1, M, NCF, NWC, E, NS, G>::NT, 1)
         const int f = cf_s[ci];
         const bool axis0 = (f >> 1) == 0;
         if (axis0 && !((f == 0 && t == 0) || (f == 1 && t == nt - 1))) continue;
-        const int64_t e = e0 + t;
-        int64_t idx[3];
-        geo.multi_index(e, idx);
-        int64_t nb;
-        if (!geo.neighbor(e, idx, f, nb)) continue;
-        const double* src = uo + nb * NV;
+        if (ti.mask(t, D) & (1 << f)) continue;
+        const double* src = uo + ti.nbr(t, f) * NV;
         double* dst = hst + ((t * NCF + ci) * NWC) * NF;
 #pragma unroll
         for (int j = 0; j < NWC; ++j) {
@@ -244,19 +241,14 @@ __global__ void __launch_bounds__(SCfg<D, N1, M, NCF, NWC, E, NS, G>::NT, 1)
     for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
       const int stage = it % NS;
       const int ob = it & 1;
-      int64_t e0;
-      int nt;
-      geo.tile_range(tile, E, e0, nt);
+      TileInfo ti;
+      ti.init(geo, tile, E);
+      const int64_t e0 = ti.e0;
+      const int nt = ti.nt;
       if (tid < E) {
         int mask = 0, cls = -1;
         if (tid < nt) {
-          const int64_t e = e0 + tid;
-          int64_t idx[3];
-          geo.multi_index(e, idx);
-          for (int f = 0; f < NFACE; ++f) {
-            int64_t nb;
-            if (!geo.neighbor(e, idx, f, nb)) mask |= 1 << f;
-          }
+          mask = ti.mask(tid, D);
           cls = a.class_of_mask[mask];
         }
         mask_s[tid] = mask;
