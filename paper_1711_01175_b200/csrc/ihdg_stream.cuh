@@ -104,17 +104,17 @@ struct SCfg {
   static constexpr int HALO = E * NCF * NWC * NF;
   static constexpr int STAGE = 2 * TILE + HALO;
   // shared memory carve (doubles)
-  static constexpr int OFF_STAGE = 0;
   static constexpr int OFF_OUT = NS * STAGE;
   static constexpr int OFF_D = OFF_OUT + 2 * TILE;
   static constexpr int OFF_T = OFF_D + TILE;
   static constexpr int OFF_Q = OFF_T + TILE;
-  static constexpr int OFF_PART = OFF_Q + E * KC;
-  static constexpr int OFF_CHOL = OFF_PART + E;
-  static constexpr int N_DBL = OFF_CHOL + N1 * N1;
+  static constexpr int OFF_RED = OFF_Q + E * KC;
+  static constexpr int N_DBL = OFF_RED + 32;
   static constexpr size_t BYTES = (size_t)N_DBL * sizeof(double) + 2 * NS * sizeof(uint64_t);
   static_assert(EG % 4 == 0, "elements per group must be a multiple of 4");
   static_assert(KC % 2 == 0, "compacted neighbour count must be even");
+  static_assert(E <= 32, "one producer lane per tile element");
+  static_assert(KC <= RP, "q is computed by the first KC row threads");
   static_assert((TILE * sizeof(double)) % 16 == 0, "tile bytes must be 16-byte multiples");
 };
 
@@ -130,8 +130,7 @@ __global__ void __launch_bounds__(SCfg<D, N1, M, NCF, NWC, E, NS, G>::NT, 1)
   double* d_s = sm + C::OFF_D;
   double* t_s = sm + C::OFF_T;
   double* q_s = sm + C::OFF_Q;
-  double* part_s = sm + C::OFF_PART;
-  double* c_s = sm + C::OFF_CHOL;
+  double* red_s = sm + C::OFF_RED;
   uint64_t* full_bar = reinterpret_cast<uint64_t*>(sm + C::N_DBL);
   uint64_t* empty_bar = full_bar + NS;
 
@@ -139,9 +138,11 @@ __global__ void __launch_bounds__(SCfg<D, N1, M, NCF, NWC, E, NS, G>::NT, 1)
   __shared__ int cf_s[NCF];                 // coupled local faces
   __shared__ int wc_s[NCF][NWC];            // weighted components
   __shared__ double ww_s[NCF][NWC];         // their weights
-  __shared__ int mask_s[E];                 // missing-neighbour bits
-  __shared__ int cls_s[E];
-  __shared__ int fast_s;
+  __shared__ double chol_s[N1 * N1];
+  // per-stage tile metadata, written by the producer before its release-arrive
+  __shared__ long long me0_s[NS];
+  __shared__ int mnt_s[NS], mfast_s[NS];
+  __shared__ int mmask_s[NS][E], mcls_s[NS][E];
   __shared__ int last_s;
 
   ihdg_iter_state* st = a.state;
@@ -155,7 +156,7 @@ __global__ void __launch_bounds__(SCfg<D, N1, M, NCF, NWC, E, NS, G>::NT, 1)
   double* __restrict__ un = a.u_new + ls * NV;
 
   for (int i = tid; i < NFACE * NF; i += blockDim.x) fv_s[i / NF][i % NF] = face_node_vidx(D, N1, i / NF, i % NF);
-  for (int i = tid; i < N1 * N1; i += blockDim.x) c_s[i] = a.chol1d[i];
+  for (int i = tid; i < N1 * N1; i += blockDim.x) chol_s[i] = a.chol1d[i];
   if (tid == 0) {
     int n = 0;
     for (int f = 0; f < NFACE && n < NCF; ++f) {
@@ -184,7 +185,6 @@ __global__ void __launch_bounds__(SCfg<D, N1, M, NCF, NWC, E, NS, G>::NT, 1)
 
   const int fast_class = a.class_of_mask[0];
   const int64_t ntiles = geo.ntiles;
-  const uint32_t tile_bytes = (uint32_t)(TILE * sizeof(double));
 
   if (tid >= NC) {
     // ============================ producer warp ============================
@@ -200,27 +200,44 @@ __global__ void __launch_bounds__(SCfg<D, N1, M, NCF, NWC, E, NS, G>::NT, 1)
       ti.init(geo, tile, E);
       const int64_t e0 = ti.e0;
       const int nt = ti.nt;
+      // tile metadata for the consumers (mask of missing neighbours, class)
+      int cls = -1;
+      if (lane < E) {
+        int mask = 0;
+        if (lane < nt) {
+          mask = ti.mask(lane, D);
+          cls = a.class_of_mask[mask];
+        }
+        mmask_s[stage][lane] = mask;
+        mcls_s[stage][lane] = cls;
+      }
+      const int fast = __all_sync(0xffffffffu, lane >= nt || cls == fast_class);
+      if (lane == 0) {
+        me0_s[stage] = e0;
+        mnt_s[stage] = nt;
+        mfast_s[stage] = fast;
+      }
+      __syncwarp();
       if (lane == 0) {
         const uint32_t bytes = (uint32_t)(nt * NV * sizeof(double));
-        mbar_arrive_expect_tx(&full_bar[stage], 2 * bytes);
+        mbar_arrive_expect_tx(&full_bar[stage], 2 * bytes);  // release: metadata above
         bulk_g2s(sst, a.s + e0 * NV, bytes, &full_bar[stage]);
         bulk_g2s(ust, uo + e0 * NV, bytes, &full_bar[stage]);
       }
-      // neighbour face nodes that are not inside this tile
-      for (int p = lane; p < nt * NCF; p += 32) {
-        const int t = p / NCF, ci = p % NCF;
+      // neighbour face nodes that are not inside this tile; consecutive lanes
+      // take consecutive face nodes of one run (coalesced 8-byte cp.async)
+      constexpr int PER_T = NCF * NWC * NF;
+      for (int item = lane; item < nt * PER_T; item += 32) {
+        const int t = item / PER_T;
+        const int rem = item % PER_T;
+        const int ci = rem / (NWC * NF);
+        const int j = (rem / NF) % NWC;
+        const int n = rem % NF;
         const int f = cf_s[ci];
-        const bool axis0 = (f >> 1) == 0;
-        if (axis0 && !((f == 0 && t == 0) || (f == 1 && t == nt - 1))) continue;
+        if ((f >> 1) == 0 && !((f == 0 && t == 0) || (f == 1 && t == nt - 1))) continue;
         if (ti.mask(t, D) & (1 << f)) continue;
-        const double* src = uo + ti.nbr(t, f) * NV;
-        double* dst = hst + ((t * NCF + ci) * NWC) * NF;
-#pragma unroll
-        for (int j = 0; j < NWC; ++j) {
-          const double* sc = src + wc_s[ci][j] * NP;
-#pragma unroll
-          for (int n = 0; n < NF; ++n) cp_async8(dst + j * NF + n, sc + fv_s[f ^ 1][n]);
-        }
+        const double* src = uo + ti.nbr(t, f) * NV + wc_s[ci][j] * NP + fv_s[f ^ 1][n];
+        cp_async8(hst + item, src);
       }
       cp_async_arrive_noinc(&full_bar[stage]);
     }
@@ -230,106 +247,124 @@ __global__ void __launch_bounds__(SCfg<D, N1, M, NCF, NWC, E, NS, G>::NT, 1)
     const int g = tid / RP;
     const bool rv = r < NV;
     const int warp = tid >> 5, lane = tid & 31;
-    // lifted operator of the interior class, one row per thread, in registers
+    // per-thread constants: row r of the lifted operator, its node indices,
+    // the Cholesky coefficients of its node along each axis
     double Lr[KC];
 #pragma unroll
     for (int k = 0; k < KC; ++k) {
       const int col = cf_s[k / NF] * NF + (k % NF);
       Lr[k] = rv ? __ldg(a.LT + ((size_t)fast_class * (NFACE * NF) + col) * NV + r) : 0.0;
     }
+    const int rr = rv ? r : 0;
+    const int ncomp = rr / NP;
+    const int node = rr % NP;
+    const double cw = rv ? a.comp_w[ncomp] * a.jac : 0.0;
+    double cc[D][N1];
+    int co[D][N1];
+    {
+      int mul = 1;
+#pragma unroll
+      for (int ax = 0; ax < D; ++ax) {
+        const int ia = (node / mul) % N1;
+#pragma unroll
+        for (int k = 0; k < N1; ++k) {
+          const bool ok = ia + k < N1;
+          cc[ax][k] = ok ? chol_s[(ia + k) * N1 + ia] : 0.0;
+          co[ax][k] = ok ? k * mul : 0;
+        }
+        mul *= N1;
+      }
+    }
+    // q thread: row thread r < KC computes neighbour scalar k = r
+    const bool qv = r < KC;
+    const int qk = qv ? r : 0;
+    const int qci = qk / NF, qn = qk % NF;
+    const int qf = cf_s[qci];
+    const bool qaxis0 = (qf >> 1) == 0;
+    const int qsrc_tile = fv_s[qf ^ 1][qn];
+    double qw[NWC];
+    int qoff[NWC];
+#pragma unroll
+    for (int j = 0; j < NWC; ++j) {
+      qw[j] = ww_s[qci][j];
+      qoff[j] = wc_s[qci][j] * NP + qsrc_tile;
+    }
+
     int it = 0;
     for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
       const int stage = it % NS;
       const int ob = it & 1;
-      TileInfo ti;
-      ti.init(geo, tile, E);
-      const int64_t e0 = ti.e0;
-      const int nt = ti.nt;
-      if (tid < E) {
-        int mask = 0, cls = -1;
-        if (tid < nt) {
-          mask = ti.mask(tid, D);
-          cls = a.class_of_mask[mask];
-        }
-        mask_s[tid] = mask;
-        cls_s[tid] = cls;
-      }
       mbar_wait(&full_bar[stage], (it / NS) & 1);
       if (tid == 0 && it >= 2) bulk_wait_read<1>();
-      consumer_bar(NC);
-      if (tid == 0) {
-        int fast = 1;
-        for (int t = 0; t < nt; ++t) fast &= (cls_s[t] == fast_class);
-        fast_s = fast;
-      }
+      const int64_t e0 = me0_s[stage];
+      const int nt = mnt_s[stage];
+      const int fast = mfast_s[stage];
       const double* sst = sm + stage * C::STAGE;
       const double* ust = sst + TILE;
       const double* hst = ust + TILE;
       // ---- neighbour face scalars q[t][k] --------------------------------
-      for (int idx = tid; idx < E * KC; idx += NC) {
-        const int t = idx / KC, k = idx % KC;
-        const int ci = k / NF, n = k % NF;
-        const int f = cf_s[ci];
-        double v = 0.0;
-        if (t < nt && !(mask_s[t] & (1 << f))) {
-          const bool axis0 = (f >> 1) == 0;
-          const bool in_tile = axis0 && !((f == 0 && t == 0) || (f == 1 && t == nt - 1));
-          if (in_tile) {
-            const double* src = ust + (t + (f == 0 ? -1 : 1)) * NV + fv_s[f ^ 1][n];
+      if (qv) {
 #pragma unroll
-            for (int j = 0; j < NWC; ++j) v = fma(ww_s[ci][j], src[wc_s[ci][j] * NP], v);
-          } else {
-            const double* src = hst + ((t * NCF + ci) * NWC) * NF + n;
+        for (int tt = 0; tt < EG; ++tt) {
+          const int t = g * EG + tt;
+          double v = 0.0;
+          if (t < nt && !(mmask_s[stage][t] & (1 << qf))) {
+            const bool in_tile = qaxis0 && !((qf == 0 && t == 0) || (qf == 1 && t == nt - 1));
+            if (in_tile) {
+              const double* src = ust + (t + (qf == 0 ? -1 : 1)) * NV;
 #pragma unroll
-            for (int j = 0; j < NWC; ++j) v = fma(ww_s[ci][j], src[j * NF], v);
+              for (int j = 0; j < NWC; ++j) v = fma(qw[j], src[qoff[j]], v);
+            } else {
+              const double* src = hst + ((t * NCF + qci) * NWC) * NF + qn;
+#pragma unroll
+              for (int j = 0; j < NWC; ++j) v = fma(qw[j], src[j * NF], v);
+            }
           }
+          q_s[t * KC + qk] = v;
         }
-        q_s[idx] = v;
       }
       consumer_bar(NC);
       // ---- lifted local solve u^{k+1} = s + L q ---------------------------
       double* outb = out_s + ob * TILE;
       if (rv) {
-        if (fast_s) {
+        if (fast) {
 #pragma unroll
           for (int tb = 0; tb < EG; tb += 4) {
             double acc[4];
 #pragma unroll
-            for (int c = 0; c < 4; ++c) {
-              const int t = g * EG + tb + c;
-              acc[c] = (t < nt) ? sst[t * NV + r] : 0.0;
-            }
+            for (int c = 0; c < 4; ++c) acc[c] = sst[(g * EG + tb + c) * NV + r];
 #pragma unroll
             for (int k = 0; k < KC; k += 2) {
 #pragma unroll
               for (int c = 0; c < 4; ++c) {
-                const int t = g * EG + tb + c;
-                const double2 qv = *reinterpret_cast<const double2*>(q_s + t * KC + k);
-                acc[c] = fma(Lr[k], qv.x, acc[c]);
-                acc[c] = fma(Lr[k + 1], qv.y, acc[c]);
+                const double2 qq = *reinterpret_cast<const double2*>(q_s + (g * EG + tb + c) * KC + k);
+                acc[c] = fma(Lr[k], qq.x, acc[c]);
+                acc[c] = fma(Lr[k + 1], qq.y, acc[c]);
               }
             }
 #pragma unroll
             for (int c = 0; c < 4; ++c) {
               const int t = g * EG + tb + c;
-              if (t < nt) {
-                outb[t * NV + r] = acc[c];
-                d_s[t * NV + r] = acc[c] - ust[t * NV + r];
-              }
+              outb[t * NV + r] = acc[c];
+              d_s[t * NV + r] = acc[c] - ust[t * NV + r];
             }
           }
         } else {
           for (int tt = 0; tt < EG; ++tt) {
             const int t = g * EG + tt;
-            if (t >= nt) continue;
-            const double* __restrict__ Lc = a.LT + (size_t)cls_s[t] * (NFACE * NF) * NV + r;
-            double acc = sst[t * NV + r];
-            for (int k = 0; k < KC; ++k) {
-              const int col = cf_s[k / NF] * NF + (k % NF);
-              acc = fma(__ldg(Lc + (size_t)col * NV), q_s[t * KC + k], acc);
+            const int cls = mcls_s[stage][t];
+            double acc = 0.0, dl = 0.0;
+            if (t < nt) {
+              const double* __restrict__ Lc = a.LT + (size_t)cls * (NFACE * NF) * NV + r;
+              acc = sst[t * NV + r];
+              for (int k = 0; k < KC; ++k) {
+                const int col = cf_s[k / NF] * NF + (k % NF);
+                acc = fma(__ldg(Lc + (size_t)col * NV), q_s[t * KC + k], acc);
+              }
+              dl = acc - ust[t * NV + r];
             }
             outb[t * NV + r] = acc;
-            d_s[t * NV + r] = acc - ust[t * NV + r];
+            d_s[t * NV + r] = dl;
           }
         }
       }
@@ -341,43 +376,40 @@ __global__ void __launch_bounds__(SCfg<D, N1, M, NCF, NWC, E, NS, G>::NT, 1)
         bulk_s2g(un + e0 * NV, outb, (uint32_t)(nt * NV * sizeof(double)));
         bulk_commit();
       }
-      // ---- ||delta||_M^2 by sum-factorised Cholesky passes ----------------
+      // ---- ||delta||_M^2: sum-factorised Cholesky passes (C^T per axis) ---
+      // M = J (M1 x M1 [x M1]), M1 = C C^T  =>  d^T M d = J |(C^T x C^T ..) d|^2
       double* src = d_s;
       double* dst = t_s;
-      int mul = 1;
+      double acc2 = 0.0;
 #pragma unroll
       for (int ax = 0; ax < D; ++ax) {
-        for (int i = tid; i < nt * NV; i += NC) {
-          const int t = i / NV, rem = i % NV;
-          const int n = rem % NP;
-          const int ia = (n / mul) % N1;
-          const int base = t * NV + rem - ia * mul;
+        const bool last_ax = ax == D - 1;
+#pragma unroll
+        for (int tt = 0; tt < EG; ++tt) {
+          const int t = g * EG + tt;
+          const double* p = src + t * NV + rr;
           double v = 0.0;
 #pragma unroll
-          for (int ip = 0; ip < N1; ++ip)
-            if (ip >= ia) v = fma(c_s[ip * N1 + ia], src[base + ip * mul], v);
-          dst[i] = v;
+          for (int k = 0; k < N1; ++k) v = fma(cc[ax][k], p[co[ax][k]], v);
+          if (last_ax) acc2 = fma(v, v, acc2);
+          else if (rv) dst[t * NV + r] = v;
         }
-        consumer_bar(NC);
-        double* tmp = src;
-        src = dst;
-        dst = tmp;
-        mul *= N1;
+        if (!last_ax) {
+          consumer_bar(NC);
+          double* tmp = src;
+          src = dst;
+          dst = tmp;
+        }
       }
-      for (int t = warp; t < nt; t += NCW) {
-        double s = 0.0;
-        for (int i = lane; i < NV; i += 32) {
-          const double v = src[t * NV + i];
-          s = fma(a.comp_w[i / NP] * v, v, s);
-        }
+      // fixed-order tile reduction: lanes -> warps -> thread 0
+      double tsum = rv ? cw * acc2 : 0.0;
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-        if (lane == 0) part_s[t] = a.jac * s;
-      }
+      for (int o = 16; o > 0; o >>= 1) tsum += __shfl_xor_sync(0xffffffffu, tsum, o);
+      if (lane == 0) red_s[warp] = tsum;
       consumer_bar(NC);
       if (tid == 0) {
         double s = 0.0;
-        for (int t = 0; t < nt; ++t) s += part_s[t];
+        for (int w = 0; w < NCW; ++w) s += red_s[w];
         a.tile_partials[tile] = s;
       }
     }
