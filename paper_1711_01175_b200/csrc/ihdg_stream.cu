@@ -76,6 +76,7 @@ const StreamEntry* stream_entry(const ihdg_sweep_args* a) {
     geo.init(g, e.E);
     if (geo.tile_len % e.E != 0) continue;                       // full tiles only
     if (g.cells[0] % e.E != 0) continue;                         // tiles inside one axis-0 row
+    if (geo.nloc + 2 * geo.ls >= (1LL << 31) || geo.ntiles >= (1LL << 31)) continue;  // 32-bit indices
     if ((geo.ls * e.NV * 8) % 16 != 0) continue;                  // ghost offset
     if (((uintptr_t)a->u_old | (uintptr_t)a->u_new | (uintptr_t)a->s) % 16 != 0) continue;
     return &e;

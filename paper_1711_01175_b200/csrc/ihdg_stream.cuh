@@ -86,6 +86,81 @@ __device__ __forceinline__ void cp_async_arrive_noinc(uint64_t* bar) {
 }
 __device__ __forceinline__ void consumer_bar(int n) { asm volatile("bar.sync 1, %0;" ::"r"(n) : "memory"); }
 
+// 32-bit tile geometry for the streaming kernel (host guarantees local
+// element and tile counts < 2^31 and cells[0] % E == 0).  Tile = E
+// consecutive elements of one axis-0 row.  Neighbour offsets across faces of
+// axes >= 1 are the same for every element of the tile.
+template <int D>
+struct STile {
+  int e0, nt, i0;
+  int has[2 * D];   // neighbour exists across face f (axis >= 1 entries only)
+  int off[2 * D];   // neighbour element offset across face f (axis >= 1)
+
+  __device__ __forceinline__ void init(const ihdg_geom& g, int tile, int E, int nlay, int ls) {
+    const int c0 = (int)g.cells[0];
+    const int segs0 = c0 / E;
+    const int xrow = tile / segs0;
+    i0 = (tile - xrow * segs0) * E;
+    e0 = xrow * c0 + i0;
+    nt = E;
+    int lay = xrow;      // local layer (D == 2)
+    if (D == 3) {
+      const int c1 = (int)g.cells[1];
+      lay = xrow / c1;
+      const int i1 = xrow - lay * c1;
+      // axis 1 (inside the layer)
+      has[2] = (i1 > 0) || g.periodic[1];
+      off[2] = i1 > 0 ? -c0 : (c1 - 1) * c0;
+      has[3] = (i1 < c1 - 1) || g.periodic[1];
+      off[3] = i1 < c1 - 1 ? c0 : -(c1 - 1) * c0;
+    }
+    if (D >= 2) {
+      // layer axis (D-1): global index, ghost layers beyond the strip
+      const int L = (int)g.cells[D - 1];
+      const int jg = (int)g.layer_begin + lay;
+      const int flo = 2 * (D - 1), fhi = flo + 1;
+      int jl = jg - 1, jh = jg + 1;
+      has[flo] = (jl >= 0) || g.periodic[D - 1];
+      has[fhi] = (jh < L) || g.periodic[D - 1];
+      if (jl < 0) jl = L - 1;
+      if (jh >= L) jh = 0;
+      int ll = jl - (int)g.layer_begin, lh = jh - (int)g.layer_begin;
+      if (!(ll >= 0 && ll < nlay)) ll = -1;
+      if (!(lh >= 0 && lh < nlay)) lh = nlay;
+      off[flo] = (ll - lay) * ls;
+      off[fhi] = (lh - lay) * ls;
+    }
+    has[0] = has[1] = 1;
+    off[0] = -1;
+    off[1] = 1;
+  }
+  __device__ __forceinline__ int face_has(int f) const {
+    int v = 0;
+#pragma unroll
+    for (int k = 2; k < 2 * D; ++k) v = (f == k) ? has[k] : v;
+    return v;
+  }
+  __device__ __forceinline__ int face_off(int f) const {
+    int v = 0;
+#pragma unroll
+    for (int k = 2; k < 2 * D; ++k) v = (f == k) ? off[k] : v;
+    return v;
+  }
+  // missing-neighbour mask of tile element t
+  __device__ __forceinline__ int mask(int t, int c0, int per0) const {
+    int m = 0;
+    const int i = i0 + t;
+    if (!per0) {
+      if (i == 0) m |= 1;
+      if (i == c0 - 1) m |= 2;
+    }
+#pragma unroll
+    for (int f = 2; f < 2 * D; ++f)
+      if (!has[f]) m |= 1 << f;
+    return m;
+  }
+};
+
 // D dims, N1 = p+1, M comps, NCF coupled faces, NWC weighted comps per face,
 // E elements per tile, NS pipeline stages, G consumer groups (split E).
 template <int D, int N1, int M, int NCF, int NWC, int E, int NS, int G>
@@ -139,6 +214,7 @@ __global__ void __launch_bounds__(SCfg<D, N1, M, NCF, NWC, E, NS, G>::NT, 1)
   __shared__ int wc_s[NCF][NWC];            // weighted components
   __shared__ double ww_s[NCF][NWC];         // their weights
   __shared__ double chol_s[N1 * N1];
+  __shared__ double cshift_s[N1 * N1];      // cshift[ia][k] = C[ia+k][ia] (0 past the end)
   // per-stage tile metadata, written by the producer before its release-arrive
   __shared__ long long me0_s[NS];
   __shared__ int mnt_s[NS], mfast_s[NS];
@@ -157,6 +233,10 @@ __global__ void __launch_bounds__(SCfg<D, N1, M, NCF, NWC, E, NS, G>::NT, 1)
 
   for (int i = tid; i < NFACE * NF; i += blockDim.x) fv_s[i / NF][i % NF] = face_node_vidx(D, N1, i / NF, i % NF);
   for (int i = tid; i < N1 * N1; i += blockDim.x) chol_s[i] = a.chol1d[i];
+  for (int i = tid; i < N1 * N1; i += blockDim.x) {
+    const int ia = i / N1, k = i % N1;
+    cshift_s[i] = (ia + k < N1) ? a.chol1d[(ia + k) * N1 + ia] : 0.0;
+  }
   if (tid == 0) {
     int n = 0;
     for (int f = 0; f < NFACE && n < NCF; ++f) {
@@ -189,29 +269,30 @@ __global__ void __launch_bounds__(SCfg<D, N1, M, NCF, NWC, E, NS, G>::NT, 1)
   if (tid >= NC) {
     // ============================ producer warp ============================
     const int lane = tid - NC;
+    const int c0 = (int)a.g.cells[0];
+    const int per0 = a.g.periodic[0];
+    const int nlay = (int)(a.g.layer_end - a.g.layer_begin);
+    const int lsi = (int)ls;
     int it = 0;
-    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+    for (int tile = blockIdx.x; tile < (int)ntiles; tile += gridDim.x, ++it) {
       const int stage = it % NS;
       if (it >= NS) mbar_wait(&empty_bar[stage], ((it / NS) - 1) & 1);
       double* sst = sm + stage * C::STAGE;
       double* ust = sst + TILE;
       double* hst = ust + TILE;
-      TileInfo ti;
-      ti.init(geo, tile, E);
-      const int64_t e0 = ti.e0;
+      STile<D> ti;
+      ti.init(a.g, tile, E, nlay, lsi);
+      const int e0 = ti.e0;
       const int nt = ti.nt;
       // tile metadata for the consumers (mask of missing neighbours, class)
       int cls = -1;
       if (lane < E) {
-        int mask = 0;
-        if (lane < nt) {
-          mask = ti.mask(lane, D);
-          cls = a.class_of_mask[mask];
-        }
+        const int mask = ti.mask(lane, c0, per0);
+        cls = a.class_of_mask[mask];
         mmask_s[stage][lane] = mask;
         mcls_s[stage][lane] = cls;
       }
-      const int fast = __all_sync(0xffffffffu, lane >= nt || cls == fast_class);
+      const int fast = __all_sync(0xffffffffu, lane >= E || cls == fast_class);
       if (lane == 0) {
         me0_s[stage] = e0;
         mnt_s[stage] = nt;
@@ -221,23 +302,37 @@ __global__ void __launch_bounds__(SCfg<D, N1, M, NCF, NWC, E, NS, G>::NT, 1)
       if (lane == 0) {
         const uint32_t bytes = (uint32_t)(nt * NV * sizeof(double));
         mbar_arrive_expect_tx(&full_bar[stage], 2 * bytes);  // release: metadata above
-        bulk_g2s(sst, a.s + e0 * NV, bytes, &full_bar[stage]);
-        bulk_g2s(ust, uo + e0 * NV, bytes, &full_bar[stage]);
+        bulk_g2s(sst, a.s + (int64_t)e0 * NV, bytes, &full_bar[stage]);
+        bulk_g2s(ust, uo + (int64_t)e0 * NV, bytes, &full_bar[stage]);
       }
-      // neighbour face nodes that are not inside this tile; consecutive lanes
-      // take consecutive face nodes of one run (coalesced 8-byte cp.async)
-      constexpr int PER_T = NCF * NWC * NF;
-      for (int item = lane; item < nt * PER_T; item += 32) {
-        const int t = item / PER_T;
-        const int rem = item % PER_T;
-        const int ci = rem / (NWC * NF);
-        const int j = (rem / NF) % NWC;
-        const int n = rem % NF;
+      // neighbour face nodes not inside the tile, as runs of face nodes
+      // (consecutive lanes -> consecutive nodes: coalesced 8-byte cp.async)
+      constexpr int RUN = NWC * NF;
+#pragma unroll
+      for (int ci = 0; ci < NCF; ++ci) {
         const int f = cf_s[ci];
-        if ((f >> 1) == 0 && !((f == 0 && t == 0) || (f == 1 && t == nt - 1))) continue;
-        if (ti.mask(t, D) & (1 << f)) continue;
-        const double* src = uo + ti.nbr(t, f) * NV + wc_s[ci][j] * NP + fv_s[f ^ 1][n];
-        cp_async8(hst + item, src);
+        if ((f >> 1) == 0) {
+          const int t = (f == 0) ? 0 : nt - 1;
+          const int i = ti.i0 + t;
+          const bool ex = (f == 0) ? (i > 0 || per0) : (i < c0 - 1 || per0);
+          if (!ex) continue;
+          const int nb = e0 + t + ((f == 0) ? (i > 0 ? -1 : c0 - 1) : (i < c0 - 1 ? 1 : -(c0 - 1)));
+          const double* base = uo + (int64_t)nb * NV;
+          for (int item = lane; item < RUN; item += 32) {
+            const int j = item / NF, n = item - (item / NF) * NF;
+            cp_async8(hst + ((t * NCF + ci) * NWC + j) * NF + n, base + wc_s[ci][j] * NP + fv_s[f ^ 1][n]);
+          }
+        } else {
+          if (!ti.face_has(f)) continue;
+          const double* base = uo + ((int64_t)e0 + ti.face_off(f)) * NV;
+          for (int item = lane; item < nt * RUN; item += 32) {
+            const int t = item / RUN;
+            const int rem = item - t * RUN;
+            const int j = rem / NF, n = rem - j * NF;
+            cp_async8(hst + ((t * NCF + ci) * NWC + j) * NF + n,
+                      base + t * NV + wc_s[ci][j] * NP + fv_s[f ^ 1][n]);
+          }
+        }
       }
       cp_async_arrive_noinc(&full_bar[stage]);
     }
@@ -259,19 +354,12 @@ __global__ void __launch_bounds__(SCfg<D, N1, M, NCF, NWC, E, NS, G>::NT, 1)
     const int ncomp = rr / NP;
     const int node = rr % NP;
     const double cw = rv ? a.comp_w[ncomp] * a.jac : 0.0;
-    double cc[D][N1];
-    int co[D][N1];
+    int ia_ax[D];
     {
       int mul = 1;
 #pragma unroll
       for (int ax = 0; ax < D; ++ax) {
-        const int ia = (node / mul) % N1;
-#pragma unroll
-        for (int k = 0; k < N1; ++k) {
-          const bool ok = ia + k < N1;
-          cc[ax][k] = ok ? chol_s[(ia + k) * N1 + ia] : 0.0;
-          co[ax][k] = ok ? k * mul : 0;
-        }
+        ia_ax[ax] = (node / mul) % N1;
         mul *= N1;
       }
     }
@@ -291,12 +379,12 @@ __global__ void __launch_bounds__(SCfg<D, N1, M, NCF, NWC, E, NS, G>::NT, 1)
     }
 
     int it = 0;
-    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+    for (int tile = blockIdx.x; tile < (int)ntiles; tile += gridDim.x, ++it) {
       const int stage = it % NS;
       const int ob = it & 1;
       mbar_wait(&full_bar[stage], (it / NS) & 1);
       if (tid == 0 && it >= 2) bulk_wait_read<1>();
-      const int64_t e0 = me0_s[stage];
+      const int e0 = (int)me0_s[stage];
       const int nt = mnt_s[stage];
       const int fast = mfast_s[stage];
       const double* sst = sm + stage * C::STAGE;
@@ -328,26 +416,23 @@ __global__ void __launch_bounds__(SCfg<D, N1, M, NCF, NWC, E, NS, G>::NT, 1)
       double* outb = out_s + ob * TILE;
       if (rv) {
         if (fast) {
+          double acc[EG];
 #pragma unroll
-          for (int tb = 0; tb < EG; tb += 4) {
-            double acc[4];
+          for (int c = 0; c < EG; ++c) acc[c] = sst[(g * EG + c) * NV + r];
 #pragma unroll
-            for (int c = 0; c < 4; ++c) acc[c] = sst[(g * EG + tb + c) * NV + r];
+          for (int k = 0; k < KC; k += 2) {
 #pragma unroll
-            for (int k = 0; k < KC; k += 2) {
-#pragma unroll
-              for (int c = 0; c < 4; ++c) {
-                const double2 qq = *reinterpret_cast<const double2*>(q_s + (g * EG + tb + c) * KC + k);
-                acc[c] = fma(Lr[k], qq.x, acc[c]);
-                acc[c] = fma(Lr[k + 1], qq.y, acc[c]);
-              }
+            for (int c = 0; c < EG; ++c) {
+              const double2 qq = *reinterpret_cast<const double2*>(q_s + (g * EG + c) * KC + k);
+              acc[c] = fma(Lr[k], qq.x, acc[c]);
+              acc[c] = fma(Lr[k + 1], qq.y, acc[c]);
             }
+          }
 #pragma unroll
-            for (int c = 0; c < 4; ++c) {
-              const int t = g * EG + tb + c;
-              outb[t * NV + r] = acc[c];
-              d_s[t * NV + r] = acc[c] - ust[t * NV + r];
-            }
+          for (int c = 0; c < EG; ++c) {
+            const int t = g * EG + c;
+            outb[t * NV + r] = acc[c];
+            d_s[t * NV + r] = acc[c] - ust[t * NV + r];
           }
         } else {
           for (int tt = 0; tt < EG; ++tt) {
@@ -373,7 +458,7 @@ __global__ void __launch_bounds__(SCfg<D, N1, M, NCF, NWC, E, NS, G>::NT, 1)
       if (lane == 0) mbar_arrive(&empty_bar[stage]);
       consumer_bar(NC);
       if (tid == 0) {
-        bulk_s2g(un + e0 * NV, outb, (uint32_t)(nt * NV * sizeof(double)));
+        bulk_s2g(un + (int64_t)e0 * NV, outb, (uint32_t)(nt * NV * sizeof(double)));
         bulk_commit();
       }
       // ---- ||delta||_M^2: sum-factorised Cholesky passes (C^T per axis) ---
@@ -381,24 +466,30 @@ __global__ void __launch_bounds__(SCfg<D, N1, M, NCF, NWC, E, NS, G>::NT, 1)
       double* src = d_s;
       double* dst = t_s;
       double acc2 = 0.0;
+      {
+        int mul = 1;
 #pragma unroll
-      for (int ax = 0; ax < D; ++ax) {
-        const bool last_ax = ax == D - 1;
+        for (int ax = 0; ax < D; ++ax) {
+          const bool last_ax = ax == D - 1;
+          const int ia = ia_ax[ax];
+          const double* cw_row = cshift_s + ia * N1;
 #pragma unroll
-        for (int tt = 0; tt < EG; ++tt) {
-          const int t = g * EG + tt;
-          const double* p = src + t * NV + rr;
-          double v = 0.0;
+          for (int tt = 0; tt < EG; ++tt) {
+            const int t = g * EG + tt;
+            const double* p = src + t * NV + rr;
+            double v = 0.0;
 #pragma unroll
-          for (int k = 0; k < N1; ++k) v = fma(cc[ax][k], p[co[ax][k]], v);
-          if (last_ax) acc2 = fma(v, v, acc2);
-          else if (rv) dst[t * NV + r] = v;
-        }
-        if (!last_ax) {
-          consumer_bar(NC);
-          double* tmp = src;
-          src = dst;
-          dst = tmp;
+            for (int k = 0; k < N1; ++k) v = fma(cw_row[k], p[(ia + k < N1) ? k * mul : 0], v);
+            if (last_ax) acc2 = fma(v, v, acc2);
+            else if (rv) dst[t * NV + r] = v;
+          }
+          if (!last_ax) {
+            consumer_bar(NC);
+            double* tmp = src;
+            src = dst;
+            dst = tmp;
+          }
+          mul *= N1;
         }
       }
       // fixed-order tile reduction: lanes -> warps -> thread 0
