@@ -84,6 +84,13 @@ __device__ __forceinline__ void cp_async8(void* dst, const void* src) {
 __device__ __forceinline__ void cp_async_arrive_noinc(uint64_t* bar) {
   asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
+// D(8x8) += A(8x4, row) * B(4x8, col), fp64 tensor core (SASS DMMA.8x8x4).
+// lane l holds A[l>>2][l&3], B[l&3][l>>2], D[l>>2][2(l&3)], D[l>>2][2(l&3)+1].
+__device__ __forceinline__ void dmma_8x8x4(double& d0, double& d1, double a, double b) {
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+      : "+d"(d0), "+d"(d1)
+      : "d"(a), "d"(b));
+}
 __device__ __forceinline__ void consumer_bar(int n) { asm volatile("bar.sync 1, %0;" ::"r"(n) : "memory"); }
 
 // 32-bit tile geometry for the streaming kernel (host guarantees local
@@ -174,7 +181,11 @@ struct SCfg {
   static constexpr int NC = G * RP;              // consumer threads
   static constexpr int NCW = NC / 32;
   static constexpr int NT = NC + 32;             // + producer warp
-  static constexpr int EG = E / G;               // elements per group
+  static constexpr int EG = E / G;               // elements per group (norm)
+  static constexpr int NRT = (NV + 7) / 8;       // DMMA row tiles
+  static constexpr int KS = KC / 4;              // DMMA k steps
+  static constexpr int NEG = E / 8;              // DMMA element groups
+  static constexpr int RTW = (NRT + NCW - 1) / NCW;  // row tiles per consumer warp
   static constexpr int TILE = E * NV;            // doubles
   static constexpr int HALO = E * NCF * NWC * NF;
   static constexpr int STAGE = 2 * TILE + HALO;
@@ -187,7 +198,8 @@ struct SCfg {
   static constexpr int N_DBL = OFF_RED + 32;
   static constexpr size_t BYTES = (size_t)N_DBL * sizeof(double) + 2 * NS * sizeof(uint64_t);
   static_assert(EG % 4 == 0, "elements per group must be a multiple of 4");
-  static_assert(KC % 2 == 0, "compacted neighbour count must be even");
+  static_assert(KC % 4 == 0, "compacted neighbour count must be a multiple of 4 (DMMA k)");
+  static_assert(E % 8 == 0, "tile must be a multiple of 8 elements (DMMA n)");
   static_assert(E <= 32, "one producer lane per tile element");
   static_assert(KC <= RP, "q is computed by the first KC row threads");
   static_assert((TILE * sizeof(double)) % 16 == 0, "tile bytes must be 16-byte multiples");
@@ -199,6 +211,7 @@ __global__ void __launch_bounds__(SCfg<D, N1, M, NCF, NWC, E, NS, G>::NT, 1)
   using C = SCfg<D, N1, M, NCF, NWC, E, NS, G>;
   constexpr int NP = C::NP, NV = C::NV, NF = C::NF, NFACE = C::NFACE, KC = C::KC;
   constexpr int RP = C::RP, NC = C::NC, NCW = C::NCW, EG = C::EG, TILE = C::TILE;
+  constexpr int NRT = C::NRT, KS = C::KS, NEG = C::NEG, RTW = C::RTW;
 
   extern __shared__ __align__(128) double sm[];
   double* out_s = sm + C::OFF_OUT;
@@ -218,6 +231,7 @@ __global__ void __launch_bounds__(SCfg<D, N1, M, NCF, NWC, E, NS, G>::NT, 1)
   // per-stage tile metadata, written by the producer before its release-arrive
   __shared__ long long me0_s[NS];
   __shared__ int mnt_s[NS], mfast_s[NS];
+  __shared__ unsigned mcset_s[NS];          // classes present in the tile (bit set)
   __shared__ int mmask_s[NS][E], mcls_s[NS][E];
   __shared__ int last_s;
 
@@ -293,10 +307,14 @@ __global__ void __launch_bounds__(SCfg<D, N1, M, NCF, NWC, E, NS, G>::NT, 1)
         mcls_s[stage][lane] = cls;
       }
       const int fast = __all_sync(0xffffffffu, lane >= E || cls == fast_class);
+      unsigned cset = (lane < E && cls >= 0 && cls < 32) ? (1u << cls) : 0u;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) cset |= __shfl_xor_sync(0xffffffffu, cset, o);
       if (lane == 0) {
         me0_s[stage] = e0;
         mnt_s[stage] = nt;
         mfast_s[stage] = fast;
+        mcset_s[stage] = cset;
       }
       __syncwarp();
       if (lane == 0) {
@@ -344,11 +362,18 @@ __global__ void __launch_bounds__(SCfg<D, N1, M, NCF, NWC, E, NS, G>::NT, 1)
     const int warp = tid >> 5, lane = tid & 31;
     // per-thread constants: row r of the lifted operator, its node indices,
     // the Cholesky coefficients of its node along each axis
-    double Lr[KC];
+    // DMMA A fragments of the interior-class operator for this warp's row
+    // tiles: Lf[j][ks] = L[8 rt_j + (lane>>2)][4 ks + (lane&3)]
+    double Lf[RTW][KS];
 #pragma unroll
-    for (int k = 0; k < KC; ++k) {
-      const int col = cf_s[k / NF] * NF + (k % NF);
-      Lr[k] = rv ? __ldg(a.LT + ((size_t)fast_class * (NFACE * NF) + col) * NV + r) : 0.0;
+    for (int j = 0; j < RTW; ++j) {
+      const int row = (warp + j * NCW) * 8 + (lane >> 2);
+#pragma unroll
+      for (int ks = 0; ks < KS; ++ks) {
+        const int k = 4 * ks + (lane & 3);
+        const int col = cf_s[k / NF] * NF + (k % NF);
+        Lf[j][ks] = (row < NV) ? __ldg(a.LT + ((size_t)fast_class * (NFACE * NF) + col) * NV + row) : 0.0;
+      }
     }
     const int rr = rv ? r : 0;
     const int ncomp = rr / NP;
@@ -412,44 +437,58 @@ __global__ void __launch_bounds__(SCfg<D, N1, M, NCF, NWC, E, NS, G>::NT, 1)
         }
       }
       consumer_bar(NC);
-      // ---- lifted local solve u^{k+1} = s + L q ---------------------------
+      // ---- lifted local solve u^{k+1} = s + L q on the fp64 tensor core --
+      // D[row][elem] = s + sum_k L[row][k] q[elem][k]: rows = 8 x NRT row
+      // tiles (warp w owns tiles w, w+NCW, ...), elements = 8 x NEG groups.
       double* outb = out_s + ob * TILE;
-      if (rv) {
+      const unsigned cset = mcset_s[stage];
+#pragma unroll
+      for (int eg = 0; eg < NEG; ++eg) {
+        double acc[RTW][2];
+        const int te = eg * 8 + 2 * (lane & 3);   // D columns (elements) of this lane
+#pragma unroll
+        for (int j = 0; j < RTW; ++j) {
+          const int row = (warp + j * NCW) * 8 + (lane >> 2);
+          const bool ok = row < NV && (warp + j * NCW) < NRT;
+          acc[j][0] = ok ? sst[te * NV + row] : 0.0;
+          acc[j][1] = ok ? sst[(te + 1) * NV + row] : 0.0;
+        }
+        const double* qb = q_s + (eg * 8 + (lane >> 2)) * KC + (lane & 3);
         if (fast) {
-          double acc[EG];
 #pragma unroll
-          for (int c = 0; c < EG; ++c) acc[c] = sst[(g * EG + c) * NV + r];
+          for (int ks = 0; ks < KS; ++ks) {
+            const double b = qb[4 * ks];
 #pragma unroll
-          for (int k = 0; k < KC; k += 2) {
-#pragma unroll
-            for (int c = 0; c < EG; ++c) {
-              const double2 qq = *reinterpret_cast<const double2*>(q_s + (g * EG + c) * KC + k);
-              acc[c] = fma(Lr[k], qq.x, acc[c]);
-              acc[c] = fma(Lr[k + 1], qq.y, acc[c]);
-            }
-          }
-#pragma unroll
-          for (int c = 0; c < EG; ++c) {
-            const int t = g * EG + c;
-            outb[t * NV + r] = acc[c];
-            d_s[t * NV + r] = acc[c] - ust[t * NV + r];
+            for (int j = 0; j < RTW; ++j) dmma_8x8x4(acc[j][0], acc[j][1], Lf[j][ks], b);
           }
         } else {
-          for (int tt = 0; tt < EG; ++tt) {
-            const int t = g * EG + tt;
-            const int cls = mcls_s[stage][t];
-            double acc = 0.0, dl = 0.0;
-            if (t < nt) {
-              const double* __restrict__ Lc = a.LT + (size_t)cls * (NFACE * NF) * NV + r;
-              acc = sst[t * NV + r];
-              for (int k = 0; k < KC; ++k) {
-                const int col = cf_s[k / NF] * NF + (k % NF);
-                acc = fma(__ldg(Lc + (size_t)col * NV), q_s[t * KC + k], acc);
+          // one masked pass per operator class present in the tile
+          const int mycls = mcls_s[stage][eg * 8 + (lane >> 2)];
+          for (unsigned rem = cset; rem != 0u; rem &= rem - 1u) {
+            const int c = __ffs(rem) - 1;
+            for (int ks = 0; ks < KS; ++ks) {
+              const double b = (mycls == c) ? qb[4 * ks] : 0.0;
+              const int k = 4 * ks + (lane & 3);
+              const int col = cf_s[k / NF] * NF + (k % NF);
+#pragma unroll
+              for (int j = 0; j < RTW; ++j) {
+                const int row = (warp + j * NCW) * 8 + (lane >> 2);
+                const double av = (row < NV) ? __ldg(a.LT + ((size_t)c * (NFACE * NF) + col) * NV + row) : 0.0;
+                dmma_8x8x4(acc[j][0], acc[j][1], av, b);
               }
-              dl = acc - ust[t * NV + r];
             }
-            outb[t * NV + r] = acc;
-            d_s[t * NV + r] = dl;
+          }
+        }
+#pragma unroll
+        for (int j = 0; j < RTW; ++j) {
+          const int row = (warp + j * NCW) * 8 + (lane >> 2);
+          if (row < NV && (warp + j * NCW) < NRT) {
+#pragma unroll
+            for (int v = 0; v < 2; ++v) {
+              const int t = te + v;
+              outb[t * NV + row] = acc[j][v];
+              d_s[t * NV + row] = acc[j][v] - ust[t * NV + row];
+            }
           }
         }
       }
