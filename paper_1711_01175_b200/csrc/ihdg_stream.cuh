@@ -213,7 +213,7 @@ __global__ void __launch_bounds__(SCfg<D, N1, M, NCF, NWC, E, NS, G>::NT, 1)
   constexpr int RP = C::RP, NC = C::NC, NCW = C::NCW, EG = C::EG, TILE = C::TILE;
   constexpr int NRT = C::NRT, KS = C::KS, NEG = C::NEG, RTW = C::RTW;
 
-  extern __shared__ __align__(128) double sm[];
+  extern __shared__ __align__(16) double sm[];
   double* out_s = sm + C::OFF_OUT;
   double* d_s = sm + C::OFF_D;
   double* t_s = sm + C::OFF_T;
@@ -228,6 +228,9 @@ __global__ void __launch_bounds__(SCfg<D, N1, M, NCF, NWC, E, NS, G>::NT, 1)
   __shared__ double ww_s[NCF][NWC];         // their weights
   __shared__ double chol_s[N1 * N1];
   __shared__ double cshift_s[N1 * N1];      // cshift[ia][k] = C[ia+k][ia] (0 past the end)
+  __shared__ int qf_s[KC];                  // face of neighbour scalar k
+  __shared__ int qt_s[KC][NWC];             // offset of its source node inside a tile element
+  __shared__ int qh_s[KC];                  // offset inside a tile element's halo block
   // per-stage tile metadata, written by the producer before its release-arrive
   __shared__ long long me0_s[NS];
   __shared__ int mnt_s[NS], mfast_s[NS];
@@ -268,6 +271,12 @@ __global__ void __launch_bounds__(SCfg<D, N1, M, NCF, NWC, E, NS, G>::NT, 1)
         ww_s[n][j] = 0.0;
       }
       ++n;
+    }
+    for (int k = 0; k < KC; ++k) {
+      const int ci = k / NF, n = k % NF, f = cf_s[ci];
+      qf_s[k] = f;
+      for (int j = 0; j < NWC; ++j) qt_s[k][j] = wc_s[ci][j] * NP + face_node_vidx(D, N1, f ^ 1, n);
+      qh_s[k] = ci * NWC * NF + n;
     }
     for (int s = 0; s < NS; ++s) {
       mbar_init(&full_bar[s], 1 + 32);
@@ -379,6 +388,12 @@ __global__ void __launch_bounds__(SCfg<D, N1, M, NCF, NWC, E, NS, G>::NT, 1)
     const int ncomp = rr / NP;
     const int node = rr % NP;
     const double cw = rv ? a.comp_w[ncomp] * a.jac : 0.0;
+    double cfr[2];
+#pragma unroll
+    for (int ks = 0; ks < 2; ++ks) {
+      const int kk = 4 * ks + (lane & 3), nn = lane >> 2;
+      cfr[ks] = (kk < N1 && nn < N1) ? chol_s[kk * N1 + nn] : 0.0;
+    }
     int ia_ax[D];
     {
       int mul = 1;
@@ -388,21 +403,6 @@ __global__ void __launch_bounds__(SCfg<D, N1, M, NCF, NWC, E, NS, G>::NT, 1)
         mul *= N1;
       }
     }
-    // q thread: row thread r < KC computes neighbour scalar k = r
-    const bool qv = r < KC;
-    const int qk = qv ? r : 0;
-    const int qci = qk / NF, qn = qk % NF;
-    const int qf = cf_s[qci];
-    const bool qaxis0 = (qf >> 1) == 0;
-    const int qsrc_tile = fv_s[qf ^ 1][qn];
-    double qw[NWC];
-    int qoff[NWC];
-#pragma unroll
-    for (int j = 0; j < NWC; ++j) {
-      qw[j] = ww_s[qci][j];
-      qoff[j] = wc_s[qci][j] * NP + qsrc_tile;
-    }
-
     int it = 0;
     for (int tile = blockIdx.x; tile < (int)ntiles; tile += gridDim.x, ++it) {
       const int stage = it % NS;
@@ -415,25 +415,28 @@ __global__ void __launch_bounds__(SCfg<D, N1, M, NCF, NWC, E, NS, G>::NT, 1)
       const double* sst = sm + stage * C::STAGE;
       const double* ust = sst + TILE;
       const double* hst = ust + TILE;
-      // ---- neighbour face scalars q[t][k] --------------------------------
-      if (qv) {
+      // ---- neighbour face scalars q[t][k] (all consumer threads) ---------
 #pragma unroll
-        for (int tt = 0; tt < EG; ++tt) {
-          const int t = g * EG + tt;
+      for (int m = 0; m < (E * KC + NC - 1) / NC; ++m) {
+        const int idx = tid + m * NC;
+        if (idx < E * KC) {
+          const int t = idx / KC, k = idx - (idx / KC) * KC;
+          const int f = qf_s[k];
           double v = 0.0;
-          if (t < nt && !(mmask_s[stage][t] & (1 << qf))) {
-            const bool in_tile = qaxis0 && !((qf == 0 && t == 0) || (qf == 1 && t == nt - 1));
+          if (!(mmask_s[stage][t] & (1 << f))) {
+            const bool in_tile = (f >> 1) == 0 && !((f == 0 && t == 0) || (f == 1 && t == nt - 1));
+            const int ci = k / NF;
             if (in_tile) {
-              const double* src = ust + (t + (qf == 0 ? -1 : 1)) * NV;
+              const double* src = ust + (t + (f == 0 ? -1 : 1)) * NV;
 #pragma unroll
-              for (int j = 0; j < NWC; ++j) v = fma(qw[j], src[qoff[j]], v);
+              for (int j = 0; j < NWC; ++j) v = fma(ww_s[ci][j], src[qt_s[k][j]], v);
             } else {
-              const double* src = hst + ((t * NCF + qci) * NWC) * NF + qn;
+              const double* src = hst + t * (NCF * NWC * NF) + qh_s[k];
 #pragma unroll
-              for (int j = 0; j < NWC; ++j) v = fma(qw[j], src[j * NF], v);
+              for (int j = 0; j < NWC; ++j) v = fma(ww_s[ci][j], src[j * NF], v);
             }
           }
-          q_s[t * KC + qk] = v;
+          q_s[idx] = v;
         }
       }
       consumer_bar(NC);
@@ -442,43 +445,55 @@ __global__ void __launch_bounds__(SCfg<D, N1, M, NCF, NWC, E, NS, G>::NT, 1)
       // tiles (warp w owns tiles w, w+NCW, ...), elements = 8 x NEG groups.
       double* outb = out_s + ob * TILE;
       const unsigned cset = mcset_s[stage];
+      double acc[NEG][RTW][2];
 #pragma unroll
       for (int eg = 0; eg < NEG; ++eg) {
-        double acc[RTW][2];
         const int te = eg * 8 + 2 * (lane & 3);   // D columns (elements) of this lane
 #pragma unroll
         for (int j = 0; j < RTW; ++j) {
           const int row = (warp + j * NCW) * 8 + (lane >> 2);
           const bool ok = row < NV && (warp + j * NCW) < NRT;
-          acc[j][0] = ok ? sst[te * NV + row] : 0.0;
-          acc[j][1] = ok ? sst[(te + 1) * NV + row] : 0.0;
+          acc[eg][j][0] = ok ? sst[te * NV + row] : 0.0;
+          acc[eg][j][1] = ok ? sst[(te + 1) * NV + row] : 0.0;
         }
-        const double* qb = q_s + (eg * 8 + (lane >> 2)) * KC + (lane & 3);
-        if (fast) {
+      }
+      const double* qb = q_s + (lane >> 2) * KC + (lane & 3);
+      if (fast) {
 #pragma unroll
+        for (int ks = 0; ks < KS; ++ks) {
+          double b[NEG];
+#pragma unroll
+          for (int eg = 0; eg < NEG; ++eg) b[eg] = qb[eg * 8 * KC + 4 * ks];
+#pragma unroll
+          for (int eg = 0; eg < NEG; ++eg)
+#pragma unroll
+            for (int j = 0; j < RTW; ++j) dmma_8x8x4(acc[eg][j][0], acc[eg][j][1], Lf[j][ks], b[eg]);
+        }
+      } else {
+        // one masked pass per operator class present in the tile
+        for (unsigned rem = cset; rem != 0u; rem &= rem - 1u) {
+          const int c = __ffs(rem) - 1;
           for (int ks = 0; ks < KS; ++ks) {
-            const double b = qb[4 * ks];
+            const int k = 4 * ks + (lane & 3);
+            const int col = cf_s[k / NF] * NF + (k % NF);
+            double av[RTW];
 #pragma unroll
-            for (int j = 0; j < RTW; ++j) dmma_8x8x4(acc[j][0], acc[j][1], Lf[j][ks], b);
-          }
-        } else {
-          // one masked pass per operator class present in the tile
-          const int mycls = mcls_s[stage][eg * 8 + (lane >> 2)];
-          for (unsigned rem = cset; rem != 0u; rem &= rem - 1u) {
-            const int c = __ffs(rem) - 1;
-            for (int ks = 0; ks < KS; ++ks) {
-              const double b = (mycls == c) ? qb[4 * ks] : 0.0;
-              const int k = 4 * ks + (lane & 3);
-              const int col = cf_s[k / NF] * NF + (k % NF);
+            for (int j = 0; j < RTW; ++j) {
+              const int row = (warp + j * NCW) * 8 + (lane >> 2);
+              av[j] = (row < NV) ? __ldg(a.LT + ((size_t)c * (NFACE * NF) + col) * NV + row) : 0.0;
+            }
 #pragma unroll
-              for (int j = 0; j < RTW; ++j) {
-                const int row = (warp + j * NCW) * 8 + (lane >> 2);
-                const double av = (row < NV) ? __ldg(a.LT + ((size_t)c * (NFACE * NF) + col) * NV + row) : 0.0;
-                dmma_8x8x4(acc[j][0], acc[j][1], av, b);
-              }
+            for (int eg = 0; eg < NEG; ++eg) {
+              const double b = (mcls_s[stage][eg * 8 + (lane >> 2)] == c) ? qb[eg * 8 * KC + 4 * ks] : 0.0;
+#pragma unroll
+              for (int j = 0; j < RTW; ++j) dmma_8x8x4(acc[eg][j][0], acc[eg][j][1], av[j], b);
             }
           }
         }
+      }
+#pragma unroll
+      for (int eg = 0; eg < NEG; ++eg) {
+        const int te = eg * 8 + 2 * (lane & 3);
 #pragma unroll
         for (int j = 0; j < RTW; ++j) {
           const int row = (warp + j * NCW) * 8 + (lane >> 2);
@@ -486,8 +501,8 @@ __global__ void __launch_bounds__(SCfg<D, N1, M, NCF, NWC, E, NS, G>::NT, 1)
 #pragma unroll
             for (int v = 0; v < 2; ++v) {
               const int t = te + v;
-              outb[t * NV + row] = acc[j][v];
-              d_s[t * NV + row] = acc[j][v] - ust[t * NV + row];
+              outb[t * NV + row] = acc[eg][j][v];
+              d_s[t * NV + row] = acc[eg][j][v] - ust[t * NV + row];
             }
           }
         }
@@ -500,12 +515,38 @@ __global__ void __launch_bounds__(SCfg<D, N1, M, NCF, NWC, E, NS, G>::NT, 1)
         bulk_s2g(un + (int64_t)e0 * NV, outb, (uint32_t)(nt * NV * sizeof(double)));
         bulk_commit();
       }
-      // ---- ||delta||_M^2: sum-factorised Cholesky passes (C^T per axis) ---
-      // M = J (M1 x M1 [x M1]), M1 = C C^T  =>  d^T M d = J |(C^T x C^T ..) d|^2
-      double* src = d_s;
-      double* dst = t_s;
+      // ---- ||delta||_M^2 ---------------------------------------------------
+      // M = J (M1 (x) M1 [(x) M1]), M1 = C C^T  =>  d^T M d = J |(C^T (x) ..) d|^2
       double acc2 = 0.0;
-      {
+      if constexpr (D == 2 && N1 <= 8) {
+        // per (element, component): Y = C^T Delta C on the fp64 tensor core,
+        // Delta[j][i] = delta at node (i, j), zero-padded to 8x8.
+        for (int u = warp; u < E * M; u += NCW) {
+          const int t = u / M, c = u - (u / M) * M;
+          const double* base = d_s + t * NV + c * NP;
+          double r0 = 0.0, r1 = 0.0;
+#pragma unroll
+          for (int ks = 0; ks < 2; ++ks) {
+            const int kk = 4 * ks + (lane & 3), nn = lane >> 2;
+            const double b = (kk < N1 && nn < N1) ? base[kk * N1 + nn] : 0.0;
+            dmma_8x8x4(r0, r1, cfr[ks], b);        // R = C^T Delta
+          }
+          double y0 = 0.0, y1 = 0.0;
+#pragma unroll
+          for (int ks = 0; ks < 2; ++ks) {
+            const int col = 4 * ks + (lane & 3);   // A fragment R[lane>>2][col]
+            const int src = (lane & ~3) | (col >> 1);
+            const double x0 = __shfl_sync(0xffffffffu, r0, src);
+            const double x1 = __shfl_sync(0xffffffffu, r1, src);
+            dmma_8x8x4(y0, y1, (col & 1) ? x1 : x0, cfr[ks]);  // Y = R C
+          }
+          acc2 = fma(a.comp_w[c] * y0, y0, acc2);
+          acc2 = fma(a.comp_w[c] * y1, y1, acc2);
+        }
+        acc2 *= a.jac;
+      } else {
+        double* src = d_s;
+        double* dst = t_s;
         int mul = 1;
 #pragma unroll
         for (int ax = 0; ax < D; ++ax) {
@@ -530,9 +571,10 @@ __global__ void __launch_bounds__(SCfg<D, N1, M, NCF, NWC, E, NS, G>::NT, 1)
           }
           mul *= N1;
         }
+        acc2 = rv ? cw * acc2 : 0.0;
       }
       // fixed-order tile reduction: lanes -> warps -> thread 0
-      double tsum = rv ? cw * acc2 : 0.0;
+      double tsum = acc2;
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) tsum += __shfl_xor_sync(0xffffffffu, tsum, o);
       if (lane == 0) red_s[warp] = tsum;
