@@ -181,29 +181,76 @@ struct SCfg {
   static constexpr int NC = G * RP;              // consumer threads
   static constexpr int NCW = NC / 32;
   static constexpr int NT = NC + 32;             // + producer warp
-  static constexpr int EG = E / G;               // elements per group (norm)
+  static constexpr int EG = E / G;               // elements per group (DFMA norm)
   static constexpr int NRT = (NV + 7) / 8;       // DMMA row tiles
   static constexpr int KS = KC / 4;              // DMMA k steps
   static constexpr int NEG = E / 8;              // DMMA element groups
   static constexpr int RTW = (NRT + NCW - 1) / NCW;  // row tiles per consumer warp
+  // 2D with p+1 <= 8: norm on the tensor core, software-pipelined one tile behind
+  static constexpr bool PIPE = (D == 2 && N1 <= 8);
+  static constexpr int UPW = (E * M + NCW - 1) / NCW;  // norm units per warp
   static constexpr int TILE = E * NV;            // doubles
   static constexpr int HALO = E * NCF * NWC * NF;
   static constexpr int STAGE = 2 * TILE + HALO;
   // shared memory carve (doubles)
   static constexpr int OFF_OUT = NS * STAGE;
-  static constexpr int OFF_D = OFF_OUT + 2 * TILE;
-  static constexpr int OFF_T = OFF_D + TILE;
+  static constexpr int OFF_D = OFF_OUT + 2 * TILE;   // delta (PIPE: double buffer)
+  static constexpr int OFF_T = OFF_D + TILE;         // DFMA pass scratch / delta buffer 1
   static constexpr int OFF_Q = OFF_T + TILE;
   static constexpr int OFF_RED = OFF_Q + E * KC;
-  static constexpr int N_DBL = OFF_RED + 32;
+  static constexpr int N_DBL = OFF_RED + 64;
   static constexpr size_t BYTES = (size_t)N_DBL * sizeof(double) + 2 * NS * sizeof(uint64_t);
   static_assert(EG % 4 == 0, "elements per group must be a multiple of 4");
   static_assert(KC % 4 == 0, "compacted neighbour count must be a multiple of 4 (DMMA k)");
   static_assert(E % 8 == 0, "tile must be a multiple of 8 elements (DMMA n)");
   static_assert(E <= 32, "one producer lane per tile element");
-  static_assert(KC <= RP, "q is computed by the first KC row threads");
+  static_assert(NCW <= 32, "warp partials fit one reduction row");
   static_assert((TILE * sizeof(double)) % 16 == 0, "tile bytes must be 16-byte multiples");
 };
+
+// ||Y||_F^2 of Y = C^T Delta C for the UPW (element, component) units of this
+// warp (2D, tensor core).  Delta[j][i] = delta at node (i, j), zero padded to
+// 8x8; cfr = C fragments.  Invalid units read zeros (uniform control flow).
+template <int N1, int M, int NP, int NV, int E, int NCW, int UPW>
+__device__ __forceinline__ double norm_units_2d(const double* __restrict__ dbuf, int warp, int lane,
+                                                const double (&cfr)[2], const double* comp_w) {
+  double acc = 0.0;
+  double r0[UPW], r1[UPW];
+#pragma unroll
+  for (int m = 0; m < UPW; ++m) {
+    const int u = warp + m * NCW;
+    const bool valid = u < E * M;
+    const int uu = valid ? u : 0;
+    const int t = uu / M, c = uu - (uu / M) * M;
+    const double* base = dbuf + t * NV + c * NP;
+    r0[m] = 0.0;
+    r1[m] = 0.0;
+#pragma unroll
+    for (int ks = 0; ks < 2; ++ks) {
+      const int kk = 4 * ks + (lane & 3), nn = lane >> 2;
+      const double b = (valid && kk < N1 && nn < N1) ? base[kk * N1 + nn] : 0.0;
+      dmma_8x8x4(r0[m], r1[m], cfr[ks], b);   // R = C^T Delta
+    }
+  }
+#pragma unroll
+  for (int m = 0; m < UPW; ++m) {
+    const int u = warp + m * NCW;
+    const int c = (u < E * M ? u : 0) % M;
+    double y0 = 0.0, y1 = 0.0;
+#pragma unroll
+    for (int ks = 0; ks < 2; ++ks) {
+      const int col = 4 * ks + (lane & 3);     // A fragment R[lane>>2][col]
+      const int src = (lane & ~3) | (col >> 1);
+      const double x0 = __shfl_sync(0xffffffffu, r0[m], src);
+      const double x1 = __shfl_sync(0xffffffffu, r1[m], src);
+      dmma_8x8x4(y0, y1, (col & 1) ? x1 : x0, cfr[ks]);  // Y = R C
+    }
+    const double w = comp_w[c];
+    acc = fma(w * y0, y0, acc);
+    acc = fma(w * y1, y1, acc);
+  }
+  return acc;
+}
 
 template <int D, int N1, int M, int NCF, int NWC, int E, int NS, int G>
 __global__ void __launch_bounds__(SCfg<D, N1, M, NCF, NWC, E, NS, G>::NT, 1)
@@ -211,7 +258,7 @@ __global__ void __launch_bounds__(SCfg<D, N1, M, NCF, NWC, E, NS, G>::NT, 1)
   using C = SCfg<D, N1, M, NCF, NWC, E, NS, G>;
   constexpr int NP = C::NP, NV = C::NV, NF = C::NF, NFACE = C::NFACE, KC = C::KC;
   constexpr int RP = C::RP, NC = C::NC, NCW = C::NCW, EG = C::EG, TILE = C::TILE;
-  constexpr int NRT = C::NRT, KS = C::KS, NEG = C::NEG, RTW = C::RTW;
+  constexpr int NRT = C::NRT, KS = C::KS, NEG = C::NEG, RTW = C::RTW, UPW = C::UPW;
 
   extern __shared__ __align__(16) double sm[];
   double* out_s = sm + C::OFF_OUT;
@@ -249,8 +296,8 @@ __global__ void __launch_bounds__(SCfg<D, N1, M, NCF, NWC, E, NS, G>::NT, 1)
   double* __restrict__ un = a.u_new + ls * NV;
 
   for (int i = tid; i < NFACE * NF; i += blockDim.x) fv_s[i / NF][i % NF] = face_node_vidx(D, N1, i / NF, i % NF);
-  for (int i = tid; i < N1 * N1; i += blockDim.x) chol_s[i] = a.chol1d[i];
   for (int i = tid; i < N1 * N1; i += blockDim.x) {
+    chol_s[i] = a.chol1d[i];
     const int ia = i / N1, k = i % N1;
     cshift_s[i] = (ia + k < N1) ? a.chol1d[(ia + k) * N1 + ia] : 0.0;
   }
@@ -273,10 +320,10 @@ __global__ void __launch_bounds__(SCfg<D, N1, M, NCF, NWC, E, NS, G>::NT, 1)
       ++n;
     }
     for (int k = 0; k < KC; ++k) {
-      const int ci = k / NF, n = k % NF, f = cf_s[ci];
+      const int ci = k / NF, nn = k % NF, f = cf_s[ci];
       qf_s[k] = f;
-      for (int j = 0; j < NWC; ++j) qt_s[k][j] = wc_s[ci][j] * NP + face_node_vidx(D, N1, f ^ 1, n);
-      qh_s[k] = ci * NWC * NF + n;
+      for (int j = 0; j < NWC; ++j) qt_s[k][j] = wc_s[ci][j] * NP + face_node_vidx(D, N1, f ^ 1, nn);
+      qh_s[k] = ci * NWC * NF + nn;
     }
     for (int s = 0; s < NS; ++s) {
       mbar_init(&full_bar[s], 1 + 32);
@@ -287,7 +334,7 @@ __global__ void __launch_bounds__(SCfg<D, N1, M, NCF, NWC, E, NS, G>::NT, 1)
   __syncthreads();
 
   const int fast_class = a.class_of_mask[0];
-  const int64_t ntiles = geo.ntiles;
+  const int ntiles = (int)geo.ntiles;
 
   if (tid >= NC) {
     // ============================ producer warp ============================
@@ -297,7 +344,7 @@ __global__ void __launch_bounds__(SCfg<D, N1, M, NCF, NWC, E, NS, G>::NT, 1)
     const int nlay = (int)(a.g.layer_end - a.g.layer_begin);
     const int lsi = (int)ls;
     int it = 0;
-    for (int tile = blockIdx.x; tile < (int)ntiles; tile += gridDim.x, ++it) {
+    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
       const int stage = it % NS;
       if (it >= NS) mbar_wait(&empty_bar[stage], ((it / NS) - 1) & 1);
       double* sst = sm + stage * C::STAGE;
@@ -369,8 +416,6 @@ __global__ void __launch_bounds__(SCfg<D, N1, M, NCF, NWC, E, NS, G>::NT, 1)
     const int g = tid / RP;
     const bool rv = r < NV;
     const int warp = tid >> 5, lane = tid & 31;
-    // per-thread constants: row r of the lifted operator, its node indices,
-    // the Cholesky coefficients of its node along each axis
     // DMMA A fragments of the interior-class operator for this warp's row
     // tiles: Lf[j][ks] = L[8 rt_j + (lane>>2)][4 ks + (lane&3)]
     double Lf[RTW][KS];
@@ -384,38 +429,40 @@ __global__ void __launch_bounds__(SCfg<D, N1, M, NCF, NWC, E, NS, G>::NT, 1)
         Lf[j][ks] = (row < NV) ? __ldg(a.LT + ((size_t)fast_class * (NFACE * NF) + col) * NV + row) : 0.0;
       }
     }
-    const int rr = rv ? r : 0;
-    const int ncomp = rr / NP;
-    const int node = rr % NP;
-    const double cw = rv ? a.comp_w[ncomp] * a.jac : 0.0;
+    // C fragments for the 2D tensor-core norm: C[4 ks + (lane&3)][lane>>2]
     double cfr[2];
 #pragma unroll
     for (int ks = 0; ks < 2; ++ks) {
       const int kk = 4 * ks + (lane & 3), nn = lane >> 2;
       cfr[ks] = (kk < N1 && nn < N1) ? chol_s[kk * N1 + nn] : 0.0;
     }
+    // per-thread constants of the DFMA (3D) norm: row r, node indices
+    const int rr = rv ? r : 0;
+    const double cw = rv ? a.comp_w[rr / NP] * a.jac : 0.0;
     int ia_ax[D];
     {
       int mul = 1;
 #pragma unroll
       for (int ax = 0; ax < D; ++ax) {
-        ia_ax[ax] = (node / mul) % N1;
+        ia_ax[ax] = ((rr % NP) / mul) % N1;
         mul *= N1;
       }
     }
+
     int it = 0;
-    for (int tile = blockIdx.x; tile < (int)ntiles; tile += gridDim.x, ++it) {
+    int prev_tile = -1;
+    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
       const int stage = it % NS;
       const int ob = it & 1;
       mbar_wait(&full_bar[stage], (it / NS) & 1);
-      if (tid == 0 && it >= 2) bulk_wait_read<1>();
+      if (tid == 0 && it >= 2) bulk_wait_read<1>();   // out[ob] free again
       const int e0 = (int)me0_s[stage];
       const int nt = mnt_s[stage];
       const int fast = mfast_s[stage];
       const double* sst = sm + stage * C::STAGE;
       const double* ust = sst + TILE;
       const double* hst = ust + TILE;
-      // ---- neighbour face scalars q[t][k] (all consumer threads) ---------
+      // ---- neighbour face scalars q[t][k] (TraceSnapshot of iterate k) ----
 #pragma unroll
       for (int m = 0; m < (E * KC + NC - 1) / NC; ++m) {
         const int idx = tid + m * NC;
@@ -440,11 +487,18 @@ __global__ void __launch_bounds__(SCfg<D, N1, M, NCF, NWC, E, NS, G>::NT, 1)
         }
       }
       consumer_bar(NC);
+      double* outb = out_s + ob * TILE;
+      double* dcur = C::PIPE ? d_s + (it & 1) * TILE : d_s;
+      // ---- (PIPE) norm of the previous tile, independent of the DMMAs below
+      double nsum = 0.0;
+      if constexpr (C::PIPE) {
+        if (it > 0)
+          nsum = norm_units_2d<N1, M, NP, NV, E, NCW, UPW>(d_s + ((it - 1) & 1) * TILE, warp, lane, cfr,
+                                                           a.comp_w);
+      }
       // ---- lifted local solve u^{k+1} = s + L q on the fp64 tensor core --
       // D[row][elem] = s + sum_k L[row][k] q[elem][k]: rows = 8 x NRT row
       // tiles (warp w owns tiles w, w+NCW, ...), elements = 8 x NEG groups.
-      double* outb = out_s + ob * TILE;
-      const unsigned cset = mcset_s[stage];
       double acc[NEG][RTW][2];
 #pragma unroll
       for (int eg = 0; eg < NEG; ++eg) {
@@ -471,6 +525,7 @@ __global__ void __launch_bounds__(SCfg<D, N1, M, NCF, NWC, E, NS, G>::NT, 1)
         }
       } else {
         // one masked pass per operator class present in the tile
+        const unsigned cset = mcset_s[stage];
         for (unsigned rem = cset; rem != 0u; rem &= rem - 1u) {
           const int c = __ffs(rem) - 1;
           for (int ks = 0; ks < KS; ++ks) {
@@ -502,9 +557,16 @@ __global__ void __launch_bounds__(SCfg<D, N1, M, NCF, NWC, E, NS, G>::NT, 1)
             for (int v = 0; v < 2; ++v) {
               const int t = te + v;
               outb[t * NV + row] = acc[eg][j][v];
-              d_s[t * NV + row] = acc[eg][j][v] - ust[t * NV + row];
+              dcur[t * NV + row] = acc[eg][j][v] - ust[t * NV + row];
             }
           }
+        }
+      }
+      if constexpr (C::PIPE) {
+        if (it > 0) {
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) nsum += __shfl_xor_sync(0xffffffffu, nsum, o);
+          if (lane == 0) red_s[((it - 1) & 1) * 32 + warp] = nsum;
         }
       }
       fence_proxy_async();
@@ -514,39 +576,17 @@ __global__ void __launch_bounds__(SCfg<D, N1, M, NCF, NWC, E, NS, G>::NT, 1)
       if (tid == 0) {
         bulk_s2g(un + (int64_t)e0 * NV, outb, (uint32_t)(nt * NV * sizeof(double)));
         bulk_commit();
-      }
-      // ---- ||delta||_M^2 ---------------------------------------------------
-      // M = J (M1 (x) M1 [(x) M1]), M1 = C C^T  =>  d^T M d = J |(C^T (x) ..) d|^2
-      double acc2 = 0.0;
-      if constexpr (D == 2 && N1 <= 8) {
-        // per (element, component): Y = C^T Delta C on the fp64 tensor core,
-        // Delta[j][i] = delta at node (i, j), zero-padded to 8x8.
-        for (int u = warp; u < E * M; u += NCW) {
-          const int t = u / M, c = u - (u / M) * M;
-          const double* base = d_s + t * NV + c * NP;
-          double r0 = 0.0, r1 = 0.0;
-#pragma unroll
-          for (int ks = 0; ks < 2; ++ks) {
-            const int kk = 4 * ks + (lane & 3), nn = lane >> 2;
-            const double b = (kk < N1 && nn < N1) ? base[kk * N1 + nn] : 0.0;
-            dmma_8x8x4(r0, r1, cfr[ks], b);        // R = C^T Delta
-          }
-          double y0 = 0.0, y1 = 0.0;
-#pragma unroll
-          for (int ks = 0; ks < 2; ++ks) {
-            const int col = 4 * ks + (lane & 3);   // A fragment R[lane>>2][col]
-            const int src = (lane & ~3) | (col >> 1);
-            const double x0 = __shfl_sync(0xffffffffu, r0, src);
-            const double x1 = __shfl_sync(0xffffffffu, r1, src);
-            dmma_8x8x4(y0, y1, (col & 1) ? x1 : x0, cfr[ks]);  // Y = R C
-          }
-          acc2 = fma(a.comp_w[c] * y0, y0, acc2);
-          acc2 = fma(a.comp_w[c] * y1, y1, acc2);
+        if (C::PIPE && it > 0) {
+          double s = 0.0;
+          for (int w = 0; w < NCW; ++w) s += red_s[((it - 1) & 1) * 32 + w];
+          a.tile_partials[prev_tile] = a.jac * s;
         }
-        acc2 *= a.jac;
-      } else {
+      }
+      if constexpr (!C::PIPE) {
+        // ---- ||delta||_M^2 by sum-factorised Cholesky passes (C^T per axis)
         double* src = d_s;
         double* dst = t_s;
+        double acc2 = 0.0;
         int mul = 1;
 #pragma unroll
         for (int ax = 0; ax < D; ++ax) {
@@ -571,18 +611,33 @@ __global__ void __launch_bounds__(SCfg<D, N1, M, NCF, NWC, E, NS, G>::NT, 1)
           }
           mul *= N1;
         }
-        acc2 = rv ? cw * acc2 : 0.0;
-      }
-      // fixed-order tile reduction: lanes -> warps -> thread 0
-      double tsum = acc2;
+        double tsum = rv ? cw * acc2 : 0.0;
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) tsum += __shfl_xor_sync(0xffffffffu, tsum, o);
-      if (lane == 0) red_s[warp] = tsum;
-      consumer_bar(NC);
-      if (tid == 0) {
-        double s = 0.0;
-        for (int w = 0; w < NCW; ++w) s += red_s[w];
-        a.tile_partials[tile] = s;
+        for (int o = 16; o > 0; o >>= 1) tsum += __shfl_xor_sync(0xffffffffu, tsum, o);
+        if (lane == 0) red_s[warp] = tsum;
+        consumer_bar(NC);
+        if (tid == 0) {
+          double s = 0.0;
+          for (int w = 0; w < NCW; ++w) s += red_s[w];
+          a.tile_partials[tile] = s;
+        }
+      }
+      prev_tile = tile;
+    }
+    if constexpr (C::PIPE) {
+      // drain: norm of the last tile
+      if (it > 0) {
+        double nsum = norm_units_2d<N1, M, NP, NV, E, NCW, UPW>(d_s + ((it - 1) & 1) * TILE, warp, lane, cfr,
+                                                                a.comp_w);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) nsum += __shfl_xor_sync(0xffffffffu, nsum, o);
+        if (lane == 0) red_s[((it - 1) & 1) * 32 + warp] = nsum;
+        consumer_bar(NC);
+        if (tid == 0) {
+          double s = 0.0;
+          for (int w = 0; w < NCW; ++w) s += red_s[((it - 1) & 1) * 32 + w];
+          a.tile_partials[prev_tile] = a.jac * s;
+        }
       }
     }
     if (tid == 0) bulk_wait<0>();
