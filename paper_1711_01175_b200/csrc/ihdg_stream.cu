@@ -4,6 +4,7 @@
 #include <string>
 
 #include "ihdg_stream.cuh"
+#include "ihdg_ws.cuh"
 
 namespace ihdg {
 
@@ -37,17 +38,38 @@ int launch_stream_t(const ihdg_sweep_args* a, cudaStream_t st) {
   return cudaGetLastError() == cudaSuccess ? 0 : -2;
 }
 
+template <int N1, int M, int NCF, int NWC, int E, int NS>
+int launch_ws_t(const ihdg_sweep_args* a, cudaStream_t st) {
+  using C = WCfg<N1, M, NCF, NWC, E, NS>;
+  static_assert(E == Cfg<2, N1, M>::TE, "ws tile must equal the generic tile (tile partial count)");
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(k_sweep_ws<N1, M, NCF, NWC, E, NS>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::BYTES);
+    if (e != cudaSuccess) return -2;
+    configured = true;
+  }
+  Geo geo;
+  geo.init(a->g, E);
+  int64_t grid = geo.ntiles < stream_sms() ? geo.ntiles : stream_sms();
+  if (grid < 1) grid = 1;
+  k_sweep_ws<N1, M, NCF, NWC, E, NS><<<(unsigned)grid, C::NT, C::BYTES, st>>>(*a);
+  return cudaGetLastError() == cudaSuccess ? 0 : -2;
+}
+
 struct StreamEntry {
   int D, N1, M, NCF, NWC, E, NV;
   int (*launch)(const ihdg_sweep_args*, cudaStream_t);
 };
 
+#define IHDG_WS(N1, M, NCF, NWC, E, NS) \
+  {2, N1, M, NCF, NWC, E, M * N1 * N1, launch_ws_t<N1, M, NCF, NWC, E, NS>},
 #define IHDG_STREAM(D, N1, M, NCF, NWC, E, NS, G) \
   {D, N1, M, NCF, NWC, E, M * Pow<N1, D>::v, launch_stream_t<D, N1, M, NCF, NWC, E, NS, G>},
 
 const StreamEntry kStream[] = {
-    IHDG_STREAM(2, 7, 3, 4, 2, 16, 3, 2)   // config 5: CD 2D p=6
-    IHDG_STREAM(2, 5, 3, 4, 2, 16, 4, 4)   // configs 2/3: CD / SW 2D p=4
+    IHDG_WS(7, 3, 4, 2, 16, 3)             // config 5: CD 2D p=6 (warp-specialised)
+    IHDG_WS(5, 3, 4, 2, 16, 4)             // configs 2/3: CD / SW 2D p=4
     IHDG_STREAM(3, 4, 1, 3, 1, 32, 3, 4)   // config 4: transport 3D p=3
 };
 
