@@ -13,7 +13,8 @@ __all__ = ["NativeUnavailable", "lib", "Geom", "IterState", "AssemblyArgs", "Cla
            "FieldArgs", "QuadArgs", "SweepArgs", "FinalizeArgs", "TraceArgs", "check",
            "LIB_PATH", "STATUS_NAMES"]
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libihdg_cuda.so")
+LIB_PATH = os.environ.get("IHDG_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)),
+                                                     "libihdg_cuda.so")
 
 IHDG_OK = 0
 RUNNING, CONVERGED, DIVERGED, NAN, MAXITER = 0, 1, 2, 3, 4

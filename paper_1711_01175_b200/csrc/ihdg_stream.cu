@@ -108,6 +108,18 @@ const StreamEntry* stream_entry(const ihdg_sweep_args* a) {
 
 }  // namespace ihdg
 
+#ifdef IHDG_WS_PROF
+// profiling build only: read (and optionally reset) the per-role counters
+extern "C" int ihdg_ws_prof(unsigned long long* out, int reset) {
+  cudaMemcpyFromSymbol(out, ihdg::g_ws_prof, sizeof(unsigned long long) * 16);
+  if (reset) {
+    unsigned long long z[16] = {0};
+    cudaMemcpyToSymbol(ihdg::g_ws_prof, z, sizeof(z));
+  }
+  return 0;
+}
+#endif
+
 // 1 if the streaming kernel is used for these args, 0 for the generic one.
 int ihdg_stream_variant(const ihdg_sweep_args* a) { return ihdg::stream_entry(a) != nullptr ? 1 : 0; }
 

@@ -20,6 +20,19 @@
 
 namespace ihdg {
 
+// Optional per-role cycle counters (build with -DIHDG_WS_PROF; tools only).
+#ifdef IHDG_WS_PROF
+__device__ unsigned long long g_ws_prof[16];
+#define WS_T0(v) const long long v = clock64()
+#define WS_ACC(slot, v)                                                  \
+  do {                                                                   \
+    if ((threadIdx.x & 31) == 0) atomicAdd(&g_ws_prof[slot], (unsigned long long)(clock64() - (v))); \
+  } while (0)
+#else
+#define WS_T0(v)
+#define WS_ACC(slot, v)
+#endif
+
 template <int N1, int M, int NCF, int NWC, int E, int NS>
 struct WCfg {
   static constexpr int D = 2;
@@ -138,6 +151,7 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS>::NT, 1)
 
   const int fast_class = a.class_of_mask[0];
   const int ntiles = (int)geo.ntiles;
+  WS_T0(tk0);
   int n_my = 0;  // tiles of this CTA
   for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) ++n_my;
 
@@ -150,7 +164,9 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS>::NT, 1)
     for (int it = 0; it < n_my; ++it) {
       const int tile = blockIdx.x + it * gridDim.x;
       const int stage = it % NS;
+      WS_T0(tw0);
       if (it >= NS) mbar_wait(&empty_bar[stage], ((it / NS) - 1) & 1);
+      WS_ACC(0, tw0);
       double* sst = sm + stage * C::STAGE;
       double* ust = sst + TILE;
       double* hst = ust + TILE;
@@ -218,7 +234,10 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS>::NT, 1)
     const int ltid = nw * 32 + lane;
     for (int it = 0; it < n_my; ++it) {
       const int b = it & 1;
+      WS_T0(tn0);
       mbar_wait(&done_bar[b], (it >> 1) & 1);
+      WS_ACC(5, tn0);
+      WS_T0(tn1);
       double* dl = d_s + b * TILE;
       // pass 1 (axis 0, in place): row (t, c, j): y_i = sum_{i' >= i} C[i'][i] delta_{i'}
 #pragma unroll
@@ -273,6 +292,7 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS>::NT, 1)
         a.tile_partials[blockIdx.x + it * gridDim.x] = a.jac * s2;
       }
       __syncwarp();
+      WS_ACC(8, tn1);
       if (lane == 0) mbar_arrive(&normdone_bar[b]);
     }
   } else if (warp >= NCW) {
@@ -281,7 +301,10 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS>::NT, 1)
     int prev_e0 = 0, prev_nt = 0, prev_tile = -1, prev2_tile = -1;
     for (int it = 0; it < n_my; ++it) {
       const int stage = it % NS;
+      WS_T0(tp0);
       mbar_wait(&full_bar[stage], (it / NS) & 1);
+      WS_ACC(1, tp0);
+      WS_T0(tp1);
       // stage metadata is read now: the stage can be refilled once the
       // consumers release it, possibly before this warp stores the tile
       const int nt = mnt_s[stage];
@@ -315,10 +338,13 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS>::NT, 1)
         qst[t * KC + k] = v;
       }
       __syncwarp();
+      WS_ACC(9, tp1);
       if (lane == 0) mbar_arrive(&qready_bar[stage]);
       if (it >= 1) {
         const int pb = (it - 1) & 1;
+        WS_T0(tp2);
         mbar_wait(&done_bar[pb], ((it - 1) >> 1) & 1);
+        WS_ACC(2, tp2);
         if (pw == 0 && lane == 0) {
           bulk_s2g(un + (int64_t)prev_e0 * NV, out_s + pb * TILE, (uint32_t)(prev_nt * NV * sizeof(double)));
           bulk_commit();
@@ -359,7 +385,10 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS>::NT, 1)
     for (int it = 0; it < n_my; ++it) {
       const int stage = it % NS;
       const int ob = it & 1;
+      WS_T0(tc0);
       mbar_wait(&qready_bar[stage], (it / NS) & 1);
+      WS_ACC(3, tc0);
+      WS_T0(tc1);
       const int fast = mfast_s[stage];
       const double* sst = sm + stage * C::STAGE;
       const double* ust = sst + TILE;
@@ -410,10 +439,13 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS>::NT, 1)
           }
         }
       }
+      WS_ACC(7, tc1);
+      WS_T0(tc2);
       if (it >= 2) {
         mbar_wait(&outfree_bar[ob], ((it - 2) >> 1) & 1);
         mbar_wait(&normdone_bar[ob], ((it - 2) >> 1) & 1);
       }
+      WS_ACC(4, tc2);
       double* outb = out_s + ob * TILE;
       double* dcur = d_s + ob * TILE;
 #pragma unroll
@@ -441,6 +473,9 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS>::NT, 1)
     }
   }
 
+#ifdef IHDG_WS_PROF
+  if (tid == 0) WS_ACC(6, tk0);
+#endif
   if (a.finalize) {
     __threadfence();
     __syncthreads();

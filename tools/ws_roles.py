@@ -1,0 +1,53 @@
+#!/usr/bin/env python
+"""Per-role cycle breakdown of the warp-specialised sweep (profiling build).
+
+    IHDG_LIB=paper_1711_01175_b200/libihdg_cuda_prof.so python tools/ws_roles.py [cells]
+"""
+import ctypes
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch  # noqa: E402
+
+from paper_1711_01175_b200 import _native as N  # noqa: E402
+from paper_1711_01175_b200.solver import DeviceSolver  # noqa: E402
+from paper_1711_01175_b200.workloads import make_config  # noqa: E402
+
+NAMES = ["producer: wait empty", "prep: wait full", "prep: wait done", "consumer: wait qready",
+         "consumer: wait outfree+normdone", "norm: wait done", "CTA total", "consumer: contraction",
+         "norm: compute", "prep: q compute"]
+
+
+def main():
+    cells = int(sys.argv[1]) if len(sys.argv) > 1 else 2048
+    wl = make_config(5, cells=cells)
+    sv = DeviceSolver(wl.mesh, wl.problem, wl.ops, dt=wl.dt, max_iters=1000)
+    for name, fld in wl.initial.items():
+        sv.set_state_component(fld, sv.spec.labels.index(name))
+    sv.begin_step()
+    sv.reset_state(0.0, 1000)
+    a = sv.sweep_args("volume", 1)
+    L = N.lib()
+    L.ihdg_ws_prof.argtypes = [ctypes.c_void_p, ctypes.c_int]
+    buf = (ctypes.c_ulonglong * 16)()
+    for _ in range(3):
+        sv.sweep_once(a=a)
+    torch.cuda.synchronize()
+    L.ihdg_ws_prof(buf, 1)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    n = 5
+    for _ in range(n):
+        sv.sweep_once(a=a)
+    e1.record()
+    torch.cuda.synchronize()
+    L.ihdg_ws_prof(buf, 0)
+    print(f"{e0.elapsed_time(e1) / n:.3f} ms / sweep")
+    total = buf[6] / n / 148  # per CTA per sweep
+    for i, nm in enumerate(NAMES):
+        print(f"{nm:36s} {buf[i] / n / 148:14.0f} cycles/CTA/sweep (warp-summed)  {buf[i] / n / 148 / max(total, 1):6.2f}x CTA")
+
+
+if __name__ == "__main__":
+    main()
