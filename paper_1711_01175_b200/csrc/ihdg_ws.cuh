@@ -8,30 +8,15 @@
 //                    into an NS-stage ring                   -> full[stage]
 //   prep warps (4) : neighbour face scalars q (TraceSnapshot) for the stage
 //                    -> qready[stage]; then, one tile behind, the bulk store
-//                    of u^{k+1}
+//                    of u^{k+1} and the fixed-order tile partial of the norm
 //   consumer warps : DMMA contraction u^{k+1} = s + L q (L fragments in
-//                    registers), delta = u^{k+1} - u^k       -> done[i&1]
-//   norm warps (4) : J |(C^T x C^T) delta|^2 by two exact triangular DFMA
-//                    passes (rows in place, then columns), fixed-order tile
-//                    partial                                 -> normdone[i&1]
+//                    registers) for tile i interleaved with the tensor-core
+//                    norm J |C^T Delta C|^2 of tile i-1      -> done[i&1]
 #pragma once
 
 #include "ihdg_stream.cuh"
 
 namespace ihdg {
-
-// Optional per-role cycle counters (build with -DIHDG_WS_PROF; tools only).
-#ifdef IHDG_WS_PROF
-__device__ unsigned long long g_ws_prof[16];
-#define WS_T0(v) const long long v = clock64()
-#define WS_ACC(slot, v)                                                  \
-  do {                                                                   \
-    if ((threadIdx.x & 31) == 0) atomicAdd(&g_ws_prof[slot], (unsigned long long)(clock64() - (v))); \
-  } while (0)
-#else
-#define WS_T0(v)
-#define WS_ACC(slot, v)
-#endif
 
 template <int N1, int M, int NCF, int NWC, int E, int NS>
 struct WCfg {
@@ -43,12 +28,11 @@ struct WCfg {
   static constexpr int NRT = (NV + 7) / 8;
   static constexpr int KS = KC / 4;
   static constexpr int NEG = E / 8;
-  static constexpr int NCW = NRT >= 16 ? 8 : (NRT >= 8 ? 8 : 4);   // consumer warps
+  static constexpr int NCW = NRT >= 16 ? 10 : (NRT >= 8 ? 8 : 4);  // consumer warps
   static constexpr int RTW = (NRT + NCW - 1) / NCW;
+  static constexpr int UPW = (E * M + NCW - 1) / NCW;
   static constexpr int NQW = 4;                                    // prep warps
-  static constexpr int NNW = 4;                                    // norm warps
-  static constexpr int NT = 32 * (NCW + NQW + NNW + 1);
-  static constexpr int NROWS = E * M * N1;                         // norm rows per tile
+  static constexpr int NT = 32 * (NCW + NQW + 1);
   static constexpr int TILE = E * NV;
   static constexpr int HALO = E * NCF * NWC * NF;
   static constexpr int QT = E * KC;
@@ -57,7 +41,7 @@ struct WCfg {
   static constexpr int OFF_D = OFF_OUT + 2 * TILE;
   static constexpr int OFF_RED = OFF_D + 2 * TILE;
   static constexpr int N_DBL = OFF_RED + 64;
-  static constexpr int NBAR = 3 * NS + 6;
+  static constexpr int NBAR = 3 * NS + 4;
   static constexpr size_t BYTES = (size_t)N_DBL * sizeof(double) + NBAR * sizeof(uint64_t);
   static_assert(KC % 4 == 0 && E % 8 == 0 && E <= 32 && N1 <= 8, "ws config");
   static_assert((TILE * sizeof(double)) % 16 == 0, "tile bytes must be 16-byte multiples");
@@ -69,8 +53,8 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS>::NT, 1)
     k_sweep_ws(const ihdg_sweep_args a) {
   using C = WCfg<N1, M, NCF, NWC, E, NS>;
   constexpr int D = 2, NP = C::NP, NV = C::NV, NF = C::NF, NFACE = 4, KC = C::KC;
-  constexpr int NRT = C::NRT, KS = C::KS, NEG = C::NEG, NCW = C::NCW, RTW = C::RTW;
-  constexpr int NQW = C::NQW, NNW = C::NNW, TILE = C::TILE;
+  constexpr int NRT = C::NRT, KS = C::KS, NEG = C::NEG, NCW = C::NCW, RTW = C::RTW, UPW = C::UPW;
+  constexpr int NQW = C::NQW, TILE = C::TILE;
 
   extern __shared__ __align__(16) double sm[];
   double* out_s = sm + C::OFF_OUT;
@@ -82,7 +66,6 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS>::NT, 1)
   uint64_t* empty_bar = bars + 2 * NS;   // [NS] consumers -> producer
   uint64_t* done_bar = bars + 3 * NS;    // [2]  consumers -> prep, consumers
   uint64_t* outfree_bar = done_bar + 2;  // [2]  prep -> consumers
-  uint64_t* normdone_bar = done_bar + 4; // [2]  norm warps -> consumers (delta buffer free)
 
   __shared__ int fv_s[NFACE][NF];
   __shared__ int cf_s[NCF];
@@ -143,7 +126,6 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS>::NT, 1)
     for (int b = 0; b < 2; ++b) {
       mbar_init(&done_bar[b], NCW);
       mbar_init(&outfree_bar[b], 1);
-      mbar_init(&normdone_bar[b], C::NNW);
     }
     fence_mbar_init();
   }
@@ -151,11 +133,10 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS>::NT, 1)
 
   const int fast_class = a.class_of_mask[0];
   const int ntiles = (int)geo.ntiles;
-  WS_T0(tk0);
   int n_my = 0;  // tiles of this CTA
   for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) ++n_my;
 
-  if (warp == NCW + NQW + NNW) {
+  if (warp == NCW + NQW) {
     // ============================ producer warp ============================
     const int c0 = (int)a.g.cells[0];
     const int per0 = a.g.periodic[0];
@@ -164,9 +145,7 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS>::NT, 1)
     for (int it = 0; it < n_my; ++it) {
       const int tile = blockIdx.x + it * gridDim.x;
       const int stage = it % NS;
-      WS_T0(tw0);
       if (it >= NS) mbar_wait(&empty_bar[stage], ((it / NS) - 1) & 1);
-      WS_ACC(0, tw0);
       double* sst = sm + stage * C::STAGE;
       double* ust = sst + TILE;
       double* hst = ust + TILE;
@@ -228,83 +207,13 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS>::NT, 1)
       }
       cp_async_arrive_noinc(&full_bar[stage]);
     }
-  } else if (warp >= NCW + NQW) {
-    // ============================ norm warps ===============================
-    const int nw = warp - NCW - NQW;
-    const int ltid = nw * 32 + lane;
-    for (int it = 0; it < n_my; ++it) {
-      const int b = it & 1;
-      WS_T0(tn0);
-      mbar_wait(&done_bar[b], (it >> 1) & 1);
-      WS_ACC(5, tn0);
-      WS_T0(tn1);
-      double* dl = d_s + b * TILE;
-      // pass 1 (axis 0, in place): row (t, c, j): y_i = sum_{i' >= i} C[i'][i] delta_{i'}
-#pragma unroll
-      for (int m = 0; m < (C::NROWS + 32 * NNW - 1) / (32 * NNW); ++m) {
-        const int rw = ltid + m * 32 * NNW;
-        if (rw < C::NROWS) {
-          double* row = dl + rw * N1;   // rows are contiguous: (t*M + c)*NP + j*N1
-          double x[N1], y[N1];
-#pragma unroll
-          for (int i = 0; i < N1; ++i) x[i] = row[i];
-#pragma unroll
-          for (int i = 0; i < N1; ++i) {
-            double v = 0.0;
-#pragma unroll
-            for (int ip = i; ip < N1; ++ip) v = fma(chol_s[ip * N1 + i], x[ip], v);
-            y[i] = v;
-          }
-#pragma unroll
-          for (int i = 0; i < N1; ++i) row[i] = y[i];
-        }
-      }
-      asm volatile("bar.sync 2, %0;" ::"n"(32 * NNW) : "memory");
-      // pass 2 (axis 1): column (t, c, i): z_j = sum_{j' >= j} C[j'][j] y_{j'}
-      double accn = 0.0;
-#pragma unroll
-      for (int m = 0; m < (C::NROWS + 32 * NNW - 1) / (32 * NNW); ++m) {
-        const int cl = ltid + m * 32 * NNW;
-        if (cl < C::NROWS) {
-          const int tc = cl / N1, i = cl - (cl / N1) * N1;
-          const double* col = dl + tc * NP + i;
-          double y[N1];
-#pragma unroll
-          for (int j = 0; j < N1; ++j) y[j] = col[j * N1];
-          double sq = 0.0;
-#pragma unroll
-          for (int j = 0; j < N1; ++j) {
-            double v = 0.0;
-#pragma unroll
-            for (int jp = j; jp < N1; ++jp) v = fma(chol_s[jp * N1 + j], y[jp], v);
-            sq = fma(v, v, sq);
-          }
-          accn = fma(a.comp_w[tc % M], sq, accn);
-        }
-      }
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) accn += __shfl_xor_sync(0xffffffffu, accn, o);
-      if (lane == 0) red_s[b * 32 + nw] = accn;
-      asm volatile("bar.sync 2, %0;" ::"n"(32 * NNW) : "memory");
-      if (ltid == 0) {
-        double s2 = 0.0;
-        for (int w = 0; w < NNW; ++w) s2 += red_s[b * 32 + w];
-        a.tile_partials[blockIdx.x + it * gridDim.x] = a.jac * s2;
-      }
-      __syncwarp();
-      WS_ACC(8, tn1);
-      if (lane == 0) mbar_arrive(&normdone_bar[b]);
-    }
   } else if (warp >= NCW) {
     // ============================ prep warps ===============================
     const int pw = warp - NCW;
     int prev_e0 = 0, prev_nt = 0, prev_tile = -1, prev2_tile = -1;
     for (int it = 0; it < n_my; ++it) {
       const int stage = it % NS;
-      WS_T0(tp0);
       mbar_wait(&full_bar[stage], (it / NS) & 1);
-      WS_ACC(1, tp0);
-      WS_T0(tp1);
       // stage metadata is read now: the stage can be refilled once the
       // consumers release it, possibly before this warp stores the tile
       const int nt = mnt_s[stage];
@@ -338,16 +247,18 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS>::NT, 1)
         qst[t * KC + k] = v;
       }
       __syncwarp();
-      WS_ACC(9, tp1);
       if (lane == 0) mbar_arrive(&qready_bar[stage]);
       if (it >= 1) {
         const int pb = (it - 1) & 1;
-        WS_T0(tp2);
         mbar_wait(&done_bar[pb], ((it - 1) >> 1) & 1);
-        WS_ACC(2, tp2);
         if (pw == 0 && lane == 0) {
           bulk_s2g(un + (int64_t)prev_e0 * NV, out_s + pb * TILE, (uint32_t)(prev_nt * NV * sizeof(double)));
           bulk_commit();
+          if (it >= 2) {
+            double s = 0.0;
+            for (int w = 0; w < NCW; ++w) s += red_s[(it & 1) * 32 + w];   // tile it-2
+            a.tile_partials[prev2_tile] = a.jac * s;
+          }
           if (it >= 2) {
             bulk_wait_read<1>();                       // store of tile it-2 has read its buffer
             mbar_arrive(&outfree_bar[it & 1]);
@@ -366,6 +277,11 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS>::NT, 1)
       if (pw == 0 && lane == 0) {
         bulk_s2g(un + (int64_t)prev_e0 * NV, out_s + (L & 1) * TILE, (uint32_t)(prev_nt * NV * sizeof(double)));
         bulk_commit();
+        if (L >= 1) {
+          double s = 0.0;
+          for (int w = 0; w < NCW; ++w) s += red_s[((L - 1) & 1) * 32 + w];
+          a.tile_partials[prev2_tile] = a.jac * s;
+        }
         bulk_wait<0>();
       }
     }
@@ -382,17 +298,27 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS>::NT, 1)
         Lf[j][ks] = (row < NV) ? __ldg(a.LT + ((size_t)fast_class * (NFACE * NF) + col) * NV + row) : 0.0;
       }
     }
+    double cfr[2];
+#pragma unroll
+    for (int ks = 0; ks < 2; ++ks) {
+      const int kk = 4 * ks + (lane & 3), nn = lane >> 2;
+      cfr[ks] = (kk < N1 && nn < N1) ? chol_s[kk * N1 + nn] : 0.0;
+    }
     for (int it = 0; it < n_my; ++it) {
       const int stage = it % NS;
       const int ob = it & 1;
-      WS_T0(tc0);
       mbar_wait(&qready_bar[stage], (it / NS) & 1);
-      WS_ACC(3, tc0);
-      WS_T0(tc1);
       const int fast = mfast_s[stage];
       const double* sst = sm + stage * C::STAGE;
       const double* ust = sst + TILE;
       const double* qst = ust + TILE + C::HALO;
+      // norm of the previous tile (needs every warp's delta of tile it-1)
+      double nsum = 0.0;
+      if (it >= 1) {
+        mbar_wait(&done_bar[(it - 1) & 1], ((it - 1) >> 1) & 1);
+        nsum = norm_units_2d<N1, M, NP, NV, E, NCW, UPW>(d_s + ((it - 1) & 1) * TILE, warp, lane, cfr,
+                                                         a.comp_w);
+      }
       double acc[NEG][RTW][2];
 #pragma unroll
       for (int eg = 0; eg < NEG; ++eg) {
@@ -439,13 +365,7 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS>::NT, 1)
           }
         }
       }
-      WS_ACC(7, tc1);
-      WS_T0(tc2);
-      if (it >= 2) {
-        mbar_wait(&outfree_bar[ob], ((it - 2) >> 1) & 1);
-        mbar_wait(&normdone_bar[ob], ((it - 2) >> 1) & 1);
-      }
-      WS_ACC(4, tc2);
+      if (it >= 2) mbar_wait(&outfree_bar[ob], ((it - 2) >> 1) & 1);
       double* outb = out_s + ob * TILE;
       double* dcur = d_s + ob * TILE;
 #pragma unroll
@@ -464,6 +384,11 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS>::NT, 1)
           }
         }
       }
+      if (it >= 1) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) nsum += __shfl_xor_sync(0xffffffffu, nsum, o);
+        if (lane == 0) red_s[((it - 1) & 1) * 32 + warp] = nsum;
+      }
       fence_proxy_async();
       __syncwarp();
       if (lane == 0) {
@@ -471,11 +396,24 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS>::NT, 1)
         mbar_arrive(&done_bar[ob]);
       }
     }
+    // drain: norm of the last tile
+    if (n_my >= 1) {
+      const int L = n_my - 1;
+      mbar_wait(&done_bar[L & 1], (L >> 1) & 1);
+      double nsum = norm_units_2d<N1, M, NP, NV, E, NCW, UPW>(d_s + (L & 1) * TILE, warp, lane, cfr, a.comp_w);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) nsum += __shfl_xor_sync(0xffffffffu, nsum, o);
+      if (lane == 0) red_s[(L & 1) * 32 + warp] = nsum;
+    }
   }
 
-#ifdef IHDG_WS_PROF
-  if (tid == 0) WS_ACC(6, tk0);
-#endif
+  __syncthreads();
+  if (tid == 0 && n_my >= 1) {
+    const int L = n_my - 1;
+    double s = 0.0;
+    for (int w = 0; w < NCW; ++w) s += red_s[(L & 1) * 32 + w];
+    a.tile_partials[blockIdx.x + L * gridDim.x] = a.jac * s;
+  }
   if (a.finalize) {
     __threadfence();
     __syncthreads();
