@@ -292,6 +292,44 @@ def run_ours(args):
                "h2d_bytes_per_step": int(nloc * nv * 8), "d2h_bytes_per_step": int(nloc * nv * 8),
                "sweeps": r.iterations, "seconds": dt_e2e,
                "what": "one backward-Euler step via DeviceSolver (upload u^m, RHS, iterate to 1e-10, download)"}
+    # ---- per-sweep throughput of the other BASELINE configs (same kernels) ----
+    others = {}
+    if args.other_configs and world == 1:
+        from paper_1711_01175_b200.workloads import make_config
+
+        for cfg in (4, 3, 2):
+            wo = make_config(cfg, seed=args.seed)
+            so = DeviceSolver(wo.mesh, wo.problem, wo.ops, dt=wo.dt, max_iters=1000)
+            if wo.problem.forcing if hasattr(wo.problem, "forcing") else None:
+                so.set_forcing(wo.problem.forcing)
+            so.zero_state()
+            for name, fld in wo.initial.items():
+                so.set_state_component(fld, so.spec.labels.index(name))
+            if wo.dt is not None:
+                so.begin_step()
+            else:
+                so.prepare_steady()
+            so.reset_state(tol=0.0, max_iters=1000)
+            ao = so.sweep_args("volume", finalize=1)
+            for _ in range(3):
+                so.sweep_once(a=ao)
+            nrep = 20
+            eo0, eo1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            torch.cuda.synchronize()
+            eo0.record(so.stream)
+            for _ in range(nrep):
+                so.sweep_once(a=ao)
+            eo1.record(so.stream)
+            torch.cuda.synchronize()
+            tms = eo0.elapsed_time(eo1) / nrep
+            dofs_o = so.nloc * so.nv
+            ach = BYTES_PER_DOF * dofs_o / (tms / 1e3) / 1e9
+            others[f"config{cfg}"] = {
+                "workload": wo.name, "dofs": int(dofs_o), "ms_per_sweep": tms,
+                "dof_updates_per_s": dofs_o / (tms / 1e3), "roofline_frac": ach / _peaks()[0],
+                "kernel": "stream" if sv.L.ihdg_stream_variant(__import__("ctypes").byref(ao)) else "generic"}
+            del so
+            torch.cuda.empty_cache()
     cpu = None
     if rank == 0 and world == 1 and args.cpu_baseline:
         threads = len(os.sched_getaffinity(0))
@@ -317,6 +355,9 @@ def run_ours(args):
             "time_to_converge": ttc or None,
             "e2e": e2e,
             "cpu_baseline": cpu,
+            "kernel": "sm_100a warp-specialised TMA/DMMA sweep" if sv.L.ihdg_stream_variant(
+                __import__("ctypes").byref(a)) else "generic sweep",
+            "other_configs": others or None,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -338,6 +379,7 @@ def main():
     ap.add_argument("--ttc-kappas", type=float, nargs="*", default=[1e-3])
     ap.add_argument("--no-e2e", dest="e2e", action="store_false")
     ap.add_argument("--no-cpu", dest="cpu_baseline", action="store_false")
+    ap.add_argument("--no-others", dest="other_configs", action="store_false")
     ap.add_argument("--cpu-rows", type=int, default=64)
     ap.add_argument("--cpu-reps", type=int, default=3)
     args = ap.parse_args()
