@@ -300,8 +300,9 @@ def run_ours(args):
         for cfg in (4, 3, 2):
             wo = make_config(cfg, seed=args.seed)
             so = DeviceSolver(wo.mesh, wo.problem, wo.ops, dt=wo.dt, max_iters=1000)
-            if wo.problem.forcing if hasattr(wo.problem, "forcing") else None:
-                so.set_forcing(wo.problem.forcing)
+            forcing = getattr(wo.problem, "forcing", None)
+            if forcing is not None:
+                so.set_forcing(forcing)
             so.zero_state()
             for name, fld in wo.initial.items():
                 so.set_state_component(fld, so.spec.labels.index(name))
