@@ -5,6 +5,7 @@
 
 #include "ihdg_stream.cuh"
 #include "ihdg_ws.cuh"
+#include "ihdg_v3.cuh"
 
 namespace ihdg {
 
@@ -57,17 +58,42 @@ int launch_ws_t(const ihdg_sweep_args* a, cudaStream_t st) {
   return cudaGetLastError() == cudaSuccess ? 0 : -2;
 }
 
+template <int D, int N1, int M, int NCF, int NWC, int NS, int NCW, int PF>
+int launch_v3_t(const ihdg_sweep_args* a, cudaStream_t st) {
+  using C = V3Cfg<D, N1, M, NCF, NWC, NS, NCW, PF>;
+  static_assert(8 * PF == Cfg<D, N1, M>::TE, "v3 logical tile must equal the generic tile (tile partial count)");
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(k_sweep_v3<D, N1, M, NCF, NWC, NS, NCW, PF>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::BYTES);
+    if (e != cudaSuccess) return -2;
+    configured = true;
+  }
+  Geo geo;
+  geo.init(a->g, 8 * PF);
+  int64_t grid = geo.ntiles < stream_sms() ? geo.ntiles : stream_sms();
+  if (grid < 1) grid = 1;
+  k_sweep_v3<D, N1, M, NCF, NWC, NS, NCW, PF><<<(unsigned)grid, C::NT, C::BYTES, st>>>(*a);
+  return cudaGetLastError() == cudaSuccess ? 0 : -2;
+}
+
 struct StreamEntry {
   int D, N1, M, NCF, NWC, E, NV;
   int (*launch)(const ihdg_sweep_args*, cudaStream_t);
+  int v3;  // version-3 kernel (physical 8-element tiles)
 };
 
+#define IHDG_V3(D, N1, M, NCF, NWC, NS, NCW, PF) \
+  {D, N1, M, NCF, NWC, 8 * PF, M * Pow<N1, D>::v, launch_v3_t<D, N1, M, NCF, NWC, NS, NCW, PF>, 1},
 #define IHDG_WS(N1, M, NCF, NWC, E, NS) \
-  {2, N1, M, NCF, NWC, E, M * N1 * N1, launch_ws_t<N1, M, NCF, NWC, E, NS>},
+  {2, N1, M, NCF, NWC, E, M * N1 * N1, launch_ws_t<N1, M, NCF, NWC, E, NS>, 0},
 #define IHDG_STREAM(D, N1, M, NCF, NWC, E, NS, G) \
-  {D, N1, M, NCF, NWC, E, M * Pow<N1, D>::v, launch_stream_t<D, N1, M, NCF, NWC, E, NS, G>},
+  {D, N1, M, NCF, NWC, E, M * Pow<N1, D>::v, launch_stream_t<D, N1, M, NCF, NWC, E, NS, G>, 0},
 
 const StreamEntry kStream[] = {
+    IHDG_V3(2, 7, 3, 4, 2, 12, 5, 2)       // config 5: CD 2D p=6 (8 warps: 255-register cap)
+    IHDG_V3(2, 5, 3, 4, 2, 16, 8, 2)       // configs 2/3: CD / SW 2D p=4
+    IHDG_V3(3, 4, 1, 3, 1, 16, 6, 4)       // config 4: transport 3D p=3
     IHDG_WS(7, 3, 4, 2, 16, 3)             // config 5: CD 2D p=6 (warp-specialised)
     IHDG_WS(5, 3, 4, 2, 16, 4)             // configs 2/3: CD / SW 2D p=4
     IHDG_STREAM(3, 4, 1, 3, 1, 32, 3, 4)   // config 4: transport 3D p=3
@@ -81,6 +107,11 @@ const StreamEntry* stream_entry(const ihdg_sweep_args* a) {
     forced_generic = (s != nullptr && std::strcmp(s, "generic") == 0) ? 1 : 0;
   }
   if (forced_generic) return nullptr;
+  static int no_v3 = -1;
+  if (no_v3 < 0) {
+    const char* s = std::getenv("IHDG_SWEEP_IMPL");
+    no_v3 = (s != nullptr && (std::strcmp(s, "ws") == 0 || std::strcmp(s, "stream") == 0)) ? 1 : 0;
+  }
   if (a->norm_kind != IHDG_NORM_VOLUME) return nullptr;
   const ihdg_geom& g = a->g;
   int ncf = 0, maxw = 0;
@@ -94,10 +125,11 @@ const StreamEntry* stream_entry(const ihdg_sweep_args* a) {
   for (const StreamEntry& e : kStream) {
     if (e.D != g.dim || e.N1 != g.order + 1 || e.M != g.ncomp) continue;
     if (e.NCF != ncf || maxw > e.NWC) continue;
+    if (e.v3 && no_v3) continue;
     Geo geo;
     geo.init(g, e.E);
     if (geo.tile_len % e.E != 0) continue;                       // full tiles only
-    if (g.cells[0] % e.E != 0) continue;                         // tiles inside one axis-0 row
+    if (g.cells[0] % (e.v3 ? 8 : e.E) != 0) continue;            // tiles inside one axis-0 row
     if (geo.nloc + 2 * geo.ls >= (1LL << 31) || geo.ntiles >= (1LL << 31)) continue;  // 32-bit indices
     if ((geo.ls * e.NV * 8) % 16 != 0) continue;                  // ghost offset
     if (((uintptr_t)a->u_old | (uintptr_t)a->u_new | (uintptr_t)a->s) % 16 != 0) continue;

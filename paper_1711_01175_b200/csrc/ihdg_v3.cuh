@@ -1,0 +1,387 @@
+// iHDG-II sweep, version 3: one consumer warp owns one 8-element tile end to
+// end, so consumer warps never wait on each other (production path for the
+// 2D and 3D BASELINE configs 2-5).
+//
+//   producer warp  : per tile, metadata + one TMA bulk copy (cp.async.bulk) of
+//                    the u^k tile + cp.async gathers of the out-of-tile
+//                    neighbour face nodes into an NS-deep stage ring (-> full);
+//                    retires stages in order (waits done) and reduces the tile
+//                    partials of the stopping norm in a fixed order.
+//   prep warps (2) : neighbour face scalars q (TraceSnapshot of iterate k)
+//                    for the stage (-> qready).
+//   consumer warps : issue the loads of s straight into the DMMA
+//                    accumulators (before waiting on the stage), run
+//                    u^{k+1} = s + L q on the fp64 tensor core
+//                    (mma.sync.m8n8k4.f64; L fragments in shared memory,
+//                    conflict-free), store u^{k+1} from registers, write
+//                    delta = u^{k+1} - u^k in place over the staged u^k tile
+//                    and reduce J |(C^T x .. x C^T) delta|^2 with exact
+//                    triangular DFMA passes (warp-local)   (-> done).
+//
+// HBM per element-DOF: s (LDG), u^k (TMA), u^{k+1} (STG) = 24 B.
+#pragma once
+
+#include "ihdg_stream.cuh"
+
+namespace ihdg {
+
+template <int D, int N1, int M, int NCF, int NWC, int NS, int NCW, int PF>
+struct V3Cfg {
+  static constexpr int E = 8;                     // elements per physical tile (DMMA n)
+  static constexpr int NP = Pow<N1, D>::v;
+  static constexpr int NV = M * NP;
+  static constexpr int NF = Pow<N1, D - 1>::v;
+  static constexpr int NFACE = 2 * D;
+  static constexpr int KC = NCF * NF;
+  static constexpr int NRT = (NV + 7) / 8;        // DMMA row tiles
+  static constexpr int KS = KC / 4;               // DMMA k steps
+  static constexpr int NQW = 2;                   // prep warps
+  static constexpr int NT = 32 * (NCW + NQW + 1);
+  static constexpr int MAXREG = (65536 / NT) / 8 * 8 > 255 ? 255 : (65536 / NT) / 8 * 8;
+  static constexpr int TILE = E * NV;
+  static constexpr int HALO = E * NCF * NWC * NF;
+  static constexpr int QT = E * KC;
+  static constexpr int STAGE = TILE + HALO + QT;  // doubles
+  static constexpr int LFR = NRT * KS * 32;       // L fragments (doubles)
+  static constexpr int OFF_L = NS * STAGE;
+  static constexpr int N_DBL = OFF_L + LFR;
+  static constexpr size_t BYTES = (size_t)N_DBL * sizeof(double) + 3 * NS * sizeof(uint64_t);
+  static constexpr int LPL = NP / N1;             // norm lines per (element, component) and axis
+  static constexpr int NLINES = E * M * LPL;
+  static_assert(KC % 4 == 0, "DMMA k");
+  static_assert(E % 2 == 0 && (TILE * sizeof(double)) % 16 == 0, "bulk copy alignment");
+  static_assert(E % NQW == 0, "prep split");
+};
+
+template <int D, int N1, int M, int NCF, int NWC, int NS, int NCW, int PF>
+__global__ void __launch_bounds__(V3Cfg<D, N1, M, NCF, NWC, NS, NCW, PF>::NT, 1) __maxnreg__((V3Cfg<D, N1, M, NCF, NWC, NS, NCW, PF>::MAXREG))
+    k_sweep_v3(const ihdg_sweep_args a) {
+  using C = V3Cfg<D, N1, M, NCF, NWC, NS, NCW, PF>;
+  constexpr int E = C::E, NP = C::NP, NV = C::NV, NF = C::NF, NFACE = C::NFACE, KC = C::KC;
+  constexpr int NRT = C::NRT, KS = C::KS, NQW = C::NQW, TILE = C::TILE;
+
+  extern __shared__ __align__(16) double sm[];
+  const double* lfr_s = sm + C::OFF_L;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sm + C::N_DBL);
+  uint64_t* full_bar = bars;
+  uint64_t* qready_bar = bars + NS;
+  uint64_t* done_bar = bars + 2 * NS;
+
+  __shared__ int fv_s[NFACE][NF];
+  __shared__ int cf_s[NCF];
+  __shared__ int wc_s[NCF][NWC];
+  __shared__ double ww_s[NCF][NWC];
+  __shared__ double chol_s[N1 * N1];
+  __shared__ double cw_s[IHDG_MAX_COMP];
+  __shared__ int qf_s[KC], qh_s[KC];
+  __shared__ int qt_s[KC][NWC];
+  __shared__ int mfast_s[NS];
+  __shared__ unsigned mcset_s[NS];
+  __shared__ int mmask_s[NS][E], mcls_s[NS][E];
+  __shared__ double part_s[NS];
+  __shared__ int last_s;
+
+  ihdg_iter_state* st = a.state;
+  if (st->status != IHDG_RUNNING) return;
+
+  const int tid = threadIdx.x;
+  const int warp = tid >> 5, lane = tid & 31;
+  Geo geo;
+  geo.init(a.g, E * PF);  // logical tile = PF physical tiles = the generic kernel's tile
+  const int64_t ls = geo.ls;
+  const double* __restrict__ uo = a.u_old + ls * NV;
+  double* __restrict__ un = a.u_new + ls * NV;
+  const int fast_class = a.class_of_mask[0];
+
+  for (int i = tid; i < NFACE * NF; i += blockDim.x) fv_s[i / NF][i % NF] = face_node_vidx(D, N1, i / NF, i % NF);
+  for (int i = tid; i < N1 * N1; i += blockDim.x) chol_s[i] = a.chol1d[i];
+  if (tid < IHDG_MAX_COMP) cw_s[tid] = a.comp_w[tid];
+  if (tid == 0) {
+    int n = 0;
+    for (int f = 0; f < NFACE && n < NCF; ++f) {
+      if (!a.coupled[f]) continue;
+      cf_s[n] = f;
+      int j = 0;
+      for (int c = 0; c < M && j < NWC; ++c)
+        if (a.face_w[f][c] != 0.0) {
+          wc_s[n][j] = c;
+          ww_s[n][j] = a.face_w[f][c];
+          ++j;
+        }
+      for (; j < NWC; ++j) {
+        wc_s[n][j] = 0;
+        ww_s[n][j] = 0.0;
+      }
+      ++n;
+    }
+    for (int k = 0; k < KC; ++k) {
+      const int ci = k / NF, nn = k % NF, f = cf_s[ci];
+      qf_s[k] = f;
+      for (int j = 0; j < NWC; ++j) qt_s[k][j] = wc_s[ci][j] * NP + face_node_vidx(D, N1, f ^ 1, nn);
+      qh_s[k] = ci * NWC * NF + nn;
+    }
+    for (int s = 0; s < NS; ++s) {
+      mbar_init(&full_bar[s], 1 + 32);
+      mbar_init(&qready_bar[s], NQW);
+      mbar_init(&done_bar[s], 1);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+  // interior-class L in DMMA A-fragment order: frag (rt, ks), lane l ->
+  // L[8 rt + (l>>2)][4 ks + (l&3)]; one 256-byte contiguous run per fragment
+  for (int idx = tid; idx < C::LFR; idx += blockDim.x) {
+    const int l = idx & 31, fr = idx >> 5;
+    const int rt = fr / KS, ks = fr - (fr / KS) * KS;
+    const int row = rt * 8 + (l >> 2);
+    const int k = 4 * ks + (l & 3);
+    const int col = cf_s[k / NF] * NF + (k % NF);
+    sm[C::OFF_L + idx] = (row < NV) ? a.LT[((size_t)fast_class * (NFACE * NF) + col) * NV + row] : 0.0;
+  }
+  __syncthreads();
+
+  const int nlog = (int)geo.ntiles;
+  const int n_log_my = nlog > (int)blockIdx.x ? (nlog - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
+  const int n_items = n_log_my * PF;
+  const int nlay = (int)(a.g.layer_end - a.g.layer_begin);
+  const int lsi = (int)ls;
+  auto phys_of = [&](int it) { return ((int)blockIdx.x + (it / PF) * (int)gridDim.x) * PF + it % PF; };
+
+  if (warp == NCW + NQW) {
+    // ============================ producer warp ============================
+    const int c0 = (int)a.g.cells[0];
+    const int per0 = a.g.periodic[0];
+    double pacc = 0.0;
+    auto retire = [&](int j) {
+      const int sj = j % NS;
+      mbar_wait(&done_bar[sj], (j / NS) & 1);
+      pacc += part_s[sj];
+      if (j % PF == PF - 1) {
+        if (lane == 0) a.tile_partials[(int)blockIdx.x + (j / PF) * (int)gridDim.x] = a.jac * pacc;
+        pacc = 0.0;
+      }
+    };
+    for (int it = 0; it < n_items; ++it) {
+      const int stage = it % NS;
+      if (it >= NS) retire(it - NS);
+      double* ust = sm + stage * C::STAGE;
+      double* hst = ust + TILE;
+      STile<D> ti;
+      ti.init(a.g, phys_of(it), E, nlay, lsi);
+      const int e0 = ti.e0;
+      int cls = -1;
+      if (lane < E) {
+        const int mask = ti.mask(lane, c0, per0);
+        cls = a.class_of_mask[mask];
+        mmask_s[stage][lane] = mask;
+        mcls_s[stage][lane] = cls;
+      }
+      const int fast = __all_sync(0xffffffffu, lane >= E || cls == fast_class);
+      unsigned cset = (lane < E && cls >= 0 && cls < 32) ? (1u << cls) : 0u;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) cset |= __shfl_xor_sync(0xffffffffu, cset, o);
+      if (lane == 0) {
+        mfast_s[stage] = fast;
+        mcset_s[stage] = cset;
+      }
+      __syncwarp();
+      if (lane == 0) {
+        constexpr uint32_t bytes = (uint32_t)(TILE * sizeof(double));
+        mbar_arrive_expect_tx(&full_bar[stage], bytes);  // release: metadata above
+        bulk_g2s(ust, uo + (int64_t)e0 * NV, bytes, &full_bar[stage]);
+      }
+      constexpr int RUN = NWC * NF;
+#pragma unroll
+      for (int ci = 0; ci < NCF; ++ci) {
+        const int f = cf_s[ci];
+        if ((f >> 1) == 0) {
+          const int t = (f == 0) ? 0 : E - 1;
+          const int i = ti.i0 + t;
+          const bool ex = (f == 0) ? (i > 0 || per0) : (i < c0 - 1 || per0);
+          if (!ex) continue;
+          const int nb = e0 + t + ((f == 0) ? (i > 0 ? -1 : c0 - 1) : (i < c0 - 1 ? 1 : -(c0 - 1)));
+          const double* base = uo + (int64_t)nb * NV;
+          for (int item = lane; item < RUN; item += 32) {
+            const int j = item / NF, n = item - (item / NF) * NF;
+            cp_async8(hst + ((t * NCF + ci) * NWC + j) * NF + n, base + wc_s[ci][j] * NP + fv_s[f ^ 1][n]);
+          }
+        } else {
+          if (!ti.face_has(f)) continue;
+          const double* base = uo + ((int64_t)e0 + ti.face_off(f)) * NV;
+          for (int item = lane; item < E * RUN; item += 32) {
+            const int t = item / RUN;
+            const int rem = item - t * RUN;
+            const int j = rem / NF, n = rem - j * NF;
+            cp_async8(hst + ((t * NCF + ci) * NWC + j) * NF + n,
+                      base + t * NV + wc_s[ci][j] * NP + fv_s[f ^ 1][n]);
+          }
+        }
+      }
+      cp_async_arrive_noinc(&full_bar[stage]);
+    }
+    for (int j = n_items > NS ? n_items - NS : 0; j < n_items; ++j) retire(j);
+  } else if (warp >= NCW) {
+    // ============================ prep warps ===============================
+    const int pw = warp - NCW;
+    constexpr int HALF = E / NQW;
+    for (int it = 0; it < n_items; ++it) {
+      const int stage = it % NS;
+      mbar_wait(&full_bar[stage], (it / NS) & 1);
+      const double* ust = sm + stage * C::STAGE;
+      const double* hst = ust + TILE;
+      double* qst = sm + stage * C::STAGE + TILE + C::HALO;
+#pragma unroll
+      for (int m = 0; m < (HALF * KC + 31) / 32; ++m) {
+        const int idx = lane + 32 * m;
+        if (idx < HALF * KC) {
+          const int t = pw * HALF + idx / KC, k = idx - (idx / KC) * KC;
+          const int f = qf_s[k];
+          double v = 0.0;
+          if (!(mmask_s[stage][t] & (1 << f))) {
+            const bool in_tile = (f >> 1) == 0 && !((f == 0 && t == 0) || (f == 1 && t == E - 1));
+            const int ci = k / NF;
+            if (in_tile) {
+              const double* src = ust + (t + (f == 0 ? -1 : 1)) * NV;
+#pragma unroll
+              for (int j = 0; j < NWC; ++j) v = fma(ww_s[ci][j], src[qt_s[k][j]], v);
+            } else {
+              const double* src = hst + t * (NCF * NWC * NF) + qh_s[k];
+#pragma unroll
+              for (int j = 0; j < NWC; ++j) v = fma(ww_s[ci][j], src[j * NF], v);
+            }
+          }
+          qst[t * KC + k] = v;
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&qready_bar[stage]);
+    }
+  } else {
+    // ============================ consumer warps ===========================
+    const int te = 2 * (lane & 3);      // D-fragment columns (elements) of this lane
+    const int rsub = lane >> 2;         // D-fragment row inside a row tile
+    for (int it = warp; it < n_items; it += NCW) {
+      const int stage = it % NS;
+      STile<D> ti;
+      ti.init(a.g, phys_of(it), E, nlay, lsi);
+      const int e0 = ti.e0;
+      // s -> accumulators (global loads in flight while the stage is prepared)
+      double acc[NRT][2];
+      const double* sg = a.s + (int64_t)e0 * NV;
+#pragma unroll
+      for (int rt = 0; rt < NRT; ++rt) {
+        const int row = rt * 8 + rsub;
+        acc[rt][0] = (row < NV) ? __ldcs(sg + te * NV + row) : 0.0;
+        acc[rt][1] = (row < NV) ? __ldcs(sg + (te + 1) * NV + row) : 0.0;
+      }
+      mbar_wait(&qready_bar[stage], (it / NS) & 1);
+      double* ust = sm + stage * C::STAGE;
+      const double* qb = ust + TILE + C::HALO + rsub * KC + (lane & 3);
+      if (mfast_s[stage]) {
+#pragma unroll
+        for (int ks = 0; ks < KS; ++ks) {
+          const double b = qb[4 * ks];
+#pragma unroll
+          for (int rt = 0; rt < NRT; ++rt) dmma_8x8x4(acc[rt][0], acc[rt][1], lfr_s[(rt * KS + ks) * 32 + lane], b);
+        }
+      } else {
+        // one masked pass per operator class present in the tile
+        const unsigned cset = mcset_s[stage];
+        const int mycls = mcls_s[stage][rsub];
+        for (unsigned rem = cset; rem != 0u; rem &= rem - 1u) {
+          const int c = __ffs(rem) - 1;
+          for (int ks = 0; ks < KS; ++ks) {
+            const double b = (mycls == c) ? qb[4 * ks] : 0.0;
+            const int k = 4 * ks + (lane & 3);
+            const int col = cf_s[k / NF] * NF + (k % NF);
+            const double* Lc = a.LT + ((size_t)c * (NFACE * NF) + col) * NV;
+#pragma unroll
+            for (int rt = 0; rt < NRT; ++rt) {
+              const int row = rt * 8 + rsub;
+              dmma_8x8x4(acc[rt][0], acc[rt][1], (row < NV) ? __ldg(Lc + row) : 0.0, b);
+            }
+          }
+        }
+      }
+      // u^{k+1} -> global (64-byte runs), delta in place over the staged u^k
+      double* ug = un + (int64_t)e0 * NV;
+#pragma unroll
+      for (int rt = 0; rt < NRT; ++rt) {
+        const int row = rt * 8 + rsub;
+        if (row < NV) {
+#pragma unroll
+          for (int v = 0; v < 2; ++v) {
+            const int t = te + v;
+            __stcs(ug + t * NV + row, acc[rt][v]);
+            ust[t * NV + row] = acc[rt][v] - ust[t * NV + row];
+          }
+        }
+      }
+      __syncwarp();
+      // ||delta||_M^2 = J |(C^T x ... x C^T) delta|^2, M1 = C C^T: one exact
+      // triangular pass per axis over the lines of the node grid (in place)
+      double nsum = 0.0;
+      int mul = 1;
+#pragma unroll
+      for (int ax = 0; ax < D; ++ax) {
+        const bool last_ax = ax == D - 1;
+#pragma unroll
+        for (int m = 0; m < (C::NLINES + 31) / 32; ++m) {
+          const int ln = lane + 32 * m;
+          if (ln < C::NLINES) {
+            const int t = ln / (M * C::LPL);
+            const int c = (ln / C::LPL) % M;
+            int rem = ln % C::LPL;
+            int base = t * NV + c * NP;
+            int mb = 1;
+#pragma unroll
+            for (int b = 0; b < D; ++b) {
+              if (b != ax) {
+                base += (rem % N1) * mb;
+                rem /= N1;
+              }
+              mb *= N1;
+            }
+            double x[N1];
+#pragma unroll
+            for (int i = 0; i < N1; ++i) x[i] = ust[base + i * mul];
+            double sq = 0.0;
+#pragma unroll
+            for (int i = 0; i < N1; ++i) {
+              double y = 0.0;
+#pragma unroll
+              for (int ip = i; ip < N1; ++ip) y = fma(chol_s[ip * N1 + i], x[ip], y);
+              if (last_ax) sq = fma(y, y, sq);
+              else ust[base + i * mul] = y;
+            }
+            if (last_ax) nsum = fma(cw_s[c], sq, nsum);
+          }
+        }
+        __syncwarp();
+        mul *= N1;
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) nsum += __shfl_xor_sync(0xffffffffu, nsum, o);
+      if (lane == 0) {
+        part_s[stage] = nsum;
+        mbar_arrive(&done_bar[stage]);  // release: part_s, stage no longer read
+      }
+    }
+  }
+
+  if (a.finalize) {
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) {
+      const unsigned tk = atomicAdd(&st->ticket, 1u);
+      last_s = (tk == gridDim.x - 1);
+    }
+    __syncthreads();
+    if (last_s) {
+      __threadfence();
+      finalize_block(a.tile_partials, geo.ntiles, st, a.norm_hist);
+    }
+  }
+}
+
+}  // namespace ihdg
