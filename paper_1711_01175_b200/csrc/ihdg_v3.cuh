@@ -260,20 +260,29 @@ __global__ void __launch_bounds__(V3Cfg<D, N1, M, NCF, NWC, NS, NCW, PF>::NT, 1)
     // ============================ consumer warps ===========================
     const int te = 2 * (lane & 3);      // D-fragment columns (elements) of this lane
     const int rsub = lane >> 2;         // D-fragment row inside a row tile
+    // s of this warp's first tile -> accumulators; afterwards the s loads of
+    // the next tile are issued before the current tile is computed
+    double acc[NRT][2], accn[NRT][2];
+    auto load_s = [&](int it_load, double (&dst)[NRT][2]) {
+      if (it_load < n_items) {
+        STile<D> tl;
+        tl.init(a.g, phys_of(it_load), E, nlay, lsi);
+        const double* sg = a.s + (int64_t)tl.e0 * NV;
+#pragma unroll
+        for (int rt = 0; rt < NRT; ++rt) {
+          const int row = rt * 8 + rsub;
+          dst[rt][0] = (row < NV) ? __ldcs(sg + te * NV + row) : 0.0;
+          dst[rt][1] = (row < NV) ? __ldcs(sg + (te + 1) * NV + row) : 0.0;
+        }
+      }
+    };
+    load_s(warp, acc);
     for (int it = warp; it < n_items; it += NCW) {
       const int stage = it % NS;
       STile<D> ti;
       ti.init(a.g, phys_of(it), E, nlay, lsi);
       const int e0 = ti.e0;
-      // s -> accumulators (global loads in flight while the stage is prepared)
-      double acc[NRT][2];
-      const double* sg = a.s + (int64_t)e0 * NV;
-#pragma unroll
-      for (int rt = 0; rt < NRT; ++rt) {
-        const int row = rt * 8 + rsub;
-        acc[rt][0] = (row < NV) ? __ldcs(sg + te * NV + row) : 0.0;
-        acc[rt][1] = (row < NV) ? __ldcs(sg + (te + 1) * NV + row) : 0.0;
-      }
+      load_s(it + NCW, accn);
       mbar_wait(&qready_bar[stage], (it / NS) & 1);
       double* ust = sm + stage * C::STAGE;
       const double* qb = ust + TILE + C::HALO + rsub * KC + (lane & 3);
@@ -365,6 +374,11 @@ __global__ void __launch_bounds__(V3Cfg<D, N1, M, NCF, NWC, NS, NCW, PF>::NT, 1)
       if (lane == 0) {
         part_s[stage] = nsum;
         mbar_arrive(&done_bar[stage]);  // release: part_s, stage no longer read
+      }
+#pragma unroll
+      for (int rt = 0; rt < NRT; ++rt) {
+        acc[rt][0] = accn[rt][0];
+        acc[rt][1] = accn[rt][1];
       }
     }
   }
