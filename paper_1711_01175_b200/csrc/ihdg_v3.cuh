@@ -25,6 +25,19 @@
 
 namespace ihdg {
 
+// Optional per-role cycle counters (profiling build, -DIHDG_WS_PROF; tools/ws_roles.py).
+#ifdef IHDG_WS_PROF
+__device__ unsigned long long g_ws_prof[16];
+#define V3_T0(v) const long long v = clock64()
+#define V3_ACC(slot, v)                                                                   \
+  do {                                                                                    \
+    if ((threadIdx.x & 31) == 0) atomicAdd(&g_ws_prof[slot], (unsigned long long)(clock64() - (v))); \
+  } while (0)
+#else
+#define V3_T0(v)
+#define V3_ACC(slot, v)
+#endif
+
 template <int D, int N1, int M, int NCF, int NWC, int NS, int NCW, int PF>
 struct V3Cfg {
   static constexpr int E = 8;                     // elements per physical tile (DMMA n)
@@ -140,6 +153,7 @@ __global__ void __launch_bounds__(V3Cfg<D, N1, M, NCF, NWC, NS, NCW, PF>::NT, 1)
   }
   __syncthreads();
 
+  V3_T0(tk0);
   const int nlog = (int)geo.ntiles;
   const int n_log_my = nlog > (int)blockIdx.x ? (nlog - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
   const int n_items = n_log_my * PF;
@@ -154,7 +168,9 @@ __global__ void __launch_bounds__(V3Cfg<D, N1, M, NCF, NWC, NS, NCW, PF>::NT, 1)
     double pacc = 0.0;
     auto retire = [&](int j) {
       const int sj = j % NS;
+      V3_T0(tr);
       mbar_wait(&done_bar[sj], (j / NS) & 1);
+      V3_ACC(0, tr);
       pacc += part_s[sj];
       if (j % PF == PF - 1) {
         if (lane == 0) a.tile_partials[(int)blockIdx.x + (j / PF) * (int)gridDim.x] = a.jac * pacc;
@@ -164,6 +180,7 @@ __global__ void __launch_bounds__(V3Cfg<D, N1, M, NCF, NWC, NS, NCW, PF>::NT, 1)
     for (int it = 0; it < n_items; ++it) {
       const int stage = it % NS;
       if (it >= NS) retire(it - NS);
+      V3_T0(tl);
       double* ust = sm + stage * C::STAGE;
       double* hst = ust + TILE;
       STile<D> ti;
@@ -218,6 +235,7 @@ __global__ void __launch_bounds__(V3Cfg<D, N1, M, NCF, NWC, NS, NCW, PF>::NT, 1)
         }
       }
       cp_async_arrive_noinc(&full_bar[stage]);
+      V3_ACC(9, tl);
     }
     for (int j = n_items > NS ? n_items - NS : 0; j < n_items; ++j) retire(j);
   } else if (warp >= NCW) {
@@ -226,7 +244,10 @@ __global__ void __launch_bounds__(V3Cfg<D, N1, M, NCF, NWC, NS, NCW, PF>::NT, 1)
     constexpr int HALF = E / NQW;
     for (int it = 0; it < n_items; ++it) {
       const int stage = it % NS;
+      V3_T0(tp);
       mbar_wait(&full_bar[stage], (it / NS) & 1);
+      V3_ACC(1, tp);
+      V3_T0(tq);
       const double* ust = sm + stage * C::STAGE;
       const double* hst = ust + TILE;
       double* qst = sm + stage * C::STAGE + TILE + C::HALO;
@@ -254,6 +275,7 @@ __global__ void __launch_bounds__(V3Cfg<D, N1, M, NCF, NWC, NS, NCW, PF>::NT, 1)
         }
       }
       __syncwarp();
+      V3_ACC(2, tq);
       if (lane == 0) mbar_arrive(&qready_bar[stage]);
     }
   } else {
@@ -283,7 +305,10 @@ __global__ void __launch_bounds__(V3Cfg<D, N1, M, NCF, NWC, NS, NCW, PF>::NT, 1)
       ti.init(a.g, phys_of(it), E, nlay, lsi);
       const int e0 = ti.e0;
       load_s(it + NCW, accn);
+      V3_T0(tc);
       mbar_wait(&qready_bar[stage], (it / NS) & 1);
+      V3_ACC(3, tc);
+      V3_T0(tm);
       double* ust = sm + stage * C::STAGE;
       const double* qb = ust + TILE + C::HALO + rsub * KC + (lane & 3);
       if (mfast_s[stage]) {
@@ -312,6 +337,8 @@ __global__ void __launch_bounds__(V3Cfg<D, N1, M, NCF, NWC, NS, NCW, PF>::NT, 1)
           }
         }
       }
+      V3_ACC(4, tm);
+      V3_T0(te2);
       // u^{k+1} -> global (64-byte runs), delta in place over the staged u^k
       double* ug = un + (int64_t)e0 * NV;
 #pragma unroll
@@ -327,6 +354,8 @@ __global__ void __launch_bounds__(V3Cfg<D, N1, M, NCF, NWC, NS, NCW, PF>::NT, 1)
         }
       }
       __syncwarp();
+      V3_ACC(5, te2);
+      V3_T0(tn);
       // ||delta||_M^2 = J |(C^T x ... x C^T) delta|^2, M1 = C C^T: one exact
       // triangular pass per axis over the lines of the node grid (in place)
       double nsum = 0.0;
@@ -371,6 +400,7 @@ __global__ void __launch_bounds__(V3Cfg<D, N1, M, NCF, NWC, NS, NCW, PF>::NT, 1)
       }
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) nsum += __shfl_xor_sync(0xffffffffu, nsum, o);
+      V3_ACC(7, tn);
       if (lane == 0) {
         part_s[stage] = nsum;
         mbar_arrive(&done_bar[stage]);  // release: part_s, stage no longer read
@@ -383,6 +413,9 @@ __global__ void __launch_bounds__(V3Cfg<D, N1, M, NCF, NWC, NS, NCW, PF>::NT, 1)
     }
   }
 
+#ifdef IHDG_WS_PROF
+  if (tid == 0) V3_ACC(6, tk0);
+#endif
   if (a.finalize) {
     __threadfence();
     __syncthreads();
