@@ -52,7 +52,7 @@ struct V3Cfg {
   static constexpr int NT = 32 * (NCW + NQW + 1);
   static constexpr int MAXREG = (65536 / NT) / 8 * 8 > 255 ? 255 : (65536 / NT) / 8 * 8;
   static constexpr int TILE = E * NV;
-  static constexpr int HALO = E * NCF * NWC * NF;
+  static constexpr int HALO = 0;                  // out-of-tile faces: prep warps load them directly
   static constexpr int QT = E * KC;
   static constexpr int STAGE = TILE + HALO + QT;  // doubles
   static constexpr int LFR = NRT * KS * 32;       // L fragments (doubles)
@@ -90,8 +90,9 @@ __global__ void __launch_bounds__(V3Cfg<D, N1, M, NCF, NWC, NS, NCW, PF>::NT, 1)
   __shared__ int qt_s[KC][NWC];
   __shared__ int mfast_s[NS];
   __shared__ unsigned mcset_s[NS];
-  __shared__ int mmask_s[NS][E], mcls_s[NS][E];
+  __shared__ int mcls_s[NS][E];
   __shared__ double part_s[NS];
+  __shared__ int com_s[64];                 // class_of_mask
   __shared__ int last_s;
 
   ihdg_iter_state* st = a.state;
@@ -109,6 +110,7 @@ __global__ void __launch_bounds__(V3Cfg<D, N1, M, NCF, NWC, NS, NCW, PF>::NT, 1)
   for (int i = tid; i < NFACE * NF; i += blockDim.x) fv_s[i / NF][i % NF] = face_node_vidx(D, N1, i / NF, i % NF);
   for (int i = tid; i < N1 * N1; i += blockDim.x) chol_s[i] = a.chol1d[i];
   if (tid < IHDG_MAX_COMP) cw_s[tid] = a.comp_w[tid];
+  if (tid < 64) com_s[tid] = a.class_of_mask[tid];
   if (tid == 0) {
     int n = 0;
     for (int f = 0; f < NFACE && n < NCF; ++f) {
@@ -134,7 +136,7 @@ __global__ void __launch_bounds__(V3Cfg<D, N1, M, NCF, NWC, NS, NCW, PF>::NT, 1)
       qh_s[k] = ci * NWC * NF + nn;
     }
     for (int s = 0; s < NS; ++s) {
-      mbar_init(&full_bar[s], 1 + 32);
+      mbar_init(&full_bar[s], 1);
       mbar_init(&qready_bar[s], NQW);
       mbar_init(&done_bar[s], 1);
     }
@@ -163,8 +165,8 @@ __global__ void __launch_bounds__(V3Cfg<D, N1, M, NCF, NWC, NS, NCW, PF>::NT, 1)
 
   if (warp == NCW + NQW) {
     // ============================ producer warp ============================
-    const int c0 = (int)a.g.cells[0];
-    const int per0 = a.g.periodic[0];
+    // retires stages in order (tile partials in a fixed order) and issues one
+    // TMA bulk copy of the u^k tile per stage
     double pacc = 0.0;
     auto retire = [&](int j) {
       const int sj = j % NS;
@@ -181,95 +183,101 @@ __global__ void __launch_bounds__(V3Cfg<D, N1, M, NCF, NWC, NS, NCW, PF>::NT, 1)
       const int stage = it % NS;
       if (it >= NS) retire(it - NS);
       V3_T0(tl);
-      double* ust = sm + stage * C::STAGE;
-      double* hst = ust + TILE;
-      STile<D> ti;
-      ti.init(a.g, phys_of(it), E, nlay, lsi);
-      const int e0 = ti.e0;
-      int cls = -1;
-      if (lane < E) {
-        const int mask = ti.mask(lane, c0, per0);
-        cls = a.class_of_mask[mask];
-        mmask_s[stage][lane] = mask;
-        mcls_s[stage][lane] = cls;
-      }
-      const int fast = __all_sync(0xffffffffu, lane >= E || cls == fast_class);
-      unsigned cset = (lane < E && cls >= 0 && cls < 32) ? (1u << cls) : 0u;
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) cset |= __shfl_xor_sync(0xffffffffu, cset, o);
       if (lane == 0) {
-        mfast_s[stage] = fast;
-        mcset_s[stage] = cset;
+        STile<D> ti;
+        ti.init(a.g, phys_of(it), E, nlay, lsi);
+        constexpr uint32_t bytes = (uint32_t)(TILE * sizeof(double));
+        mbar_arrive_expect_tx(&full_bar[stage], bytes);
+        bulk_g2s(sm + stage * C::STAGE, uo + (int64_t)ti.e0 * NV, bytes, &full_bar[stage]);
       }
       __syncwarp();
-      if (lane == 0) {
-        constexpr uint32_t bytes = (uint32_t)(TILE * sizeof(double));
-        mbar_arrive_expect_tx(&full_bar[stage], bytes);  // release: metadata above
-        bulk_g2s(ust, uo + (int64_t)e0 * NV, bytes, &full_bar[stage]);
-      }
-      constexpr int RUN = NWC * NF;
-#pragma unroll
-      for (int ci = 0; ci < NCF; ++ci) {
-        const int f = cf_s[ci];
-        if ((f >> 1) == 0) {
-          const int t = (f == 0) ? 0 : E - 1;
-          const int i = ti.i0 + t;
-          const bool ex = (f == 0) ? (i > 0 || per0) : (i < c0 - 1 || per0);
-          if (!ex) continue;
-          const int nb = e0 + t + ((f == 0) ? (i > 0 ? -1 : c0 - 1) : (i < c0 - 1 ? 1 : -(c0 - 1)));
-          const double* base = uo + (int64_t)nb * NV;
-          for (int item = lane; item < RUN; item += 32) {
-            const int j = item / NF, n = item - (item / NF) * NF;
-            cp_async8(hst + ((t * NCF + ci) * NWC + j) * NF + n, base + wc_s[ci][j] * NP + fv_s[f ^ 1][n]);
-          }
-        } else {
-          if (!ti.face_has(f)) continue;
-          const double* base = uo + ((int64_t)e0 + ti.face_off(f)) * NV;
-          for (int item = lane; item < E * RUN; item += 32) {
-            const int t = item / RUN;
-            const int rem = item - t * RUN;
-            const int j = rem / NF, n = rem - j * NF;
-            cp_async8(hst + ((t * NCF + ci) * NWC + j) * NF + n,
-                      base + t * NV + wc_s[ci][j] * NP + fv_s[f ^ 1][n]);
-          }
-        }
-      }
-      cp_async_arrive_noinc(&full_bar[stage]);
       V3_ACC(9, tl);
     }
     for (int j = n_items > NS ? n_items - NS : 0; j < n_items; ++j) retire(j);
   } else if (warp >= NCW) {
     // ============================ prep warps ===============================
+    // per stage: tile metadata + neighbour face scalars q (TraceSnapshot of
+    // iterate k).  Out-of-tile neighbour face nodes are loaded from global
+    // (L2) straight into registers before waiting for the u^k tile.
     const int pw = warp - NCW;
+    const int c0 = (int)a.g.cells[0];
+    const int per0 = a.g.periodic[0];
     constexpr int HALF = E / NQW;
+    constexpr int QM = (HALF * KC + 31) / 32;
     for (int it = 0; it < n_items; ++it) {
       const int stage = it % NS;
+      STile<D> ti;
+      ti.init(a.g, phys_of(it), E, nlay, lsi);
+      const int e0 = ti.e0;
+      double gv[QM][NWC];
+      int qstate[QM];   // 0: zero, 1: in tile, 2: loaded
+#pragma unroll
+      for (int m = 0; m < QM; ++m) {
+        const int idx = lane + 32 * m;
+        qstate[m] = 0;
+#pragma unroll
+        for (int j = 0; j < NWC; ++j) gv[m][j] = 0.0;
+        if (idx < HALF * KC) {
+          const int t = pw * HALF + idx / KC, k = idx - (idx / KC) * KC;
+          const int f = qf_s[k];
+          if (!(ti.mask(t, c0, per0) & (1 << f))) {
+            const bool in_tile = (f >> 1) == 0 && !((f == 0 && t == 0) || (f == 1 && t == E - 1));
+            if (in_tile) {
+              qstate[m] = 1;
+            } else {
+              qstate[m] = 2;
+              int nb;
+              if (f >= 2) {
+                nb = e0 + t + ti.face_off(f);
+              } else {
+                const int i = ti.i0 + t;
+                nb = e0 + t + ((f == 0) ? (i > 0 ? -1 : c0 - 1) : (i < c0 - 1 ? 1 : -(c0 - 1)));
+              }
+              const double* src = uo + (int64_t)nb * NV;
+#pragma unroll
+              for (int j = 0; j < NWC; ++j) gv[m][j] = __ldg(src + qt_s[k][j]);
+            }
+          }
+        }
+      }
       V3_T0(tp);
       mbar_wait(&full_bar[stage], (it / NS) & 1);
       V3_ACC(1, tp);
       V3_T0(tq);
-      const double* ust = sm + stage * C::STAGE;
-      const double* hst = ust + TILE;
-      double* qst = sm + stage * C::STAGE + TILE + C::HALO;
+      // stage metadata: written only after full (the producer refills a stage
+      // after its previous consumer is done with it)
+      if (pw == 0) {
+        int cls = -1;
+        if (lane < E) {
+          cls = com_s[ti.mask(lane, c0, per0)];
+          mcls_s[stage][lane] = cls;
+        }
+        const int fast = __all_sync(0xffffffffu, lane >= E || cls == fast_class);
+        unsigned cset = (lane < E && cls >= 0 && cls < 32) ? (1u << cls) : 0u;
 #pragma unroll
-      for (int m = 0; m < (HALF * KC + 31) / 32; ++m) {
+        for (int o = 16; o > 0; o >>= 1) cset |= __shfl_xor_sync(0xffffffffu, cset, o);
+        if (lane == 0) {
+          mfast_s[stage] = fast;
+          mcset_s[stage] = cset;
+        }
+      }
+      const double* ust = sm + stage * C::STAGE;
+      double* qst = sm + stage * C::STAGE + TILE;
+#pragma unroll
+      for (int m = 0; m < QM; ++m) {
         const int idx = lane + 32 * m;
         if (idx < HALF * KC) {
           const int t = pw * HALF + idx / KC, k = idx - (idx / KC) * KC;
-          const int f = qf_s[k];
+          const int ci = k / NF;
           double v = 0.0;
-          if (!(mmask_s[stage][t] & (1 << f))) {
-            const bool in_tile = (f >> 1) == 0 && !((f == 0 && t == 0) || (f == 1 && t == E - 1));
-            const int ci = k / NF;
-            if (in_tile) {
-              const double* src = ust + (t + (f == 0 ? -1 : 1)) * NV;
+          if (qstate[m] == 1) {
+            const int f = qf_s[k];
+            const double* src = ust + (t + (f == 0 ? -1 : 1)) * NV;
 #pragma unroll
-              for (int j = 0; j < NWC; ++j) v = fma(ww_s[ci][j], src[qt_s[k][j]], v);
-            } else {
-              const double* src = hst + t * (NCF * NWC * NF) + qh_s[k];
+            for (int j = 0; j < NWC; ++j) v = fma(ww_s[ci][j], src[qt_s[k][j]], v);
+          } else if (qstate[m] == 2) {
 #pragma unroll
-              for (int j = 0; j < NWC; ++j) v = fma(ww_s[ci][j], src[j * NF], v);
-            }
+            for (int j = 0; j < NWC; ++j) v = fma(ww_s[ci][j], gv[m][j], v);
           }
           qst[t * KC + k] = v;
         }
