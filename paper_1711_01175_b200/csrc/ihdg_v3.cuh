@@ -137,7 +137,7 @@ __global__ void __launch_bounds__(V3Cfg<D, N1, M, NCF, NWC, NS, NCW, PF>::NT, 1)
     }
     for (int s = 0; s < NS; ++s) {
       mbar_init(&full_bar[s], 1);
-      mbar_init(&qready_bar[s], NQW);
+      mbar_init(&qready_bar[s], 1);
       mbar_init(&done_bar[s], 1);
     }
     fence_mbar_init();
@@ -196,57 +196,66 @@ __global__ void __launch_bounds__(V3Cfg<D, N1, M, NCF, NWC, NS, NCW, PF>::NT, 1)
     for (int j = n_items > NS ? n_items - NS : 0; j < n_items; ++j) retire(j);
   } else if (warp >= NCW) {
     // ============================ prep warps ===============================
-    // per stage: tile metadata + neighbour face scalars q (TraceSnapshot of
-    // iterate k).  Out-of-tile neighbour face nodes are loaded from global
-    // (L2) straight into registers before waiting for the u^k tile.
+    // prep warp pw owns items pw, pw + NQW, ...: tile metadata + neighbour
+    // face scalars q (TraceSnapshot of iterate k).  Out-of-tile neighbour face
+    // nodes of its NEXT item are loaded from global (L2) into registers while
+    // the current item is processed.
     const int pw = warp - NCW;
     const int c0 = (int)a.g.cells[0];
     const int per0 = a.g.periodic[0];
-    constexpr int HALF = E / NQW;
-    constexpr int QM = (HALF * KC + 31) / 32;
-    for (int it = 0; it < n_items; ++it) {
-      const int stage = it % NS;
-      STile<D> ti;
-      ti.init(a.g, phys_of(it), E, nlay, lsi);
-      const int e0 = ti.e0;
-      double gv[QM][NWC];
-      int qstate[QM];   // 0: zero, 1: in tile, 2: loaded
+    constexpr int QM = (E * KC + 31) / 32;
+    double gv[QM][NWC], gvn[QM][NWC];
+    int qsn = 0;      // bit m: entry m of the next item is an in-tile neighbour
+    int qln = 0;      // bit m: entry m of the next item was loaded from global
+    int qs = 0, ql = 0;
+    auto gather = [&](int itg, double (&dst)[QM][NWC], int& in_tile_bits, int& load_bits) {
+      in_tile_bits = 0;
+      load_bits = 0;
+      if (itg >= n_items) return;
+      STile<D> tg;
+      tg.init(a.g, phys_of(itg), E, nlay, lsi);
 #pragma unroll
       for (int m = 0; m < QM; ++m) {
         const int idx = lane + 32 * m;
-        qstate[m] = 0;
 #pragma unroll
-        for (int j = 0; j < NWC; ++j) gv[m][j] = 0.0;
-        if (idx < HALF * KC) {
-          const int t = pw * HALF + idx / KC, k = idx - (idx / KC) * KC;
+        for (int j = 0; j < NWC; ++j) dst[m][j] = 0.0;
+        if (idx < E * KC) {
+          const int t = idx / KC, k = idx - (idx / KC) * KC;
           const int f = qf_s[k];
-          if (!(ti.mask(t, c0, per0) & (1 << f))) {
+          if (!(tg.mask(t, c0, per0) & (1 << f))) {
             const bool in_tile = (f >> 1) == 0 && !((f == 0 && t == 0) || (f == 1 && t == E - 1));
             if (in_tile) {
-              qstate[m] = 1;
+              in_tile_bits |= 1 << m;
             } else {
-              qstate[m] = 2;
+              load_bits |= 1 << m;
               int nb;
               if (f >= 2) {
-                nb = e0 + t + ti.face_off(f);
+                nb = tg.e0 + t + tg.face_off(f);
               } else {
-                const int i = ti.i0 + t;
-                nb = e0 + t + ((f == 0) ? (i > 0 ? -1 : c0 - 1) : (i < c0 - 1 ? 1 : -(c0 - 1)));
+                const int i = tg.i0 + t;
+                nb = tg.e0 + t + ((f == 0) ? (i > 0 ? -1 : c0 - 1) : (i < c0 - 1 ? 1 : -(c0 - 1)));
               }
               const double* src = uo + (int64_t)nb * NV;
 #pragma unroll
-              for (int j = 0; j < NWC; ++j) gv[m][j] = __ldg(src + qt_s[k][j]);
+              for (int j = 0; j < NWC; ++j) dst[m][j] = __ldg(src + qt_s[k][j]);
             }
           }
         }
       }
+    };
+    gather(pw, gv, qs, ql);
+    for (int it = pw; it < n_items; it += NQW) {
+      const int stage = it % NS;
+      gather(it + NQW, gvn, qsn, qln);
+      STile<D> ti;
+      ti.init(a.g, phys_of(it), E, nlay, lsi);
       V3_T0(tp);
       mbar_wait(&full_bar[stage], (it / NS) & 1);
       V3_ACC(1, tp);
       V3_T0(tq);
       // stage metadata: written only after full (the producer refills a stage
       // after its previous consumer is done with it)
-      if (pw == 0) {
+      {
         int cls = -1;
         if (lane < E) {
           cls = com_s[ti.mask(lane, c0, per0)];
@@ -266,16 +275,16 @@ __global__ void __launch_bounds__(V3Cfg<D, N1, M, NCF, NWC, NS, NCW, PF>::NT, 1)
 #pragma unroll
       for (int m = 0; m < QM; ++m) {
         const int idx = lane + 32 * m;
-        if (idx < HALF * KC) {
-          const int t = pw * HALF + idx / KC, k = idx - (idx / KC) * KC;
+        if (idx < E * KC) {
+          const int t = idx / KC, k = idx - (idx / KC) * KC;
           const int ci = k / NF;
           double v = 0.0;
-          if (qstate[m] == 1) {
+          if (qs & (1 << m)) {
             const int f = qf_s[k];
             const double* src = ust + (t + (f == 0 ? -1 : 1)) * NV;
 #pragma unroll
             for (int j = 0; j < NWC; ++j) v = fma(ww_s[ci][j], src[qt_s[k][j]], v);
-          } else if (qstate[m] == 2) {
+          } else if (ql & (1 << m)) {
 #pragma unroll
             for (int j = 0; j < NWC; ++j) v = fma(ww_s[ci][j], gv[m][j], v);
           }
@@ -285,6 +294,12 @@ __global__ void __launch_bounds__(V3Cfg<D, N1, M, NCF, NWC, NS, NCW, PF>::NT, 1)
       __syncwarp();
       V3_ACC(2, tq);
       if (lane == 0) mbar_arrive(&qready_bar[stage]);
+#pragma unroll
+      for (int m = 0; m < QM; ++m)
+#pragma unroll
+        for (int j = 0; j < NWC; ++j) gv[m][j] = gvn[m][j];
+      qs = qsn;
+      ql = qln;
     }
   } else {
     // ============================ consumer warps ===========================
