@@ -91,7 +91,7 @@ struct StreamEntry {
   {D, N1, M, NCF, NWC, E, M * Pow<N1, D>::v, launch_stream_t<D, N1, M, NCF, NWC, E, NS, G>, 0},
 
 const StreamEntry kStream[] = {
-    IHDG_V3(2, 7, 3, 4, 2, 12, 4, 2)       // config 5: CD 2D p=6 (one consumer warp per SMSP, 255 regs)
+    IHDG_V3(2, 7, 3, 4, 2, 12, 8, 2)       // config 5: CD 2D p=6 (two consumer warps per SMSP)
     IHDG_V3(2, 5, 3, 4, 2, 16, 8, 2)       // configs 2/3: CD / SW 2D p=4
     IHDG_V3(3, 4, 1, 3, 1, 16, 8, 4)       // config 4: transport 3D p=3 (two consumer warps per SMSP)
     IHDG_WS(7, 3, 4, 2, 16, 3)             // config 5: CD 2D p=6 (warp-specialised)

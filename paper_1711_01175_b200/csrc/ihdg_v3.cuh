@@ -50,7 +50,12 @@ struct V3Cfg {
   static constexpr int KS = KC / 4;               // DMMA k steps
   static constexpr int NQW = 2;                   // prep warps
   static constexpr int NT = 32 * (NCW + NQW + 1);
-  static constexpr int MAXREG = (65536 / NT) / 8 * 8 > 255 ? 255 : (65536 / NT) / 8 * 8;
+  // registers: the file is split over 4 SMSPs, so the cap follows the busiest SMSP
+  static constexpr int WPS = (NT / 32 + 3) / 4;   // warps per SMSP
+  static constexpr int MAXREG = (16384 / (32 * WPS)) / 8 * 8 > 255 ? 255 : (16384 / (32 * WPS)) / 8 * 8;
+  // register prefetch of the next tile's s only when one warp per SMSP cannot
+  // be covered by another consumer warp
+  static constexpr bool PREF = WPS <= 2 && NCW <= 4;
   static constexpr int TILE = E * NV;
   static constexpr int HALO = 0;                  // out-of-tile faces: prep warps load them directly
   static constexpr int QT = E * KC;
@@ -307,7 +312,7 @@ __global__ void __launch_bounds__(V3Cfg<D, N1, M, NCF, NWC, NS, NCW, PF>::NT, 1)
     const int rsub = lane >> 2;         // D-fragment row inside a row tile
     // s of this warp's first tile -> accumulators; afterwards the s loads of
     // the next tile are issued before the current tile is computed
-    double acc[NRT][2], accn[NRT][2];
+    double acc[NRT][2], accn[C::PREF ? NRT : 1][2];
     auto load_s = [&](int it_load, double (&dst)[NRT][2]) {
       if (it_load < n_items) {
         STile<D> tl;
@@ -321,13 +326,14 @@ __global__ void __launch_bounds__(V3Cfg<D, N1, M, NCF, NWC, NS, NCW, PF>::NT, 1)
         }
       }
     };
-    load_s(warp, acc);
+    if constexpr (C::PREF) load_s(warp, acc);
     for (int it = warp; it < n_items; it += NCW) {
       const int stage = it % NS;
       STile<D> ti;
       ti.init(a.g, phys_of(it), E, nlay, lsi);
       const int e0 = ti.e0;
-      load_s(it + NCW, accn);
+      if constexpr (C::PREF) load_s(it + NCW, *reinterpret_cast<double(*)[NRT][2]>(&accn[0][0]));
+      else load_s(it, acc);
       V3_T0(tc);
       mbar_wait(&qready_bar[stage], (it / NS) & 1);
       V3_ACC(3, tc);
@@ -428,10 +434,12 @@ __global__ void __launch_bounds__(V3Cfg<D, N1, M, NCF, NWC, NS, NCW, PF>::NT, 1)
         part_s[stage] = nsum;
         mbar_arrive(&done_bar[stage]);  // release: part_s, stage no longer read
       }
+      if constexpr (C::PREF) {
 #pragma unroll
-      for (int rt = 0; rt < NRT; ++rt) {
-        acc[rt][0] = accn[rt][0];
-        acc[rt][1] = accn[rt][1];
+        for (int rt = 0; rt < NRT; ++rt) {
+          acc[rt][0] = accn[rt][0];
+          acc[rt][1] = accn[rt][1];
+        }
       }
     }
   }
