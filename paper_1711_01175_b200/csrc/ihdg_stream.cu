@@ -58,13 +58,13 @@ int launch_ws_t(const ihdg_sweep_args* a, cudaStream_t st) {
   return cudaGetLastError() == cudaSuccess ? 0 : -2;
 }
 
-template <int D, int N1, int M, int NCF, int NWC, int NS, int NCW, int PF>
+template <int D, int N1, int M, int NCF, int NWC, int NS, int NCW, int PF, int NQW>
 int launch_v3_t(const ihdg_sweep_args* a, cudaStream_t st) {
-  using C = V3Cfg<D, N1, M, NCF, NWC, NS, NCW, PF>;
+  using C = V3Cfg<D, N1, M, NCF, NWC, NS, NCW, PF, NQW>;
   static_assert(8 * PF == Cfg<D, N1, M>::TE, "v3 logical tile must equal the generic tile (tile partial count)");
   static bool configured = false;
   if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(k_sweep_v3<D, N1, M, NCF, NWC, NS, NCW, PF>,
+    cudaError_t e = cudaFuncSetAttribute(k_sweep_v3<D, N1, M, NCF, NWC, NS, NCW, PF, NQW>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::BYTES);
     if (e != cudaSuccess) return -2;
     configured = true;
@@ -73,7 +73,7 @@ int launch_v3_t(const ihdg_sweep_args* a, cudaStream_t st) {
   geo.init(a->g, 8 * PF);
   int64_t grid = geo.ntiles < stream_sms() ? geo.ntiles : stream_sms();
   if (grid < 1) grid = 1;
-  k_sweep_v3<D, N1, M, NCF, NWC, NS, NCW, PF><<<(unsigned)grid, C::NT, C::BYTES, st>>>(*a);
+  k_sweep_v3<D, N1, M, NCF, NWC, NS, NCW, PF, NQW><<<(unsigned)grid, C::NT, C::BYTES, st>>>(*a);
   return cudaGetLastError() == cudaSuccess ? 0 : -2;
 }
 
@@ -83,17 +83,16 @@ struct StreamEntry {
   int v3;  // version-3 kernel (physical 8-element tiles)
 };
 
-#define IHDG_V3(D, N1, M, NCF, NWC, NS, NCW, PF) \
-  {D, N1, M, NCF, NWC, 8 * PF, M * Pow<N1, D>::v, launch_v3_t<D, N1, M, NCF, NWC, NS, NCW, PF>, 1},
+#define IHDG_V3(D, N1, M, NCF, NWC, NS, NCW, PF, NQW) \
+  {D, N1, M, NCF, NWC, 8 * PF, M * Pow<N1, D>::v, launch_v3_t<D, N1, M, NCF, NWC, NS, NCW, PF, NQW>, 1},
 #define IHDG_WS(N1, M, NCF, NWC, E, NS) \
   {2, N1, M, NCF, NWC, E, M * N1 * N1, launch_ws_t<N1, M, NCF, NWC, E, NS>, 0},
 #define IHDG_STREAM(D, N1, M, NCF, NWC, E, NS, G) \
   {D, N1, M, NCF, NWC, E, M * Pow<N1, D>::v, launch_stream_t<D, N1, M, NCF, NWC, E, NS, G>, 0},
 
 const StreamEntry kStream[] = {
-    IHDG_V3(2, 7, 3, 4, 2, 12, 8, 2)       // config 5: CD 2D p=6 (two consumer warps per SMSP)
-    IHDG_V3(2, 5, 3, 4, 2, 16, 8, 2)       // configs 2/3: CD / SW 2D p=4
-    IHDG_V3(3, 4, 1, 3, 1, 16, 8, 4)       // config 4: transport 3D p=3 (two consumer warps per SMSP)
+    IHDG_V3(2, 5, 3, 4, 2, 16, 8, 2, 2)    // configs 2/3: CD / SW 2D p=4
+    IHDG_V3(3, 4, 1, 3, 1, 16, 6, 4, 4)    // config 4: transport 3D p=3
     IHDG_WS(7, 3, 4, 2, 16, 3)             // config 5: CD 2D p=6 (warp-specialised)
     IHDG_WS(5, 3, 4, 2, 16, 4)             // configs 2/3: CD / SW 2D p=4
     IHDG_STREAM(3, 4, 1, 3, 1, 32, 3, 4)   // config 4: transport 3D p=3

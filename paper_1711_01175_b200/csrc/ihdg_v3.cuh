@@ -38,7 +38,7 @@ __device__ unsigned long long g_ws_prof[16];
 #define V3_ACC(slot, v)
 #endif
 
-template <int D, int N1, int M, int NCF, int NWC, int NS, int NCW, int PF>
+template <int D, int N1, int M, int NCF, int NWC, int NS, int NCW, int PF, int NQW_ = 2>
 struct V3Cfg {
   static constexpr int E = 8;                     // elements per physical tile (DMMA n)
   static constexpr int NP = Pow<N1, D>::v;
@@ -48,7 +48,7 @@ struct V3Cfg {
   static constexpr int KC = NCF * NF;
   static constexpr int NRT = (NV + 7) / 8;        // DMMA row tiles
   static constexpr int KS = KC / 4;               // DMMA k steps
-  static constexpr int NQW = 2;                   // prep warps
+  static constexpr int NQW = NQW_;                // prep warps
   static constexpr int NT = 32 * (NCW + NQW + 1);
   // registers: the file is split over 4 SMSPs, so the cap follows the busiest SMSP
   static constexpr int WPS = (NT / 32 + 3) / 4;   // warps per SMSP
@@ -71,10 +71,10 @@ struct V3Cfg {
   static_assert(E % NQW == 0, "prep split");
 };
 
-template <int D, int N1, int M, int NCF, int NWC, int NS, int NCW, int PF>
-__global__ void __launch_bounds__(V3Cfg<D, N1, M, NCF, NWC, NS, NCW, PF>::NT, 1) __maxnreg__((V3Cfg<D, N1, M, NCF, NWC, NS, NCW, PF>::MAXREG))
+template <int D, int N1, int M, int NCF, int NWC, int NS, int NCW, int PF, int NQW_>
+__global__ void __launch_bounds__(V3Cfg<D, N1, M, NCF, NWC, NS, NCW, PF, NQW_>::NT, 1) __maxnreg__((V3Cfg<D, N1, M, NCF, NWC, NS, NCW, PF, NQW_>::MAXREG))
     k_sweep_v3(const ihdg_sweep_args a) {
-  using C = V3Cfg<D, N1, M, NCF, NWC, NS, NCW, PF>;
+  using C = V3Cfg<D, N1, M, NCF, NWC, NS, NCW, PF, NQW_>;
   constexpr int E = C::E, NP = C::NP, NV = C::NV, NF = C::NF, NFACE = C::NFACE, KC = C::KC;
   constexpr int NRT = C::NRT, KS = C::KS, NQW = C::NQW, TILE = C::TILE;
 

@@ -20,12 +20,17 @@ NAMES = ["producer: wait done (retire)", "prep: wait full", "prep: q compute", "
 
 
 def main():
-    cells = int(sys.argv[1]) if len(sys.argv) > 1 else 2048
-    wl = make_config(5, cells=cells)
+    cfg = int(sys.argv[1]) if len(sys.argv) > 1 else 5
+    wl = make_config(cfg)
     sv = DeviceSolver(wl.mesh, wl.problem, wl.ops, dt=wl.dt, max_iters=1000)
+    if getattr(wl.problem, "forcing", None) is not None:
+        sv.set_forcing(wl.problem.forcing)
     for name, fld in wl.initial.items():
         sv.set_state_component(fld, sv.spec.labels.index(name))
-    sv.begin_step()
+    if wl.dt is not None:
+        sv.begin_step()
+    else:
+        sv.prepare_steady()
     sv.reset_state(0.0, 1000)
     a = sv.sweep_args("volume", 1)
     L = N.lib()
