@@ -19,6 +19,10 @@
 
 namespace ihdg {
 
+#ifndef WS_NORM_DMMA
+#define WS_NORM_DMMA 1   // 1: tensor-core norm (measured faster), 0: exact DFMA passes
+#endif
+
 template <int N1, int M, int NCF, int NWC, int E, int NS>
 struct WCfg {
   static constexpr int D = 2;
@@ -342,6 +346,12 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS>::NT, 1)
         Lf[j][ks] = (row < NV) ? __ldg(a.LT + ((size_t)fast_class * (NFACE * NF) + col) * NV + row) : 0.0;
       }
     }
+    double cfr[2];
+#pragma unroll
+    for (int ks = 0; ks < 2; ++ks) {
+      const int kk = 4 * ks + (lane & 3), nn = lane >> 2;
+      cfr[ks] = (kk < N1 && nn < N1) ? chol_s[kk * N1 + nn] : 0.0;
+    }
     for (int it = 0; it < n_my; ++it) {
       const int stage = it % NS;
       const int ob = it & 1;
@@ -401,7 +411,9 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS>::NT, 1)
       double nsum = 0.0;
       if (it >= 1) {
         mbar_wait(&done_bar[(it - 1) & 1], ((it - 1) >> 1) & 1);
-        nsum = norm_units_dfma<N1, M, NP, NV, E, NCW>(d_s + ((it - 1) & 1) * TILE, warp, lane, chol_s, cw_s);
+        nsum = WS_NORM_DMMA ? norm_units_2d<N1, M, NP, NV, E, NCW, C::UPW>(d_s + ((it - 1) & 1) * TILE, warp, lane,
+                                                                           cfr, cw_s)
+                            : norm_units_dfma<N1, M, NP, NV, E, NCW>(d_s + ((it - 1) & 1) * TILE, warp, lane, chol_s, cw_s);
       }
       if (it >= 2) mbar_wait(&outfree_bar[ob], ((it - 2) >> 1) & 1);
       double* outb = out_s + ob * TILE;
@@ -438,7 +450,9 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS>::NT, 1)
     if (n_my >= 1) {
       const int L = n_my - 1;
       mbar_wait(&done_bar[L & 1], (L >> 1) & 1);
-      double nsum = norm_units_dfma<N1, M, NP, NV, E, NCW>(d_s + (L & 1) * TILE, warp, lane, chol_s, cw_s);
+      double nsum = WS_NORM_DMMA ? norm_units_2d<N1, M, NP, NV, E, NCW, C::UPW>(d_s + (L & 1) * TILE, warp, lane,
+                                                                                 cfr, cw_s)
+                                  : norm_units_dfma<N1, M, NP, NV, E, NCW>(d_s + (L & 1) * TILE, warp, lane, chol_s, cw_s);
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) nsum += __shfl_xor_sync(0xffffffffu, nsum, o);
       if (lane == 0) red_s[(L & 1) * 32 + warp] = nsum;
