@@ -10,18 +10,13 @@
 //                    -> qready[stage]; then, one tile behind, the bulk store
 //                    of u^{k+1} and the fixed-order tile partial of the norm
 //   consumer warps : DMMA contraction u^{k+1} = s + L q (L fragments in
-//                    registers) for tile i, then (once every warp finished
-//                    tile i-1) the norm J |(C^T x C^T) delta|^2 of tile i-1
-//                    by exact triangular DFMA line passes      -> done[i&1]
+//                    registers) for tile i interleaved with the tensor-core
+//                    norm J |C^T Delta C|^2 of tile i-1      -> done[i&1]
 #pragma once
 
 #include "ihdg_stream.cuh"
 
 namespace ihdg {
-
-#ifndef WS_NORM_DMMA
-#define WS_NORM_DMMA 1   // 1: tensor-core norm (measured faster), 0: exact DFMA passes
-#endif
 
 template <int N1, int M, int NCF, int NWC, int E, int NS>
 struct WCfg {
@@ -53,53 +48,12 @@ struct WCfg {
   static_assert(E % NQW == 0, "prep warps split the tile");
 };
 
-// ||Y||^2, Y = (C^T x C^T) delta, for this warp's (element, component) units
-// u = warp + m NCW: exact triangular DFMA passes over the node-grid lines of
-// the units (rows in place, then columns); 2D.
-template <int N1, int M, int NP, int NV, int E, int NCW>
-__device__ __forceinline__ double norm_units_dfma(double* __restrict__ dbuf, int warp, int lane,
-                                                  const double* chol, const double* cw) {
-  constexpr int UPW = (E * M + NCW - 1) / NCW;
-  constexpr int NL = UPW * N1;                  // lines per pass for this warp
-  constexpr int IT = (NL + 31) / 32;
-  double acc = 0.0;
-#pragma unroll
-  for (int pass = 0; pass < 2; ++pass) {
-#pragma unroll
-    for (int m = 0; m < IT; ++m) {
-      const int ln = lane + 32 * m;
-      const int ul = ln / N1, line = ln - (ln / N1) * N1;
-      const int u = warp + ul * NCW;
-      if (ln < NL && u < E * M) {
-        const int t = u / M, c = u - (u / M) * M;
-        double* base = dbuf + t * NV + c * NP + (pass == 0 ? line * N1 : line);
-        const int stride = pass == 0 ? 1 : N1;
-        double x[N1];
-#pragma unroll
-        for (int i = 0; i < N1; ++i) x[i] = base[i * stride];
-        double sq = 0.0;
-#pragma unroll
-        for (int i = 0; i < N1; ++i) {
-          double y = 0.0;
-#pragma unroll
-          for (int ip = i; ip < N1; ++ip) y = fma(chol[ip * N1 + i], x[ip], y);
-          if (pass == 0) base[i * stride] = y;
-          else sq = fma(y, y, sq);
-        }
-        if (pass == 1) acc = fma(cw[c], sq, acc);
-      }
-    }
-    __syncwarp();
-  }
-  return acc;
-}
-
 template <int N1, int M, int NCF, int NWC, int E, int NS>
 __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS>::NT, 1)
     k_sweep_ws(const ihdg_sweep_args a) {
   using C = WCfg<N1, M, NCF, NWC, E, NS>;
   constexpr int D = 2, NP = C::NP, NV = C::NV, NF = C::NF, NFACE = 4, KC = C::KC;
-  constexpr int NRT = C::NRT, KS = C::KS, NEG = C::NEG, NCW = C::NCW, RTW = C::RTW;
+  constexpr int NRT = C::NRT, KS = C::KS, NEG = C::NEG, NCW = C::NCW, RTW = C::RTW, UPW = C::UPW;
   constexpr int NQW = C::NQW, TILE = C::TILE;
 
   extern __shared__ __align__(16) double sm[];
@@ -118,7 +72,6 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS>::NT, 1)
   __shared__ int wc_s[NCF][NWC];
   __shared__ double ww_s[NCF][NWC];
   __shared__ double chol_s[N1 * N1];
-  __shared__ double cw_s[IHDG_MAX_COMP];
   __shared__ int qf_s[KC], qh_s[KC];
   __shared__ int qt_s[KC][NWC];
   __shared__ long long me0_s[NS];
@@ -141,7 +94,6 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS>::NT, 1)
 
   for (int i = tid; i < NFACE * NF; i += blockDim.x) fv_s[i / NF][i % NF] = face_node_vidx(D, N1, i / NF, i % NF);
   for (int i = tid; i < N1 * N1; i += blockDim.x) chol_s[i] = a.chol1d[i];
-  if (tid < IHDG_MAX_COMP) cw_s[tid] = a.comp_w[tid];
   if (tid == 0) {
     int n = 0;
     for (int f = 0; f < NFACE && n < NCF; ++f) {
@@ -360,6 +312,13 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS>::NT, 1)
       const double* sst = sm + stage * C::STAGE;
       const double* ust = sst + TILE;
       const double* qst = ust + TILE + C::HALO;
+      // norm of the previous tile (needs every warp's delta of tile it-1)
+      double nsum = 0.0;
+      if (it >= 1) {
+        mbar_wait(&done_bar[(it - 1) & 1], ((it - 1) >> 1) & 1);
+        nsum = norm_units_2d<N1, M, NP, NV, E, NCW, UPW>(d_s + ((it - 1) & 1) * TILE, warp, lane, cfr,
+                                                         a.comp_w);
+      }
       double acc[NEG][RTW][2];
 #pragma unroll
       for (int eg = 0; eg < NEG; ++eg) {
@@ -406,15 +365,6 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS>::NT, 1)
           }
         }
       }
-      // norm of the previous tile (needs every warp's delta of tile it-1); the
-      // contraction above did not have to wait for the other warps
-      double nsum = 0.0;
-      if (it >= 1) {
-        mbar_wait(&done_bar[(it - 1) & 1], ((it - 1) >> 1) & 1);
-        nsum = WS_NORM_DMMA ? norm_units_2d<N1, M, NP, NV, E, NCW, C::UPW>(d_s + ((it - 1) & 1) * TILE, warp, lane,
-                                                                           cfr, cw_s)
-                            : norm_units_dfma<N1, M, NP, NV, E, NCW>(d_s + ((it - 1) & 1) * TILE, warp, lane, chol_s, cw_s);
-      }
       if (it >= 2) mbar_wait(&outfree_bar[ob], ((it - 2) >> 1) & 1);
       double* outb = out_s + ob * TILE;
       double* dcur = d_s + ob * TILE;
@@ -450,9 +400,7 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS>::NT, 1)
     if (n_my >= 1) {
       const int L = n_my - 1;
       mbar_wait(&done_bar[L & 1], (L >> 1) & 1);
-      double nsum = WS_NORM_DMMA ? norm_units_2d<N1, M, NP, NV, E, NCW, C::UPW>(d_s + (L & 1) * TILE, warp, lane,
-                                                                                 cfr, cw_s)
-                                  : norm_units_dfma<N1, M, NP, NV, E, NCW>(d_s + (L & 1) * TILE, warp, lane, chol_s, cw_s);
+      double nsum = norm_units_2d<N1, M, NP, NV, E, NCW, UPW>(d_s + (L & 1) * TILE, warp, lane, cfr, a.comp_w);
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) nsum += __shfl_xor_sync(0xffffffffu, nsum, o);
       if (lane == 0) red_s[(L & 1) * 32 + warp] = nsum;
