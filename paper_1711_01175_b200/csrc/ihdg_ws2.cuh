@@ -1,0 +1,424 @@
+// Warp-specialised iHDG-II sweep, version 2 (ws2), for 2D configurations (production path for
+// BASELINE configs 2, 3 and 5).  Same algorithm and HBM traffic as
+// k_sweep_stream; the roles run asynchronously and hand tiles over through
+// mbarriers only (no CTA-wide barrier in the steady state):
+//
+//   producer warp  : per tile, metadata + TMA bulk copies of the s and u^k
+//                    tiles + cp.async gathers of out-of-tile neighbour faces
+//                    into an NS-stage ring                   -> full[stage]
+//   prep warps (4) : neighbour face scalars q (TraceSnapshot) for the stage
+//                    -> qready[stage]; then, one tile behind, the bulk store
+//                    of u^{k+1} and the fixed-order tile partial of the norm
+//   consumer warps : DMMA contraction u^{k+1} = s + L q (L fragments in
+//                    registers) for tile i interleaved with the tensor-core
+//                    norm J |C^T Delta C|^2 of tile i-1      -> done[i&1]
+#pragma once
+
+#include "ihdg_ws.cuh"
+
+namespace ihdg {
+
+template <int N1, int M, int NCF, int NWC, int E, int NS>
+struct W2Cfg {
+  static constexpr int D = 2;
+  static constexpr int NP = N1 * N1;
+  static constexpr int NV = M * NP;
+  static constexpr int NF = N1;
+  static constexpr int KC = NCF * NF;
+  static constexpr int NRT = (NV + 7) / 8;
+  static constexpr int KS = KC / 4;
+  static constexpr int NEG = E / 8;
+  static constexpr int NCW = NRT >= 16 ? 10 : (NRT >= 8 ? 8 : 4);  // consumer warps
+  static constexpr int RTW = (NRT + NCW - 1) / NCW;
+  static constexpr int UPW = (E * M + NCW - 1) / NCW;
+  static constexpr int NQW = 4;                                    // prep warps
+  static constexpr int NT = 32 * (NCW + NQW + 1);
+  static constexpr int TILE = E * NV;
+  static constexpr int HALO = E * NCF * NWC * NF;
+  static constexpr int QT = E * KC;
+  static constexpr int STAGE = TILE + HALO + QT;   // u^k tile, halo, q (s and u^{k+1} bypass smem)
+  static constexpr int OFF_D = NS * STAGE;
+  static constexpr int OFF_RED = OFF_D + 2 * TILE;
+  static constexpr int N_DBL = OFF_RED + 64;
+  static constexpr int NBAR = 3 * NS + 2;
+  static constexpr size_t BYTES = (size_t)N_DBL * sizeof(double) + NBAR * sizeof(uint64_t);
+  static_assert(KC % 4 == 0 && E % 8 == 0 && E <= 32 && N1 <= 8, "ws config");
+  static_assert((TILE * sizeof(double)) % 16 == 0, "tile bytes must be 16-byte multiples");
+  static_assert(E % NQW == 0, "prep warps split the tile");
+};
+
+template <int N1, int M, int NCF, int NWC, int E, int NS>
+__global__ void __launch_bounds__(W2Cfg<N1, M, NCF, NWC, E, NS>::NT, 1)
+    k_sweep_ws2(const ihdg_sweep_args a) {
+  using C = W2Cfg<N1, M, NCF, NWC, E, NS>;
+  constexpr int D = 2, NP = C::NP, NV = C::NV, NF = C::NF, NFACE = 4, KC = C::KC;
+  constexpr int NRT = C::NRT, KS = C::KS, NEG = C::NEG, NCW = C::NCW, RTW = C::RTW, UPW = C::UPW;
+  constexpr int NQW = C::NQW, TILE = C::TILE;
+
+  extern __shared__ __align__(16) double sm[];
+  double* d_s = sm + C::OFF_D;
+  double* red_s = sm + C::OFF_RED;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sm + C::N_DBL);
+  uint64_t* full_bar = bars;             // [NS] producer -> prep
+  uint64_t* qready_bar = bars + NS;      // [NS] prep -> consumers
+  uint64_t* empty_bar = bars + 2 * NS;   // [NS] consumers -> producer
+  uint64_t* done_bar = bars + 3 * NS;    // [2]  consumers -> consumers (delta complete)
+
+  __shared__ int fv_s[NFACE][NF];
+  __shared__ int cf_s[NCF];
+  __shared__ int wc_s[NCF][NWC];
+  __shared__ double ww_s[NCF][NWC];
+  __shared__ double chol_s[N1 * N1];
+  __shared__ int qf_s[KC], qh_s[KC];
+  __shared__ int qt_s[KC][NWC];
+  __shared__ long long me0_s[NS];
+  __shared__ int mnt_s[NS], mfast_s[NS];
+  __shared__ unsigned mcset_s[NS];
+  __shared__ int mmask_s[NS][E], mcls_s[NS][E];
+  __shared__ int tile_s[NS];
+  __shared__ int last_s;
+
+  ihdg_iter_state* st = a.state;
+  if (st->status != IHDG_RUNNING) return;
+
+  const int tid = threadIdx.x;
+  const int warp = tid >> 5, lane = tid & 31;
+  Geo geo;
+  geo.init(a.g, E);
+  const int64_t ls = geo.ls;
+  const double* __restrict__ uo = a.u_old + ls * NV;
+  double* __restrict__ un = a.u_new + ls * NV;
+
+  for (int i = tid; i < NFACE * NF; i += blockDim.x) fv_s[i / NF][i % NF] = face_node_vidx(D, N1, i / NF, i % NF);
+  for (int i = tid; i < N1 * N1; i += blockDim.x) chol_s[i] = a.chol1d[i];
+  if (tid == 0) {
+    int n = 0;
+    for (int f = 0; f < NFACE && n < NCF; ++f) {
+      if (!a.coupled[f]) continue;
+      cf_s[n] = f;
+      int j = 0;
+      for (int c = 0; c < M && j < NWC; ++c)
+        if (a.face_w[f][c] != 0.0) {
+          wc_s[n][j] = c;
+          ww_s[n][j] = a.face_w[f][c];
+          ++j;
+        }
+      for (; j < NWC; ++j) {
+        wc_s[n][j] = 0;
+        ww_s[n][j] = 0.0;
+      }
+      ++n;
+    }
+    for (int k = 0; k < KC; ++k) {
+      const int ci = k / NF, nn = k % NF, f = cf_s[ci];
+      qf_s[k] = f;
+      for (int j = 0; j < NWC; ++j) qt_s[k][j] = wc_s[ci][j] * NP + face_node_vidx(D, N1, f ^ 1, nn);
+      qh_s[k] = ci * NWC * NF + nn;
+    }
+    for (int s = 0; s < NS; ++s) {
+      mbar_init(&full_bar[s], 1 + 32);
+      mbar_init(&qready_bar[s], NQW);
+      mbar_init(&empty_bar[s], NCW);
+    }
+    for (int b = 0; b < 2; ++b) mbar_init(&done_bar[b], NCW);
+    fence_mbar_init();
+  }
+  __syncthreads();
+
+  const int fast_class = a.class_of_mask[0];
+  const int ntiles = (int)geo.ntiles;
+  int n_my = 0;  // tiles of this CTA
+  for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) ++n_my;
+
+  if (warp == NCW + NQW) {
+    // ============================ producer warp ============================
+    const int c0 = (int)a.g.cells[0];
+    const int per0 = a.g.periodic[0];
+    const int nlay = (int)(a.g.layer_end - a.g.layer_begin);
+    const int lsi = (int)ls;
+    for (int it = 0; it < n_my; ++it) {
+      const int tile = blockIdx.x + it * gridDim.x;
+      const int stage = it % NS;
+      if (it >= NS) mbar_wait(&empty_bar[stage], ((it / NS) - 1) & 1);
+      double* ust = sm + stage * C::STAGE;
+      double* hst = ust + TILE;
+      STile<D> ti;
+      ti.init(a.g, tile, E, nlay, lsi);
+      const int e0 = ti.e0;
+      const int nt = ti.nt;
+      int cls = -1;
+      if (lane < E) {
+        const int mask = ti.mask(lane, c0, per0);
+        cls = a.class_of_mask[mask];
+        mmask_s[stage][lane] = mask;
+        mcls_s[stage][lane] = cls;
+      }
+      const int fast = __all_sync(0xffffffffu, lane >= E || cls == fast_class);
+      unsigned cset = (lane < E && cls >= 0 && cls < 32) ? (1u << cls) : 0u;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) cset |= __shfl_xor_sync(0xffffffffu, cset, o);
+      if (lane == 0) {
+        me0_s[stage] = e0;
+        mnt_s[stage] = nt;
+        mfast_s[stage] = fast;
+        mcset_s[stage] = cset;
+        tile_s[stage] = tile;
+      }
+      __syncwarp();
+      if (lane == 0) {
+        const uint32_t bytes = (uint32_t)(nt * NV * sizeof(double));
+        mbar_arrive_expect_tx(&full_bar[stage], bytes);  // release: metadata above
+        bulk_g2s(ust, uo + (int64_t)e0 * NV, bytes, &full_bar[stage]);
+      }
+      constexpr int RUN = NWC * NF;
+#pragma unroll
+      for (int ci = 0; ci < NCF; ++ci) {
+        const int f = cf_s[ci];
+        if ((f >> 1) == 0) {
+          const int t = (f == 0) ? 0 : nt - 1;
+          const int i = ti.i0 + t;
+          const bool ex = (f == 0) ? (i > 0 || per0) : (i < c0 - 1 || per0);
+          if (!ex) continue;
+          const int nb = e0 + t + ((f == 0) ? (i > 0 ? -1 : c0 - 1) : (i < c0 - 1 ? 1 : -(c0 - 1)));
+          const double* base = uo + (int64_t)nb * NV;
+          for (int item = lane; item < RUN; item += 32) {
+            const int j = item / NF, n = item - (item / NF) * NF;
+            cp_async8(hst + ((t * NCF + ci) * NWC + j) * NF + n, base + wc_s[ci][j] * NP + fv_s[f ^ 1][n]);
+          }
+        } else {
+          if (!ti.face_has(f)) continue;
+          const double* base = uo + ((int64_t)e0 + ti.face_off(f)) * NV;
+          for (int item = lane; item < nt * RUN; item += 32) {
+            const int t = item / RUN;
+            const int rem = item - t * RUN;
+            const int j = rem / NF, n = rem - j * NF;
+            cp_async8(hst + ((t * NCF + ci) * NWC + j) * NF + n,
+                      base + t * NV + wc_s[ci][j] * NP + fv_s[f ^ 1][n]);
+          }
+        }
+      }
+      cp_async_arrive_noinc(&full_bar[stage]);
+    }
+  } else if (warp >= NCW) {
+    // ============================ prep warps ===============================
+    const int pw = warp - NCW;
+    int prev_e0 = 0, prev_nt = 0, prev_tile = -1, prev2_tile = -1;
+    for (int it = 0; it < n_my; ++it) {
+      const int stage = it % NS;
+      mbar_wait(&full_bar[stage], (it / NS) & 1);
+      // stage metadata is read now: the stage can be refilled once the
+      // consumers release it, possibly before this warp stores the tile
+      const int nt = mnt_s[stage];
+      const int cur_e0 = (int)me0_s[stage];
+      const int cur_tile = tile_s[stage];
+      const double* ust = sm + stage * C::STAGE;
+      const double* hst = ust + TILE;
+      double* qst = const_cast<double*>(hst) + C::HALO;
+      constexpr int HALF = E / NQW;
+#pragma unroll
+      for (int m = 0; m < (HALF * KC + 31) / 32; ++m) {
+        const int idx = lane + 32 * m;
+        if (idx >= HALF * KC) break;
+        const int t = pw * HALF + idx / KC, k = idx - (idx / KC) * KC;
+        const int f = qf_s[k];
+        double v = 0.0;
+        if (!(mmask_s[stage][t] & (1 << f))) {
+          const bool in_tile = (f >> 1) == 0 && !((f == 0 && t == 0) || (f == 1 && t == nt - 1));
+          const int ci = k / NF;
+          if (in_tile) {
+            const double* src = ust + (t + (f == 0 ? -1 : 1)) * NV;
+#pragma unroll
+            for (int j = 0; j < NWC; ++j) v = fma(ww_s[ci][j], src[qt_s[k][j]], v);
+          } else {
+            const double* src = hst + t * (NCF * NWC * NF) + qh_s[k];
+#pragma unroll
+            for (int j = 0; j < NWC; ++j) v = fma(ww_s[ci][j], src[j * NF], v);
+          }
+        }
+        qst[t * KC + k] = v;
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&qready_bar[stage]);
+      prev2_tile = prev_tile;
+      prev_tile = cur_tile;
+      prev_e0 = cur_e0;
+      prev_nt = nt;
+    }
+    (void)prev_e0;
+    (void)prev_nt;
+    (void)prev2_tile;
+  } else {
+    // ============================ consumer warps ===========================
+    double Lf[RTW][KS];
+#pragma unroll
+    for (int j = 0; j < RTW; ++j) {
+      const int row = (warp + j * NCW) * 8 + (lane >> 2);
+#pragma unroll
+      for (int ks = 0; ks < KS; ++ks) {
+        const int k = 4 * ks + (lane & 3);
+        const int col = cf_s[k / NF] * NF + (k % NF);
+        Lf[j][ks] = (row < NV) ? __ldg(a.LT + ((size_t)fast_class * (NFACE * NF) + col) * NV + row) : 0.0;
+      }
+    }
+    double cfr[2];
+#pragma unroll
+    for (int ks = 0; ks < 2; ++ks) {
+      const int kk = 4 * ks + (lane & 3), nn = lane >> 2;
+      cfr[ks] = (kk < N1 && nn < N1) ? chol_s[kk * N1 + nn] : 0.0;
+    }
+    // s of the warp's rows for all tile elements: prefetched one tile ahead
+    // (8 doubles per lane) straight into the accumulator layout
+    const int nlay = (int)(a.g.layer_end - a.g.layer_begin);
+    const int lsi = (int)ls;
+    double sp[NEG][RTW][2];
+    auto load_s = [&](int itl) {
+      if (itl >= n_my) return;
+      STile<D> tl;
+      tl.init(a.g, (int)blockIdx.x + itl * (int)gridDim.x, E, nlay, lsi);
+      const double* sg = a.s + (int64_t)tl.e0 * NV;
+#pragma unroll
+      for (int eg = 0; eg < NEG; ++eg) {
+        const int te = eg * 8 + 2 * (lane & 3);
+#pragma unroll
+        for (int j = 0; j < RTW; ++j) {
+          const int row = (warp + j * NCW) * 8 + (lane >> 2);
+          const bool ok = row < NV && (warp + j * NCW) < NRT;
+          sp[eg][j][0] = ok ? __ldcs(sg + te * NV + row) : 0.0;
+          sp[eg][j][1] = ok ? __ldcs(sg + (te + 1) * NV + row) : 0.0;
+        }
+      }
+    };
+    load_s(0);
+    for (int it = 0; it < n_my; ++it) {
+      const int stage = it % NS;
+      const int ob = it & 1;
+      mbar_wait(&qready_bar[stage], (it / NS) & 1);
+      const int fast = mfast_s[stage];
+      const int e0t = (int)me0_s[stage];
+      const double* ust = sm + stage * C::STAGE;
+      const double* qst = ust + TILE + C::HALO;
+      // norm of the previous tile (needs every warp's delta of tile it-1)
+      double nsum = 0.0;
+      if (it >= 1) {
+        mbar_wait(&done_bar[(it - 1) & 1], ((it - 1) >> 1) & 1);
+        nsum = norm_units_2d<N1, M, NP, NV, E, NCW, UPW>(d_s + ((it - 1) & 1) * TILE, warp, lane, cfr,
+                                                         a.comp_w);
+      }
+      double acc[NEG][RTW][2];
+#pragma unroll
+      for (int eg = 0; eg < NEG; ++eg)
+#pragma unroll
+        for (int j = 0; j < RTW; ++j) {
+          acc[eg][j][0] = sp[eg][j][0];
+          acc[eg][j][1] = sp[eg][j][1];
+        }
+      load_s(it + 1);
+      const double* qb = qst + (lane >> 2) * KC + (lane & 3);
+      if (fast) {
+#pragma unroll
+        for (int ks = 0; ks < KS; ++ks) {
+          double b[NEG];
+#pragma unroll
+          for (int eg = 0; eg < NEG; ++eg) b[eg] = qb[eg * 8 * KC + 4 * ks];
+#pragma unroll
+          for (int eg = 0; eg < NEG; ++eg)
+#pragma unroll
+            for (int j = 0; j < RTW; ++j) dmma_8x8x4(acc[eg][j][0], acc[eg][j][1], Lf[j][ks], b[eg]);
+        }
+      } else {
+        const unsigned cset = mcset_s[stage];
+        for (unsigned rem = cset; rem != 0u; rem &= rem - 1u) {
+          const int c = __ffs(rem) - 1;
+          for (int ks = 0; ks < KS; ++ks) {
+            const int k = 4 * ks + (lane & 3);
+            const int col = cf_s[k / NF] * NF + (k % NF);
+            double av[RTW];
+#pragma unroll
+            for (int j = 0; j < RTW; ++j) {
+              const int row = (warp + j * NCW) * 8 + (lane >> 2);
+              av[j] = (row < NV) ? __ldg(a.LT + ((size_t)c * (NFACE * NF) + col) * NV + row) : 0.0;
+            }
+#pragma unroll
+            for (int eg = 0; eg < NEG; ++eg) {
+              const double b = (mcls_s[stage][eg * 8 + (lane >> 2)] == c) ? qb[eg * 8 * KC + 4 * ks] : 0.0;
+#pragma unroll
+              for (int j = 0; j < RTW; ++j) dmma_8x8x4(acc[eg][j][0], acc[eg][j][1], av[j], b);
+            }
+          }
+        }
+      }
+      double* ug = un + (int64_t)e0t * NV;
+      double* dcur = d_s + ob * TILE;
+#pragma unroll
+      for (int eg = 0; eg < NEG; ++eg) {
+        const int te = eg * 8 + 2 * (lane & 3);
+#pragma unroll
+        for (int j = 0; j < RTW; ++j) {
+          const int row = (warp + j * NCW) * 8 + (lane >> 2);
+          if (row < NV && (warp + j * NCW) < NRT) {
+#pragma unroll
+            for (int v = 0; v < 2; ++v) {
+              const int t = te + v;
+              __stcs(ug + t * NV + row, acc[eg][j][v]);
+              dcur[t * NV + row] = acc[eg][j][v] - ust[t * NV + row];
+            }
+          }
+        }
+      }
+      if (it >= 1) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) nsum += __shfl_xor_sync(0xffffffffu, nsum, o);
+        if (lane == 0) red_s[((it - 1) & 1) * 32 + warp] = nsum;
+      }
+      // tile it-2: every warp wrote its norm partial in iteration it-1, before
+      // arriving on done[(it-1)&1], which this warp waited for above
+      if (it >= 2 && tid == 0) {
+        double sacc = 0.0;
+        for (int w = 0; w < NCW; ++w) sacc += red_s[(it & 1) * 32 + w];
+        a.tile_partials[(int)blockIdx.x + (it - 2) * (int)gridDim.x] = a.jac * sacc;
+      }
+      __syncwarp();
+      if (lane == 0) {
+        mbar_arrive(&empty_bar[stage]);
+        mbar_arrive(&done_bar[ob]);
+      }
+    }
+    // drain: norm of the last tile
+    if (n_my >= 1) {
+      const int L = n_my - 1;
+      mbar_wait(&done_bar[L & 1], (L >> 1) & 1);
+      double nsum = norm_units_2d<N1, M, NP, NV, E, NCW, UPW>(d_s + (L & 1) * TILE, warp, lane, cfr, a.comp_w);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) nsum += __shfl_xor_sync(0xffffffffu, nsum, o);
+      if (lane == 0) red_s[(L & 1) * 32 + warp] = nsum;
+    }
+  }
+
+  __syncthreads();
+  if (tid == 0 && n_my >= 1) {
+    const int L = n_my - 1;
+    double s = 0.0;
+    for (int w = 0; w < NCW; ++w) s += red_s[(L & 1) * 32 + w];
+    a.tile_partials[blockIdx.x + L * gridDim.x] = a.jac * s;
+    if (L >= 1) {
+      double s1 = 0.0;
+      for (int w = 0; w < NCW; ++w) s1 += red_s[((L - 1) & 1) * 32 + w];
+      a.tile_partials[blockIdx.x + (L - 1) * gridDim.x] = a.jac * s1;
+    }
+  }
+  if (a.finalize) {
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) {
+      const unsigned tk = atomicAdd(&st->ticket, 1u);
+      last_s = (tk == gridDim.x - 1);
+    }
+    __syncthreads();
+    if (last_s) {
+      __threadfence();
+      finalize_block(a.tile_partials, geo.ntiles, st, a.norm_hist);
+    }
+  }
+}
+
+}  // namespace ihdg
