@@ -134,10 +134,12 @@ const StreamEntry* stream_entry(const ihdg_sweep_args* a) {
     const char* s = std::getenv("IHDG_SWEEP_IMPL");
     no_v3 = (s != nullptr && (std::strcmp(s, "ws") == 0 || std::strcmp(s, "stream") == 0)) ? 1 : 0;
   }
-  static int no_ws2 = -1;
-  if (no_ws2 < 0) {
+  // IHDG_SWEEP_IMPL: "ws2" opts in to the experimental ws2 kernel (slower than
+  // ws on config 5); "ws"/"stream" skip v3; "generic" skips all
+  static int want_ws2 = -1;
+  if (want_ws2 < 0) {
     const char* s = std::getenv("IHDG_SWEEP_IMPL");
-    no_ws2 = (s != nullptr && std::strcmp(s, "ws") == 0) ? 1 : 0;
+    want_ws2 = (s != nullptr && std::strcmp(s, "ws2") == 0) ? 1 : 0;
   }
   if (a->norm_kind != IHDG_NORM_VOLUME) return nullptr;
   const ihdg_geom& g = a->g;
@@ -153,7 +155,8 @@ const StreamEntry* stream_entry(const ihdg_sweep_args* a) {
     if (e.D != g.dim || e.N1 != g.order + 1 || e.M != g.ncomp) continue;
     if (e.NCF != ncf || maxw > e.NWC) continue;
     if (e.v3 && no_v3) continue;
-    if (e.launch == (int (*)(const ihdg_sweep_args*, cudaStream_t))launch_ws2_t<7, 3, 4, 2, 16, 6> && no_ws2) continue;
+    if (e.launch == (int (*)(const ihdg_sweep_args*, cudaStream_t))launch_ws2_t<7, 3, 4, 2, 16, 6> && !want_ws2)
+      continue;
     Geo geo;
     geo.init(g, e.E);
     if (geo.tile_len % e.E != 0) continue;                       // full tiles only

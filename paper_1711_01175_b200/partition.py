@@ -39,7 +39,7 @@ def halo_ops(rank: int, world: int, periodic: bool):
 
 
 def halo_exchange(buf, layer_elems: int, n_local_layers: int, rank: int, world: int,
-                  periodic: bool, group=None) -> None:
+                  periodic: bool, group=None, host_staging: bool = False) -> None:
     """Fill the ghost layers of the ghost-padded state ``buf``
     [(n_local_layers + 2) * layer_elems, NV] from the neighbouring ranks.
 
@@ -51,6 +51,19 @@ def halo_exchange(buf, layer_elems: int, n_local_layers: int, rank: int, world: 
     if world == 1:
         return
     L, nL = layer_elems, n_local_layers
+    if host_staging and buf.is_cuda:
+        # gloo path for device buffers: exchange host copies of the boundary
+        # layers (test mode on a single GPU; no kernel waits on another rank)
+        stage = buf.new_zeros(((nL + 2) * L,) + tuple(buf.shape[1:]), device="cpu")
+        stage[L: 2 * L] = buf[L: 2 * L].cpu()
+        stage[nL * L: (nL + 1) * L] = buf[nL * L: (nL + 1) * L].cpu()
+        halo_exchange(stage, L, nL, rank, world, periodic, group)
+        lower, upper = halo_ops(rank, world, periodic)
+        if lower is not None:
+            buf[0: L].copy_(stage[0: L])
+        if upper is not None:
+            buf[(nL + 1) * L: (nL + 2) * L].copy_(stage[(nL + 1) * L: (nL + 2) * L])
+        return
     first = buf[L: 2 * L]
     last = buf[nL * L: (nL + 1) * L]
     ghost_lo = buf[0: L]

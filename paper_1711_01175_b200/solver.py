@@ -30,6 +30,10 @@ def _torch():
     return torch
 
 
+def torch_cpu_zeros_like(t):
+    return t.new_zeros(t.shape, device="cpu")
+
+
 def _ptr(t) -> int:
     return 0 if t is None else int(t.data_ptr())
 
@@ -336,8 +340,12 @@ class DistributedSweeper:
     derives the same device-side convergence flag.
     """
 
-    def __init__(self, solver: DeviceSolver, rank: int, world: int, group=None):
+    def __init__(self, solver: DeviceSolver, rank: int, world: int, group=None,
+                 host_staging: bool = False):
+        """``host_staging``: exchange halos and partials through host memory
+        (gloo); used to test this path with several ranks on one GPU."""
         self.sv, self.rank, self.world, self.group = solver, rank, world, group
+        self.host_staging = host_staging
         torch = solver.torch
         self.ntiles_rank = solver.ntiles
         self.global_partials = torch.zeros(self.ntiles_rank * world, dtype=torch.float64,
@@ -350,7 +358,7 @@ class DistributedSweeper:
 
         sv = self.sv
         halo_exchange(sv.u[sv.cur], sv.ls, self.nlay, self.rank, self.world, self.periodic_last,
-                      self.group)
+                      self.group, host_staging=self.host_staging)
 
     def sweep(self, a: N.SweepArgs) -> None:
         import torch.distributed as dist
@@ -359,7 +367,12 @@ class DistributedSweeper:
         self._exchange()
         a.u_old, a.u_new = _ptr(sv.u[sv.cur]), _ptr(sv.u[1 - sv.cur])
         N.check(sv.L.ihdg_sweep(C.byref(a), sv._sptr), "ihdg_sweep")
-        dist.all_gather_into_tensor(self.global_partials, sv.partials, group=self.group)
+        if self.host_staging:
+            parts = [torch_cpu_zeros_like(sv.partials) for _ in range(self.world)]
+            dist.all_gather(parts, sv.partials.cpu(), group=self.group)
+            self.global_partials.copy_(sv.torch.cat(parts))
+        else:
+            dist.all_gather_into_tensor(self.global_partials, sv.partials, group=self.group)
         f = N.FinalizeArgs()
         f.tile_partials, f.n_tiles = _ptr(self.global_partials), self.global_partials.numel()
         f.state, f.norm_hist = _ptr(sv.state_dev), _ptr(sv.norm_hist)

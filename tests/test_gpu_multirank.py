@@ -1,0 +1,105 @@
+"""The strip-partitioned device path (solver.DistributedSweeper) with two
+ranks sharing cuda:0.
+
+The ranks use the gloo backend with host staging of the halo layers and
+tile partials, so no kernel ever waits on another rank.  The NCCL variant
+differs only in the transport call.  The sweep kernels, the ghost-layer
+addressing, the all-gather of tile partials and the fixed-order finalize are
+the same.  For an even split the result must be bit-identical to one rank:
+same iteration count, same norms, same fields.
+"""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _setup(wl, layers=None):
+    from paper_1711_01175_b200.solver import DeviceSolver
+
+    sv = DeviceSolver(wl.mesh, wl.problem, wl.ops, dt=wl.dt, layers=layers, max_iters=5000)
+    forcing = getattr(wl.problem, "forcing", None)
+    if forcing is not None:
+        sv.set_forcing(forcing)
+    sv.zero_state()
+    for name, fld in wl.initial.items():
+        sv.set_state_component(fld, sv.spec.labels.index(name))
+    if wl.dt is not None:
+        sv.begin_step()
+    else:
+        sv.prepare_steady()
+    return sv
+
+
+def _worker(rank, world, port, cfg, kw, q):
+    import torch
+    import torch.distributed as dist
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_1711_01175_b200.partition import strip_range
+        from paper_1711_01175_b200.solver import DistributedSweeper
+        from paper_1711_01175_b200.workloads import make_config
+
+        wl = make_config(cfg, seed=1, **kw)
+        layers = strip_range(wl.mesh.cells[-1], rank, world)
+        sv = _setup(wl, layers)
+        ds = DistributedSweeper(sv, rank, world, host_staging=True)
+        res = ds.iterate(tol=1e-10, max_iters=5000, norm="volume", batch=8)
+        q.put((rank, layers, res.iterations, res.status, res.norms, sv.get_state()))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("cfg,kw", [
+    (3, dict(cells=16, n_steps=1)),            # periodic shallow water (wrap across ranks)
+    (5, dict(cells=32, kappa=1e-1, n_steps=1)),  # convection-diffusion p=6, 9 operator classes
+    (4, dict(cells=8)),                        # 3D transport
+])
+def test_two_ranks_bit_identical_to_one(cfg, kw):
+    import torch
+    import torch.multiprocessing as mp
+
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    from paper_1711_01175_b200.workloads import make_config
+
+    torch.cuda.set_device(0)
+    wl = make_config(cfg, seed=1, **kw)
+    sv = _setup(wl)
+    ref = sv.iterate(tol=1e-10, max_iters=5000, norm="volume", batch=8)
+    ref_state = sv.get_state()
+    del sv
+    torch.cuda.empty_cache()
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, cfg, kw, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    out = sorted([q.get(timeout=600) for _ in range(2)], key=lambda x: x[0])
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    ls = int(np.prod(wl.mesh.cells[:-1]))
+    for rank, (lb, le), iters, status, norms, state in out:
+        assert status == ref.status == "converged"
+        assert iters == ref.iterations
+        np.testing.assert_array_equal(norms, ref.norms)
+        np.testing.assert_array_equal(state, ref_state[lb * ls:le * ls])
