@@ -27,6 +27,19 @@
 
 namespace ihdg {
 
+// Optional per-role cycle counters (profiling build, -DIHDG_WS_PROF; tools/ws_roles.py).
+#ifdef IHDG_WS_PROF
+__device__ unsigned long long g_ws_prof[16];
+#define V3_T0(v) const long long v = clock64()
+#define V3_ACC(slot, v)                                                                   \
+  do {                                                                                    \
+    if ((threadIdx.x & 31) == 0) atomicAdd(&g_ws_prof[slot], (unsigned long long)(clock64() - (v))); \
+  } while (0)
+#else
+#define V3_T0(v)
+#define V3_ACC(slot, v)
+#endif
+
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }

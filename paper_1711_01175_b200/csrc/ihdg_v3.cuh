@@ -25,19 +25,6 @@
 
 namespace ihdg {
 
-// Optional per-role cycle counters (profiling build, -DIHDG_WS_PROF; tools/ws_roles.py).
-#ifdef IHDG_WS_PROF
-__device__ unsigned long long g_ws_prof[16];
-#define V3_T0(v) const long long v = clock64()
-#define V3_ACC(slot, v)                                                                   \
-  do {                                                                                    \
-    if ((threadIdx.x & 31) == 0) atomicAdd(&g_ws_prof[slot], (unsigned long long)(clock64() - (v))); \
-  } while (0)
-#else
-#define V3_T0(v)
-#define V3_ACC(slot, v)
-#endif
-
 template <int D, int N1, int M, int NCF, int NWC, int NS, int NCW, int PF, int NQW_ = 2>
 struct V3Cfg {
   static constexpr int E = 8;                     // elements per physical tile (DMMA n)

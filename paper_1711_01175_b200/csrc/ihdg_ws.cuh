@@ -34,7 +34,7 @@ struct WCfg {
   static constexpr int NQW = 4;                                    // prep warps
   static constexpr int NT = 32 * (NCW + NQW + 1);
   static constexpr int TILE = E * NV;
-  static constexpr int HALO = E * NCF * NWC * NF;
+  static constexpr int HALO = 0;   // out-of-tile faces: prep warps load them into registers
   static constexpr int QT = E * KC;
   static constexpr int STAGE = 2 * TILE + HALO + QT;
   static constexpr int OFF_OUT = NS * STAGE;
@@ -79,6 +79,7 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS>::NT, 1)
   __shared__ unsigned mcset_s[NS];
   __shared__ int mmask_s[NS][E], mcls_s[NS][E];
   __shared__ int tile_s[NS];
+  __shared__ int com_s[64];
   __shared__ int last_s;
 
   ihdg_iter_state* st = a.state;
@@ -94,6 +95,7 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS>::NT, 1)
 
   for (int i = tid; i < NFACE * NF; i += blockDim.x) fv_s[i / NF][i % NF] = face_node_vidx(D, N1, i / NF, i % NF);
   for (int i = tid; i < N1 * N1; i += blockDim.x) chol_s[i] = a.chol1d[i];
+  if (tid < 64) com_s[tid] = a.class_of_mask[tid];
   if (tid == 0) {
     int n = 0;
     for (int f = 0; f < NFACE && n < NCF; ++f) {
@@ -119,7 +121,7 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS>::NT, 1)
       qh_s[k] = ci * NWC * NF + nn;
     }
     for (int s = 0; s < NS; ++s) {
-      mbar_init(&full_bar[s], 1 + 32);
+      mbar_init(&full_bar[s], 1);
       mbar_init(&qready_bar[s], NQW);
       mbar_init(&empty_bar[s], NCW);
     }
@@ -133,6 +135,7 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS>::NT, 1)
 
   const int fast_class = a.class_of_mask[0];
   const int ntiles = (int)geo.ntiles;
+  V3_T0(tk0);
   int n_my = 0;  // tiles of this CTA
   for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) ++n_my;
 
@@ -145,10 +148,12 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS>::NT, 1)
     for (int it = 0; it < n_my; ++it) {
       const int tile = blockIdx.x + it * gridDim.x;
       const int stage = it % NS;
+      V3_T0(tw);
       if (it >= NS) mbar_wait(&empty_bar[stage], ((it / NS) - 1) & 1);
+      V3_ACC(0, tw);
+      V3_T0(tl);
       double* sst = sm + stage * C::STAGE;
       double* ust = sst + TILE;
-      double* hst = ust + TILE;
       STile<D> ti;
       ti.init(a.g, tile, E, nlay, lsi);
       const int e0 = ti.e0;
@@ -156,7 +161,7 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS>::NT, 1)
       int cls = -1;
       if (lane < E) {
         const int mask = ti.mask(lane, c0, per0);
-        cls = a.class_of_mask[mask];
+        cls = com_s[mask];
         mmask_s[stage][lane] = mask;
         mcls_s[stage][lane] = cls;
       }
@@ -178,42 +183,65 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS>::NT, 1)
         bulk_g2s(sst, a.s + (int64_t)e0 * NV, bytes, &full_bar[stage]);
         bulk_g2s(ust, uo + (int64_t)e0 * NV, bytes, &full_bar[stage]);
       }
-      constexpr int RUN = NWC * NF;
-#pragma unroll
-      for (int ci = 0; ci < NCF; ++ci) {
-        const int f = cf_s[ci];
-        if ((f >> 1) == 0) {
-          const int t = (f == 0) ? 0 : nt - 1;
-          const int i = ti.i0 + t;
-          const bool ex = (f == 0) ? (i > 0 || per0) : (i < c0 - 1 || per0);
-          if (!ex) continue;
-          const int nb = e0 + t + ((f == 0) ? (i > 0 ? -1 : c0 - 1) : (i < c0 - 1 ? 1 : -(c0 - 1)));
-          const double* base = uo + (int64_t)nb * NV;
-          for (int item = lane; item < RUN; item += 32) {
-            const int j = item / NF, n = item - (item / NF) * NF;
-            cp_async8(hst + ((t * NCF + ci) * NWC + j) * NF + n, base + wc_s[ci][j] * NP + fv_s[f ^ 1][n]);
-          }
-        } else {
-          if (!ti.face_has(f)) continue;
-          const double* base = uo + ((int64_t)e0 + ti.face_off(f)) * NV;
-          for (int item = lane; item < nt * RUN; item += 32) {
-            const int t = item / RUN;
-            const int rem = item - t * RUN;
-            const int j = rem / NF, n = rem - j * NF;
-            cp_async8(hst + ((t * NCF + ci) * NWC + j) * NF + n,
-                      base + t * NV + wc_s[ci][j] * NP + fv_s[f ^ 1][n]);
-          }
-        }
-      }
-      cp_async_arrive_noinc(&full_bar[stage]);
+      V3_ACC(9, tl);
     }
   } else if (warp >= NCW) {
     // ============================ prep warps ===============================
     const int pw = warp - NCW;
+    const int c0 = (int)a.g.cells[0];
+    const int per0 = a.g.periodic[0];
+    const int nlay = (int)(a.g.layer_end - a.g.layer_begin);
+    const int lsi = (int)ls;
     int prev_e0 = 0, prev_nt = 0, prev_tile = -1, prev2_tile = -1;
+    constexpr int HALF = E / NQW;
+    constexpr int QM = (HALF * KC + 31) / 32;
+    // out-of-tile neighbour face nodes of this warp's entries, loaded from
+    // global (L2) into registers one tile ahead
+    double gv[QM][NWC], gvn[QM][NWC];
+    int qs = 0, ql = 0, qsn = 0, qln = 0;
+    auto gather = [&](int itg, double (&dst)[QM][NWC], int& in_bits, int& ld_bits) {
+      in_bits = 0;
+      ld_bits = 0;
+      if (itg >= n_my) return;
+      STile<D> tg;
+      tg.init(a.g, (int)blockIdx.x + itg * (int)gridDim.x, E, nlay, lsi);
+#pragma unroll
+      for (int m = 0; m < QM; ++m) {
+        const int idx = lane + 32 * m;
+#pragma unroll
+        for (int j = 0; j < NWC; ++j) dst[m][j] = 0.0;
+        if (idx < HALF * KC) {
+          const int t = pw * HALF + idx / KC, k = idx - (idx / KC) * KC;
+          const int f = qf_s[k];
+          if (!(tg.mask(t, c0, per0) & (1 << f))) {
+            const bool in_tile = (f >> 1) == 0 && !((f == 0 && t == 0) || (f == 1 && t == E - 1));
+            if (in_tile) {
+              in_bits |= 1 << m;
+            } else {
+              ld_bits |= 1 << m;
+              int nb;
+              if (f >= 2) {
+                nb = tg.e0 + t + tg.face_off(f);
+              } else {
+                const int i = tg.i0 + t;
+                nb = tg.e0 + t + ((f == 0) ? (i > 0 ? -1 : c0 - 1) : (i < c0 - 1 ? 1 : -(c0 - 1)));
+              }
+              const double* src = uo + (int64_t)nb * NV;
+#pragma unroll
+              for (int j = 0; j < NWC; ++j) dst[m][j] = __ldg(src + qt_s[k][j]);
+            }
+          }
+        }
+      }
+    };
+    gather(0, gv, qs, ql);
     for (int it = 0; it < n_my; ++it) {
       const int stage = it % NS;
+      gather(it + 1, gvn, qsn, qln);
+      V3_T0(tp);
       mbar_wait(&full_bar[stage], (it / NS) & 1);
+      V3_ACC(1, tp);
+      V3_T0(tq);
       // stage metadata is read now: the stage can be refilled once the
       // consumers release it, possibly before this warp stores the tile
       const int nt = mnt_s[stage];
@@ -221,32 +249,34 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS>::NT, 1)
       const int cur_tile = tile_s[stage];
       const double* sst = sm + stage * C::STAGE;
       const double* ust = sst + TILE;
-      const double* hst = ust + TILE;
-      double* qst = const_cast<double*>(hst) + C::HALO;
-      constexpr int HALF = E / NQW;
+      double* qst = const_cast<double*>(ust) + TILE + C::HALO;
 #pragma unroll
-      for (int m = 0; m < (HALF * KC + 31) / 32; ++m) {
+      for (int m = 0; m < QM; ++m) {
         const int idx = lane + 32 * m;
-        if (idx >= HALF * KC) break;
-        const int t = pw * HALF + idx / KC, k = idx - (idx / KC) * KC;
-        const int f = qf_s[k];
-        double v = 0.0;
-        if (!(mmask_s[stage][t] & (1 << f))) {
-          const bool in_tile = (f >> 1) == 0 && !((f == 0 && t == 0) || (f == 1 && t == nt - 1));
+        if (idx < HALF * KC) {
+          const int t = pw * HALF + idx / KC, k = idx - (idx / KC) * KC;
           const int ci = k / NF;
-          if (in_tile) {
+          double v = 0.0;
+          if (qs & (1 << m)) {
+            const int f = qf_s[k];
             const double* src = ust + (t + (f == 0 ? -1 : 1)) * NV;
 #pragma unroll
             for (int j = 0; j < NWC; ++j) v = fma(ww_s[ci][j], src[qt_s[k][j]], v);
-          } else {
-            const double* src = hst + t * (NCF * NWC * NF) + qh_s[k];
+          } else if (ql & (1 << m)) {
 #pragma unroll
-            for (int j = 0; j < NWC; ++j) v = fma(ww_s[ci][j], src[j * NF], v);
+            for (int j = 0; j < NWC; ++j) v = fma(ww_s[ci][j], gv[m][j], v);
           }
+          qst[t * KC + k] = v;
         }
-        qst[t * KC + k] = v;
       }
+#pragma unroll
+      for (int m = 0; m < QM; ++m)
+#pragma unroll
+        for (int j = 0; j < NWC; ++j) gv[m][j] = gvn[m][j];
+      qs = qsn;
+      ql = qln;
       __syncwarp();
+      V3_ACC(2, tq);
       if (lane == 0) mbar_arrive(&qready_bar[stage]);
       if (it >= 1) {
         const int pb = (it - 1) & 1;
@@ -307,7 +337,9 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS>::NT, 1)
     for (int it = 0; it < n_my; ++it) {
       const int stage = it % NS;
       const int ob = it & 1;
+      V3_T0(tc);
       mbar_wait(&qready_bar[stage], (it / NS) & 1);
+      V3_ACC(3, tc);
       const int fast = mfast_s[stage];
       const double* sst = sm + stage * C::STAGE;
       const double* ust = sst + TILE;
@@ -315,10 +347,13 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS>::NT, 1)
       // norm of the previous tile (needs every warp's delta of tile it-1)
       double nsum = 0.0;
       if (it >= 1) {
+        V3_T0(td);
         mbar_wait(&done_bar[(it - 1) & 1], ((it - 1) >> 1) & 1);
+        V3_ACC(8, td);
         nsum = norm_units_2d<N1, M, NP, NV, E, NCW, UPW>(d_s + ((it - 1) & 1) * TILE, warp, lane, cfr,
                                                          a.comp_w);
       }
+      V3_T0(tm);
       double acc[NEG][RTW][2];
 #pragma unroll
       for (int eg = 0; eg < NEG; ++eg) {
@@ -365,7 +400,10 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS>::NT, 1)
           }
         }
       }
+      V3_ACC(4, tm);
+      V3_T0(to);
       if (it >= 2) mbar_wait(&outfree_bar[ob], ((it - 2) >> 1) & 1);
+      V3_ACC(5, to);
       double* outb = out_s + ob * TILE;
       double* dcur = d_s + ob * TILE;
 #pragma unroll
@@ -414,6 +452,9 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS>::NT, 1)
     for (int w = 0; w < NCW; ++w) s += red_s[(L & 1) * 32 + w];
     a.tile_partials[blockIdx.x + L * gridDim.x] = a.jac * s;
   }
+#ifdef IHDG_WS_PROF
+  if (tid == 0) V3_ACC(6, tk0);
+#endif
   if (a.finalize) {
     __threadfence();
     __syncthreads();

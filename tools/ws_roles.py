@@ -14,9 +14,9 @@ from paper_1711_01175_b200 import _native as N  # noqa: E402
 from paper_1711_01175_b200.solver import DeviceSolver  # noqa: E402
 from paper_1711_01175_b200.workloads import make_config  # noqa: E402
 
-NAMES = ["producer: wait done (retire)", "prep: wait full", "prep: q compute", "consumer: wait qready",
-         "consumer: contraction", "consumer: epilogue", "CTA total", "consumer: norm", "-",
-         "producer: load issue"]
+NAMES = ["producer: wait (empty/done)", "prep: wait full", "prep: q compute", "consumer: wait qready",
+         "consumer: contraction", "consumer: epilogue / wait outfree (ws)", "CTA total",
+         "consumer: norm (v3)", "consumer: wait done prev (ws)", "producer: load issue"]
 
 
 def main():
