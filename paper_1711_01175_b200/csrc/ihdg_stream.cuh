@@ -30,14 +30,24 @@ namespace ihdg {
 // Optional per-role cycle counters (profiling build, -DIHDG_WS_PROF; tools/ws_roles.py).
 #ifdef IHDG_WS_PROF
 __device__ unsigned long long g_ws_prof[16];
+// per-CTA shared counters, flushed once per CTA (V3_FLUSH) to keep the
+// measurement from perturbing the kernel
+#define V3_DECL __shared__ unsigned long long prof_s[16]; if (threadIdx.x < 16) prof_s[threadIdx.x] = 0ull;
 #define V3_T0(v) const long long v = clock64()
-#define V3_ACC(slot, v)                                                                   \
-  do {                                                                                    \
-    if ((threadIdx.x & 31) == 0) atomicAdd(&g_ws_prof[slot], (unsigned long long)(clock64() - (v))); \
+#define V3_ACC(slot, v)                                                                              \
+  do {                                                                                               \
+    if ((threadIdx.x & 31) == 0) atomicAdd(&prof_s[slot], (unsigned long long)(clock64() - (v)));    \
+  } while (0)
+#define V3_FLUSH                                                                                     \
+  do {                                                                                               \
+    __syncthreads();                                                                                 \
+    if (threadIdx.x < 16) atomicAdd(&g_ws_prof[threadIdx.x], prof_s[threadIdx.x]);                   \
   } while (0)
 #else
+#define V3_DECL
 #define V3_T0(v)
 #define V3_ACC(slot, v)
+#define V3_FLUSH
 #endif
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -224,7 +234,7 @@ struct SCfg {
 // ||Y||_F^2 of Y = C^T Delta C for the UPW (element, component) units of this
 // warp (2D, tensor core).  Delta[j][i] = delta at node (i, j), zero padded to
 // 8x8; cfr = C fragments.  Invalid units read zeros (uniform control flow).
-template <int N1, int M, int NP, int NV, int E, int NCW, int UPW>
+template <int N1, int M, int NP, int NV, int E, int NCW, int UPW, int PS = 0>
 __device__ __forceinline__ double norm_units_2d(const double* __restrict__ dbuf, int warp, int lane,
                                                 const double (&cfr)[2], const double* comp_w) {
   double acc = 0.0;
@@ -235,7 +245,8 @@ __device__ __forceinline__ double norm_units_2d(const double* __restrict__ dbuf,
     const bool valid = u < E * M;
     const int uu = valid ? u : 0;
     const int t = uu / M, c = uu - (uu / M) * M;
-    const double* base = dbuf + t * NV + c * NP;
+    // element offset: plain (t NV) or padded element pairs (pair stride PS)
+    const double* base = dbuf + (PS ? (t >> 1) * PS + (t & 1) * NV : t * NV) + c * NP;
     r0[m] = 0.0;
     r1[m] = 0.0;
 #pragma unroll

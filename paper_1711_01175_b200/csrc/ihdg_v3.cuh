@@ -89,6 +89,7 @@ __global__ void __launch_bounds__(V3Cfg<D, N1, M, NCF, NWC, NS, NCW, PF, NQW_>::
 
   ihdg_iter_state* st = a.state;
   if (st->status != IHDG_RUNNING) return;
+  V3_DECL
 
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
@@ -433,6 +434,7 @@ __global__ void __launch_bounds__(V3Cfg<D, N1, M, NCF, NWC, NS, NCW, PF, NQW_>::
 
 #ifdef IHDG_WS_PROF
   if (tid == 0) V3_ACC(6, tk0);
+  V3_FLUSH;
 #endif
   if (a.finalize) {
     __threadfence();
