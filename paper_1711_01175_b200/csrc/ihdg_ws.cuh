@@ -46,8 +46,7 @@ struct WCfg {
   static constexpr int OFF_D = OFF_OUT + 2 * TILE;
   static constexpr int OFF_RED = OFF_D + 2 * TILE;
   static constexpr int N_DBL = OFF_RED + 64;
-  static constexpr int NBAR = 3 * NS + 6;
-  static constexpr int UPQ = (E * M + NQW - 1) / NQW;  // norm units per prep warp
+  static constexpr int NBAR = 3 * NS + 4;
   static constexpr size_t BYTES = (size_t)N_DBL * sizeof(double) + NBAR * sizeof(uint64_t);
   static_assert(KC % 4 == 0 && E % 8 == 0 && E <= 32 && N1 <= 8, "ws config");
   static_assert((TILE * sizeof(double)) % 16 == 0, "tile bytes must be 16-byte multiples");
@@ -61,7 +60,7 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS>::NT, 1)
     k_sweep_ws(const ihdg_sweep_args a) {
   using C = WCfg<N1, M, NCF, NWC, E, NS>;
   constexpr int D = 2, NP = C::NP, NV = C::NV, NF = C::NF, NFACE = 4, KC = C::KC;
-  constexpr int NRT = C::NRT, KS = C::KS, NEG = C::NEG, NCW = C::NCW, RTW = C::RTW;
+  constexpr int NRT = C::NRT, KS = C::KS, NEG = C::NEG, NCW = C::NCW, RTW = C::RTW, UPW = C::UPW;
   constexpr int NQW = C::NQW, TILE = C::TILE;
 
   extern __shared__ __align__(16) double sm[];
@@ -73,15 +72,13 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS>::NT, 1)
   uint64_t* qready_bar = bars + NS;      // [NS] prep -> consumers
   uint64_t* empty_bar = bars + 2 * NS;   // [NS] consumers -> producer
   uint64_t* done_bar = bars + 3 * NS;    // [2]  consumers -> prep, consumers
-  uint64_t* outfree_bar = done_bar + 2;  // [2]  prep -> consumers (out buffer free)
-  uint64_t* normdone_bar = done_bar + 4; // [2]  prep -> consumers (delta buffer free)
+  uint64_t* outfree_bar = done_bar + 2;  // [2]  prep -> consumers
 
   __shared__ int fv_s[NFACE][NF];
   __shared__ int cf_s[NCF];
   __shared__ int wc_s[NCF][NWC];
   __shared__ double ww_s[NCF][NWC];
   __shared__ double chol_s[N1 * N1];
-  __shared__ double cw_s[IHDG_MAX_COMP];
   __shared__ int qf_s[KC], qh_s[KC];
   __shared__ int qt_s[KC][NWC];
   __shared__ long long me0_s[NS];
@@ -107,7 +104,6 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS>::NT, 1)
   for (int i = tid; i < NFACE * NF; i += blockDim.x) fv_s[i / NF][i % NF] = face_node_vidx(D, N1, i / NF, i % NF);
   for (int i = tid; i < N1 * N1; i += blockDim.x) chol_s[i] = a.chol1d[i];
   if (tid < 64) com_s[tid] = a.class_of_mask[tid];
-  if (tid < IHDG_MAX_COMP) cw_s[tid] = a.comp_w[tid];
   if (tid == 0) {
     int n = 0;
     for (int f = 0; f < NFACE && n < NCF; ++f) {
@@ -140,7 +136,6 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS>::NT, 1)
     for (int b = 0; b < 2; ++b) {
       mbar_init(&done_bar[b], NCW);
       mbar_init(&outfree_bar[b], 1);
-      mbar_init(&normdone_bar[b], NQW);
     }
     fence_mbar_init();
   }
@@ -204,12 +199,6 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS>::NT, 1)
   } else if (warp >= NCW) {
     // ============================ prep warps ===============================
     const int pw = warp - NCW;
-    double cfr[2];   // C fragments of the tensor-core norm: C[4 ks + (lane&3)][lane>>2]
-#pragma unroll
-    for (int ks = 0; ks < 2; ++ks) {
-      const int kk = 4 * ks + (lane & 3), nn = lane >> 2;
-      cfr[ks] = (kk < N1 && nn < N1) ? chol_s[kk * N1 + nn] : 0.0;
-    }
     const int c0 = (int)a.g.cells[0];
     const int per0 = a.g.periodic[0];
     const int nlay = (int)(a.g.layer_end - a.g.layer_begin);
@@ -303,21 +292,16 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS>::NT, 1)
       if (it >= 1) {
         const int pb = (it - 1) & 1;
         mbar_wait(&done_bar[pb], ((it - 1) >> 1) & 1);
-        // stopping norm of tile it-1 (tensor core), this warp's units
-        double nsum = norm_units_2d<N1, M, NP, NV, E, NQW, C::UPQ, C::PS>(d_s + pb * TILE, pw, lane, cfr, cw_s);
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) nsum += __shfl_xor_sync(0xffffffffu, nsum, o);
-        if (lane == 0) red_s[pb * 32 + pw] = nsum;
-        asm volatile("bar.sync 2, %0;" ::"n"(32 * NQW) : "memory");
-        if (lane == 0) mbar_arrive(&normdone_bar[pb]);   // delta buffer pb free again
         if (pw == 0 && lane == 0) {
-          double s = 0.0;
-          for (int w = 0; w < NQW; ++w) s += red_s[pb * 32 + w];
-          a.tile_partials[prev_tile] = a.jac * s;
           for (int p = 0; p < prev_nt / 2; ++p)
             bulk_s2g(un + (int64_t)(prev_e0 + 2 * p) * NV, out_s + pb * TILE + p * C::PS,
                      (uint32_t)(2 * NV * sizeof(double)));
           bulk_commit();
+          if (it >= 2) {
+            double s = 0.0;
+            for (int w = 0; w < NCW; ++w) s += red_s[(it & 1) * 32 + w];   // tile it-2
+            a.tile_partials[prev2_tile] = a.jac * s;
+          }
           if (it >= 2) {
             bulk_wait_read<1>();                       // store of tile it-2 has read its buffer
             mbar_arrive(&outfree_bar[it & 1]);
@@ -329,23 +313,20 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS>::NT, 1)
       prev_e0 = cur_e0;
       prev_nt = nt;
     }
-    // drain: norm, partial and store of the last tile
+    // drain: store of the last tile, partial of the one before
     if (n_my >= 1) {
       const int L = n_my - 1;
       mbar_wait(&done_bar[L & 1], (L >> 1) & 1);
-      double nsum = norm_units_2d<N1, M, NP, NV, E, NQW, C::UPQ, C::PS>(d_s + (L & 1) * TILE, pw, lane, cfr, cw_s);
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) nsum += __shfl_xor_sync(0xffffffffu, nsum, o);
-      if (lane == 0) red_s[(L & 1) * 32 + pw] = nsum;
-      asm volatile("bar.sync 2, %0;" ::"n"(32 * NQW) : "memory");
       if (pw == 0 && lane == 0) {
-        double s = 0.0;
-        for (int w = 0; w < NQW; ++w) s += red_s[(L & 1) * 32 + w];
-        a.tile_partials[prev_tile] = a.jac * s;
         for (int p = 0; p < prev_nt / 2; ++p)
           bulk_s2g(un + (int64_t)(prev_e0 + 2 * p) * NV, out_s + (L & 1) * TILE + p * C::PS,
                    (uint32_t)(2 * NV * sizeof(double)));
         bulk_commit();
+        if (L >= 1) {
+          double s = 0.0;
+          for (int w = 0; w < NCW; ++w) s += red_s[((L - 1) & 1) * 32 + w];
+          a.tile_partials[prev2_tile] = a.jac * s;
+        }
         bulk_wait<0>();
       }
     }
@@ -362,6 +343,12 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS>::NT, 1)
         Lf[j][ks] = (row < NV) ? __ldg(a.LT + ((size_t)fast_class * (NFACE * NF) + col) * NV + row) : 0.0;
       }
     }
+    double cfr[2];
+#pragma unroll
+    for (int ks = 0; ks < 2; ++ks) {
+      const int kk = 4 * ks + (lane & 3), nn = lane >> 2;
+      cfr[ks] = (kk < N1 && nn < N1) ? chol_s[kk * N1 + nn] : 0.0;
+    }
     for (int it = 0; it < n_my; ++it) {
       const int stage = it % NS;
       const int ob = it & 1;
@@ -372,6 +359,17 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS>::NT, 1)
       const double* sst = sm + stage * C::STAGE;
       const double* ust = sst + TILE;
       const double* qst = ust + TILE + C::HALO;
+      // norm of the previous tile (needs every warp's delta of tile it-1)
+      double nsum = 0.0;
+      if (it >= 1) {
+        V3_T0(td);
+        mbar_wait(&done_bar[(it - 1) & 1], ((it - 1) >> 1) & 1);
+        V3_ACC(8, td);
+        V3_T0(tnn);
+        nsum = norm_units_2d<N1, M, NP, NV, E, NCW, UPW, C::PS>(d_s + ((it - 1) & 1) * TILE, warp, lane, cfr,
+                                                         a.comp_w);
+        V3_ACC(7, tnn);
+      }
       V3_T0(tm);
       double acc[NEG][RTW][2];
 #pragma unroll
@@ -422,10 +420,7 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS>::NT, 1)
       }
       V3_ACC(4, tm);
       V3_T0(to);
-      if (it >= 2) {
-        mbar_wait(&outfree_bar[ob], ((it - 2) >> 1) & 1);
-        mbar_wait(&normdone_bar[ob], ((it - 2) >> 1) & 1);
-      }
+      if (it >= 2) mbar_wait(&outfree_bar[ob], ((it - 2) >> 1) & 1);
       V3_ACC(5, to);
       V3_T0(tep);
       double* outb = out_s + ob * TILE;
@@ -446,6 +441,11 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS>::NT, 1)
           }
         }
       }
+      if (it >= 1) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) nsum += __shfl_xor_sync(0xffffffffu, nsum, o);
+        if (lane == 0) red_s[((it - 1) & 1) * 32 + warp] = nsum;
+      }
       fence_proxy_async();
       __syncwarp();
       V3_ACC(10, tep);
@@ -454,9 +454,24 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS>::NT, 1)
         mbar_arrive(&done_bar[ob]);
       }
     }
+    // drain: norm of the last tile
+    if (n_my >= 1) {
+      const int L = n_my - 1;
+      mbar_wait(&done_bar[L & 1], (L >> 1) & 1);
+      double nsum = norm_units_2d<N1, M, NP, NV, E, NCW, UPW, C::PS>(d_s + (L & 1) * TILE, warp, lane, cfr, a.comp_w);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) nsum += __shfl_xor_sync(0xffffffffu, nsum, o);
+      if (lane == 0) red_s[(L & 1) * 32 + warp] = nsum;
+    }
   }
 
   __syncthreads();
+  if (tid == 0 && n_my >= 1) {
+    const int L = n_my - 1;
+    double s = 0.0;
+    for (int w = 0; w < NCW; ++w) s += red_s[(L & 1) * 32 + w];
+    a.tile_partials[blockIdx.x + L * gridDim.x] = a.jac * s;
+  }
 #ifdef IHDG_WS_PROF
   if (tid == 0) V3_ACC(6, tk0);
   V3_FLUSH;
