@@ -33,12 +33,7 @@ struct WCfg {
   static constexpr int UPW = (E * M + NCW - 1) / NCW;
   static constexpr int NQW = 4;                                    // prep warps
   static constexpr int NT = 32 * (NCW + NQW + 1);
-  // shared tiles hold element PAIRS at stride PS = 2 NV + pad with
-  // PS = 8 (mod 16) doubles: the DMMA fragment accesses (8 rows x 4 element
-  // pairs) then hit every 8-byte bank pair exactly twice (no conflicts), and
-  // each pair is one 16-byte aligned 2 NV * 8 byte bulk copy
-  static constexpr int PS = 2 * NV + ((8 - (2 * NV) % 16) + 16) % 16;
-  static constexpr int TILE = (E / 2) * PS;
+  static constexpr int TILE = E * NV;
   static constexpr int HALO = 0;   // out-of-tile faces: prep warps load them into registers
   static constexpr int QT = E * KC;
   static constexpr int STAGE = 2 * TILE + HALO + QT;
@@ -50,8 +45,6 @@ struct WCfg {
   static constexpr size_t BYTES = (size_t)N_DBL * sizeof(double) + NBAR * sizeof(uint64_t);
   static_assert(KC % 4 == 0 && E % 8 == 0 && E <= 32 && N1 <= 8, "ws config");
   static_assert((TILE * sizeof(double)) % 16 == 0, "tile bytes must be 16-byte multiples");
-  static_assert(E % 2 == 0 && (2 * NV * sizeof(double)) % 16 == 0, "element pairs are bulk-copy units");
-  __host__ __device__ static constexpr int eoff(int t) { return (t >> 1) * PS + (t & 1) * NV; }
   static_assert(E % NQW == 0, "prep warps split the tile");
 };
 
@@ -91,7 +84,6 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS>::NT, 1)
 
   ihdg_iter_state* st = a.state;
   if (st->status != IHDG_RUNNING) return;
-  V3_DECL
 
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
@@ -188,11 +180,8 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS>::NT, 1)
       if (lane == 0) {
         const uint32_t bytes = (uint32_t)(nt * NV * sizeof(double));
         mbar_arrive_expect_tx(&full_bar[stage], 2 * bytes);  // release: metadata above
-        constexpr uint32_t pb = (uint32_t)(2 * NV * sizeof(double));
-        for (int p = 0; p < nt / 2; ++p) {
-          bulk_g2s(sst + p * C::PS, a.s + (int64_t)(e0 + 2 * p) * NV, pb, &full_bar[stage]);
-          bulk_g2s(ust + p * C::PS, uo + (int64_t)(e0 + 2 * p) * NV, pb, &full_bar[stage]);
-        }
+        bulk_g2s(sst, a.s + (int64_t)e0 * NV, bytes, &full_bar[stage]);
+        bulk_g2s(ust, uo + (int64_t)e0 * NV, bytes, &full_bar[stage]);
       }
       V3_ACC(9, tl);
     }
@@ -270,7 +259,7 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS>::NT, 1)
           double v = 0.0;
           if (qs & (1 << m)) {
             const int f = qf_s[k];
-            const double* src = ust + C::eoff(t + (f == 0 ? -1 : 1));
+            const double* src = ust + (t + (f == 0 ? -1 : 1)) * NV;
 #pragma unroll
             for (int j = 0; j < NWC; ++j) v = fma(ww_s[ci][j], src[qt_s[k][j]], v);
           } else if (ql & (1 << m)) {
@@ -293,9 +282,7 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS>::NT, 1)
         const int pb = (it - 1) & 1;
         mbar_wait(&done_bar[pb], ((it - 1) >> 1) & 1);
         if (pw == 0 && lane == 0) {
-          for (int p = 0; p < prev_nt / 2; ++p)
-            bulk_s2g(un + (int64_t)(prev_e0 + 2 * p) * NV, out_s + pb * TILE + p * C::PS,
-                     (uint32_t)(2 * NV * sizeof(double)));
+          bulk_s2g(un + (int64_t)prev_e0 * NV, out_s + pb * TILE, (uint32_t)(prev_nt * NV * sizeof(double)));
           bulk_commit();
           if (it >= 2) {
             double s = 0.0;
@@ -318,9 +305,7 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS>::NT, 1)
       const int L = n_my - 1;
       mbar_wait(&done_bar[L & 1], (L >> 1) & 1);
       if (pw == 0 && lane == 0) {
-        for (int p = 0; p < prev_nt / 2; ++p)
-          bulk_s2g(un + (int64_t)(prev_e0 + 2 * p) * NV, out_s + (L & 1) * TILE + p * C::PS,
-                   (uint32_t)(2 * NV * sizeof(double)));
+        bulk_s2g(un + (int64_t)prev_e0 * NV, out_s + (L & 1) * TILE, (uint32_t)(prev_nt * NV * sizeof(double)));
         bulk_commit();
         if (L >= 1) {
           double s = 0.0;
@@ -365,10 +350,8 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS>::NT, 1)
         V3_T0(td);
         mbar_wait(&done_bar[(it - 1) & 1], ((it - 1) >> 1) & 1);
         V3_ACC(8, td);
-        V3_T0(tnn);
-        nsum = norm_units_2d<N1, M, NP, NV, E, NCW, UPW, C::PS>(d_s + ((it - 1) & 1) * TILE, warp, lane, cfr,
+        nsum = norm_units_2d<N1, M, NP, NV, E, NCW, UPW>(d_s + ((it - 1) & 1) * TILE, warp, lane, cfr,
                                                          a.comp_w);
-        V3_ACC(7, tnn);
       }
       V3_T0(tm);
       double acc[NEG][RTW][2];
@@ -379,8 +362,8 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS>::NT, 1)
         for (int j = 0; j < RTW; ++j) {
           const int row = (warp + j * NCW) * 8 + (lane >> 2);
           const bool ok = row < NV && (warp + j * NCW) < NRT;
-          acc[eg][j][0] = ok ? sst[C::eoff(te) + row] : 0.0;
-          acc[eg][j][1] = ok ? sst[C::eoff(te + 1) + row] : 0.0;
+          acc[eg][j][0] = ok ? sst[te * NV + row] : 0.0;
+          acc[eg][j][1] = ok ? sst[(te + 1) * NV + row] : 0.0;
         }
       }
       const double* qb = qst + (lane >> 2) * KC + (lane & 3);
@@ -393,8 +376,7 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS>::NT, 1)
 #pragma unroll
           for (int eg = 0; eg < NEG; ++eg)
 #pragma unroll
-            for (int j = 0; j < RTW; ++j)
-              if (warp + j * NCW < NRT) dmma_8x8x4(acc[eg][j][0], acc[eg][j][1], Lf[j][ks], b[eg]);
+            for (int j = 0; j < RTW; ++j) dmma_8x8x4(acc[eg][j][0], acc[eg][j][1], Lf[j][ks], b[eg]);
         }
       } else {
         const unsigned cset = mcset_s[stage];
@@ -422,7 +404,6 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS>::NT, 1)
       V3_T0(to);
       if (it >= 2) mbar_wait(&outfree_bar[ob], ((it - 2) >> 1) & 1);
       V3_ACC(5, to);
-      V3_T0(tep);
       double* outb = out_s + ob * TILE;
       double* dcur = d_s + ob * TILE;
 #pragma unroll
@@ -435,8 +416,8 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS>::NT, 1)
 #pragma unroll
             for (int v = 0; v < 2; ++v) {
               const int t = te + v;
-              outb[C::eoff(t) + row] = acc[eg][j][v];
-              dcur[C::eoff(t) + row] = acc[eg][j][v] - ust[C::eoff(t) + row];
+              outb[t * NV + row] = acc[eg][j][v];
+              dcur[t * NV + row] = acc[eg][j][v] - ust[t * NV + row];
             }
           }
         }
@@ -448,7 +429,6 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS>::NT, 1)
       }
       fence_proxy_async();
       __syncwarp();
-      V3_ACC(10, tep);
       if (lane == 0) {
         mbar_arrive(&empty_bar[stage]);
         mbar_arrive(&done_bar[ob]);
@@ -458,7 +438,7 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS>::NT, 1)
     if (n_my >= 1) {
       const int L = n_my - 1;
       mbar_wait(&done_bar[L & 1], (L >> 1) & 1);
-      double nsum = norm_units_2d<N1, M, NP, NV, E, NCW, UPW, C::PS>(d_s + (L & 1) * TILE, warp, lane, cfr, a.comp_w);
+      double nsum = norm_units_2d<N1, M, NP, NV, E, NCW, UPW>(d_s + (L & 1) * TILE, warp, lane, cfr, a.comp_w);
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) nsum += __shfl_xor_sync(0xffffffffu, nsum, o);
       if (lane == 0) red_s[(L & 1) * 32 + warp] = nsum;
@@ -474,7 +454,6 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS>::NT, 1)
   }
 #ifdef IHDG_WS_PROF
   if (tid == 0) V3_ACC(6, tk0);
-  V3_FLUSH;
 #endif
   if (a.finalize) {
     __threadfence();
