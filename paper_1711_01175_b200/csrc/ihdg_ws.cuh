@@ -18,6 +18,12 @@
 
 namespace ihdg {
 
+#ifdef IHDG_MEMONLY
+#define IHDG_MEMONLY_ON 1   // data-movement-only build (tools/memonly experiment)
+#else
+#define IHDG_MEMONLY_ON 0
+#endif
+
 template <int N1, int M, int NCF, int NWC, int E, int NS>
 struct WCfg {
   static constexpr int D = 2;
@@ -350,8 +356,10 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS>::NT, 1)
         V3_T0(td);
         mbar_wait(&done_bar[(it - 1) & 1], ((it - 1) >> 1) & 1);
         V3_ACC(8, td);
+#ifndef IHDG_MEMONLY
         nsum = norm_units_2d<N1, M, NP, NV, E, NCW, UPW>(d_s + ((it - 1) & 1) * TILE, warp, lane, cfr,
                                                          a.comp_w);
+#endif
       }
       V3_T0(tm);
       double acc[NEG][RTW][2];
@@ -367,7 +375,11 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS>::NT, 1)
         }
       }
       const double* qb = qst + (lane >> 2) * KC + (lane & 3);
+#ifdef IHDG_MEMONLY
+      if (false) {
+#else
       if (fast) {
+#endif
 #pragma unroll
         for (int ks = 0; ks < KS; ++ks) {
           double b[NEG];
@@ -378,7 +390,7 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS>::NT, 1)
 #pragma unroll
             for (int j = 0; j < RTW; ++j) dmma_8x8x4(acc[eg][j][0], acc[eg][j][1], Lf[j][ks], b[eg]);
         }
-      } else {
+      } else if (!IHDG_MEMONLY_ON) {
         const unsigned cset = mcset_s[stage];
         for (unsigned rem = cset; rem != 0u; rem &= rem - 1u) {
           const int c = __ffs(rem) - 1;
