@@ -9,7 +9,7 @@ mkdir -p "$tmp/paper_1711_01175_b200/csrc" "$tmp/include"
 for f in $(git ls-tree --name-only "$rev" paper_1711_01175_b200/csrc/); do git show "$rev:$f" > "$tmp/$f"; done
 git show "$rev:include/ihdg.h" > "$tmp/include/ihdg.h"
 for f in "$tmp"/paper_1711_01175_b200/csrc/*.cu; do
-  nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -I "$tmp/include" -c "$f" -o "$f.o" &
+  nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC $EXTRA -I "$tmp/include" -c "$f" -o "$f.o" &
 done
 wait
 nvcc -gencode arch=compute_100a,code=sm_100a -shared -o "$out" "$tmp"/paper_1711_01175_b200/csrc/*.o
