@@ -130,7 +130,7 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS>::NT, 1)
     for (int s = 0; s < NS; ++s) {
       mbar_init(&full_bar[s], 1);
       mbar_init(&qready_bar[s], NQW);
-      mbar_init(&empty_bar[s], NCW);
+      mbar_init(&empty_bar[s], NCW + 1);   // + the store of the stage has read it
     }
     for (int b = 0; b < 2; ++b) mbar_init(&done_bar[b], NCW);
     fence_mbar_init();
@@ -307,6 +307,8 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS>::NT, 1)
         bulk_s2g(un + (int64_t)e0_s[j & 1] * NV, psst, (uint32_t)(nt_s[j & 1] * NV * sizeof(double)));
         bulk_commit();
         if (j >= 1) {
+          bulk_wait_read<1>();                     // store of tile j-1 has read its stage
+          mbar_arrive(&empty_bar[(j - 1) % NS]);
           double s = 0.0;
           for (int w = 0; w < NCW; ++w) s += red_s[((j - 1) & 1) * 32 + w];
           a.tile_partials[tl_s[(j - 1) & 1]] = a.jac * s;
@@ -320,7 +322,6 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS>::NT, 1)
       for (int o = 16; o > 0; o >>= 1) nsum += __shfl_xor_sync(0xffffffffu, nsum, o);
       if (lane == 0) {
         red_s[(j & 1) * 32 + warp] = nsum;
-        if (warp == 0) bulk_wait_read<0>();   // the store has read the stage
         mbar_arrive(&empty_bar[pstage]);
       }
     };
