@@ -108,7 +108,7 @@ struct StreamEntry {
 #define IHDG_WS2(N1, M, NCF, NWC, E, NS) \
   {2, N1, M, NCF, NWC, E, M * N1 * N1, launch_ws2_t<N1, M, NCF, NWC, E, NS>, 0},
 #ifndef IHDG_WS5_NS
-#define IHDG_WS5_NS 5   // stage count of the config-5 ring (A/B builds override it)
+#define IHDG_WS5_NS 3   // stage count of the config-5 ring (A/B builds override it)
 #endif
 #define IHDG_WS(N1, M, NCF, NWC, E, NS) \
   {2, N1, M, NCF, NWC, E, M * N1 * N1, launch_ws_t<N1, M, NCF, NWC, E, NS>, 0},
@@ -120,7 +120,7 @@ const StreamEntry kStream[] = {
     IHDG_V3(3, 4, 1, 3, 1, 16, 6, 4, 4)    // config 4: transport 3D p=3
     IHDG_WS2(7, 3, 4, 2, 16, 6)            // config 5: CD 2D p=6 (ws2: s / u^{k+1} bypass smem)
     IHDG_WS(7, 3, 4, 2, 16, IHDG_WS5_NS)   // config 5: CD 2D p=6 (warp-specialised)
-    IHDG_WS(5, 3, 4, 2, 16, 8)             // configs 2/3: CD / SW 2D p=4
+    IHDG_WS(5, 3, 4, 2, 16, 4)             // configs 2/3: CD / SW 2D p=4
     IHDG_STREAM(3, 4, 1, 3, 1, 32, 3, 4)   // config 4: transport 3D p=3
 };
 

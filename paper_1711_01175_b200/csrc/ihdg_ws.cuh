@@ -4,30 +4,19 @@
 // mbarriers only (no CTA-wide barrier in the steady state):
 //
 //   producer warp  : per tile, metadata + TMA bulk copies of the s and u^k
-//                    tiles into an NS-stage ring             -> full[stage]
-//   prep warps (4) : neighbour face scalars q (TraceSnapshot) for the stage;
-//                    out-of-tile faces come from L2 into registers one tile
-//                    ahead                                   -> qready[stage]
+//                    tiles + cp.async gathers of out-of-tile neighbour faces
+//                    into an NS-stage ring                   -> full[stage]
+//   prep warps (4) : neighbour face scalars q (TraceSnapshot) for the stage
+//                    -> qready[stage]; then, one tile behind, the bulk store
+//                    of u^{k+1} and the fixed-order tile partial of the norm
 //   consumer warps : DMMA contraction u^{k+1} = s + L q (L fragments in
-//                    registers) for tile i, written IN PLACE over s in the
-//                    stage, delta = u^{k+1} - u^k in place over u^k
-//                                                            -> done[i&1]
-//                    then, for tile i-1: bulk store of u^{k+1} straight from
-//                    the stage (warp 0), the tensor-core norm J |C^T Delta C|^2
-//                    and the fixed-order tile partial        -> empty[stage]
-// Keeping u^{k+1} and delta in the stage (no separate out/delta buffers) buys
-// two more stages, i.e. more bytes in flight per SM while the FP64 pipe is busy.
+//                    registers) for tile i interleaved with the tensor-core
+//                    norm J |C^T Delta C|^2 of tile i-1      -> done[i&1]
 #pragma once
 
 #include "ihdg_stream.cuh"
 
 namespace ihdg {
-
-#ifdef IHDG_MEMONLY
-#define IHDG_MEMONLY_ON 1   // data-movement-only build (tools/memonly experiment)
-#else
-#define IHDG_MEMONLY_ON 0
-#endif
 
 template <int N1, int M, int NCF, int NWC, int E, int NS>
 struct WCfg {
@@ -48,9 +37,11 @@ struct WCfg {
   static constexpr int HALO = 0;   // out-of-tile faces: prep warps load them into registers
   static constexpr int QT = E * KC;
   static constexpr int STAGE = 2 * TILE + HALO + QT;
-  static constexpr int OFF_RED = NS * STAGE;
+  static constexpr int OFF_OUT = NS * STAGE;
+  static constexpr int OFF_D = OFF_OUT + 2 * TILE;
+  static constexpr int OFF_RED = OFF_D + 2 * TILE;
   static constexpr int N_DBL = OFF_RED + 64;
-  static constexpr int NBAR = 3 * NS + 2;
+  static constexpr int NBAR = 3 * NS + 4;
   static constexpr size_t BYTES = (size_t)N_DBL * sizeof(double) + NBAR * sizeof(uint64_t);
   static_assert(KC % 4 == 0 && E % 8 == 0 && E <= 32 && N1 <= 8, "ws config");
   static_assert((TILE * sizeof(double)) % 16 == 0, "tile bytes must be 16-byte multiples");
@@ -66,12 +57,15 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS>::NT, 1)
   constexpr int NQW = C::NQW, TILE = C::TILE;
 
   extern __shared__ __align__(16) double sm[];
+  double* out_s = sm + C::OFF_OUT;
+  double* d_s = sm + C::OFF_D;
   double* red_s = sm + C::OFF_RED;
   uint64_t* bars = reinterpret_cast<uint64_t*>(sm + C::N_DBL);
   uint64_t* full_bar = bars;             // [NS] producer -> prep
   uint64_t* qready_bar = bars + NS;      // [NS] prep -> consumers
   uint64_t* empty_bar = bars + 2 * NS;   // [NS] consumers -> producer
-  uint64_t* done_bar = bars + 3 * NS;    // [2]  consumers -> consumers
+  uint64_t* done_bar = bars + 3 * NS;    // [2]  consumers -> prep, consumers
+  uint64_t* outfree_bar = done_bar + 2;  // [2]  prep -> consumers
 
   __shared__ int fv_s[NFACE][NF];
   __shared__ int cf_s[NCF];
@@ -85,7 +79,6 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS>::NT, 1)
   __shared__ unsigned mcset_s[NS];
   __shared__ int mmask_s[NS][E], mcls_s[NS][E];
   __shared__ int tile_s[NS];
-  __shared__ int e0_s[2], nt_s[2], tl_s[2];  // consumer-side copy of tiles it-1, it
   __shared__ int com_s[64];
   __shared__ int last_s;
 
@@ -130,9 +123,12 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS>::NT, 1)
     for (int s = 0; s < NS; ++s) {
       mbar_init(&full_bar[s], 1);
       mbar_init(&qready_bar[s], NQW);
-      mbar_init(&empty_bar[s], NCW + 1);   // + the store of the stage has read it
+      mbar_init(&empty_bar[s], NCW);
     }
-    for (int b = 0; b < 2; ++b) mbar_init(&done_bar[b], NCW);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&done_bar[b], NCW);
+      mbar_init(&outfree_bar[b], 1);
+    }
     fence_mbar_init();
   }
   __syncthreads();
@@ -187,6 +183,14 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS>::NT, 1)
         bulk_g2s(sst, a.s + (int64_t)e0 * NV, bytes, &full_bar[stage]);
         bulk_g2s(ust, uo + (int64_t)e0 * NV, bytes, &full_bar[stage]);
       }
+      if (IHDG_WS_PF > 0 && lane == 0 && it + IHDG_WS_PF < n_my) {
+        // tile it+PF will be copied into a stage PF tiles from now: pull it into L2
+        STile<D> tp;
+        tp.init(a.g, tile + IHDG_WS_PF * (int)gridDim.x, E, nlay, lsi);
+        const uint32_t pb = (uint32_t)(tp.nt * NV * sizeof(double));
+        bulk_prefetch_l2(a.s + (int64_t)tp.e0 * NV, pb);
+        bulk_prefetch_l2(uo + (int64_t)tp.e0 * NV, pb);
+      }
       V3_ACC(9, tl);
     }
   } else if (warp >= NCW) {
@@ -196,6 +200,7 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS>::NT, 1)
     const int per0 = a.g.periodic[0];
     const int nlay = (int)(a.g.layer_end - a.g.layer_begin);
     const int lsi = (int)ls;
+    int prev_e0 = 0, prev_nt = 0, prev_tile = -1, prev2_tile = -1;
     constexpr int HALF = E / NQW;
     constexpr int QM = (HALF * KC + 31) / 32;
     // out-of-tile neighbour face nodes of this warp's entries, loaded from
@@ -245,6 +250,11 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS>::NT, 1)
       mbar_wait(&full_bar[stage], (it / NS) & 1);
       V3_ACC(1, tp);
       V3_T0(tq);
+      // stage metadata is read now: the stage can be refilled once the
+      // consumers release it, possibly before this warp stores the tile
+      const int nt = mnt_s[stage];
+      const int cur_e0 = (int)me0_s[stage];
+      const int cur_tile = tile_s[stage];
       const double* sst = sm + stage * C::STAGE;
       const double* ust = sst + TILE;
       double* qst = const_cast<double*>(ust) + TILE + C::HALO;
@@ -276,6 +286,42 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS>::NT, 1)
       __syncwarp();
       V3_ACC(2, tq);
       if (lane == 0) mbar_arrive(&qready_bar[stage]);
+      if (it >= 1) {
+        const int pb = (it - 1) & 1;
+        mbar_wait(&done_bar[pb], ((it - 1) >> 1) & 1);
+        if (pw == 0 && lane == 0) {
+          bulk_s2g(un + (int64_t)prev_e0 * NV, out_s + pb * TILE, (uint32_t)(prev_nt * NV * sizeof(double)));
+          bulk_commit();
+          if (it >= 2) {
+            double s = 0.0;
+            for (int w = 0; w < NCW; ++w) s += red_s[(it & 1) * 32 + w];   // tile it-2
+            a.tile_partials[prev2_tile] = a.jac * s;
+          }
+          if (it >= 2) {
+            bulk_wait_read<1>();                       // store of tile it-2 has read its buffer
+            mbar_arrive(&outfree_bar[it & 1]);
+          }
+        }
+      }
+      prev2_tile = prev_tile;
+      prev_tile = cur_tile;
+      prev_e0 = cur_e0;
+      prev_nt = nt;
+    }
+    // drain: store of the last tile, partial of the one before
+    if (n_my >= 1) {
+      const int L = n_my - 1;
+      mbar_wait(&done_bar[L & 1], (L >> 1) & 1);
+      if (pw == 0 && lane == 0) {
+        bulk_s2g(un + (int64_t)prev_e0 * NV, out_s + (L & 1) * TILE, (uint32_t)(prev_nt * NV * sizeof(double)));
+        bulk_commit();
+        if (L >= 1) {
+          double s = 0.0;
+          for (int w = 0; w < NCW; ++w) s += red_s[((L - 1) & 1) * 32 + w];
+          a.tile_partials[prev2_tile] = a.jac * s;
+        }
+        bulk_wait<0>();
+      }
     }
   } else {
     // ============================ consumer warps ===========================
@@ -296,35 +342,6 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS>::NT, 1)
       const int kk = 4 * ks + (lane & 3), nn = lane >> 2;
       cfr[ks] = (kk < N1 && nn < N1) ? chol_s[kk * N1 + nn] : 0.0;
     }
-    // tile it-1: bulk store from its stage (warp 0), then the norm of its
-    // delta, then release the stage.  red_s[(j & 1) * 32 + w] holds warp w's
-    // norm sum of tile j; warp 0 folds it into tile_partials one tile later,
-    // after done[] guarantees every warp has written it.
-    auto retire = [&](int j) {
-      const int pstage = j % NS;
-      double* psst = sm + pstage * C::STAGE;
-      if (warp == 0 && lane == 0) {
-        bulk_s2g(un + (int64_t)e0_s[j & 1] * NV, psst, (uint32_t)(nt_s[j & 1] * NV * sizeof(double)));
-        bulk_commit();
-        if (j >= 1) {
-          bulk_wait_read<1>();                     // store of tile j-1 has read its stage
-          mbar_arrive(&empty_bar[(j - 1) % NS]);
-          double s = 0.0;
-          for (int w = 0; w < NCW; ++w) s += red_s[((j - 1) & 1) * 32 + w];
-          a.tile_partials[tl_s[(j - 1) & 1]] = a.jac * s;
-        }
-      }
-      double nsum = 0.0;
-#ifndef IHDG_MEMONLY
-      nsum = norm_units_2d<N1, M, NP, NV, E, NCW, UPW>(psst + TILE, warp, lane, cfr, a.comp_w);
-#endif
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) nsum += __shfl_xor_sync(0xffffffffu, nsum, o);
-      if (lane == 0) {
-        red_s[(j & 1) * 32 + warp] = nsum;
-        mbar_arrive(&empty_bar[pstage]);
-      }
-    };
     for (int it = 0; it < n_my; ++it) {
       const int stage = it % NS;
       const int ob = it & 1;
@@ -332,19 +349,17 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS>::NT, 1)
       mbar_wait(&qready_bar[stage], (it / NS) & 1);
       V3_ACC(3, tc);
       const int fast = mfast_s[stage];
-      double* sst = sm + stage * C::STAGE;
-      double* ust = sst + TILE;
+      const double* sst = sm + stage * C::STAGE;
+      const double* ust = sst + TILE;
       const double* qst = ust + TILE + C::HALO;
+      // norm of the previous tile (needs every warp's delta of tile it-1)
+      double nsum = 0.0;
       if (it >= 1) {
         V3_T0(td);
         mbar_wait(&done_bar[(it - 1) & 1], ((it - 1) >> 1) & 1);
         V3_ACC(8, td);
-        retire(it - 1);
-      }
-      if (warp == 0 && lane == 0) {
-        e0_s[ob] = (int)me0_s[stage];
-        nt_s[ob] = mnt_s[stage];
-        tl_s[ob] = tile_s[stage];
+        nsum = norm_units_2d<N1, M, NP, NV, E, NCW, UPW>(d_s + ((it - 1) & 1) * TILE, warp, lane, cfr,
+                                                         a.comp_w);
       }
       V3_T0(tm);
       double acc[NEG][RTW][2];
@@ -360,11 +375,7 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS>::NT, 1)
         }
       }
       const double* qb = qst + (lane >> 2) * KC + (lane & 3);
-#ifdef IHDG_MEMONLY
-      if (false) {
-#else
       if (fast) {
-#endif
 #pragma unroll
         for (int ks = 0; ks < KS; ++ks) {
           double b[NEG];
@@ -375,7 +386,7 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS>::NT, 1)
 #pragma unroll
             for (int j = 0; j < RTW; ++j) dmma_8x8x4(acc[eg][j][0], acc[eg][j][1], Lf[j][ks], b[eg]);
         }
-      } else if (!IHDG_MEMONLY_ON) {
+      } else {
         const unsigned cset = mcset_s[stage];
         for (unsigned rem = cset; rem != 0u; rem &= rem - 1u) {
           const int c = __ffs(rem) - 1;
@@ -398,6 +409,11 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS>::NT, 1)
         }
       }
       V3_ACC(4, tm);
+      V3_T0(to);
+      if (it >= 2) mbar_wait(&outfree_bar[ob], ((it - 2) >> 1) & 1);
+      V3_ACC(5, to);
+      double* outb = out_s + ob * TILE;
+      double* dcur = d_s + ob * TILE;
 #pragma unroll
       for (int eg = 0; eg < NEG; ++eg) {
         const int te = eg * 8 + 2 * (lane & 3);
@@ -408,22 +424,32 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS>::NT, 1)
 #pragma unroll
             for (int v = 0; v < 2; ++v) {
               const int t = te + v;
-              sst[t * NV + row] = acc[eg][j][v];
-              ust[t * NV + row] = acc[eg][j][v] - ust[t * NV + row];
+              outb[t * NV + row] = acc[eg][j][v];
+              dcur[t * NV + row] = acc[eg][j][v] - ust[t * NV + row];
             }
           }
         }
       }
+      if (it >= 1) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) nsum += __shfl_xor_sync(0xffffffffu, nsum, o);
+        if (lane == 0) red_s[((it - 1) & 1) * 32 + warp] = nsum;
+      }
       fence_proxy_async();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&done_bar[ob]);
+      if (lane == 0) {
+        mbar_arrive(&empty_bar[stage]);
+        mbar_arrive(&done_bar[ob]);
+      }
     }
-    // drain: the last tile
+    // drain: norm of the last tile
     if (n_my >= 1) {
       const int L = n_my - 1;
       mbar_wait(&done_bar[L & 1], (L >> 1) & 1);
-      retire(L);
-      if (warp == 0 && lane == 0) bulk_wait<0>();
+      double nsum = norm_units_2d<N1, M, NP, NV, E, NCW, UPW>(d_s + (L & 1) * TILE, warp, lane, cfr, a.comp_w);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) nsum += __shfl_xor_sync(0xffffffffu, nsum, o);
+      if (lane == 0) red_s[(L & 1) * 32 + warp] = nsum;
     }
   }
 
