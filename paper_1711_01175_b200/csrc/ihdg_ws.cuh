@@ -14,9 +14,133 @@
 //                    norm J |C^T Delta C|^2 of tile i-1      -> done[i&1]
 #pragma once
 
+#include <type_traits>
+#include <utility>
+
 #include "ihdg_stream.cuh"
 
 namespace ihdg {
+
+#ifndef IHDG_WS_PF
+#define IHDG_WS_PF 0   // L2 prefetch distance in tiles (0 = off; measured no gain on config 5)
+#endif
+#ifdef IHDG_MEMONLY
+#define IHDG_MEMONLY_ON 1   // data-movement-only build (A/B experiment)
+#else
+#define IHDG_MEMONLY_ON 0
+#endif
+
+// Consumer work plan.  The FP64 pipe is per SMSP (warp w runs on SMSP w % 4)
+// and the consumers meet once per tile, so the tile time is set by the most
+// loaded SMSP, not by the most loaded warp.  Row tiles of the contraction
+// (KS * NEG DMMAs each) and norm units (4 DMMAs each) go greedily to the least
+// loaded SMSP, then to its least loaded warp; padding row tiles / units are
+// not issued at all.
+template <int NCW, int NRT, int NU, int MAXR, int MAXU>
+struct WPlan {
+  int rt[NCW][MAXR];   // row tiles of warp w (-1 = none)
+  int un[NCW][MAXU];   // norm units of warp w (-1 = none)
+  int nr[NCW], nu[NCW];
+  int maxr, maxu;
+};
+template <int NCW, int NRT, int NU, int MAXR, int MAXU>
+constexpr WPlan<NCW, NRT, NU, MAXR, MAXU> make_wplan(int rt_cost, int u_cost) {
+  WPlan<NCW, NRT, NU, MAXR, MAXU> p{};
+  int sl[4] = {0, 0, 0, 0};
+  int wl[NCW] = {};
+  for (int w = 0; w < NCW; ++w) {
+    p.nr[w] = 0;
+    p.nu[w] = 0;
+    for (int j = 0; j < MAXR; ++j) p.rt[w][j] = -1;
+    for (int j = 0; j < MAXU; ++j) p.un[w][j] = -1;
+  }
+  for (int pass = 0; pass < 2; ++pass) {
+    const int n = pass == 0 ? NRT : NU, cost = pass == 0 ? rt_cost : u_cost, cap = pass == 0 ? MAXR : MAXU;
+    for (int i = 0; i < n; ++i) {
+      int bw = -1;
+      for (int w = 0; w < NCW; ++w) {
+        const int cnt = pass == 0 ? p.nr[w] : p.nu[w];
+        if (cnt >= cap) continue;
+        if (bw < 0 || sl[w % 4] < sl[bw % 4] || (sl[w % 4] == sl[bw % 4] && wl[w] < wl[bw])) bw = w;
+      }
+      if (pass == 0) p.rt[bw][p.nr[bw]++] = i;
+      else p.un[bw][p.nu[bw]++] = i;
+      sl[bw % 4] += cost;
+      wl[bw] += cost;
+    }
+  }
+  p.maxr = 0;
+  p.maxu = 0;
+  for (int w = 0; w < NCW; ++w) {
+    p.maxr = p.nr[w] > p.maxr ? p.nr[w] : p.maxr;
+    p.maxu = p.nu[w] > p.maxu ? p.nu[w] : p.maxu;
+  }
+  return p;
+}
+
+// this warp's plan rows as compile-time constants (a constexpr aggregate
+// cannot be read from device code; its elements as template arguments can)
+template <class C, int W, int... J>
+__device__ __forceinline__ void plan_rt(int* rt, std::integer_sequence<int, J...>) {
+  ((rt[J] = std::integral_constant<int, C::PLAN.rt[W][J]>::value), ...);
+}
+template <class C, int W, int... J>
+__device__ __forceinline__ void plan_un(int* un, std::integer_sequence<int, J...>) {
+  ((un[J] = std::integral_constant<int, C::PLAN.un[W][J]>::value), ...);
+}
+template <class C, int W = 0>
+__device__ __forceinline__ void plan_get(int warp, int* rt, int* un) {
+  if constexpr (W < C::NCW) {
+    if (warp == W) {
+      plan_rt<C, W>(rt, std::make_integer_sequence<int, C::RTW>{});
+      plan_un<C, W>(un, std::make_integer_sequence<int, C::UPW>{});
+    } else {
+      plan_get<C, W + 1>(warp, rt, un);
+    }
+  }
+}
+
+// norm units listed in uid (-1 = none): sum of w_c |C^T Delta_{t,c} C|_F^2
+template <int N1, int M, int NP, int NV, int UM>
+__device__ __forceinline__ double norm_units_list(const double* __restrict__ dbuf, const int (&uid)[UM], int lane,
+                                                  const double (&cfr)[2], const double* comp_w) {
+  double acc = 0.0;
+  double r0[UM], r1[UM];
+#pragma unroll
+  for (int m = 0; m < UM; ++m) {
+    r0[m] = 0.0;
+    r1[m] = 0.0;
+    if (uid[m] >= 0) {
+      const int t = uid[m] / M, c = uid[m] - (uid[m] / M) * M;
+      const double* base = dbuf + t * NV + c * NP;
+#pragma unroll
+      for (int ks = 0; ks < 2; ++ks) {
+        const int kk = 4 * ks + (lane & 3), nn = lane >> 2;
+        const double b = (kk < N1 && nn < N1) ? base[kk * N1 + nn] : 0.0;
+        dmma_8x8x4(r0[m], r1[m], cfr[ks], b);   // R = C^T Delta
+      }
+    }
+  }
+#pragma unroll
+  for (int m = 0; m < UM; ++m) {
+    if (uid[m] >= 0) {
+      const int c = uid[m] % M;
+      double y0 = 0.0, y1 = 0.0;
+#pragma unroll
+      for (int ks = 0; ks < 2; ++ks) {
+        const int col = 4 * ks + (lane & 3);
+        const int src = (lane & ~3) | (col >> 1);
+        const double x0 = __shfl_sync(0xffffffffu, r0[m], src);
+        const double x1 = __shfl_sync(0xffffffffu, r1[m], src);
+        dmma_8x8x4(y0, y1, (col & 1) ? x1 : x0, cfr[ks]);  // Y = R C
+      }
+      const double w = comp_w[c];
+      acc = fma(w * y0, y0, acc);
+      acc = fma(w * y1, y1, acc);
+    }
+  }
+  return acc;
+}
 
 template <int N1, int M, int NCF, int NWC, int E, int NS>
 struct WCfg {
@@ -28,9 +152,12 @@ struct WCfg {
   static constexpr int NRT = (NV + 7) / 8;
   static constexpr int KS = KC / 4;
   static constexpr int NEG = E / 8;
-  static constexpr int NCW = NRT >= 16 ? 10 : (NRT >= 8 ? 8 : 4);  // consumer warps
-  static constexpr int RTW = (NRT + NCW - 1) / NCW;
-  static constexpr int UPW = (E * M + NCW - 1) / NCW;
+  static constexpr int NCW = NRT >= 8 ? 8 : 4;                     // consumer warps (2 or 1 per SMSP)
+  static constexpr int NU = E * M;                                  // norm units per tile
+  static constexpr auto PLAN0 = make_wplan<NCW, NRT, NU, 8, 16>(KS * NEG, 4);
+  static constexpr int RTW = PLAN0.maxr;                            // row tiles per warp (max)
+  static constexpr int UPW = PLAN0.maxu;                            // norm units per warp (max)
+  static constexpr auto PLAN = make_wplan<NCW, NRT, NU, RTW, UPW>(KS * NEG, 4);
   static constexpr int NQW = 4;                                    // prep warps
   static constexpr int NT = 32 * (NCW + NQW + 1);
   static constexpr int TILE = E * NV;
@@ -191,6 +318,14 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS>::NT, 1)
         bulk_prefetch_l2(a.s + (int64_t)tp.e0 * NV, pb);
         bulk_prefetch_l2(uo + (int64_t)tp.e0 * NV, pb);
       }
+      if (IHDG_WS_PF > 0 && lane == 0 && it + IHDG_WS_PF < n_my) {
+        // tile it+PF will be copied into a stage PF tiles from now: pull it into L2
+        STile<D> tp;
+        tp.init(a.g, tile + IHDG_WS_PF * (int)gridDim.x, E, nlay, lsi);
+        const uint32_t pb = (uint32_t)(tp.nt * NV * sizeof(double));
+        bulk_prefetch_l2(a.s + (int64_t)tp.e0 * NV, pb);
+        bulk_prefetch_l2(uo + (int64_t)tp.e0 * NV, pb);
+      }
       V3_ACC(9, tl);
     }
   } else if (warp >= NCW) {
@@ -325,10 +460,12 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS>::NT, 1)
     }
   } else {
     // ============================ consumer warps ===========================
+    int rtid[RTW], uid[UPW];   // this warp's row tiles and norm units (C::PLAN)
+    plan_get<C>(warp, rtid, uid);
     double Lf[RTW][KS];
 #pragma unroll
     for (int j = 0; j < RTW; ++j) {
-      const int row = (warp + j * NCW) * 8 + (lane >> 2);
+      const int row = (rtid[j] < 0 ? NRT : rtid[j]) * 8 + (lane >> 2);
 #pragma unroll
       for (int ks = 0; ks < KS; ++ks) {
         const int k = 4 * ks + (lane & 3);
@@ -358,8 +495,7 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS>::NT, 1)
         V3_T0(td);
         mbar_wait(&done_bar[(it - 1) & 1], ((it - 1) >> 1) & 1);
         V3_ACC(8, td);
-        nsum = norm_units_2d<N1, M, NP, NV, E, NCW, UPW>(d_s + ((it - 1) & 1) * TILE, warp, lane, cfr,
-                                                         a.comp_w);
+        nsum = norm_units_list<N1, M, NP, NV, UPW>(d_s + ((it - 1) & 1) * TILE, uid, lane, cfr, a.comp_w);
       }
       V3_T0(tm);
       double acc[NEG][RTW][2];
@@ -368,14 +504,14 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS>::NT, 1)
         const int te = eg * 8 + 2 * (lane & 3);
 #pragma unroll
         for (int j = 0; j < RTW; ++j) {
-          const int row = (warp + j * NCW) * 8 + (lane >> 2);
-          const bool ok = row < NV && (warp + j * NCW) < NRT;
+          const int row = rtid[j] * 8 + (lane >> 2);
+          const bool ok = rtid[j] >= 0 && row < NV;
           acc[eg][j][0] = ok ? sst[te * NV + row] : 0.0;
           acc[eg][j][1] = ok ? sst[(te + 1) * NV + row] : 0.0;
         }
       }
       const double* qb = qst + (lane >> 2) * KC + (lane & 3);
-      if (fast) {
+      if (fast && !IHDG_MEMONLY_ON) {
 #pragma unroll
         for (int ks = 0; ks < KS; ++ks) {
           double b[NEG];
@@ -384,9 +520,10 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS>::NT, 1)
 #pragma unroll
           for (int eg = 0; eg < NEG; ++eg)
 #pragma unroll
-            for (int j = 0; j < RTW; ++j) dmma_8x8x4(acc[eg][j][0], acc[eg][j][1], Lf[j][ks], b[eg]);
+            for (int j = 0; j < RTW; ++j)
+              if (rtid[j] >= 0) dmma_8x8x4(acc[eg][j][0], acc[eg][j][1], Lf[j][ks], b[eg]);
         }
-      } else {
+      } else if (!IHDG_MEMONLY_ON) {
         const unsigned cset = mcset_s[stage];
         for (unsigned rem = cset; rem != 0u; rem &= rem - 1u) {
           const int c = __ffs(rem) - 1;
@@ -396,14 +533,15 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS>::NT, 1)
             double av[RTW];
 #pragma unroll
             for (int j = 0; j < RTW; ++j) {
-              const int row = (warp + j * NCW) * 8 + (lane >> 2);
-              av[j] = (row < NV) ? __ldg(a.LT + ((size_t)c * (NFACE * NF) + col) * NV + row) : 0.0;
+              const int row = rtid[j] * 8 + (lane >> 2);
+              av[j] = (rtid[j] >= 0 && row < NV) ? __ldg(a.LT + ((size_t)c * (NFACE * NF) + col) * NV + row) : 0.0;
             }
 #pragma unroll
             for (int eg = 0; eg < NEG; ++eg) {
               const double b = (mcls_s[stage][eg * 8 + (lane >> 2)] == c) ? qb[eg * 8 * KC + 4 * ks] : 0.0;
 #pragma unroll
-              for (int j = 0; j < RTW; ++j) dmma_8x8x4(acc[eg][j][0], acc[eg][j][1], av[j], b);
+              for (int j = 0; j < RTW; ++j)
+                if (rtid[j] >= 0) dmma_8x8x4(acc[eg][j][0], acc[eg][j][1], av[j], b);
             }
           }
         }
@@ -419,8 +557,8 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS>::NT, 1)
         const int te = eg * 8 + 2 * (lane & 3);
 #pragma unroll
         for (int j = 0; j < RTW; ++j) {
-          const int row = (warp + j * NCW) * 8 + (lane >> 2);
-          if (row < NV && (warp + j * NCW) < NRT) {
+          const int row = rtid[j] * 8 + (lane >> 2);
+          if (rtid[j] >= 0 && row < NV) {
 #pragma unroll
             for (int v = 0; v < 2; ++v) {
               const int t = te + v;
@@ -446,7 +584,7 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS>::NT, 1)
     if (n_my >= 1) {
       const int L = n_my - 1;
       mbar_wait(&done_bar[L & 1], (L >> 1) & 1);
-      double nsum = norm_units_2d<N1, M, NP, NV, E, NCW, UPW>(d_s + (L & 1) * TILE, warp, lane, cfr, a.comp_w);
+      double nsum = norm_units_list<N1, M, NP, NV, UPW>(d_s + (L & 1) * TILE, uid, lane, cfr, a.comp_w);
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) nsum += __shfl_xor_sync(0xffffffffu, nsum, o);
       if (lane == 0) red_s[(L & 1) * 32 + warp] = nsum;
