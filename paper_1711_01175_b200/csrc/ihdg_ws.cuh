@@ -42,6 +42,8 @@ struct WPlan {
   int un[NCW][MAXU];   // norm units of warp w (-1 = none)
   int nr[NCW], nu[NCW];
   int maxr, maxu;
+  int cls[NCW];          // warps with equal (nr, nu) share one code path
+  int cnr[NCW], cnu[NCW], ncls;
 };
 template <int NCW, int NRT, int NU, int MAXR, int MAXU>
 constexpr WPlan<NCW, NRT, NU, MAXR, MAXU> make_wplan(int rt_cost, int u_cost) {
@@ -75,27 +77,49 @@ constexpr WPlan<NCW, NRT, NU, MAXR, MAXU> make_wplan(int rt_cost, int u_cost) {
     p.maxr = p.nr[w] > p.maxr ? p.nr[w] : p.maxr;
     p.maxu = p.nu[w] > p.maxu ? p.nu[w] : p.maxu;
   }
+  p.ncls = 0;
+  for (int w = 0; w < NCW; ++w) {
+    int k = 0;
+    while (k < p.ncls && !(p.cnr[k] == p.nr[w] && p.cnu[k] == p.nu[w])) ++k;
+    if (k == p.ncls) {
+      p.cnr[k] = p.nr[w];
+      p.cnu[k] = p.nu[w];
+      ++p.ncls;
+    }
+    p.cls[w] = k;
+  }
   return p;
 }
 
-// this warp's plan rows as compile-time constants (a constexpr aggregate
-// cannot be read from device code; its elements as template arguments can)
+// The plan as compile-time constants: a constexpr aggregate cannot be read
+// from device code, its elements as template arguments can.  plan_fill
+// copies the per-warp lists to shared memory; plan_dispatch calls f with the
+// warp's (row tiles, units) counts as integral constants, so every class of
+// warps runs a fully unrolled, branch-free body.
 template <class C, int W, int... J>
-__device__ __forceinline__ void plan_rt(int* rt, std::integer_sequence<int, J...>) {
-  ((rt[J] = std::integral_constant<int, C::PLAN.rt[W][J]>::value), ...);
+__device__ __forceinline__ void plan_fill_rt(int* rt, std::integer_sequence<int, J...>) {
+  ((rt[W * C::RTW + J] = std::integral_constant<int, C::PLAN.rt[W][J]>::value), ...);
 }
 template <class C, int W, int... J>
-__device__ __forceinline__ void plan_un(int* un, std::integer_sequence<int, J...>) {
-  ((un[J] = std::integral_constant<int, C::PLAN.un[W][J]>::value), ...);
+__device__ __forceinline__ void plan_fill_un(int* un, std::integer_sequence<int, J...>) {
+  ((un[W * C::UPW + J] = std::integral_constant<int, C::PLAN.un[W][J]>::value), ...);
 }
 template <class C, int W = 0>
-__device__ __forceinline__ void plan_get(int warp, int* rt, int* un) {
+__device__ __forceinline__ void plan_fill(int* rt, int* un, int* cls) {
   if constexpr (W < C::NCW) {
-    if (warp == W) {
-      plan_rt<C, W>(rt, std::make_integer_sequence<int, C::RTW>{});
-      plan_un<C, W>(un, std::make_integer_sequence<int, C::UPW>{});
+    plan_fill_rt<C, W>(rt, std::make_integer_sequence<int, C::RTW>{});
+    plan_fill_un<C, W>(un, std::make_integer_sequence<int, C::UPW>{});
+    cls[W] = std::integral_constant<int, C::PLAN.cls[W]>::value;
+    plan_fill<C, W + 1>(rt, un, cls);
+  }
+}
+template <class C, int K = 0, class F>
+__device__ __forceinline__ void plan_dispatch(int k, F&& f) {
+  if constexpr (K < C::PLAN.ncls) {
+    if (k == K) {
+      f(std::integral_constant<int, C::PLAN.cnr[K]>{}, std::integral_constant<int, C::PLAN.cnu[K]>{});
     } else {
-      plan_get<C, W + 1>(warp, rt, un);
+      plan_dispatch<C, K + 1>(k, f);
     }
   }
 }
@@ -208,6 +232,7 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS>::NT, 1)
   __shared__ int tile_s[NS];
   __shared__ int com_s[64];
   __shared__ int last_s;
+  __shared__ int prt_s[C::NCW * C::RTW], pun_s[C::NCW * C::UPW], pcls_s[C::NCW];
 
   ihdg_iter_state* st = a.state;
   if (st->status != IHDG_RUNNING) return;
@@ -223,6 +248,7 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS>::NT, 1)
   for (int i = tid; i < NFACE * NF; i += blockDim.x) fv_s[i / NF][i % NF] = face_node_vidx(D, N1, i / NF, i % NF);
   for (int i = tid; i < N1 * N1; i += blockDim.x) chol_s[i] = a.chol1d[i];
   if (tid < 64) com_s[tid] = a.class_of_mask[tid];
+  if (tid == 32) plan_fill<C>(prt_s, pun_s, pcls_s);
   if (tid == 0) {
     int n = 0;
     for (int f = 0; f < NFACE && n < NCF; ++f) {
@@ -460,135 +486,142 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS>::NT, 1)
     }
   } else {
     // ============================ consumer warps ===========================
-    int rtid[RTW], uid[UPW];   // this warp's row tiles and norm units (C::PLAN)
-    plan_get<C>(warp, rtid, uid);
-    double Lf[RTW][KS];
-#pragma unroll
-    for (int j = 0; j < RTW; ++j) {
-      const int row = (rtid[j] < 0 ? NRT : rtid[j]) * 8 + (lane >> 2);
-#pragma unroll
-      for (int ks = 0; ks < KS; ++ks) {
-        const int k = 4 * ks + (lane & 3);
-        const int col = cf_s[k / NF] * NF + (k % NF);
-        Lf[j][ks] = (row < NV) ? __ldg(a.LT + ((size_t)fast_class * (NFACE * NF) + col) * NV + row) : 0.0;
-      }
-    }
-    double cfr[2];
-#pragma unroll
-    for (int ks = 0; ks < 2; ++ks) {
-      const int kk = 4 * ks + (lane & 3), nn = lane >> 2;
-      cfr[ks] = (kk < N1 && nn < N1) ? chol_s[kk * N1 + nn] : 0.0;
-    }
-    for (int it = 0; it < n_my; ++it) {
-      const int stage = it % NS;
-      const int ob = it & 1;
-      V3_T0(tc);
-      mbar_wait(&qready_bar[stage], (it / NS) & 1);
-      V3_ACC(3, tc);
-      const int fast = mfast_s[stage];
-      const double* sst = sm + stage * C::STAGE;
-      const double* ust = sst + TILE;
-      const double* qst = ust + TILE + C::HALO;
-      // norm of the previous tile (needs every warp's delta of tile it-1)
-      double nsum = 0.0;
-      if (it >= 1) {
-        V3_T0(td);
-        mbar_wait(&done_bar[(it - 1) & 1], ((it - 1) >> 1) & 1);
-        V3_ACC(8, td);
-        nsum = norm_units_list<N1, M, NP, NV, UPW>(d_s + ((it - 1) & 1) * TILE, uid, lane, cfr, a.comp_w);
-      }
-      V3_T0(tm);
-      double acc[NEG][RTW][2];
-#pragma unroll
-      for (int eg = 0; eg < NEG; ++eg) {
-        const int te = eg * 8 + 2 * (lane & 3);
-#pragma unroll
-        for (int j = 0; j < RTW; ++j) {
-          const int row = rtid[j] * 8 + (lane >> 2);
-          const bool ok = rtid[j] >= 0 && row < NV;
-          acc[eg][j][0] = ok ? sst[te * NV + row] : 0.0;
-          acc[eg][j][1] = ok ? sst[(te + 1) * NV + row] : 0.0;
-        }
-      }
-      const double* qb = qst + (lane >> 2) * KC + (lane & 3);
-      if (fast && !IHDG_MEMONLY_ON) {
-#pragma unroll
+    auto consume = [&](auto nr_c, auto nu_c) {
+      constexpr int NR = decltype(nr_c)::value, NU = decltype(nu_c)::value;
+      int rtid[NR], uid[NU];   // this warp's row tiles and norm units (C::PLAN)
+  #pragma unroll
+      for (int j = 0; j < NR; ++j) rtid[j] = prt_s[warp * RTW + j];
+  #pragma unroll
+      for (int m = 0; m < NU; ++m) uid[m] = pun_s[warp * UPW + m];
+      double Lf[NR][KS];
+  #pragma unroll
+      for (int j = 0; j < NR; ++j) {
+        const int row = rtid[j] * 8 + (lane >> 2);
+  #pragma unroll
         for (int ks = 0; ks < KS; ++ks) {
-          double b[NEG];
-#pragma unroll
-          for (int eg = 0; eg < NEG; ++eg) b[eg] = qb[eg * 8 * KC + 4 * ks];
-#pragma unroll
-          for (int eg = 0; eg < NEG; ++eg)
-#pragma unroll
-            for (int j = 0; j < RTW; ++j)
-              if (rtid[j] >= 0) dmma_8x8x4(acc[eg][j][0], acc[eg][j][1], Lf[j][ks], b[eg]);
+          const int k = 4 * ks + (lane & 3);
+          const int col = cf_s[k / NF] * NF + (k % NF);
+          Lf[j][ks] = (row < NV) ? __ldg(a.LT + ((size_t)fast_class * (NFACE * NF) + col) * NV + row) : 0.0;
         }
-      } else if (!IHDG_MEMONLY_ON) {
-        const unsigned cset = mcset_s[stage];
-        for (unsigned rem = cset; rem != 0u; rem &= rem - 1u) {
-          const int c = __ffs(rem) - 1;
+      }
+      double cfr[2];
+  #pragma unroll
+      for (int ks = 0; ks < 2; ++ks) {
+        const int kk = 4 * ks + (lane & 3), nn = lane >> 2;
+        cfr[ks] = (kk < N1 && nn < N1) ? chol_s[kk * N1 + nn] : 0.0;
+      }
+      for (int it = 0; it < n_my; ++it) {
+        const int stage = it % NS;
+        const int ob = it & 1;
+        V3_T0(tc);
+        mbar_wait(&qready_bar[stage], (it / NS) & 1);
+        V3_ACC(3, tc);
+        const int fast = mfast_s[stage];
+        const double* sst = sm + stage * C::STAGE;
+        const double* ust = sst + TILE;
+        const double* qst = ust + TILE + C::HALO;
+        // norm of the previous tile (needs every warp's delta of tile it-1)
+        double nsum = 0.0;
+        if (it >= 1) {
+          V3_T0(td);
+          mbar_wait(&done_bar[(it - 1) & 1], ((it - 1) >> 1) & 1);
+          V3_ACC(8, td);
+          nsum = norm_units_list<N1, M, NP, NV, NU>(d_s + ((it - 1) & 1) * TILE, uid, lane, cfr, a.comp_w);
+        }
+        V3_T0(tm);
+        double acc[NEG][NR][2];
+  #pragma unroll
+        for (int eg = 0; eg < NEG; ++eg) {
+          const int te = eg * 8 + 2 * (lane & 3);
+  #pragma unroll
+          for (int j = 0; j < NR; ++j) {
+            const int row = rtid[j] * 8 + (lane >> 2);
+            const bool ok = row < NV;
+            acc[eg][j][0] = ok ? sst[te * NV + row] : 0.0;
+            acc[eg][j][1] = ok ? sst[(te + 1) * NV + row] : 0.0;
+          }
+        }
+        const double* qb = qst + (lane >> 2) * KC + (lane & 3);
+        if (fast && !IHDG_MEMONLY_ON) {
+  #pragma unroll
           for (int ks = 0; ks < KS; ++ks) {
-            const int k = 4 * ks + (lane & 3);
-            const int col = cf_s[k / NF] * NF + (k % NF);
-            double av[RTW];
-#pragma unroll
-            for (int j = 0; j < RTW; ++j) {
-              const int row = rtid[j] * 8 + (lane >> 2);
-              av[j] = (rtid[j] >= 0 && row < NV) ? __ldg(a.LT + ((size_t)c * (NFACE * NF) + col) * NV + row) : 0.0;
-            }
-#pragma unroll
-            for (int eg = 0; eg < NEG; ++eg) {
-              const double b = (mcls_s[stage][eg * 8 + (lane >> 2)] == c) ? qb[eg * 8 * KC + 4 * ks] : 0.0;
-#pragma unroll
-              for (int j = 0; j < RTW; ++j)
-                if (rtid[j] >= 0) dmma_8x8x4(acc[eg][j][0], acc[eg][j][1], av[j], b);
+            double b[NEG];
+  #pragma unroll
+            for (int eg = 0; eg < NEG; ++eg) b[eg] = qb[eg * 8 * KC + 4 * ks];
+  #pragma unroll
+            for (int eg = 0; eg < NEG; ++eg)
+  #pragma unroll
+              for (int j = 0; j < NR; ++j)
+                dmma_8x8x4(acc[eg][j][0], acc[eg][j][1], Lf[j][ks], b[eg]);
+          }
+        } else if (!IHDG_MEMONLY_ON) {
+          const unsigned cset = mcset_s[stage];
+          for (unsigned rem = cset; rem != 0u; rem &= rem - 1u) {
+            const int c = __ffs(rem) - 1;
+            for (int ks = 0; ks < KS; ++ks) {
+              const int k = 4 * ks + (lane & 3);
+              const int col = cf_s[k / NF] * NF + (k % NF);
+              double av[NR];
+  #pragma unroll
+              for (int j = 0; j < NR; ++j) {
+                const int row = rtid[j] * 8 + (lane >> 2);
+                av[j] = (row < NV) ? __ldg(a.LT + ((size_t)c * (NFACE * NF) + col) * NV + row) : 0.0;
+              }
+  #pragma unroll
+              for (int eg = 0; eg < NEG; ++eg) {
+                const double b = (mcls_s[stage][eg * 8 + (lane >> 2)] == c) ? qb[eg * 8 * KC + 4 * ks] : 0.0;
+  #pragma unroll
+                for (int j = 0; j < NR; ++j)
+                  dmma_8x8x4(acc[eg][j][0], acc[eg][j][1], av[j], b);
+              }
             }
           }
         }
-      }
-      V3_ACC(4, tm);
-      V3_T0(to);
-      if (it >= 2) mbar_wait(&outfree_bar[ob], ((it - 2) >> 1) & 1);
-      V3_ACC(5, to);
-      double* outb = out_s + ob * TILE;
-      double* dcur = d_s + ob * TILE;
-#pragma unroll
-      for (int eg = 0; eg < NEG; ++eg) {
-        const int te = eg * 8 + 2 * (lane & 3);
-#pragma unroll
-        for (int j = 0; j < RTW; ++j) {
-          const int row = rtid[j] * 8 + (lane >> 2);
-          if (rtid[j] >= 0 && row < NV) {
-#pragma unroll
-            for (int v = 0; v < 2; ++v) {
-              const int t = te + v;
-              outb[t * NV + row] = acc[eg][j][v];
-              dcur[t * NV + row] = acc[eg][j][v] - ust[t * NV + row];
+        V3_ACC(4, tm);
+        V3_T0(to);
+        if (it >= 2) mbar_wait(&outfree_bar[ob], ((it - 2) >> 1) & 1);
+        V3_ACC(5, to);
+        double* outb = out_s + ob * TILE;
+        double* dcur = d_s + ob * TILE;
+  #pragma unroll
+        for (int eg = 0; eg < NEG; ++eg) {
+          const int te = eg * 8 + 2 * (lane & 3);
+  #pragma unroll
+          for (int j = 0; j < NR; ++j) {
+            const int row = rtid[j] * 8 + (lane >> 2);
+            if (row < NV) {
+  #pragma unroll
+              for (int v = 0; v < 2; ++v) {
+                const int t = te + v;
+                outb[t * NV + row] = acc[eg][j][v];
+                dcur[t * NV + row] = acc[eg][j][v] - ust[t * NV + row];
+              }
             }
           }
         }
+        if (it >= 1) {
+  #pragma unroll
+          for (int o = 16; o > 0; o >>= 1) nsum += __shfl_xor_sync(0xffffffffu, nsum, o);
+          if (lane == 0) red_s[((it - 1) & 1) * 32 + warp] = nsum;
+        }
+        fence_proxy_async();
+        __syncwarp();
+        if (lane == 0) {
+          mbar_arrive(&empty_bar[stage]);
+          mbar_arrive(&done_bar[ob]);
+        }
       }
-      if (it >= 1) {
-#pragma unroll
+      // drain: norm of the last tile
+      if (n_my >= 1) {
+        const int L = n_my - 1;
+        mbar_wait(&done_bar[L & 1], (L >> 1) & 1);
+        double nsum = norm_units_list<N1, M, NP, NV, NU>(d_s + (L & 1) * TILE, uid, lane, cfr, a.comp_w);
+  #pragma unroll
         for (int o = 16; o > 0; o >>= 1) nsum += __shfl_xor_sync(0xffffffffu, nsum, o);
-        if (lane == 0) red_s[((it - 1) & 1) * 32 + warp] = nsum;
+        if (lane == 0) red_s[(L & 1) * 32 + warp] = nsum;
       }
-      fence_proxy_async();
-      __syncwarp();
-      if (lane == 0) {
-        mbar_arrive(&empty_bar[stage]);
-        mbar_arrive(&done_bar[ob]);
-      }
-    }
-    // drain: norm of the last tile
-    if (n_my >= 1) {
-      const int L = n_my - 1;
-      mbar_wait(&done_bar[L & 1], (L >> 1) & 1);
-      double nsum = norm_units_list<N1, M, NP, NV, UPW>(d_s + (L & 1) * TILE, uid, lane, cfr, a.comp_w);
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) nsum += __shfl_xor_sync(0xffffffffu, nsum, o);
-      if (lane == 0) red_s[(L & 1) * 32 + warp] = nsum;
-    }
+    };
+    plan_dispatch<C>(pcls_s[warp], consume);
   }
 
   __syncthreads();
