@@ -124,7 +124,7 @@ __device__ __forceinline__ void plan_dispatch(int k, F&& f) {
   }
 }
 
-// norm units listed in uid (-1 = none): sum of w_c |C^T Delta_{t,c} C|_F^2
+// norm units listed in uid (all valid): sum of w_c |C^T Delta_{t,c} C|_F^2
 template <int N1, int M, int NP, int NV, int UM>
 __device__ __forceinline__ double norm_units_list(const double* __restrict__ dbuf, const int (&uid)[UM], int lane,
                                                   const double (&cfr)[2], const double* comp_w) {
@@ -134,7 +134,7 @@ __device__ __forceinline__ double norm_units_list(const double* __restrict__ dbu
   for (int m = 0; m < UM; ++m) {
     r0[m] = 0.0;
     r1[m] = 0.0;
-    if (uid[m] >= 0) {
+    {
       const int t = uid[m] / M, c = uid[m] - (uid[m] / M) * M;
       const double* base = dbuf + t * NV + c * NP;
 #pragma unroll
@@ -147,7 +147,7 @@ __device__ __forceinline__ double norm_units_list(const double* __restrict__ dbu
   }
 #pragma unroll
   for (int m = 0; m < UM; ++m) {
-    if (uid[m] >= 0) {
+    {
       const int c = uid[m] % M;
       double y0 = 0.0, y1 = 0.0;
 #pragma unroll
@@ -236,6 +236,7 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS>::NT, 1)
 
   ihdg_iter_state* st = a.state;
   if (st->status != IHDG_RUNNING) return;
+  V3_DECL
 
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
@@ -489,15 +490,15 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS>::NT, 1)
     auto consume = [&](auto nr_c, auto nu_c) {
       constexpr int NR = decltype(nr_c)::value, NU = decltype(nu_c)::value;
       int rtid[NR], uid[NU];   // this warp's row tiles and norm units (C::PLAN)
-  #pragma unroll
+#pragma unroll
       for (int j = 0; j < NR; ++j) rtid[j] = prt_s[warp * RTW + j];
-  #pragma unroll
+#pragma unroll
       for (int m = 0; m < NU; ++m) uid[m] = pun_s[warp * UPW + m];
       double Lf[NR][KS];
-  #pragma unroll
+#pragma unroll
       for (int j = 0; j < NR; ++j) {
         const int row = rtid[j] * 8 + (lane >> 2);
-  #pragma unroll
+#pragma unroll
         for (int ks = 0; ks < KS; ++ks) {
           const int k = 4 * ks + (lane & 3);
           const int col = cf_s[k / NF] * NF + (k % NF);
@@ -505,7 +506,7 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS>::NT, 1)
         }
       }
       double cfr[2];
-  #pragma unroll
+#pragma unroll
       for (int ks = 0; ks < 2; ++ks) {
         const int kk = 4 * ks + (lane & 3), nn = lane >> 2;
         cfr[ks] = (kk < N1 && nn < N1) ? chol_s[kk * N1 + nn] : 0.0;
@@ -526,14 +527,16 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS>::NT, 1)
           V3_T0(td);
           mbar_wait(&done_bar[(it - 1) & 1], ((it - 1) >> 1) & 1);
           V3_ACC(8, td);
+          V3_T0(tn);
           nsum = norm_units_list<N1, M, NP, NV, NU>(d_s + ((it - 1) & 1) * TILE, uid, lane, cfr, a.comp_w);
+          V3_ACC(7, tn);
         }
         V3_T0(tm);
         double acc[NEG][NR][2];
-  #pragma unroll
+#pragma unroll
         for (int eg = 0; eg < NEG; ++eg) {
           const int te = eg * 8 + 2 * (lane & 3);
-  #pragma unroll
+#pragma unroll
           for (int j = 0; j < NR; ++j) {
             const int row = rtid[j] * 8 + (lane >> 2);
             const bool ok = row < NV;
@@ -543,14 +546,14 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS>::NT, 1)
         }
         const double* qb = qst + (lane >> 2) * KC + (lane & 3);
         if (fast && !IHDG_MEMONLY_ON) {
-  #pragma unroll
+#pragma unroll
           for (int ks = 0; ks < KS; ++ks) {
             double b[NEG];
-  #pragma unroll
+#pragma unroll
             for (int eg = 0; eg < NEG; ++eg) b[eg] = qb[eg * 8 * KC + 4 * ks];
-  #pragma unroll
+#pragma unroll
             for (int eg = 0; eg < NEG; ++eg)
-  #pragma unroll
+#pragma unroll
               for (int j = 0; j < NR; ++j)
                 dmma_8x8x4(acc[eg][j][0], acc[eg][j][1], Lf[j][ks], b[eg]);
           }
@@ -562,15 +565,15 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS>::NT, 1)
               const int k = 4 * ks + (lane & 3);
               const int col = cf_s[k / NF] * NF + (k % NF);
               double av[NR];
-  #pragma unroll
+#pragma unroll
               for (int j = 0; j < NR; ++j) {
                 const int row = rtid[j] * 8 + (lane >> 2);
                 av[j] = (row < NV) ? __ldg(a.LT + ((size_t)c * (NFACE * NF) + col) * NV + row) : 0.0;
               }
-  #pragma unroll
+#pragma unroll
               for (int eg = 0; eg < NEG; ++eg) {
                 const double b = (mcls_s[stage][eg * 8 + (lane >> 2)] == c) ? qb[eg * 8 * KC + 4 * ks] : 0.0;
-  #pragma unroll
+#pragma unroll
                 for (int j = 0; j < NR; ++j)
                   dmma_8x8x4(acc[eg][j][0], acc[eg][j][1], av[j], b);
               }
@@ -581,16 +584,17 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS>::NT, 1)
         V3_T0(to);
         if (it >= 2) mbar_wait(&outfree_bar[ob], ((it - 2) >> 1) & 1);
         V3_ACC(5, to);
+        V3_T0(te);
         double* outb = out_s + ob * TILE;
         double* dcur = d_s + ob * TILE;
-  #pragma unroll
+#pragma unroll
         for (int eg = 0; eg < NEG; ++eg) {
           const int te = eg * 8 + 2 * (lane & 3);
-  #pragma unroll
+#pragma unroll
           for (int j = 0; j < NR; ++j) {
             const int row = rtid[j] * 8 + (lane >> 2);
             if (row < NV) {
-  #pragma unroll
+#pragma unroll
               for (int v = 0; v < 2; ++v) {
                 const int t = te + v;
                 outb[t * NV + row] = acc[eg][j][v];
@@ -599,8 +603,9 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS>::NT, 1)
             }
           }
         }
+        V3_ACC(10, te);
         if (it >= 1) {
-  #pragma unroll
+#pragma unroll
           for (int o = 16; o > 0; o >>= 1) nsum += __shfl_xor_sync(0xffffffffu, nsum, o);
           if (lane == 0) red_s[((it - 1) & 1) * 32 + warp] = nsum;
         }
@@ -616,7 +621,7 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS>::NT, 1)
         const int L = n_my - 1;
         mbar_wait(&done_bar[L & 1], (L >> 1) & 1);
         double nsum = norm_units_list<N1, M, NP, NV, NU>(d_s + (L & 1) * TILE, uid, lane, cfr, a.comp_w);
-  #pragma unroll
+#pragma unroll
         for (int o = 16; o > 0; o >>= 1) nsum += __shfl_xor_sync(0xffffffffu, nsum, o);
         if (lane == 0) red_s[(L & 1) * 32 + warp] = nsum;
       }
@@ -633,6 +638,7 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS>::NT, 1)
   }
 #ifdef IHDG_WS_PROF
   if (tid == 0) V3_ACC(6, tk0);
+  V3_FLUSH;
 #endif
   if (a.finalize) {
     __threadfence();
