@@ -21,6 +21,9 @@
 
 namespace ihdg {
 
+#ifndef IHDG_WS_NCW_BIG
+#define IHDG_WS_NCW_BIG 12   // consumer warps when the row tiles allow (A/B builds override)
+#endif
 #ifndef IHDG_WS_PF
 #define IHDG_WS_PF 0   // L2 prefetch distance in tiles (0 = off; measured no gain on config 5)
 #endif
@@ -176,13 +179,16 @@ struct WCfg {
   static constexpr int NRT = (NV + 7) / 8;
   static constexpr int KS = KC / 4;
   static constexpr int NEG = E / 8;
-  static constexpr int NCW = NRT >= 8 ? 8 : 4;                     // consumer warps (2 or 1 per SMSP)
+  // consumer warps: the consumers are latency-bound per warp (dependent DMMA
+  // chains, shuffles, smem epilogue), so more warps with less work each win
+  // over fewer, fuller warps; 3 per SMSP at the 128-register cap
+  static constexpr int NCW = NRT >= 16 ? IHDG_WS_NCW_BIG : (NRT >= 8 ? 8 : 4);
   static constexpr int NU = E * M;                                  // norm units per tile
   static constexpr auto PLAN0 = make_wplan<NCW, NRT, NU, 8, 16>(KS * NEG, 4);
   static constexpr int RTW = PLAN0.maxr;                            // row tiles per warp (max)
   static constexpr int UPW = PLAN0.maxu;                            // norm units per warp (max)
   static constexpr auto PLAN = make_wplan<NCW, NRT, NU, RTW, UPW>(KS * NEG, 4);
-  static constexpr int NQW = 4;                                    // prep warps
+  static constexpr int NQW = NCW >= 12 ? 2 : 4;                    // prep warps (15 or 13 warps in all)
   static constexpr int NT = 32 * (NCW + NQW + 1);
   static constexpr int TILE = E * NV;
   static constexpr int HALO = 0;   // out-of-tile faces: prep warps load them into registers
