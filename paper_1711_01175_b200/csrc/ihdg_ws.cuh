@@ -14,16 +14,10 @@
 //                    norm J |C^T Delta C|^2 of tile i-1      -> done[i&1]
 #pragma once
 
-#include <type_traits>
-#include <utility>
-
 #include "ihdg_stream.cuh"
 
 namespace ihdg {
 
-#ifndef IHDG_WS_NCW_BIG
-#define IHDG_WS_NCW_BIG 12   // consumer warps when the row tiles allow (A/B builds override)
-#endif
 #ifndef IHDG_WS_PF
 #define IHDG_WS_PF 0   // L2 prefetch distance in tiles (0 = off; measured no gain on config 5)
 #endif
@@ -32,142 +26,6 @@ namespace ihdg {
 #else
 #define IHDG_MEMONLY_ON 0
 #endif
-
-// Consumer work plan.  The FP64 pipe is per SMSP (warp w runs on SMSP w % 4)
-// and the consumers meet once per tile, so the tile time is set by the most
-// loaded SMSP, not by the most loaded warp.  Row tiles of the contraction
-// (KS * NEG DMMAs each) and norm units (4 DMMAs each) go greedily to the least
-// loaded SMSP, then to its least loaded warp; padding row tiles / units are
-// not issued at all.
-template <int NCW, int NRT, int NU, int MAXR, int MAXU>
-struct WPlan {
-  int rt[NCW][MAXR];   // row tiles of warp w (-1 = none)
-  int un[NCW][MAXU];   // norm units of warp w (-1 = none)
-  int nr[NCW], nu[NCW];
-  int maxr, maxu;
-  int cls[NCW];          // warps with equal (nr, nu) share one code path
-  int cnr[NCW], cnu[NCW], ncls;
-};
-template <int NCW, int NRT, int NU, int MAXR, int MAXU>
-constexpr WPlan<NCW, NRT, NU, MAXR, MAXU> make_wplan(int rt_cost, int u_cost) {
-  WPlan<NCW, NRT, NU, MAXR, MAXU> p{};
-  int sl[4] = {0, 0, 0, 0};
-  int wl[NCW] = {};
-  for (int w = 0; w < NCW; ++w) {
-    p.nr[w] = 0;
-    p.nu[w] = 0;
-    for (int j = 0; j < MAXR; ++j) p.rt[w][j] = -1;
-    for (int j = 0; j < MAXU; ++j) p.un[w][j] = -1;
-  }
-  for (int pass = 0; pass < 2; ++pass) {
-    const int n = pass == 0 ? NRT : NU, cost = pass == 0 ? rt_cost : u_cost, cap = pass == 0 ? MAXR : MAXU;
-    for (int i = 0; i < n; ++i) {
-      int bw = -1;
-      for (int w = 0; w < NCW; ++w) {
-        const int cnt = pass == 0 ? p.nr[w] : p.nu[w];
-        if (cnt >= cap) continue;
-        if (bw < 0 || sl[w % 4] < sl[bw % 4] || (sl[w % 4] == sl[bw % 4] && wl[w] < wl[bw])) bw = w;
-      }
-      if (pass == 0) p.rt[bw][p.nr[bw]++] = i;
-      else p.un[bw][p.nu[bw]++] = i;
-      sl[bw % 4] += cost;
-      wl[bw] += cost;
-    }
-  }
-  p.maxr = 0;
-  p.maxu = 0;
-  for (int w = 0; w < NCW; ++w) {
-    p.maxr = p.nr[w] > p.maxr ? p.nr[w] : p.maxr;
-    p.maxu = p.nu[w] > p.maxu ? p.nu[w] : p.maxu;
-  }
-  p.ncls = 0;
-  for (int w = 0; w < NCW; ++w) {
-    int k = 0;
-    while (k < p.ncls && !(p.cnr[k] == p.nr[w] && p.cnu[k] == p.nu[w])) ++k;
-    if (k == p.ncls) {
-      p.cnr[k] = p.nr[w];
-      p.cnu[k] = p.nu[w];
-      ++p.ncls;
-    }
-    p.cls[w] = k;
-  }
-  return p;
-}
-
-// The plan as compile-time constants: a constexpr aggregate cannot be read
-// from device code, its elements as template arguments can.  plan_fill
-// copies the per-warp lists to shared memory; plan_dispatch calls f with the
-// warp's (row tiles, units) counts as integral constants, so every class of
-// warps runs a fully unrolled, branch-free body.
-template <class C, int W, int... J>
-__device__ __forceinline__ void plan_fill_rt(int* rt, std::integer_sequence<int, J...>) {
-  ((rt[W * C::RTW + J] = std::integral_constant<int, C::PLAN.rt[W][J]>::value), ...);
-}
-template <class C, int W, int... J>
-__device__ __forceinline__ void plan_fill_un(int* un, std::integer_sequence<int, J...>) {
-  ((un[W * C::UPW + J] = std::integral_constant<int, C::PLAN.un[W][J]>::value), ...);
-}
-template <class C, int W = 0>
-__device__ __forceinline__ void plan_fill(int* rt, int* un, int* cls) {
-  if constexpr (W < C::NCW) {
-    plan_fill_rt<C, W>(rt, std::make_integer_sequence<int, C::RTW>{});
-    plan_fill_un<C, W>(un, std::make_integer_sequence<int, C::UPW>{});
-    cls[W] = std::integral_constant<int, C::PLAN.cls[W]>::value;
-    plan_fill<C, W + 1>(rt, un, cls);
-  }
-}
-template <class C, int K = 0, class F>
-__device__ __forceinline__ void plan_dispatch(int k, F&& f) {
-  if constexpr (K < C::PLAN.ncls) {
-    if (k == K) {
-      f(std::integral_constant<int, C::PLAN.cnr[K]>{}, std::integral_constant<int, C::PLAN.cnu[K]>{});
-    } else {
-      plan_dispatch<C, K + 1>(k, f);
-    }
-  }
-}
-
-// norm units listed in uid (all valid): sum of w_c |C^T Delta_{t,c} C|_F^2
-template <int N1, int M, int NP, int NV, int UM>
-__device__ __forceinline__ double norm_units_list(const double* __restrict__ dbuf, const int (&uid)[UM], int lane,
-                                                  const double (&cfr)[2], const double* comp_w) {
-  double acc = 0.0;
-  double r0[UM], r1[UM];
-#pragma unroll
-  for (int m = 0; m < UM; ++m) {
-    r0[m] = 0.0;
-    r1[m] = 0.0;
-    {
-      const int t = uid[m] / M, c = uid[m] - (uid[m] / M) * M;
-      const double* base = dbuf + t * NV + c * NP;
-#pragma unroll
-      for (int ks = 0; ks < 2; ++ks) {
-        const int kk = 4 * ks + (lane & 3), nn = lane >> 2;
-        const double b = (kk < N1 && nn < N1) ? base[kk * N1 + nn] : 0.0;
-        dmma_8x8x4(r0[m], r1[m], cfr[ks], b);   // R = C^T Delta
-      }
-    }
-  }
-#pragma unroll
-  for (int m = 0; m < UM; ++m) {
-    {
-      const int c = uid[m] % M;
-      double y0 = 0.0, y1 = 0.0;
-#pragma unroll
-      for (int ks = 0; ks < 2; ++ks) {
-        const int col = 4 * ks + (lane & 3);
-        const int src = (lane & ~3) | (col >> 1);
-        const double x0 = __shfl_sync(0xffffffffu, r0[m], src);
-        const double x1 = __shfl_sync(0xffffffffu, r1[m], src);
-        dmma_8x8x4(y0, y1, (col & 1) ? x1 : x0, cfr[ks]);  // Y = R C
-      }
-      const double w = comp_w[c];
-      acc = fma(w * y0, y0, acc);
-      acc = fma(w * y1, y1, acc);
-    }
-  }
-  return acc;
-}
 
 template <int N1, int M, int NCF, int NWC, int E, int NS>
 struct WCfg {
@@ -179,16 +37,10 @@ struct WCfg {
   static constexpr int NRT = (NV + 7) / 8;
   static constexpr int KS = KC / 4;
   static constexpr int NEG = E / 8;
-  // consumer warps: the consumers are latency-bound per warp (dependent DMMA
-  // chains, shuffles, smem epilogue), so more warps with less work each win
-  // over fewer, fuller warps; 3 per SMSP at the 128-register cap
-  static constexpr int NCW = NRT >= 16 ? IHDG_WS_NCW_BIG : (NRT >= 8 ? 8 : 4);
-  static constexpr int NU = E * M;                                  // norm units per tile
-  static constexpr auto PLAN0 = make_wplan<NCW, NRT, NU, 8, 16>(KS * NEG, 4);
-  static constexpr int RTW = PLAN0.maxr;                            // row tiles per warp (max)
-  static constexpr int UPW = PLAN0.maxu;                            // norm units per warp (max)
-  static constexpr auto PLAN = make_wplan<NCW, NRT, NU, RTW, UPW>(KS * NEG, 4);
-  static constexpr int NQW = NCW >= 12 ? 2 : 4;                    // prep warps (15 or 13 warps in all)
+  static constexpr int NCW = NRT >= 16 ? 10 : (NRT >= 8 ? 8 : 4);  // consumer warps
+  static constexpr int RTW = (NRT + NCW - 1) / NCW;
+  static constexpr int UPW = (E * M + NCW - 1) / NCW;
+  static constexpr int NQW = 4;                                    // prep warps
   static constexpr int NT = 32 * (NCW + NQW + 1);
   static constexpr int TILE = E * NV;
   static constexpr int HALO = 0;   // out-of-tile faces: prep warps load them into registers
@@ -238,7 +90,6 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS>::NT, 1)
   __shared__ int tile_s[NS];
   __shared__ int com_s[64];
   __shared__ int last_s;
-  __shared__ int prt_s[C::NCW * C::RTW], pun_s[C::NCW * C::UPW], pcls_s[C::NCW];
 
   ihdg_iter_state* st = a.state;
   if (st->status != IHDG_RUNNING) return;
@@ -255,7 +106,6 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS>::NT, 1)
   for (int i = tid; i < NFACE * NF; i += blockDim.x) fv_s[i / NF][i % NF] = face_node_vidx(D, N1, i / NF, i % NF);
   for (int i = tid; i < N1 * N1; i += blockDim.x) chol_s[i] = a.chol1d[i];
   if (tid < 64) com_s[tid] = a.class_of_mask[tid];
-  if (tid == 32) plan_fill<C>(prt_s, pun_s, pcls_s);
   if (tid == 0) {
     int n = 0;
     for (int f = 0; f < NFACE && n < NCF; ++f) {
@@ -342,14 +192,6 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS>::NT, 1)
         mbar_arrive_expect_tx(&full_bar[stage], 2 * bytes);  // release: metadata above
         bulk_g2s(sst, a.s + (int64_t)e0 * NV, bytes, &full_bar[stage]);
         bulk_g2s(ust, uo + (int64_t)e0 * NV, bytes, &full_bar[stage]);
-      }
-      if (IHDG_WS_PF > 0 && lane == 0 && it + IHDG_WS_PF < n_my) {
-        // tile it+PF will be copied into a stage PF tiles from now: pull it into L2
-        STile<D> tp;
-        tp.init(a.g, tile + IHDG_WS_PF * (int)gridDim.x, E, nlay, lsi);
-        const uint32_t pb = (uint32_t)(tp.nt * NV * sizeof(double));
-        bulk_prefetch_l2(a.s + (int64_t)tp.e0 * NV, pb);
-        bulk_prefetch_l2(uo + (int64_t)tp.e0 * NV, pb);
       }
       if (IHDG_WS_PF > 0 && lane == 0 && it + IHDG_WS_PF < n_my) {
         // tile it+PF will be copied into a stage PF tiles from now: pull it into L2
@@ -493,146 +335,136 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS>::NT, 1)
     }
   } else {
     // ============================ consumer warps ===========================
-    auto consume = [&](auto nr_c, auto nu_c) {
-      constexpr int NR = decltype(nr_c)::value, NU = decltype(nu_c)::value;
-      int rtid[NR], uid[NU];   // this warp's row tiles and norm units (C::PLAN)
+    double Lf[RTW][KS];
 #pragma unroll
-      for (int j = 0; j < NR; ++j) rtid[j] = prt_s[warp * RTW + j];
+    for (int j = 0; j < RTW; ++j) {
+      const int row = (warp + j * NCW) * 8 + (lane >> 2);
 #pragma unroll
-      for (int m = 0; m < NU; ++m) uid[m] = pun_s[warp * UPW + m];
-      double Lf[NR][KS];
+      for (int ks = 0; ks < KS; ++ks) {
+        const int k = 4 * ks + (lane & 3);
+        const int col = cf_s[k / NF] * NF + (k % NF);
+        Lf[j][ks] = (row < NV) ? __ldg(a.LT + ((size_t)fast_class * (NFACE * NF) + col) * NV + row) : 0.0;
+      }
+    }
+    double cfr[2];
 #pragma unroll
-      for (int j = 0; j < NR; ++j) {
-        const int row = rtid[j] * 8 + (lane >> 2);
+    for (int ks = 0; ks < 2; ++ks) {
+      const int kk = 4 * ks + (lane & 3), nn = lane >> 2;
+      cfr[ks] = (kk < N1 && nn < N1) ? chol_s[kk * N1 + nn] : 0.0;
+    }
+    for (int it = 0; it < n_my; ++it) {
+      const int stage = it % NS;
+      const int ob = it & 1;
+      V3_T0(tc);
+      mbar_wait(&qready_bar[stage], (it / NS) & 1);
+      V3_ACC(3, tc);
+      const int fast = mfast_s[stage];
+      const double* sst = sm + stage * C::STAGE;
+      const double* ust = sst + TILE;
+      const double* qst = ust + TILE + C::HALO;
+      // norm of the previous tile (needs every warp's delta of tile it-1)
+      double nsum = 0.0;
+      if (it >= 1) {
+        V3_T0(td);
+        mbar_wait(&done_bar[(it - 1) & 1], ((it - 1) >> 1) & 1);
+        V3_ACC(8, td);
+        V3_T0(tn);
+        nsum = norm_units_2d<N1, M, NP, NV, E, NCW, UPW>(d_s + ((it - 1) & 1) * TILE, warp, lane, cfr,
+                                                         a.comp_w);
+        V3_ACC(7, tn);
+      }
+      V3_T0(tm);
+      double acc[NEG][RTW][2];
+#pragma unroll
+      for (int eg = 0; eg < NEG; ++eg) {
+        const int te = eg * 8 + 2 * (lane & 3);
+#pragma unroll
+        for (int j = 0; j < RTW; ++j) {
+          const int row = (warp + j * NCW) * 8 + (lane >> 2);
+          const bool ok = row < NV && (warp + j * NCW) < NRT;
+          acc[eg][j][0] = ok ? sst[te * NV + row] : 0.0;
+          acc[eg][j][1] = ok ? sst[(te + 1) * NV + row] : 0.0;
+        }
+      }
+      const double* qb = qst + (lane >> 2) * KC + (lane & 3);
+      if (fast && !IHDG_MEMONLY_ON) {
 #pragma unroll
         for (int ks = 0; ks < KS; ++ks) {
-          const int k = 4 * ks + (lane & 3);
-          const int col = cf_s[k / NF] * NF + (k % NF);
-          Lf[j][ks] = (row < NV) ? __ldg(a.LT + ((size_t)fast_class * (NFACE * NF) + col) * NV + row) : 0.0;
+          double b[NEG];
+#pragma unroll
+          for (int eg = 0; eg < NEG; ++eg) b[eg] = qb[eg * 8 * KC + 4 * ks];
+#pragma unroll
+          for (int eg = 0; eg < NEG; ++eg)
+#pragma unroll
+            for (int j = 0; j < RTW; ++j) dmma_8x8x4(acc[eg][j][0], acc[eg][j][1], Lf[j][ks], b[eg]);
         }
-      }
-      double cfr[2];
-#pragma unroll
-      for (int ks = 0; ks < 2; ++ks) {
-        const int kk = 4 * ks + (lane & 3), nn = lane >> 2;
-        cfr[ks] = (kk < N1 && nn < N1) ? chol_s[kk * N1 + nn] : 0.0;
-      }
-      for (int it = 0; it < n_my; ++it) {
-        const int stage = it % NS;
-        const int ob = it & 1;
-        V3_T0(tc);
-        mbar_wait(&qready_bar[stage], (it / NS) & 1);
-        V3_ACC(3, tc);
-        const int fast = mfast_s[stage];
-        const double* sst = sm + stage * C::STAGE;
-        const double* ust = sst + TILE;
-        const double* qst = ust + TILE + C::HALO;
-        // norm of the previous tile (needs every warp's delta of tile it-1)
-        double nsum = 0.0;
-        if (it >= 1) {
-          V3_T0(td);
-          mbar_wait(&done_bar[(it - 1) & 1], ((it - 1) >> 1) & 1);
-          V3_ACC(8, td);
-          V3_T0(tn);
-          nsum = norm_units_list<N1, M, NP, NV, NU>(d_s + ((it - 1) & 1) * TILE, uid, lane, cfr, a.comp_w);
-          V3_ACC(7, tn);
-        }
-        V3_T0(tm);
-        double acc[NEG][NR][2];
-#pragma unroll
-        for (int eg = 0; eg < NEG; ++eg) {
-          const int te = eg * 8 + 2 * (lane & 3);
-#pragma unroll
-          for (int j = 0; j < NR; ++j) {
-            const int row = rtid[j] * 8 + (lane >> 2);
-            const bool ok = row < NV;
-            acc[eg][j][0] = ok ? sst[te * NV + row] : 0.0;
-            acc[eg][j][1] = ok ? sst[(te + 1) * NV + row] : 0.0;
-          }
-        }
-        const double* qb = qst + (lane >> 2) * KC + (lane & 3);
-        if (fast && !IHDG_MEMONLY_ON) {
-#pragma unroll
+      } else if (!IHDG_MEMONLY_ON) {
+        const unsigned cset = mcset_s[stage];
+        for (unsigned rem = cset; rem != 0u; rem &= rem - 1u) {
+          const int c = __ffs(rem) - 1;
           for (int ks = 0; ks < KS; ++ks) {
-            double b[NEG];
+            const int k = 4 * ks + (lane & 3);
+            const int col = cf_s[k / NF] * NF + (k % NF);
+            double av[RTW];
 #pragma unroll
-            for (int eg = 0; eg < NEG; ++eg) b[eg] = qb[eg * 8 * KC + 4 * ks];
+            for (int j = 0; j < RTW; ++j) {
+              const int row = (warp + j * NCW) * 8 + (lane >> 2);
+              av[j] = (row < NV) ? __ldg(a.LT + ((size_t)c * (NFACE * NF) + col) * NV + row) : 0.0;
+            }
 #pragma unroll
-            for (int eg = 0; eg < NEG; ++eg)
+            for (int eg = 0; eg < NEG; ++eg) {
+              const double b = (mcls_s[stage][eg * 8 + (lane >> 2)] == c) ? qb[eg * 8 * KC + 4 * ks] : 0.0;
 #pragma unroll
-              for (int j = 0; j < NR; ++j)
-                dmma_8x8x4(acc[eg][j][0], acc[eg][j][1], Lf[j][ks], b[eg]);
-          }
-        } else if (!IHDG_MEMONLY_ON) {
-          const unsigned cset = mcset_s[stage];
-          for (unsigned rem = cset; rem != 0u; rem &= rem - 1u) {
-            const int c = __ffs(rem) - 1;
-            for (int ks = 0; ks < KS; ++ks) {
-              const int k = 4 * ks + (lane & 3);
-              const int col = cf_s[k / NF] * NF + (k % NF);
-              double av[NR];
-#pragma unroll
-              for (int j = 0; j < NR; ++j) {
-                const int row = rtid[j] * 8 + (lane >> 2);
-                av[j] = (row < NV) ? __ldg(a.LT + ((size_t)c * (NFACE * NF) + col) * NV + row) : 0.0;
-              }
-#pragma unroll
-              for (int eg = 0; eg < NEG; ++eg) {
-                const double b = (mcls_s[stage][eg * 8 + (lane >> 2)] == c) ? qb[eg * 8 * KC + 4 * ks] : 0.0;
-#pragma unroll
-                for (int j = 0; j < NR; ++j)
-                  dmma_8x8x4(acc[eg][j][0], acc[eg][j][1], av[j], b);
-              }
+              for (int j = 0; j < RTW; ++j) dmma_8x8x4(acc[eg][j][0], acc[eg][j][1], av[j], b);
             }
           }
-        }
-        V3_ACC(4, tm);
-        V3_T0(to);
-        if (it >= 2) mbar_wait(&outfree_bar[ob], ((it - 2) >> 1) & 1);
-        V3_ACC(5, to);
-        V3_T0(te);
-        double* outb = out_s + ob * TILE;
-        double* dcur = d_s + ob * TILE;
-#pragma unroll
-        for (int eg = 0; eg < NEG; ++eg) {
-          const int te = eg * 8 + 2 * (lane & 3);
-#pragma unroll
-          for (int j = 0; j < NR; ++j) {
-            const int row = rtid[j] * 8 + (lane >> 2);
-            if (row < NV) {
-#pragma unroll
-              for (int v = 0; v < 2; ++v) {
-                const int t = te + v;
-                outb[t * NV + row] = acc[eg][j][v];
-                dcur[t * NV + row] = acc[eg][j][v] - ust[t * NV + row];
-              }
-            }
-          }
-        }
-        V3_ACC(10, te);
-        if (it >= 1) {
-#pragma unroll
-          for (int o = 16; o > 0; o >>= 1) nsum += __shfl_xor_sync(0xffffffffu, nsum, o);
-          if (lane == 0) red_s[((it - 1) & 1) * 32 + warp] = nsum;
-        }
-        fence_proxy_async();
-        __syncwarp();
-        if (lane == 0) {
-          mbar_arrive(&empty_bar[stage]);
-          mbar_arrive(&done_bar[ob]);
         }
       }
-      // drain: norm of the last tile
-      if (n_my >= 1) {
-        const int L = n_my - 1;
-        mbar_wait(&done_bar[L & 1], (L >> 1) & 1);
-        double nsum = norm_units_list<N1, M, NP, NV, NU>(d_s + (L & 1) * TILE, uid, lane, cfr, a.comp_w);
+      V3_ACC(4, tm);
+      V3_T0(to);
+      if (it >= 2) mbar_wait(&outfree_bar[ob], ((it - 2) >> 1) & 1);
+      V3_ACC(5, to);
+      V3_T0(te);
+      double* outb = out_s + ob * TILE;
+      double* dcur = d_s + ob * TILE;
+#pragma unroll
+      for (int eg = 0; eg < NEG; ++eg) {
+        const int te = eg * 8 + 2 * (lane & 3);
+#pragma unroll
+        for (int j = 0; j < RTW; ++j) {
+          const int row = (warp + j * NCW) * 8 + (lane >> 2);
+          if (row < NV && (warp + j * NCW) < NRT) {
+#pragma unroll
+            for (int v = 0; v < 2; ++v) {
+              const int t = te + v;
+              outb[t * NV + row] = acc[eg][j][v];
+              dcur[t * NV + row] = acc[eg][j][v] - ust[t * NV + row];
+            }
+          }
+        }
+      }
+      V3_ACC(10, te);
+      if (it >= 1) {
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) nsum += __shfl_xor_sync(0xffffffffu, nsum, o);
-        if (lane == 0) red_s[(L & 1) * 32 + warp] = nsum;
+        if (lane == 0) red_s[((it - 1) & 1) * 32 + warp] = nsum;
       }
-    };
-    plan_dispatch<C>(pcls_s[warp], consume);
+      fence_proxy_async();
+      __syncwarp();
+      if (lane == 0) {
+        mbar_arrive(&empty_bar[stage]);
+        mbar_arrive(&done_bar[ob]);
+      }
+    }
+    // drain: norm of the last tile
+    if (n_my >= 1) {
+      const int L = n_my - 1;
+      mbar_wait(&done_bar[L & 1], (L >> 1) & 1);
+      double nsum = norm_units_2d<N1, M, NP, NV, E, NCW, UPW>(d_s + (L & 1) * TILE, warp, lane, cfr, a.comp_w);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) nsum += __shfl_xor_sync(0xffffffffu, nsum, o);
+      if (lane == 0) red_s[(L & 1) * 32 + warp] = nsum;
+    }
   }
 
   __syncthreads();
