@@ -287,12 +287,6 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS>::NT, 1)
           qst[t * KC + k] = v;
         }
       }
-#pragma unroll
-      for (int m = 0; m < QM; ++m)
-#pragma unroll
-        for (int j = 0; j < NWC; ++j) gv[m][j] = gvn[m][j];
-      qs = qsn;
-      ql = qln;
       __syncwarp();
       V3_ACC(2, tq);
       if (lane == 0) mbar_arrive(&qready_bar[stage]);
@@ -317,6 +311,14 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS>::NT, 1)
       prev_tile = cur_tile;
       prev_e0 = cur_e0;
       prev_nt = nt;
+      // the gathers of tile it+1 are consumed only here (a register move
+      // waits on the load), i.e. after qready(it) and the done wait
+#pragma unroll
+      for (int m = 0; m < QM; ++m)
+#pragma unroll
+        for (int j = 0; j < NWC; ++j) gv[m][j] = gvn[m][j];
+      qs = qsn;
+      ql = qln;
     }
     // drain: store of the last tile, partial of the one before
     if (n_my >= 1) {
