@@ -17,7 +17,8 @@ from paper_1711_01175_b200.workloads import make_config  # noqa: E402
 NAMES = ["producer: wait (empty/done)", "prep: wait full", "prep: q compute", "consumer: wait qready",
          "consumer: contraction", "consumer: epilogue / wait outfree (ws)", "CTA total",
          "consumer: norm", "consumer: wait done prev (ws)", "producer: load issue",
-         "consumer: epilogue stores (ws)"]
+         "consumer: epilogue stores (ws)", "consumer: norm reduce (ws)", "consumer: fence.proxy.async (ws)",
+         "consumer: whole iteration (ws)"]
 
 
 def main():
@@ -51,7 +52,7 @@ def main():
     L.ihdg_ws_prof(buf, 0)
     print(f"{e0.elapsed_time(e1) / n:.3f} ms / sweep")
     total = buf[6] / n / 148  # per CTA per sweep
-    for i, nm in enumerate(NAMES[:11]):
+    for i, nm in enumerate(NAMES):
         print(f"{nm:36s} {buf[i] / n / 148:14.0f} cycles/CTA/sweep (warp-summed)  {buf[i] / n / 148 / max(total, 1):6.2f}x CTA")
 
 
