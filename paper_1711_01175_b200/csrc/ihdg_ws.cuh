@@ -27,50 +27,6 @@ namespace ihdg {
 #define IHDG_MEMONLY_ON 0
 #endif
 
-// tensor-core norm of a tile whose delta is formed on the fly from u^{k+1}
-// (out buffer) and u^k (stage): units u = warp + m NCW, (element, component)
-template <int N1, int M, int NP, int NV, int E, int NCW, int UPW>
-__device__ __forceinline__ double norm_units_diff(const double* __restrict__ obuf, const double* __restrict__ ubuf,
-                                                  int warp, int lane, const double (&cfr)[2], const double* comp_w) {
-  double acc = 0.0;
-  double r0[UPW], r1[UPW];
-#pragma unroll
-  for (int m = 0; m < UPW; ++m) {
-    const int u = warp + m * NCW;
-    const bool valid = u < E * M;
-    const int uu = valid ? u : 0;
-    const int t = uu / M, c = uu - (uu / M) * M;
-    const int off = t * NV + c * NP;
-    r0[m] = 0.0;
-    r1[m] = 0.0;
-#pragma unroll
-    for (int ks = 0; ks < 2; ++ks) {
-      const int kk = 4 * ks + (lane & 3), nn = lane >> 2;
-      const int o = off + kk * N1 + nn;
-      const double b = (valid && kk < N1 && nn < N1) ? obuf[o] - ubuf[o] : 0.0;
-      dmma_8x8x4(r0[m], r1[m], cfr[ks], b);   // R = C^T Delta
-    }
-  }
-#pragma unroll
-  for (int m = 0; m < UPW; ++m) {
-    const int u = warp + m * NCW;
-    const int c = (u < E * M ? u : 0) % M;
-    double y0 = 0.0, y1 = 0.0;
-#pragma unroll
-    for (int ks = 0; ks < 2; ++ks) {
-      const int col = 4 * ks + (lane & 3);
-      const int src = (lane & ~3) | (col >> 1);
-      const double x0 = __shfl_sync(0xffffffffu, r0[m], src);
-      const double x1 = __shfl_sync(0xffffffffu, r1[m], src);
-      dmma_8x8x4(y0, y1, (col & 1) ? x1 : x0, cfr[ks]);  // Y = R C
-    }
-    const double w = comp_w[c];
-    acc = fma(w * y0, y0, acc);
-    acc = fma(w * y1, y1, acc);
-  }
-  return acc;
-}
-
 template <int N1, int M, int NCF, int NWC, int E, int NS>
 struct WCfg {
   static constexpr int D = 2;
@@ -91,7 +47,8 @@ struct WCfg {
   static constexpr int QT = E * KC;
   static constexpr int STAGE = 2 * TILE + HALO + QT;
   static constexpr int OFF_OUT = NS * STAGE;
-  static constexpr int OFF_RED = OFF_OUT + 2 * TILE;
+  static constexpr int OFF_D = OFF_OUT + 2 * TILE;
+  static constexpr int OFF_RED = OFF_D + 2 * TILE;
   static constexpr int N_DBL = OFF_RED + 64;
   static constexpr int NBAR = 3 * NS + 4;
   static constexpr size_t BYTES = (size_t)N_DBL * sizeof(double) + NBAR * sizeof(uint64_t);
@@ -110,6 +67,7 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS>::NT, 1)
 
   extern __shared__ __align__(16) double sm[];
   double* out_s = sm + C::OFF_OUT;
+  double* d_s = sm + C::OFF_D;
   double* red_s = sm + C::OFF_RED;
   uint64_t* bars = reinterpret_cast<uint64_t*>(sm + C::N_DBL);
   uint64_t* full_bar = bars;             // [NS] producer -> prep
@@ -397,7 +355,6 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS>::NT, 1)
       cfr[ks] = (kk < N1 && nn < N1) ? chol_s[kk * N1 + nn] : 0.0;
     }
     for (int it = 0; it < n_my; ++it) {
-      V3_T0(tit);
       const int stage = it % NS;
       const int ob = it & 1;
       V3_T0(tc);
@@ -414,12 +371,9 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS>::NT, 1)
         mbar_wait(&done_bar[(it - 1) & 1], ((it - 1) >> 1) & 1);
         V3_ACC(8, td);
         V3_T0(tn);
-        const int pstage = (it - 1) % NS;
-        nsum = norm_units_diff<N1, M, NP, NV, E, NCW, UPW>(out_s + ((it - 1) & 1) * TILE,
-                                                           sm + pstage * C::STAGE + TILE, warp, lane, cfr, a.comp_w);
+        nsum = norm_units_2d<N1, M, NP, NV, E, NCW, UPW>(d_s + ((it - 1) & 1) * TILE, warp, lane, cfr,
+                                                         a.comp_w);
         V3_ACC(7, tn);
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&empty_bar[pstage]);   // u^k of tile it-1 no longer needed
       }
       V3_T0(tm);
       double acc[NEG][RTW][2];
@@ -474,6 +428,7 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS>::NT, 1)
       V3_ACC(5, to);
       V3_T0(te);
       double* outb = out_s + ob * TILE;
+      double* dcur = d_s + ob * TILE;
 #pragma unroll
       for (int eg = 0; eg < NEG; ++eg) {
         const int te = eg * 8 + 2 * (lane & 3);
@@ -485,31 +440,29 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS>::NT, 1)
             for (int v = 0; v < 2; ++v) {
               const int t = te + v;
               outb[t * NV + row] = acc[eg][j][v];
+              dcur[t * NV + row] = acc[eg][j][v] - ust[t * NV + row];
             }
           }
         }
       }
       V3_ACC(10, te);
-      V3_T0(tt);
       if (it >= 1) {
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) nsum += __shfl_xor_sync(0xffffffffu, nsum, o);
         if (lane == 0) red_s[((it - 1) & 1) * 32 + warp] = nsum;
       }
-      V3_ACC(11, tt);
-      V3_T0(tf);
       fence_proxy_async();
       __syncwarp();
-      V3_ACC(12, tf);
-      if (lane == 0) mbar_arrive(&done_bar[ob]);
-      V3_ACC(13, tit);
+      if (lane == 0) {
+        mbar_arrive(&empty_bar[stage]);
+        mbar_arrive(&done_bar[ob]);
+      }
     }
     // drain: norm of the last tile
     if (n_my >= 1) {
       const int L = n_my - 1;
       mbar_wait(&done_bar[L & 1], (L >> 1) & 1);
-      double nsum = norm_units_diff<N1, M, NP, NV, E, NCW, UPW>(out_s + (L & 1) * TILE, sm + (L % NS) * C::STAGE + TILE,
-                                                                warp, lane, cfr, a.comp_w);
+      double nsum = norm_units_2d<N1, M, NP, NV, E, NCW, UPW>(d_s + (L & 1) * TILE, warp, lane, cfr, a.comp_w);
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) nsum += __shfl_xor_sync(0xffffffffu, nsum, o);
       if (lane == 0) red_s[(L & 1) * 32 + warp] = nsum;
