@@ -27,6 +27,66 @@ namespace ihdg {
 #define IHDG_MEMONLY_ON 0
 #endif
 
+// Element <-> DMMA column map of the consumers: column 2a+v of element group
+// eg (a = lane & 3 for the accumulators) holds element a*2*NEG + 2*eg + v.
+// With an odd element stride NV the four elements a half-warp touches then
+// sit 4*NV = 4 (mod 16) double-banks apart: s, u^k and u^{k+1} tile accesses
+// are conflict-free without padding the TMA-copied tiles.
+template <int NEG>
+__device__ __forceinline__ int ws_elem(int a, int eg, int v) { return a * 2 * NEG + 2 * eg + v; }
+// column slot (eg * 8 + n) of element t: q is stored in column order so the
+// B-operand loads stay conflict-free
+template <int NEG>
+__device__ __forceinline__ int ws_qcol(int t) {
+  const int a = t / (2 * NEG), r = t - a * 2 * NEG;
+  return (r >> 1) * 8 + 2 * a + (r & 1);
+}
+// swizzled offset of node (kk, nn) inside a delta unit
+__device__ __forceinline__ int ws_dnode(int kk, int nn) { return kk * 8 + (nn ^ (4 * ((kk >> 1) & 1))); }
+
+// tensor-core norm over the swizzled delta tile: units u = warp + m NCW,
+// (element, component); sum of w_c |C^T Delta C|_F^2
+template <int N1, int M, int E, int NCW, int UPW, int DUE, int DUC>
+__device__ __forceinline__ double norm_units_swz(const double* __restrict__ dbuf, int warp, int lane,
+                                                 const double (&cfr)[2], const double* comp_w) {
+  double acc = 0.0;
+  double r0[UPW], r1[UPW];
+#pragma unroll
+  for (int m = 0; m < UPW; ++m) {
+    const int u = warp + m * NCW;
+    const bool valid = u < E * M;
+    const int uu = valid ? u : 0;
+    const int t = uu / M, c = uu - (uu / M) * M;
+    const double* base = dbuf + t * DUE + c * DUC;
+    r0[m] = 0.0;
+    r1[m] = 0.0;
+#pragma unroll
+    for (int ks = 0; ks < 2; ++ks) {
+      const int kk = 4 * ks + (lane & 3), nn = lane >> 2;
+      const double b = (valid && kk < N1 && nn < N1) ? base[ws_dnode(kk, nn)] : 0.0;
+      dmma_8x8x4(r0[m], r1[m], cfr[ks], b);   // R = C^T Delta
+    }
+  }
+#pragma unroll
+  for (int m = 0; m < UPW; ++m) {
+    const int u = warp + m * NCW;
+    const int c = (u < E * M ? u : 0) % M;
+    double y0 = 0.0, y1 = 0.0;
+#pragma unroll
+    for (int ks = 0; ks < 2; ++ks) {
+      const int col = 4 * ks + (lane & 3);
+      const int src = (lane & ~3) | (col >> 1);
+      const double x0 = __shfl_sync(0xffffffffu, r0[m], src);
+      const double x1 = __shfl_sync(0xffffffffu, r1[m], src);
+      dmma_8x8x4(y0, y1, (col & 1) ? x1 : x0, cfr[ks]);  // Y = R C
+    }
+    const double w = comp_w[c];
+    acc = fma(w * y0, y0, acc);
+    acc = fma(w * y1, y1, acc);
+  }
+  return acc;
+}
+
 template <int N1, int M, int NCF, int NWC, int E, int NS>
 struct WCfg {
   static constexpr int D = 2;
@@ -47,8 +107,14 @@ struct WCfg {
   static constexpr int QT = E * KC;
   static constexpr int STAGE = 2 * TILE + HALO + QT;
   static constexpr int OFF_OUT = NS * STAGE;
+  // delta tiles: bank-conflict-free swizzled layout (node row stride 8,
+  // column XOR 4 on every other pair of rows; component stride DUC, element
+  // stride DUE), written by the epilogue and read by the norm
+  static constexpr int DUC = 8 * N1 + 3;
+  static constexpr int DUE = M * DUC;
+  static constexpr int DT = E * DUE;
   static constexpr int OFF_D = OFF_OUT + 2 * TILE;
-  static constexpr int OFF_RED = OFF_D + 2 * TILE;
+  static constexpr int OFF_RED = OFF_D + 2 * DT;
   static constexpr int N_DBL = OFF_RED + 64;
   static constexpr int NBAR = 3 * NS + 4;
   static constexpr size_t BYTES = (size_t)N_DBL * sizeof(double) + NBAR * sizeof(uint64_t);
@@ -284,7 +350,7 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS>::NT, 1)
 #pragma unroll
             for (int j = 0; j < NWC; ++j) v = fma(ww_s[ci][j], gv[m][j], v);
           }
-          qst[t * KC + k] = v;
+          qst[ws_qcol<C::NEG>(t) * KC + k] = v;
         }
       }
       __syncwarp();
@@ -348,6 +414,14 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS>::NT, 1)
         Lf[j][ks] = (row < NV) ? __ldg(a.LT + ((size_t)fast_class * (NFACE * NF) + col) * NV + row) : 0.0;
       }
     }
+    int doff[RTW];   // swizzled delta offset of this lane's row in each row tile
+#pragma unroll
+    for (int j = 0; j < RTW; ++j) {
+      const int row = (warp + j * NCW) * 8 + (lane >> 2);
+      const int r = row < NV ? row : 0;
+      const int c = r / NP, node = r - c * NP;
+      doff[j] = c * C::DUC + ws_dnode(node / N1, node - (node / N1) * N1);
+    }
     double cfr[2];
 #pragma unroll
     for (int ks = 0; ks < 2; ++ks) {
@@ -371,15 +445,15 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS>::NT, 1)
         mbar_wait(&done_bar[(it - 1) & 1], ((it - 1) >> 1) & 1);
         V3_ACC(8, td);
         V3_T0(tn);
-        nsum = norm_units_2d<N1, M, NP, NV, E, NCW, UPW>(d_s + ((it - 1) & 1) * TILE, warp, lane, cfr,
-                                                         a.comp_w);
+        nsum = norm_units_swz<N1, M, E, NCW, UPW, C::DUE, C::DUC>(d_s + ((it - 1) & 1) * C::DT, warp, lane, cfr,
+                                                                  a.comp_w);
         V3_ACC(7, tn);
       }
       V3_T0(tm);
       double acc[NEG][RTW][2];
 #pragma unroll
       for (int eg = 0; eg < NEG; ++eg) {
-        const int te = eg * 8 + 2 * (lane & 3);
+        const int te = ws_elem<NEG>(lane & 3, eg, 0);
 #pragma unroll
         for (int j = 0; j < RTW; ++j) {
           const int row = (warp + j * NCW) * 8 + (lane >> 2);
@@ -415,7 +489,8 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS>::NT, 1)
             }
 #pragma unroll
             for (int eg = 0; eg < NEG; ++eg) {
-              const double b = (mcls_s[stage][eg * 8 + (lane >> 2)] == c) ? qb[eg * 8 * KC + 4 * ks] : 0.0;
+              const int n = lane >> 2;
+              const double b = (mcls_s[stage][ws_elem<NEG>(n >> 1, eg, n & 1)] == c) ? qb[eg * 8 * KC + 4 * ks] : 0.0;
 #pragma unroll
               for (int j = 0; j < RTW; ++j) dmma_8x8x4(acc[eg][j][0], acc[eg][j][1], av[j], b);
             }
@@ -428,10 +503,10 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS>::NT, 1)
       V3_ACC(5, to);
       V3_T0(te);
       double* outb = out_s + ob * TILE;
-      double* dcur = d_s + ob * TILE;
+      double* dcur = d_s + ob * C::DT;
 #pragma unroll
       for (int eg = 0; eg < NEG; ++eg) {
-        const int te = eg * 8 + 2 * (lane & 3);
+        const int te = ws_elem<NEG>(lane & 3, eg, 0);
 #pragma unroll
         for (int j = 0; j < RTW; ++j) {
           const int row = (warp + j * NCW) * 8 + (lane >> 2);
@@ -440,7 +515,7 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS>::NT, 1)
             for (int v = 0; v < 2; ++v) {
               const int t = te + v;
               outb[t * NV + row] = acc[eg][j][v];
-              dcur[t * NV + row] = acc[eg][j][v] - ust[t * NV + row];
+              dcur[t * C::DUE + doff[j]] = acc[eg][j][v] - ust[t * NV + row];
             }
           }
         }
@@ -462,7 +537,8 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS>::NT, 1)
     if (n_my >= 1) {
       const int L = n_my - 1;
       mbar_wait(&done_bar[L & 1], (L >> 1) & 1);
-      double nsum = norm_units_2d<N1, M, NP, NV, E, NCW, UPW>(d_s + (L & 1) * TILE, warp, lane, cfr, a.comp_w);
+      double nsum = norm_units_swz<N1, M, E, NCW, UPW, C::DUE, C::DUC>(d_s + (L & 1) * C::DT, warp, lane, cfr,
+                                                                       a.comp_w);
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) nsum += __shfl_xor_sync(0xffffffffu, nsum, o);
       if (lane == 0) red_s[(L & 1) * 32 + warp] = nsum;

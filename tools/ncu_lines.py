@@ -26,6 +26,8 @@ def main(rep, kname, obj):
     iA, iS = hdr.index("Address"), hdr.index("Source")
     iSm = hdr.index("Warp Stall Sampling (All Samples)")
     iEx = hdr.index("Instructions Executed")
+    iWx = hdr.index("L1 Wavefronts Shared Excessive") if "L1 Wavefronts Shared Excessive" in hdr else None
+    iW = hdr.index("L1 Wavefronts Shared") if "L1 Wavefronts Shared" in hdr else None
     base = int(data[0][iA], 16)
     tmp = tempfile.mkdtemp()
     subprocess.run(["cuobjdump", "-xelf", "all", os.path.abspath(obj)], cwd=tmp, capture_output=True)
@@ -44,14 +46,23 @@ def main(rep, kname, obj):
             if m and cur_fn and kname in cur_fn:
                 lines[int(m.group(1), 16)] = cur_line
     agg_s, agg_e = collections.Counter(), collections.Counter()
+    agg_w, agg_wx = collections.Counter(), collections.Counter()
     for r in data:
         off = int(r[iA], 16) - base
         key = lines.get(off, "?")
         agg_s[key] += float(r[iSm] or 0)
         agg_e[key] += float(r[iEx] or 0)
+        if iW is not None:
+            agg_w[key] += float(r[iW] or 0)
+            agg_wx[key] += float(r[iWx] or 0)
     ts, te = sum(agg_s.values()) or 1, sum(agg_e.values()) or 1
     for key, v in agg_s.most_common(35):
         print(f"{v / ts * 100:5.1f}% stall  {agg_e[key] / te * 100:5.1f}% inst  {key}")
+    if agg_w:
+        tw = sum(agg_w.values()) or 1
+        print("shared-memory wavefronts (total / excess from bank conflicts) by line:")
+        for key, v in agg_w.most_common(20):
+            print(f"{v / tw * 100:5.1f}% wavefronts  excess {agg_wx[key] / max(v, 1) * 100:5.1f}%  {key}")
 
 
 if __name__ == "__main__":
