@@ -18,6 +18,9 @@
 
 namespace ihdg {
 
+#ifndef IHDG_WS_NCW_BIG
+#define IHDG_WS_NCW_BIG 12   // consumer warps for the large (config 5) tiles
+#endif
 #ifndef IHDG_WS_PF
 #define IHDG_WS_PF 0   // L2 prefetch distance in tiles (0 = off; measured no gain on config 5)
 #endif
@@ -97,10 +100,14 @@ struct WCfg {
   static constexpr int NRT = (NV + 7) / 8;
   static constexpr int KS = KC / 4;
   static constexpr int NEG = E / 8;
-  static constexpr int NCW = NRT >= 16 ? 10 : (NRT >= 8 ? 8 : 4);  // consumer warps
+  // consumer warps (warp w runs on SMSP w % 4: a multiple of 4 keeps the
+  // per-SMSP DMMA load even) and prep warps; at most 16 warps in all keeps
+  // the 128-register cap
+  static constexpr int NCW = NRT >= 16 ? IHDG_WS_NCW_BIG : (NRT >= 8 ? 8 : 4);
   static constexpr int RTW = (NRT + NCW - 1) / NCW;
   static constexpr int UPW = (E * M + NCW - 1) / NCW;
-  static constexpr int NQW = 4;                                    // prep warps
+  static constexpr int NQW = NCW >= 12 ? 3 : 4;
+  static constexpr int QCH = ((E * KC + NQW - 1) / NQW + 31) / 32 * 32;   // q entries per prep warp
   static constexpr int NT = 32 * (NCW + NQW + 1);
   static constexpr int TILE = E * NV;
   static constexpr int HALO = 0;   // out-of-tile faces: prep warps load them into registers
@@ -120,7 +127,6 @@ struct WCfg {
   static constexpr size_t BYTES = (size_t)N_DBL * sizeof(double) + NBAR * sizeof(uint64_t);
   static_assert(KC % 4 == 0 && E % 8 == 0 && E <= 32 && N1 <= 8, "ws config");
   static_assert((TILE * sizeof(double)) % 16 == 0, "tile bytes must be 16-byte multiples");
-  static_assert(E % NQW == 0, "prep warps split the tile");
 };
 
 template <int N1, int M, int NCF, int NWC, int E, int NS>
@@ -277,8 +283,8 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS>::NT, 1)
     const int nlay = (int)(a.g.layer_end - a.g.layer_begin);
     const int lsi = (int)ls;
     int prev_e0 = 0, prev_nt = 0, prev_tile = -1, prev2_tile = -1;
-    constexpr int HALF = E / NQW;
-    constexpr int QM = (HALF * KC + 31) / 32;
+    constexpr int QCH = C::QCH;
+    constexpr int QM = QCH / 32;
     // out-of-tile neighbour face nodes of this warp's entries, loaded from
     // global (L2) into registers one tile ahead
     double gv[QM][NWC], gvn[QM][NWC];
@@ -294,8 +300,9 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS>::NT, 1)
         const int idx = lane + 32 * m;
 #pragma unroll
         for (int j = 0; j < NWC; ++j) dst[m][j] = 0.0;
-        if (idx < HALF * KC) {
-          const int t = pw * HALF + idx / KC, k = idx - (idx / KC) * KC;
+        const int g = pw * QCH + idx;
+        if (g < E * KC) {
+          const int t = g / KC, k = g - (g / KC) * KC;
           const int f = qf_s[k];
           if (!(tg.mask(t, c0, per0) & (1 << f))) {
             const bool in_tile = (f >> 1) == 0 && !((f == 0 && t == 0) || (f == 1 && t == E - 1));
@@ -337,8 +344,9 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS>::NT, 1)
 #pragma unroll
       for (int m = 0; m < QM; ++m) {
         const int idx = lane + 32 * m;
-        if (idx < HALF * KC) {
-          const int t = pw * HALF + idx / KC, k = idx - (idx / KC) * KC;
+        const int g = pw * QCH + idx;
+        if (g < E * KC) {
+          const int t = g / KC, k = g - (g / KC) * KC;
           const int ci = k / NF;
           double v = 0.0;
           if (qs & (1 << m)) {

@@ -18,7 +18,7 @@ if timeout 300 $CMD > $O/${TAG}_bench_short.json 2>&1; then
 fi
 CMD3="python bench.py --steps 3 --warmup 3 --ttc-steps 0 --no-e2e --no-cpu --no-others"
 if timeout 300 $CMD3 > $O/${TAG}_bench_short3.json 2>&1; then
-  timeout 1200 ncu --set full --clock-control none --import-source on -k regex:k_sweep_ws -s 2 -c 1 \
+  timeout 1200 ncu --set full --clock-control none --import-source on -k regex:^k_sweep_ws$ -s 2 -c 1 \
     -o $O/${TAG}_ws_full -f $CMD3 > $O/${TAG}_ncu_full.log 2>&1
 fi
 echo done
