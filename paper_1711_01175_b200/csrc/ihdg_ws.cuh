@@ -18,11 +18,11 @@
 
 namespace ihdg {
 
-#ifndef IHDG_WS_NCW_BIG
-#define IHDG_WS_NCW_BIG 12   // consumer warps for the large (config 5) tiles
+#ifndef IHDG_WS_LAG
+#define IHDG_WS_LAG 2   // the norm of tile i-LAG runs in iteration i (1 = lock-step per tile)
 #endif
 #ifndef IHDG_WS_PF
-#define IHDG_WS_PF 0   // L2 prefetch distance in tiles (0 = off; measured no gain on config 5)
+#define IHDG_WS_PF 2   // L2 prefetch distance in tiles (0 = off)
 #endif
 #ifdef IHDG_MEMONLY
 #define IHDG_MEMONLY_ON 1   // data-movement-only build (A/B experiment)
@@ -100,14 +100,10 @@ struct WCfg {
   static constexpr int NRT = (NV + 7) / 8;
   static constexpr int KS = KC / 4;
   static constexpr int NEG = E / 8;
-  // consumer warps (warp w runs on SMSP w % 4: a multiple of 4 keeps the
-  // per-SMSP DMMA load even) and prep warps; at most 16 warps in all keeps
-  // the 128-register cap
-  static constexpr int NCW = NRT >= 16 ? IHDG_WS_NCW_BIG : (NRT >= 8 ? 8 : 4);
+  static constexpr int NCW = NRT >= 16 ? 10 : (NRT >= 8 ? 8 : 4);  // consumer warps
   static constexpr int RTW = (NRT + NCW - 1) / NCW;
   static constexpr int UPW = (E * M + NCW - 1) / NCW;
-  static constexpr int NQW = NCW >= 12 ? 3 : 4;
-  static constexpr int QCH = ((E * KC + NQW - 1) / NQW + 31) / 32 * 32;   // q entries per prep warp
+  static constexpr int NQW = 4;                                    // prep warps
   static constexpr int NT = 32 * (NCW + NQW + 1);
   static constexpr int TILE = E * NV;
   static constexpr int HALO = 0;   // out-of-tile faces: prep warps load them into registers
@@ -120,13 +116,19 @@ struct WCfg {
   static constexpr int DUC = 8 * N1 + 3;
   static constexpr int DUE = M * DUC;
   static constexpr int DT = E * DUE;
+  // delta/partial rings: in iteration i a warp knows every warp has finished
+  // iteration i-LAG, i.e. the norms up to tile i-2 LAG, so 2 LAG slots keep
+  // every slot's readers done before it is rewritten
+  static constexpr int LAG = IHDG_WS_LAG;
+  static constexpr int NDB = 2 * LAG;
   static constexpr int OFF_D = OFF_OUT + 2 * TILE;
-  static constexpr int OFF_RED = OFF_D + 2 * DT;
-  static constexpr int N_DBL = OFF_RED + 64;
+  static constexpr int OFF_RED = OFF_D + NDB * DT;
+  static constexpr int N_DBL = OFF_RED + 32 * NDB;
   static constexpr int NBAR = 3 * NS + 4;
   static constexpr size_t BYTES = (size_t)N_DBL * sizeof(double) + NBAR * sizeof(uint64_t);
   static_assert(KC % 4 == 0 && E % 8 == 0 && E <= 32 && N1 <= 8, "ws config");
   static_assert((TILE * sizeof(double)) % 16 == 0, "tile bytes must be 16-byte multiples");
+  static_assert(E % NQW == 0, "prep warps split the tile");
 };
 
 template <int N1, int M, int NCF, int NWC, int E, int NS>
@@ -282,9 +284,11 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS>::NT, 1)
     const int per0 = a.g.periodic[0];
     const int nlay = (int)(a.g.layer_end - a.g.layer_begin);
     const int lsi = (int)ls;
-    int prev_e0 = 0, prev_nt = 0, prev_tile = -1, prev2_tile = -1;
-    constexpr int QCH = C::QCH;
-    constexpr int QM = QCH / 32;
+    int prev_e0 = 0, prev_nt = 0;
+    int hist[4] = {-1, -1, -1, -1};   // tile ids of the last iterations (it & 3)
+    static_assert(C::LAG + 1 <= 4, "tile history");
+    constexpr int HALF = E / NQW;
+    constexpr int QM = (HALF * KC + 31) / 32;
     // out-of-tile neighbour face nodes of this warp's entries, loaded from
     // global (L2) into registers one tile ahead
     double gv[QM][NWC], gvn[QM][NWC];
@@ -300,9 +304,8 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS>::NT, 1)
         const int idx = lane + 32 * m;
 #pragma unroll
         for (int j = 0; j < NWC; ++j) dst[m][j] = 0.0;
-        const int g = pw * QCH + idx;
-        if (g < E * KC) {
-          const int t = g / KC, k = g - (g / KC) * KC;
+        if (idx < HALF * KC) {
+          const int t = pw * HALF + idx / KC, k = idx - (idx / KC) * KC;
           const int f = qf_s[k];
           if (!(tg.mask(t, c0, per0) & (1 << f))) {
             const bool in_tile = (f >> 1) == 0 && !((f == 0 && t == 0) || (f == 1 && t == E - 1));
@@ -344,9 +347,8 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS>::NT, 1)
 #pragma unroll
       for (int m = 0; m < QM; ++m) {
         const int idx = lane + 32 * m;
-        const int g = pw * QCH + idx;
-        if (g < E * KC) {
-          const int t = g / KC, k = g - (g / KC) * KC;
+        if (idx < HALF * KC) {
+          const int t = pw * HALF + idx / KC, k = idx - (idx / KC) * KC;
           const int ci = k / NF;
           double v = 0.0;
           if (qs & (1 << m)) {
@@ -370,10 +372,11 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS>::NT, 1)
         if (pw == 0 && lane == 0) {
           bulk_s2g(un + (int64_t)prev_e0 * NV, out_s + pb * TILE, (uint32_t)(prev_nt * NV * sizeof(double)));
           bulk_commit();
-          if (it >= 2) {
+          const int jt = it - 1 - C::LAG;   // every warp has reduced tile jt by done(it-1)
+          if (jt >= 0) {
             double s = 0.0;
-            for (int w = 0; w < NCW; ++w) s += red_s[(it & 1) * 32 + w];   // tile it-2
-            a.tile_partials[prev2_tile] = a.jac * s;
+            for (int w = 0; w < NCW; ++w) s += red_s[(jt % C::NDB) * 32 + w];
+            a.tile_partials[hist[jt & 3]] = a.jac * s;
           }
           if (it >= 2) {
             bulk_wait_read<1>();                       // store of tile it-2 has read its buffer
@@ -381,8 +384,7 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS>::NT, 1)
           }
         }
       }
-      prev2_tile = prev_tile;
-      prev_tile = cur_tile;
+      hist[it & 3] = cur_tile;
       prev_e0 = cur_e0;
       prev_nt = nt;
       // the gathers of tile it+1 are consumed only here (a register move
@@ -401,10 +403,11 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS>::NT, 1)
       if (pw == 0 && lane == 0) {
         bulk_s2g(un + (int64_t)prev_e0 * NV, out_s + (L & 1) * TILE, (uint32_t)(prev_nt * NV * sizeof(double)));
         bulk_commit();
-        if (L >= 1) {
+        const int jt = L - C::LAG;
+        if (jt >= 0) {
           double s = 0.0;
-          for (int w = 0; w < NCW; ++w) s += red_s[((L - 1) & 1) * 32 + w];
-          a.tile_partials[prev2_tile] = a.jac * s;
+          for (int w = 0; w < NCW; ++w) s += red_s[(jt % C::NDB) * 32 + w];
+          a.tile_partials[hist[jt & 3]] = a.jac * s;
         }
         bulk_wait<0>();
       }
@@ -448,12 +451,13 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS>::NT, 1)
       const double* qst = ust + TILE + C::HALO;
       // norm of the previous tile (needs every warp's delta of tile it-1)
       double nsum = 0.0;
-      if (it >= 1) {
+      if (it >= C::LAG) {
+        const int jn = it - C::LAG;
         V3_T0(td);
-        mbar_wait(&done_bar[(it - 1) & 1], ((it - 1) >> 1) & 1);
+        mbar_wait(&done_bar[jn & 1], (jn >> 1) & 1);
         V3_ACC(8, td);
         V3_T0(tn);
-        nsum = norm_units_swz<N1, M, E, NCW, UPW, C::DUE, C::DUC>(d_s + ((it - 1) & 1) * C::DT, warp, lane, cfr,
+        nsum = norm_units_swz<N1, M, E, NCW, UPW, C::DUE, C::DUC>(d_s + (jn % C::NDB) * C::DT, warp, lane, cfr,
                                                                   a.comp_w);
         V3_ACC(7, tn);
       }
@@ -511,7 +515,7 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS>::NT, 1)
       V3_ACC(5, to);
       V3_T0(te);
       double* outb = out_s + ob * TILE;
-      double* dcur = d_s + ob * C::DT;
+      double* dcur = d_s + (it % C::NDB) * C::DT;
 #pragma unroll
       for (int eg = 0; eg < NEG; ++eg) {
         const int te = ws_elem<NEG>(lane & 3, eg, 0);
@@ -529,10 +533,10 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS>::NT, 1)
         }
       }
       V3_ACC(10, te);
-      if (it >= 1) {
+      if (it >= C::LAG) {
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) nsum += __shfl_xor_sync(0xffffffffu, nsum, o);
-        if (lane == 0) red_s[((it - 1) & 1) * 32 + warp] = nsum;
+        if (lane == 0) red_s[((it - C::LAG) % C::NDB) * 32 + warp] = nsum;
       }
       fence_proxy_async();
       __syncwarp();
@@ -541,24 +545,26 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS>::NT, 1)
         mbar_arrive(&done_bar[ob]);
       }
     }
-    // drain: norm of the last tile
-    if (n_my >= 1) {
-      const int L = n_my - 1;
-      mbar_wait(&done_bar[L & 1], (L >> 1) & 1);
-      double nsum = norm_units_swz<N1, M, E, NCW, UPW, C::DUE, C::DUC>(d_s + (L & 1) * C::DT, warp, lane, cfr,
+    // drain: norms of the last LAG tiles
+    for (int jn = n_my - C::LAG > 0 ? n_my - C::LAG : 0; jn < n_my; ++jn) {
+      mbar_wait(&done_bar[jn & 1], (jn >> 1) & 1);
+      double nsum = norm_units_swz<N1, M, E, NCW, UPW, C::DUE, C::DUC>(d_s + (jn % C::NDB) * C::DT, warp, lane, cfr,
                                                                        a.comp_w);
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) nsum += __shfl_xor_sync(0xffffffffu, nsum, o);
-      if (lane == 0) red_s[(L & 1) * 32 + warp] = nsum;
+      if (lane == 0) red_s[(jn % C::NDB) * 32 + warp] = nsum;
     }
   }
 
   __syncthreads();
-  if (tid == 0 && n_my >= 1) {
-    const int L = n_my - 1;
-    double s = 0.0;
-    for (int w = 0; w < NCW; ++w) s += red_s[(L & 1) * 32 + w];
-    a.tile_partials[blockIdx.x + L * gridDim.x] = a.jac * s;
+  if (tid == 0) {
+    // the last LAG tiles (the prep warp wrote the partials before them)
+    for (int jn = n_my - C::LAG > 0 ? n_my - C::LAG : 0; jn < n_my; ++jn) {
+      if (jn <= n_my - 1 - C::LAG) continue;
+      double s = 0.0;
+      for (int w = 0; w < NCW; ++w) s += red_s[(jn % C::NDB) * 32 + w];
+      a.tile_partials[blockIdx.x + jn * gridDim.x] = a.jac * s;
+    }
   }
 #ifdef IHDG_WS_PROF
   if (tid == 0) V3_ACC(6, tk0);
