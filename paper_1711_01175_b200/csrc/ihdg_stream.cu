@@ -108,7 +108,7 @@ struct StreamEntry {
 #define IHDG_WS2(N1, M, NCF, NWC, E, NS) \
   {2, N1, M, NCF, NWC, E, M * N1 * N1, launch_ws2_t<N1, M, NCF, NWC, E, NS>, 0},
 #ifndef IHDG_WS5_NS
-#define IHDG_WS5_NS 2   // stage count of the config-5 ring (A/B builds override it)
+#define IHDG_WS5_NS 3   // stage count of the config-5 ring (A/B builds override it)
 #endif
 #define IHDG_WS(N1, M, NCF, NWC, E, NS) \
   {2, N1, M, NCF, NWC, E, M * N1 * N1, launch_ws_t<N1, M, NCF, NWC, E, NS>, 0},

@@ -19,10 +19,10 @@
 namespace ihdg {
 
 #ifndef IHDG_WS_LAG
-#define IHDG_WS_LAG 2   // the norm of tile i-LAG runs in iteration i (1 = lock-step per tile)
+#define IHDG_WS_LAG 1   // the norm of tile i-LAG runs in iteration i (2 measured no gain)
 #endif
 #ifndef IHDG_WS_PF
-#define IHDG_WS_PF 2   // L2 prefetch distance in tiles (0 = off)
+#define IHDG_WS_PF 0   // L2 prefetch distance in tiles (0 = off; 1/2/4 measured no gain)
 #endif
 #ifdef IHDG_MEMONLY
 #define IHDG_MEMONLY_ON 1   // data-movement-only build (A/B experiment)
