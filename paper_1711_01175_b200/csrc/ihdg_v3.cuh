@@ -43,9 +43,16 @@ struct V3Cfg {
   // register prefetch of the next tile's s only when one warp per SMSP cannot
   // be covered by another consumer warp
   static constexpr bool PREF = WPS <= 2 && NCW <= 4;
-  static constexpr int TILE = E * NV;
+  // shared-memory strides, chosen bank-conflict-free (64-bit accesses, one
+  // wavefront per half-warp): the staged u^k tile is copied per element into
+  // an element stride ES with 2 ES = 4 (mod 16) double-banks when NV is even
+  // (one 16-byte-aligned bulk copy per element); q rows use KCP = 4 (mod 8).
+  static constexpr int ES = (NV % 2 == 0) ? NV + ((2 - NV % 8 + 8) % 8) : NV;
+  static constexpr int KCP = KC + ((4 - KC % 8 + 8) % 8);
+  static constexpr bool TFAST = ES != NV;   // norm lines: element index fastest
+  static constexpr int TILE = E * ES;
   static constexpr int HALO = 0;                  // out-of-tile faces: prep warps load them directly
-  static constexpr int QT = E * KC;
+  static constexpr int QT = E * KCP;
   static constexpr int STAGE = TILE + HALO + QT;  // doubles
   static constexpr int LFR = NRT * KS * 32;       // L fragments (doubles)
   static constexpr int OFF_L = NS * STAGE;
@@ -54,7 +61,9 @@ struct V3Cfg {
   static constexpr int LPL = NP / N1;             // norm lines per (element, component) and axis
   static constexpr int NLINES = E * M * LPL;
   static_assert(KC % 4 == 0, "DMMA k");
-  static_assert(E % 2 == 0 && (TILE * sizeof(double)) % 16 == 0, "bulk copy alignment");
+  static_assert(E % 2 == 0 && (E * NV * sizeof(double)) % 16 == 0, "bulk copy alignment");
+  static_assert(ES == NV || ((NV * sizeof(double)) % 16 == 0 && (ES * sizeof(double)) % 16 == 0),
+                "per-element bulk copies need 16-byte sizes and strides");
   static_assert(E % NQW == 0, "prep split");
 };
 
@@ -179,9 +188,16 @@ __global__ void __launch_bounds__(V3Cfg<D, N1, M, NCF, NWC, NS, NCW, PF, NQW_>::
       if (lane == 0) {
         STile<D> ti;
         ti.init(a.g, phys_of(it), E, nlay, lsi);
-        constexpr uint32_t bytes = (uint32_t)(TILE * sizeof(double));
+        constexpr uint32_t bytes = (uint32_t)(E * NV * sizeof(double));
         mbar_arrive_expect_tx(&full_bar[stage], bytes);
-        bulk_g2s(sm + stage * C::STAGE, uo + (int64_t)ti.e0 * NV, bytes, &full_bar[stage]);
+        if constexpr (C::ES == NV) {
+          bulk_g2s(sm + stage * C::STAGE, uo + (int64_t)ti.e0 * NV, bytes, &full_bar[stage]);
+        } else {
+#pragma unroll
+          for (int t = 0; t < E; ++t)
+            bulk_g2s(sm + stage * C::STAGE + t * C::ES, uo + (int64_t)(ti.e0 + t) * NV,
+                     (uint32_t)(NV * sizeof(double)), &full_bar[stage]);
+        }
       }
       __syncwarp();
       V3_ACC(9, tl);
@@ -274,14 +290,14 @@ __global__ void __launch_bounds__(V3Cfg<D, N1, M, NCF, NWC, NS, NCW, PF, NQW_>::
           double v = 0.0;
           if (qs & (1 << m)) {
             const int f = qf_s[k];
-            const double* src = ust + (t + (f == 0 ? -1 : 1)) * NV;
+            const double* src = ust + (t + (f == 0 ? -1 : 1)) * C::ES;
 #pragma unroll
             for (int j = 0; j < NWC; ++j) v = fma(ww_s[ci][j], src[qt_s[k][j]], v);
           } else if (ql & (1 << m)) {
 #pragma unroll
             for (int j = 0; j < NWC; ++j) v = fma(ww_s[ci][j], gv[m][j], v);
           }
-          qst[t * KC + k] = v;
+          qst[t * C::KCP + k] = v;
         }
       }
       __syncwarp();
@@ -327,7 +343,7 @@ __global__ void __launch_bounds__(V3Cfg<D, N1, M, NCF, NWC, NS, NCW, PF, NQW_>::
       V3_ACC(3, tc);
       V3_T0(tm);
       double* ust = sm + stage * C::STAGE;
-      const double* qb = ust + TILE + C::HALO + rsub * KC + (lane & 3);
+      const double* qb = ust + TILE + C::HALO + rsub * C::KCP + (lane & 3);
       if (mfast_s[stage]) {
 #pragma unroll
         for (int ks = 0; ks < KS; ++ks) {
@@ -366,7 +382,7 @@ __global__ void __launch_bounds__(V3Cfg<D, N1, M, NCF, NWC, NS, NCW, PF, NQW_>::
           for (int v = 0; v < 2; ++v) {
             const int t = te + v;
             __stcs(ug + t * NV + row, acc[rt][v]);
-            ust[t * NV + row] = acc[rt][v] - ust[t * NV + row];
+            ust[t * C::ES + row] = acc[rt][v] - ust[t * C::ES + row];
           }
         }
       }
@@ -384,10 +400,17 @@ __global__ void __launch_bounds__(V3Cfg<D, N1, M, NCF, NWC, NS, NCW, PF, NQW_>::
         for (int m = 0; m < (C::NLINES + 31) / 32; ++m) {
           const int ln = lane + 32 * m;
           if (ln < C::NLINES) {
-            const int t = ln / (M * C::LPL);
-            const int c = (ln / C::LPL) % M;
-            int rem = ln % C::LPL;
-            int base = t * NV + c * NP;
+            int t, c, rem;
+            if constexpr (C::TFAST) {
+              t = ln % E;
+              c = (ln / E) % M;
+              rem = ln / (E * M);
+            } else {
+              t = ln / (M * C::LPL);
+              c = (ln / C::LPL) % M;
+              rem = ln % C::LPL;
+            }
+            int base = t * C::ES + c * NP;
             int mb = 1;
 #pragma unroll
             for (int b = 0; b < D; ++b) {

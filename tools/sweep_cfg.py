@@ -1,0 +1,48 @@
+#!/usr/bin/env python
+"""Time N sweeps of one BASELINE config (for ncu captures and A/B runs).
+
+    python tools/sweep_cfg.py <config 1-5> [n_sweeps] [warmup]
+"""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch  # noqa: E402
+
+from paper_1711_01175_b200.solver import DeviceSolver  # noqa: E402
+from paper_1711_01175_b200.workloads import make_config  # noqa: E402
+
+
+def main():
+    cfg = int(sys.argv[1])
+    n = int(sys.argv[2]) if len(sys.argv) > 2 else 20
+    warm = int(sys.argv[3]) if len(sys.argv) > 3 else 3
+    wl = make_config(cfg)
+    sv = DeviceSolver(wl.mesh, wl.problem, wl.ops, dt=wl.dt, max_iters=100000)
+    if getattr(wl.problem, "forcing", None) is not None:
+        sv.set_forcing(wl.problem.forcing)
+    sv.zero_state()
+    for name, fld in wl.initial.items():
+        sv.set_state_component(fld, sv.spec.labels.index(name))
+    if wl.dt is not None:
+        sv.begin_step()
+    else:
+        sv.prepare_steady()
+    sv.reset_state(0.0, 100000)
+    a = sv.sweep_args("volume", 1)
+    for _ in range(warm):
+        sv.sweep_once(a=a)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record(sv.stream)
+    for _ in range(n):
+        sv.sweep_once(a=a)
+    e1.record(sv.stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / n
+    dofs = sv.nloc * sv.nv
+    print(f"config {cfg}: {ms:.4f} ms/sweep, {dofs * 24 / ms / 1e6:.1f} GB/s algorithmic, {dofs} DOFs")
+
+
+if __name__ == "__main__":
+    main()
