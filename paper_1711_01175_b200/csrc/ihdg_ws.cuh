@@ -21,9 +21,6 @@ namespace ihdg {
 #ifndef IHDG_WS_LAG
 #define IHDG_WS_LAG 1   // the norm of tile i-LAG runs in iteration i (2 measured no gain)
 #endif
-#ifndef IHDG_WS_EARLY
-#define IHDG_WS_EARLY 1   // consumer: s and u^k loads issued before the previous tile's norm
-#endif
 #ifndef IHDG_WS_PF
 #define IHDG_WS_PF 0   // L2 prefetch distance in tiles (0 = off; 1/2/4 measured no gain)
 #endif
@@ -452,34 +449,6 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS>::NT, 1)
       const double* sst = sm + stage * C::STAGE;
       const double* ust = sst + TILE;
       const double* qst = ust + TILE + C::HALO;
-#if IHDG_WS_EARLY
-      // s loads into the accumulators and the u^k values of the epilogue are
-      // issued before the norm of the previous tile, whose DMMAs hide them
-      double acc[NEG][RTW][2];
-#pragma unroll
-      for (int eg = 0; eg < NEG; ++eg) {
-        const int te = ws_elem<NEG>(lane & 3, eg, 0);
-#pragma unroll
-        for (int j = 0; j < RTW; ++j) {
-          const int row = (warp + j * NCW) * 8 + (lane >> 2);
-          const bool ok = row < NV && (warp + j * NCW) < NRT;
-          acc[eg][j][0] = ok ? sst[te * NV + row] : 0.0;
-          acc[eg][j][1] = ok ? sst[(te + 1) * NV + row] : 0.0;
-        }
-      }
-      double uo_r[NEG][RTW][2];
-#pragma unroll
-      for (int eg = 0; eg < NEG; ++eg) {
-        const int te = ws_elem<NEG>(lane & 3, eg, 0);
-#pragma unroll
-        for (int j = 0; j < RTW; ++j) {
-          const int row = (warp + j * NCW) * 8 + (lane >> 2);
-          const bool ok = row < NV && (warp + j * NCW) < NRT;
-          uo_r[eg][j][0] = ok ? ust[te * NV + row] : 0.0;
-          uo_r[eg][j][1] = ok ? ust[(te + 1) * NV + row] : 0.0;
-        }
-      }
-#endif
       // norm of the previous tile (needs every warp's delta of tile it-1)
       double nsum = 0.0;
       if (it >= C::LAG) {
@@ -493,7 +462,6 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS>::NT, 1)
         V3_ACC(7, tn);
       }
       V3_T0(tm);
-#if !IHDG_WS_EARLY
       double acc[NEG][RTW][2];
 #pragma unroll
       for (int eg = 0; eg < NEG; ++eg) {
@@ -506,7 +474,6 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS>::NT, 1)
           acc[eg][j][1] = ok ? sst[(te + 1) * NV + row] : 0.0;
         }
       }
-#endif
       const double* qb = qst + (lane >> 2) * KC + (lane & 3);
       if (fast && !IHDG_MEMONLY_ON) {
 #pragma unroll
@@ -560,11 +527,7 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS>::NT, 1)
             for (int v = 0; v < 2; ++v) {
               const int t = te + v;
               outb[t * NV + row] = acc[eg][j][v];
-#if IHDG_WS_EARLY
-              dcur[t * C::DUE + doff[j]] = acc[eg][j][v] - uo_r[eg][j][v];
-#else
               dcur[t * C::DUE + doff[j]] = acc[eg][j][v] - ust[t * NV + row];
-#endif
             }
           }
         }
