@@ -54,10 +54,11 @@
 extern "C" {
 #endif
 
-#define IHDG_ABI_VERSION 1
+#define IHDG_ABI_VERSION 2
 #define IHDG_MAX_DIM 3
 #define IHDG_MAX_COMP 4
 #define IHDG_MAX_FACE 6
+#define IHDG_CHOL_MAX 64 /* (order+1)^2 entries of the 1D mass Cholesky factor, order <= 7 */
 
 /* return codes */
 #define IHDG_OK 0
@@ -206,6 +207,8 @@ typedef struct {
   int32_t norm_kind;          /* IHDG_NORM_VOLUME / IHDG_NORM_TRACE */
   int32_t finalize;           /* 1: fused last-CTA finalize (single rank) */
   int64_t tile_offset;        /* global index of this strip's first tile */
+  double chol[IHDG_CHOL_MAX]; /* chol1d by value, row-major [N1][N1] (kernel-parameter
+                                 constants for the DFMA stopping norm) */
 } ihdg_sweep_args;
 
 /* K3 (multi-rank): reduce globally gathered tile partials, update *state. */

@@ -75,7 +75,7 @@ class SweepArgs(C.Structure):
                 ("norm_hist", _p), ("face_w", (_f64 * 4) * 6), ("comp_w", _f64 * 4),
                 ("out_w", (_f64 * 4) * 6), ("jac", _f64), ("jac_face", _f64 * 3),
                 ("coupled", _i32 * 6), ("out_face", _i32 * 6), ("norm_kind", _i32),
-                ("finalize", _i32), ("tile_offset", _i64)]
+                ("finalize", _i32), ("tile_offset", _i64), ("chol", _f64 * 64)]
 
 
 class FinalizeArgs(C.Structure):
@@ -131,7 +131,7 @@ def lib():
         fn = getattr(L, name)
         fn.restype = res
         fn.argtypes = args
-    if L.ihdg_abi_version() != 1:
+    if L.ihdg_abi_version() != 2:
         raise NativeUnavailable("libihdg_cuda.so ABI version mismatch")
     for i, st in enumerate(_STRUCTS):
         if L.ihdg_struct_size(i) != C.sizeof(st):

@@ -255,6 +255,10 @@ class DeviceSolver:
         a.g = self.geom
         a.s, a.LT = _ptr(self.s), _ptr(self.LT)
         a.class_of_mask, a.chol1d = _ptr(self.class_of_mask), _ptr(self.chol)
+        ch = np.ascontiguousarray(self.ops.chol1d, dtype=np.float64).ravel()
+        if ch.size <= 64:
+            for i, v in enumerate(ch):
+                a.chol[i] = float(v)
         a.tile_partials, a.state, a.norm_hist = _ptr(self.partials), _ptr(self.state_dev), _ptr(self.norm_hist)
         for f in range(6):
             for c in range(4):

@@ -179,3 +179,17 @@ def test_config4_full_size_layer_count():
     r2 = run(wl.mesh, wl.problem, wl.ops, IterationConfig(), return_trace=False)
     assert r1.iterations == r2.iterations < 191
     assert np.array_equal(r1.state.data, r2.state.data)
+
+
+@pytest.mark.parametrize("impl", ["ws3", "ws2", "ws", "generic"])
+def test_sweep_impl_parity(impl):
+    """Every selectable sweep kernel (IHDG_SWEEP_IMPL) on config 5 reduced."""
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, IHDG_SWEEP_IMPL=impl)
+    r = subprocess.run([sys.executable, os.path.join(root, "tests", "_impl_child.py"), "1e-1"], env=env,
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout + r.stderr

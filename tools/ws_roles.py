@@ -17,8 +17,8 @@ from paper_1711_01175_b200.workloads import make_config  # noqa: E402
 NAMES = ["producer: wait (empty/done)", "prep: wait full", "prep: q compute", "consumer: wait qready",
          "consumer: contraction", "consumer: epilogue / wait outfree (ws)", "CTA total",
          "consumer: norm", "consumer: wait done prev (ws)", "producer: load issue",
-         "consumer: epilogue stores (ws)", "consumer: norm reduce (ws)", "consumer: fence.proxy.async (ws)",
-         "consumer: whole iteration (ws)"]
+         "consumer: epilogue stores (ws)", "prep: gather issue (ws)", "prep: wait done (ws)",
+         "prep: gather consume (ws)"]
 
 
 def main():
