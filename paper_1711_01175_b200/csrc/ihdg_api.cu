@@ -1,5 +1,7 @@
 // extern "C" entry points of libihdg_cuda.so (declared in include/ihdg.h).
 #include <cstdio>
+#include <cstdlib>
+#include <cstring>
 #include <string>
 
 #include "ihdg_kernels.cuh"
@@ -288,6 +290,66 @@ int ihdg_copy_state(const ihdg_geom* g, const double* src, double* dst, void* st
   return IHDG_OK;
 }
 
+// A batch of sweeps as one CUDA graph (launch-bound small meshes): captured
+// once per (args, buffers, batch, stream) and replayed; an even batch keeps
+// the buffer parity of every replay at buf0 -> buf1.
+struct SweepGraph {
+  ihdg_sweep_args a;
+  double* b0 = nullptr;
+  double* b1 = nullptr;
+  int nb = 0;
+  cudaStream_t st = nullptr;
+  cudaGraphExec_t exec = nullptr;
+};
+
+static bool graphs_enabled() {
+  static int on = -1;
+  if (on < 0) {
+    const char* s = std::getenv("IHDG_NO_GRAPH");
+    on = (s != nullptr && s[0] != '\0' && s[0] != '0') ? 0 : 1;
+  }
+  return on == 1;
+}
+
+static cudaGraphExec_t sweep_graph(const Entry* e, const ihdg_sweep_args& a, double* b0, double* b1, int nb,
+                                   cudaStream_t st) {
+  static thread_local SweepGraph cache;
+  if (cache.exec != nullptr && cache.b0 == b0 && cache.b1 == b1 && cache.nb == nb && cache.st == st &&
+      std::memcmp(&cache.a, &a, sizeof(a)) == 0)
+    return cache.exec;
+  if (cache.exec != nullptr) {
+    cudaGraphExecDestroy(cache.exec);
+    cache.exec = nullptr;
+  }
+  if (cudaStreamBeginCapture(st, cudaStreamCaptureModeRelaxed) != cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  ihdg_sweep_args s = a;
+  bool ok = true;
+  for (int j = 0; j < nb && ok; ++j) {
+    s.u_old = (j & 1) ? b1 : b0;
+    s.u_new = (j & 1) ? b0 : b1;
+    ok = do_sweep(e, &s, st) == IHDG_OK;
+  }
+  cudaGraph_t g = nullptr;
+  const cudaError_t ce = cudaStreamEndCapture(st, &g);
+  cudaGraphExec_t ex = nullptr;
+  if (ok && ce == cudaSuccess && g != nullptr && cudaGraphInstantiate(&ex, g, 0) == cudaSuccess) {
+    cache.a = a;
+    cache.b0 = b0;
+    cache.b1 = b1;
+    cache.nb = nb;
+    cache.st = st;
+    cache.exec = ex;
+  } else {
+    ex = nullptr;
+  }
+  if (g != nullptr) cudaGraphDestroy(g);
+  cudaGetLastError();
+  return ex;
+}
+
 int ihdg_iterate(const ihdg_sweep_args* a0, double* buf0, double* buf1, int32_t batch, void* stream,
                  ihdg_iter_state* state_out, int64_t* n_launched) {
   if (a0 == nullptr || buf0 == nullptr || buf1 == nullptr || state_out == nullptr)
@@ -300,18 +362,41 @@ int ihdg_iterate(const ihdg_sweep_args* a0, double* buf0, double* buf1, int32_t 
   static thread_local ihdg_iter_state* hs = nullptr;
   if (hs == nullptr) IHDG_CUDA_TRY(cudaMallocHost((void**)&hs, sizeof(ihdg_iter_state)));
   cudaStream_t st = (cudaStream_t)stream;
+  if (graphs_enabled() && (st == nullptr || st == cudaStreamLegacy || st == cudaStreamPerThread)) {
+    // the default stream cannot be captured: run the loop on a private
+    // stream ordered after the caller's work (the call is synchronous)
+    static thread_local cudaStream_t own = nullptr;
+    static thread_local cudaEvent_t ev = nullptr;
+    if (own == nullptr) {
+      IHDG_CUDA_TRY(cudaStreamCreateWithFlags(&own, cudaStreamNonBlocking));
+      IHDG_CUDA_TRY(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    }
+    IHDG_CUDA_TRY(cudaEventRecord(ev, st));
+    IHDG_CUDA_TRY(cudaStreamWaitEvent(own, ev, 0));
+    st = own;
+  }
   ihdg_sweep_args a = *a0;
   a.finalize = 1;
+  a.u_old = a.u_new = nullptr;
   int64_t launched = 0;
+  // sweeps after the stop are no-ops on the device, so a batch rounded up to
+  // an even count changes nothing but the launch count
+  const int nb = batch + (batch & 1);
+  cudaGraphExec_t ex = graphs_enabled() ? sweep_graph(e, a, buf0, buf1, nb, st) : nullptr;
   for (;;) {
-    for (int j = 0; j < batch; ++j) {
-      a.u_old = (launched & 1) ? buf1 : buf0;
-      a.u_new = (launched & 1) ? buf0 : buf1;
-      rc = do_sweep(e, &a, st);
-      if (rc) return rc;
-      ++launched;
+    if (ex != nullptr) {
+      IHDG_CUDA_TRY(cudaGraphLaunch(ex, st));
+      launched += nb;
+    } else {
+      for (int j = 0; j < batch; ++j) {
+        a.u_old = (launched & 1) ? buf1 : buf0;
+        a.u_new = (launched & 1) ? buf0 : buf1;
+        rc = do_sweep(e, &a, st);
+        if (rc) return rc;
+        ++launched;
+      }
     }
-    IHDG_CUDA_TRY(cudaMemcpyAsync(hs, a.state, sizeof(ihdg_iter_state), cudaMemcpyDeviceToHost, st));
+    IHDG_CUDA_TRY(cudaMemcpyAsync(hs, a0->state, sizeof(ihdg_iter_state), cudaMemcpyDeviceToHost, st));
     IHDG_CUDA_TRY(cudaStreamSynchronize(st));
     if (hs->status != IHDG_RUNNING) break;
   }

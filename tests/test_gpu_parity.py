@@ -181,15 +181,16 @@ def test_config4_full_size_layer_count():
     assert np.array_equal(r1.state.data, r2.state.data)
 
 
-@pytest.mark.parametrize("impl", ["ws3", "ws2", "ws", "generic"])
+@pytest.mark.parametrize("impl", ["ws3", "ws2", "ws", "generic", "nograph"])
 def test_sweep_impl_parity(impl):
-    """Every selectable sweep kernel (IHDG_SWEEP_IMPL) on config 5 reduced."""
+    """Every selectable sweep kernel (IHDG_SWEEP_IMPL) on config 5 reduced,
+    and the stream-launched (not graph-replayed) iterate loop."""
     import os
     import subprocess
     import sys
 
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    env = dict(os.environ, IHDG_SWEEP_IMPL=impl)
+    env = dict(os.environ, IHDG_NO_GRAPH="1") if impl == "nograph" else dict(os.environ, IHDG_SWEEP_IMPL=impl)
     r = subprocess.run([sys.executable, os.path.join(root, "tests", "_impl_child.py"), "1e-1"], env=env,
                        capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout + r.stderr
