@@ -76,6 +76,8 @@ extern "C" {
 
 /* stopping norms */
 #define IHDG_NORM_VOLUME 0 /* ||u^k - u^{k-1}||_{L2(Omega)} */
+#define IHDG_SCHEME_II 0   /* iHDG-II: own iterate k+1 in the trace */
+#define IHDG_SCHEME_I 1    /* iHDG-I: all-iterate-k trace */
 #define IHDG_NORM_TRACE 1  /* skeleton L2 norm of the trace update */
 
 /* Structured-mesh geometry of one rank's strip (mesh.py:33-77).  Elements are
@@ -209,6 +211,11 @@ typedef struct {
   int64_t tile_offset;        /* global index of this strip's first tile */
   double chol[IHDG_CHOL_MAX]; /* chol1d by value, row-major [N1][N1] (kernel-parameter
                                  constants for the DFMA stopping norm) */
+  double own_w[IHDG_MAX_FACE][IHDG_MAX_COMP]; /* iHDG-I: q[K][f][n] += sum_c own_w[f][c] *
+                                 u_old[K][c][face f node n] on every face, boundary or not
+                                 (all-iterate-k trace); zero for iHDG-II */
+  int32_t scheme;             /* IHDG_SCHEME_II / IHDG_SCHEME_I */
+  int32_t pad1;
 } ihdg_sweep_args;
 
 /* K3 (multi-rank): reduce globally gathered tile partials, update *state. */

@@ -239,9 +239,16 @@ def _blocks(m, npn):
     return [slice(c * npn, (c + 1) * npn) for c in range(m)]
 
 
-def local_operators(prob: OracleProblem, el: _Element, mask: int, dt=None):
+def local_operators(prob: OracleProblem, el: _Element, mask: int, dt=None, scheme: str = "II"):
     """A (own, LHS), N[f] (neighbour iterate-k -> RHS), R (time level -> RHS),
-    H_own[f], H_nbr[f] (trace at face NODES as maps of own / neighbour state)."""
+    H_own[f], H_nbr[f] (trace at face NODES as maps of own / neighbour state),
+    Own (own iterate-k -> RHS; zero for iHDG-II).
+
+    scheme "II": the trace u_hat^{k,k+1} takes the element's own iterate k+1
+    (PAPER.md:320-337, iHDGtrace).  scheme "I" (iHDG-I, PAPER.md:272-279,
+    SPEC.md:249, 295): the all-iterate-k trace u_hat^k, i.e. the own part T
+    of every u_hat term moves from the LHS to the RHS at iterate k:
+    A_I = A_II - T, Own = -T."""
     d, npn, m = el.d, el.np, prob.m
     nv = m * npn
     sl = _blocks(m, npn)
@@ -252,6 +259,7 @@ def local_operators(prob: OracleProblem, el: _Element, mask: int, dt=None):
     Hnbr = [np.zeros((el.n1 ** (d - 1), nv)) for _ in range(2 * d)]
     inv_dt = 0.0 if dt is None else 1.0 / dt
     R = np.zeros((nv, nv))
+    T = np.zeros((nv, nv))   # own-iterate part of the u_hat terms in A
 
     def fl(f):  # opposite face of the neighbour
         return f ^ 1
@@ -273,6 +281,7 @@ def local_operators(prob: OracleProblem, el: _Element, mask: int, dt=None):
             # 2|bn| u_hat = (bn+|bn|) u^- + (|bn|-bn) u^+ (transportLocale)
             if not boundary:
                 A += el.fmass(f, P, (bn + ab - 0.5 * (bn + ab)) * P)
+                T -= 0.5 * (bn + ab) * el.fmass(f, P, P)
                 Nf[f] += 0.5 * (ab - bn) * el.fmass(f, P, Pn)
                 if ab > 0:
                     Hown[f] = (bn + ab) / (2 * ab) * el.Pn[f]
@@ -284,6 +293,7 @@ def local_operators(prob: OracleProblem, el: _Element, mask: int, dt=None):
                 pass
             else:          # outflow boundary: u_hat = u^-
                 A += el.fmass(f, P, bn * P)
+                T -= bn * el.fmass(f, P, P)
                 Hown[f] = el.Pn[f]
     elif prob.kind == "cd":
         beta = prob.beta
@@ -318,6 +328,7 @@ def local_operators(prob: OracleProblem, el: _Element, mask: int, dt=None):
                 Hnbr[f][:, sl[U]] = (-bn + tp) / alpha * el.Pn[fl(f)]
             # sigma_a rows: + <u_hat n_a, w>
             A[sl[a], :] += sgn * el.fmass(f, P, Ho)
+            T[sl[a], :] += sgn * el.fmass(f, P, Ho)
             Nf[f][sl[a], :] -= sgn * el.fmass(f, P, Hn)
             # u rows: <bn u + s.n + tau (u - u_hat), v>
             own = np.zeros((P.shape[0], nv))
@@ -325,6 +336,7 @@ def local_operators(prob: OracleProblem, el: _Element, mask: int, dt=None):
             own[:, sl[a]] += sgn * P
             own -= tm * Ho
             A[sl[U], :] += el.fmass(f, P, own)
+            T[sl[U], :] -= tm * el.fmass(f, P, Ho)
             Nf[f][sl[U], :] += tm * el.fmass(f, P, Hn)
     elif prob.kind == "sw":
         if d != 2:
@@ -368,13 +380,19 @@ def local_operators(prob: OracleProblem, el: _Element, mask: int, dt=None):
             own[:, sl[0]] += sP * P
             own -= sP * Ho
             A[sl[0], :] += el.fmass(f, P, own)
+            T[sl[0], :] -= sP * el.fmass(f, P, Ho)
             Nf[f][sl[0], :] += sP * el.fmass(f, P, Hn)
             # theta_a rows: <Phi phi_hat n_a, phi2>
             A[sl[th], :] += Phi * sgn * el.fmass(f, P, Ho)
+            T[sl[th], :] += Phi * sgn * el.fmass(f, P, Ho)
             Nf[f][sl[th], :] -= Phi * sgn * el.fmass(f, P, Hn)
     else:
         raise ValueError(prob.kind)
-    return A, Nf, R, Hown, Hnbr
+    if scheme == "I":
+        return A - T, Nf, R, Hown, Hnbr, -T
+    if scheme != "II":
+        raise ValueError(scheme)
+    return A, Nf, R, Hown, Hnbr, np.zeros((nv, nv))
 
 
 # --------------------------------------------------------------------------
@@ -414,9 +432,10 @@ def _p(a):
 class OracleSolver:
     """Factor-once local systems + the iHDG-II iteration on the CPU."""
 
-    def __init__(self, prob: OracleProblem, cells, p: int, box=None, periodic=None, dt=None):
+    def __init__(self, prob: OracleProblem, cells, p: int, box=None, periodic=None, dt=None,
+                 scheme: str = "II"):
         d = prob.dim
-        self.prob, self.p, self.dt = prob, p, dt
+        self.prob, self.p, self.dt, self.scheme = prob, p, dt, scheme
         self.cells = [int(c) for c in cells]
         self.periodic = [False] * d if periodic is None else [bool(x) for x in periodic]
         lo = np.zeros(d) if box is None else np.asarray(box[0], float)
@@ -439,14 +458,15 @@ class OracleSolver:
             # except through inflow/outflow, which is the same on every element
             pass
         for ci, mk in enumerate(masks):
-            A, Nf, R, Ho, Hn = local_operators(prob, self.el, mk if prob.kind != "transport" else 0, dt)
+            A, Nf, R, Ho, Hn, Own = local_operators(prob, self.el, mk if prob.kind != "transport" else 0, dt,
+                                                    scheme)
             lu, piv = sla.lu_factor(A)
-            self.classes[mk] = dict(idx=ci, A=A, N=Nf, R=R, lu=lu, piv=piv, Hown=Ho, Hnbr=Hn)
+            self.classes[mk] = dict(idx=ci, A=A, N=Nf, R=R, lu=lu, piv=piv, Hown=Ho, Hnbr=Hn, Own=Own)
         if prob.kind == "transport":
             self.cls[:] = 0
             self.class_list = [self.classes[0]]
             # boundary handling for transport uses the per-face masks (inflow u_ext = g = 0)
-            _, _, _, Hob, _ = local_operators(prob, self.el, (1 << (2 * d)) - 1, dt)
+            _, _, _, Hob, _, _ = local_operators(prob, self.el, (1 << (2 * d)) - 1, dt)
             self._transport_bnd_H = Hob
         else:
             self.class_list = [self.classes[mk] for mk in masks]
@@ -495,12 +515,14 @@ class OracleSolver:
         return rhs
 
     def sweep(self, u_old, rhs):
-        """One iHDG-II sweep: u^{k+1}_K = A_K^-1 (rhs_K + sum_f N_f u^k_nbr(f))."""
+        """One sweep: u^{k+1}_K = A_K^-1 (rhs_K + sum_f N_f u^k_nbr(f) [+ Own u^k_K, iHDG-I])."""
         d = self.prob.dim
         u_new = np.empty_like(u_old)
         for ci, C in enumerate(self.class_list):
             sel = np.nonzero(self.cls == ci)[0]
             r = rhs[sel].copy()
+            if self.scheme == "I":
+                r += u_old[sel] @ C["Own"].T
             for f in range(2 * d):
                 nb = self.nbr[sel, f]
                 ok = nb != BOUNDARY

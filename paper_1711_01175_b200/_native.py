@@ -21,6 +21,7 @@ RUNNING, CONVERGED, DIVERGED, NAN, MAXITER = 0, 1, 2, 3, 4
 STATUS_NAMES = {RUNNING: "running", CONVERGED: "converged", DIVERGED: "diverged",
                 NAN: "diverged", MAXITER: "max-iter"}
 NORM_VOLUME, NORM_TRACE = 0, 1
+SCHEME_II, SCHEME_I = 0, 1
 
 _p = C.c_void_p
 _i32 = C.c_int32
@@ -75,7 +76,8 @@ class SweepArgs(C.Structure):
                 ("norm_hist", _p), ("face_w", (_f64 * 4) * 6), ("comp_w", _f64 * 4),
                 ("out_w", (_f64 * 4) * 6), ("jac", _f64), ("jac_face", _f64 * 3),
                 ("coupled", _i32 * 6), ("out_face", _i32 * 6), ("norm_kind", _i32),
-                ("finalize", _i32), ("tile_offset", _i64), ("chol", _f64 * 64)]
+                ("finalize", _i32), ("tile_offset", _i64), ("chol", _f64 * 64),
+                ("own_w", (_f64 * 4) * 6), ("scheme", _i32), ("pad1", _i32)]
 
 
 class FinalizeArgs(C.Structure):

@@ -38,6 +38,19 @@ shallow water, unknowns (phi, u, v),
     wall face (mirror state): phi_hat = phi + sqrt(Phi) theta.n
                     (th_a,phi) += Phi sgn Mf      (th_a,th_a) += Phi sqrt(Phi) Mf
     Coriolis f and friction gamma implicit.
+
+iHDG-I (scheme="iHDG-I"): the trace is
+the all-iterate-k u_hat^k, so the own part of every u_hat term leaves A and
+enters the RHS at iterate k.  The element's own face scalar has the same
+form as the neighbour's (q_own above), so face f couples through ONE scalar
+per face node, q_f = q_nbr + q_own (own_w = the q_own weights), with the same
+B column as iHDG-II:
+    transport: outflow faces A (beta.n) -> 2 beta.n, B_f = beta.n Bf, q = u_own
+    CD interior: A loses the 1/alpha terms: (s_a,s_a) 0, (s_a,u) 0,
+                 (u,s_a) sgn, (u,u) beta.n + tau;  Dirichlet faces unchanged
+    SW interior: (phi,phi) sqrt(Phi), (phi,th_a) Phi sgn, (th_a, .) 0
+       wall:     (phi,phi) sqrt(Phi), (phi,th_a) Phi sgn,
+                 B: phi row sqrt(Phi) Bf, th_a row -Phi sgn Bf  (q = q_own)
 """
 
 from __future__ import annotations
@@ -80,12 +93,14 @@ class OperatorSpec:
     coupled: np.ndarray         # (6,) int32
     out_face: np.ndarray        # (6,) int32 (trace norm faces)
     out_w: np.ndarray           # (6, 4)
+    own_w: np.ndarray           # (6, 4) iHDG-I own face-scalar weights (0 for iHDG-II)
     comp_w: np.ndarray          # (4,)
     trace_w: dict               # int_own, int_nbr, lo, hi : (3, 4)
     jac: float
     jac_face: np.ndarray        # (3,)
     periodic: tuple
     boundary_rhs: list = field(default_factory=list)
+    scheme: str = "iHDG-II"
 
     @property
     def n1(self):
@@ -159,7 +174,13 @@ def _class_masks(mesh) -> list[int]:
     return sorted(set(masks))
 
 
-def build_spec(mesh, problem, ops: ElementOperators, dt=None, norm="auto") -> OperatorSpec:
+SCHEMES = ("iHDG-II", "iHDG-I")
+
+
+def build_spec(mesh, problem, ops: ElementOperators, dt=None, norm="auto", scheme: str = "iHDG-II") -> OperatorSpec:
+    if scheme not in SCHEMES:
+        raise ValueError(f"unknown scheme {scheme!r}")
+    one = scheme == "iHDG-I"
     d = mesh.dim
     if ops.dim != d:
         raise ValueError("ops.dim != mesh.dim")
@@ -176,6 +197,7 @@ def build_spec(mesh, problem, ops: ElementOperators, dt=None, norm="auto") -> Op
     coupled = np.zeros(6, dtype=np.int32)
     out_face = np.zeros(6, dtype=np.int32)
     out_w = np.zeros((6, 4))
+    own_w = np.zeros((6, 4))
     comp_w = np.zeros(4)
     tw = {k: np.zeros((3, 4)) for k in ("int_own", "int_nbr", "lo", "hi")}
     inv_dt = 0.0 if dt is None else 1.0 / float(dt)
@@ -202,9 +224,13 @@ def build_spec(mesh, problem, ops: ElementOperators, dt=None, norm="auto") -> Op
             sgn = 1.0 if s else -1.0
             bn = beta[a] * sgn
             if bn > 0:
-                terms.vol(cls, A_T, 0, 0, bn * Jf[a], axis=a, op=E(s))
+                terms.vol(cls, A_T, 0, 0, (2.0 if one else 1.0) * bn * Jf[a], axis=a, op=E(s))
                 out_face[f] = 1
                 out_w[f, 0] = 1.0
+                if one:
+                    terms.vol(cls, B_T, 0, f, bn * Jf[a], axis=a, op=Cc(s))
+                    coupled[f] = 1
+                    own_w[f, 0] = 1.0
             elif bn < 0:
                 terms.vol(cls, B_T, 0, f, -bn * Jf[a], axis=a, op=Cc(s))
                 coupled[f] = 1
@@ -256,6 +282,11 @@ def build_spec(mesh, problem, ops: ElementOperators, dt=None, norm="auto") -> Op
                 if mk & (1 << f):
                     terms.vol(ci, A_T, U, a, sgn * Jf[a], axis=a, op=E(s))
                     terms.vol(ci, A_T, U, U, (bn + tau) * Jf[a], axis=a, op=E(s))
+                elif one:
+                    terms.vol(ci, A_T, U, a, sgn * Jf[a], axis=a, op=E(s))
+                    terms.vol(ci, A_T, U, U, (bn + tau) * Jf[a], axis=a, op=E(s))
+                    terms.vol(ci, B_T, a, f, -sgn / alpha * Jf[a], axis=a, op=Cc(s))
+                    terms.vol(ci, B_T, U, f, tau / alpha * Jf[a], axis=a, op=Cc(s))
                 else:
                     terms.vol(ci, A_T, a, a, Jf[a] / alpha, axis=a, op=E(s))
                     terms.vol(ci, A_T, a, U, sgn * cp / alpha * Jf[a], axis=a, op=E(s))
@@ -273,6 +304,9 @@ def build_spec(mesh, problem, ops: ElementOperators, dt=None, norm="auto") -> Op
             face_w[f, a] = -sgn
             face_w[f, U] = 0.5 * (alpha - bn)
             coupled[f] = 1
+            if one:
+                own_w[f, a] = sgn
+                own_w[f, U] = 0.5 * (alpha + bn)
         for a in range(d):
             alpha = np.sqrt(beta[a] ** 2 + 4.0)
             tw["int_own"][a, a] = 1.0 / alpha
@@ -313,7 +347,13 @@ def build_spec(mesh, problem, ops: ElementOperators, dt=None, norm="auto") -> Op
                 a, s = divmod(f, 2)
                 sgn = 1.0 if s else -1.0
                 th = 1 + a
-                if mk & (1 << f):  # reflective wall
+                if one:
+                    terms.vol(ci, A_T, 0, 0, sP * Jf[a], axis=a, op=E(s))
+                    terms.vol(ci, A_T, 0, th, P * sgn * Jf[a], axis=a, op=E(s))
+                    w = 1.0 if mk & (1 << f) else 0.5   # wall: phi_hat^k = q_own
+                    terms.vol(ci, B_T, 0, f, w * sP * Jf[a], axis=a, op=Cc(s))
+                    terms.vol(ci, B_T, th, f, -w * P * sgn * Jf[a], axis=a, op=Cc(s))
+                elif mk & (1 << f):  # reflective wall
                     terms.vol(ci, A_T, th, 0, P * sgn * Jf[a], axis=a, op=E(s))
                     terms.vol(ci, A_T, th, th, P * sP * Jf[a], axis=a, op=E(s))
                 else:
@@ -332,6 +372,9 @@ def build_spec(mesh, problem, ops: ElementOperators, dt=None, norm="auto") -> Op
             face_w[f, 0] = 1.0
             face_w[f, 1 + a] = -sP * sgn
             coupled[f] = 1
+            if one:
+                own_w[f, 0] = 1.0
+                own_w[f, 1 + a] = sP * sgn
         for a in range(2):
             tw["int_own"][a, 0] = 0.5
             tw["int_own"][a, 1 + a] = 0.5 * sP
@@ -354,8 +397,8 @@ def build_spec(mesh, problem, ops: ElementOperators, dt=None, norm="auto") -> Op
         class_masks=list(masks), class_of_mask=class_of_mask, ops1d=T, op_ncols=ncols,
         terms=terms_arr, coefs=np.asarray(terms.coefs, dtype=float), nr=nr,
         time_comp0=tc0, n_time_comp=ntc, forcing_comp=fcomp, face_w=face_w, coupled=coupled,
-        out_face=out_face, out_w=out_w, comp_w=comp_w, trace_w=tw, jac=J, jac_face=jac_face,
-        periodic=tuple(mesh.periodic))
+        out_face=out_face, out_w=out_w, own_w=own_w, comp_w=comp_w, trace_w=tw, jac=J, jac_face=jac_face,
+        periodic=tuple(mesh.periodic), scheme=scheme)
 
 
 def evaluate_terms(spec: OperatorSpec):
@@ -407,6 +450,21 @@ def face_node_indices(dim: int, n1: int, f: int) -> np.ndarray:
             mul *= n1
         out.append(v)
     return np.array(out, dtype=np.int64)
+
+
+def own_coupling(spec: OperatorSpec, B: np.ndarray, mask: int) -> np.ndarray:
+    """(NV x NV) map own iterate-k volume state -> RHS (iHDG-I): sum over faces
+    of B[:, face block f] @ (q_own extraction with own_w from the own face f).
+    Host mirror of the own-face part of the gather in k_sweep (tests only)."""
+    npn, nv, nf = spec.n_nodes, spec.nv, spec.n1 ** (spec.dim - 1)
+    out = np.zeros((nv, nv))
+    for f in range(2 * spec.dim):
+        W = np.zeros((nf, nv))
+        idx = face_node_indices(spec.dim, spec.n1, f)
+        for c in range(spec.ncomp):
+            W[np.arange(nf), c * npn + idx] = spec.own_w[f, c]
+        out += B[:, f * nf:(f + 1) * nf] @ W
+    return out
 
 
 def neighbor_coupling(spec: OperatorSpec, B: np.ndarray, f: int) -> np.ndarray:

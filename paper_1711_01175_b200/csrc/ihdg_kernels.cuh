@@ -140,6 +140,12 @@ __global__ void __launch_bounds__(Cfg<D, N1, M>::NT)
 #pragma unroll
           for (int c = 0; c < M; ++c) v = fma(a.face_w[f][c], __ldg(p + c * NP), v);
         }
+        if (a.scheme == IHDG_SCHEME_I) {
+          // iHDG-I: the element's own iterate-k face scalar joins the trace
+          const double* po = uo + (e0 + t) * NV + fv_s[f][n];
+#pragma unroll
+          for (int c = 0; c < M; ++c) v = fma(a.own_w[f][c], __ldg(po + c * NP), v);
+        }
       }
       q_s[i] = v;
     }

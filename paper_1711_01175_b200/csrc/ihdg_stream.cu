@@ -178,6 +178,7 @@ const StreamEntry* stream_entry(const ihdg_sweep_args* a) {
     want_ws3 = (s != nullptr && std::strcmp(s, "ws3") == 0) ? 1 : 0;
   }
   if (a->norm_kind != IHDG_NORM_VOLUME) return nullptr;
+  if (a->scheme != IHDG_SCHEME_II) return nullptr;   // iHDG-I: generic kernel
   const ihdg_geom& g = a->g;
   int ncf = 0, maxw = 0;
   for (int f = 0; f < 2 * g.dim; ++f) {

@@ -43,8 +43,8 @@ class IterationConfig:
             raise ValueError("tolerance must be > 0")
         if self.max_iters is not None and self.max_iters < 1:
             raise ValueError("max_iters must be >= 1")
-        if self.scheme not in ("iHDG-II",):
-            raise NotImplementedError(f"scheme {self.scheme!r}: only iHDG-II is on the device path")
+        if self.scheme not in ("iHDG-II", "iHDG-I"):
+            raise ValueError(f"unknown scheme {self.scheme!r} (iHDG-I or iHDG-II)")
         if self.stop not in ("successive", "trace"):
             raise NotImplementedError(f"stopping rule {self.stop!r} not on the device path")
 
@@ -98,12 +98,13 @@ def _set_initial(solver: DeviceSolver, init):
 def run(mesh, problem, ops: ElementOperators, cfg: Optional[IterationConfig] = None,
         solver: Optional[DeviceSolver] = None, return_state: bool = True,
         return_trace: bool = True) -> IterationReport:
-    """Steady iHDG-II solve (Algorithm 1)."""
+    """Steady solve (Algorithm 1); cfg.scheme selects
+    iHDG-II (default) or iHDG-I (all-iterate-k trace)."""
     cfg = cfg or IterationConfig()
     t0 = time.perf_counter()
     if solver is None:
         solver = DeviceSolver(mesh, problem, ops, dt=None,
-                              max_iters=cfg.max_iters or default_max_iters(mesh))
+                              max_iters=cfg.max_iters or default_max_iters(mesh), scheme=cfg.scheme)
     forcing = getattr(problem, "forcing", None)
     if forcing is not None and solver.s_static is None:
         solver.set_forcing(forcing)
@@ -132,7 +133,7 @@ def run_time_dependent(mesh, problem, ops: ElementOperators, cfg: Optional[Itera
         n_steps = int(round(T / dt))
     if solver is None:
         solver = DeviceSolver(mesh, problem, ops, dt=dt,
-                              max_iters=cfg.max_iters or default_max_iters(mesh))
+                              max_iters=cfg.max_iters or default_max_iters(mesh), scheme=cfg.scheme)
     forcing = getattr(problem, "forcing", None)
     if forcing is not None and solver.s_static is None:
         solver.set_forcing(forcing)

@@ -57,13 +57,14 @@ class DeviceSolver:
     """
 
     def __init__(self, mesh, problem, ops: ElementOperators, dt=None, layers=None,
-                 device=None, max_iters: int = 100000, spec: Optional[OperatorSpec] = None):
+                 device=None, max_iters: int = 100000, spec: Optional[OperatorSpec] = None,
+                 scheme: str = "iHDG-II"):
         torch = _torch()
         L = N.lib()
         self.torch = torch
         self.L = L
         self.mesh, self.problem, self.ops, self.dt = mesh, problem, ops, dt
-        self.spec = spec if spec is not None else build_spec(mesh, problem, ops, dt)
+        self.spec = spec if spec is not None else build_spec(mesh, problem, ops, dt, scheme=scheme)
         sp = self.spec
         d = mesh.dim
         if not L.ihdg_supported(d, ops.p, sp.ncomp):
@@ -265,6 +266,8 @@ class DeviceSolver:
                 a.face_w[f][c] = float(sp.face_w[f, c])
                 a.out_w[f][c] = float(sp.out_w[f, c])
             a.coupled[f] = int(sp.coupled[f])
+            for c in range(4):
+                a.own_w[f][c] = float(sp.own_w[f, c])
             a.out_face[f] = int(sp.out_face[f])
         for c in range(4):
             a.comp_w[c] = float(sp.comp_w[c])
@@ -274,6 +277,7 @@ class DeviceSolver:
         a.norm_kind = N.NORM_TRACE if norm == "trace" else N.NORM_VOLUME
         a.finalize = finalize
         a.tile_offset = 0
+        a.scheme = N.SCHEME_I if sp.scheme == "iHDG-I" else N.SCHEME_II
         return a
 
     def reset_state(self, tol: float, max_iters: int, diverge_factor: float = 1e6) -> None:

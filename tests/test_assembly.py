@@ -5,7 +5,7 @@ import numpy as np
 import pytest
 
 from oracle.ihdg_oracle import OracleSolver
-from paper_1711_01175_b200.assembly import build_spec, evaluate_terms, neighbor_coupling
+from paper_1711_01175_b200.assembly import build_spec, evaluate_terms, neighbor_coupling, own_coupling
 from paper_1711_01175_b200.basis import build_operators
 from paper_1711_01175_b200.mesh import build_mesh
 from paper_1711_01175_b200.pde import ConvectionDiffusionProblem, ShallowWaterProblem, TransportProblem
@@ -49,6 +49,27 @@ def test_local_operators_match_oracle(name, dim, cells, p, prob, dt, periodic):
             assert np.max(np.abs(R[ci][:, : spec.nr] - C["R"][:, cols])) <= 1e-12 * scale
     # lifted form L = A^-1 B is well defined (factor once)
     for ci in range(spec.n_class):
+        assert np.isfinite(np.linalg.cond(A[ci]))
+
+
+@pytest.mark.parametrize("name,dim,cells,p,prob,dt,periodic", CASES, ids=[c[0] for c in CASES])
+def test_ihdg1_operators_match_oracle(name, dim, cells, p, prob, dt, periodic):
+    """iHDG-I (all-iterate-k trace): A_I, neighbour and own
+    couplings from the term lists vs the oracle's A - T and Own = -T."""
+    mesh = build_mesh(dim, cells, periodic=periodic)
+    ops = build_operators(p, dim, mesh.h)
+    spec = build_spec(mesh, prob, ops, dt, scheme="iHDG-I")
+    A, B, R = evaluate_terms(spec)
+    S = OracleSolver(oracle_problem(prob, dim), cells, p, periodic=[periodic] * dim, dt=dt, scheme="I")
+    for ci, mk in enumerate(spec.class_masks):
+        C = S.classes[mk if prob.kind != "transport" else 0]
+        scale = max(np.max(np.abs(C["A"])), 1.0)
+        assert np.max(np.abs(A[ci] - C["A"])) <= 1e-12 * scale, f"A_I mismatch class {mk}"
+        for f in range(2 * dim):
+            if mk & (1 << f):
+                continue
+            assert np.max(np.abs(neighbor_coupling(spec, B[ci], f) - C["N"][f])) <= 1e-12 * scale
+        assert np.max(np.abs(own_coupling(spec, B[ci], mk) - C["Own"])) <= 1e-12 * scale, f"own class {mk}"
         assert np.isfinite(np.linalg.cond(A[ci]))
 
 

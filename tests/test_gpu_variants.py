@@ -38,8 +38,7 @@ CASES = [
 ]
 
 
-@pytest.mark.parametrize("name,dim,cells,p,kind,params,dt,periodic,init", CASES, ids=[c[0] for c in CASES])
-def test_variant_parity(name, dim, cells, p, kind, params, dt, periodic, init):
+def _check(name, dim, cells, p, kind, params, dt, periodic, init, scheme="iHDG-II"):
     from oracle.ihdg_oracle import OracleProblem, OracleSolver
     from paper_1711_01175_b200.basis import build_operators
     from paper_1711_01175_b200.iteration import IterationConfig, run, run_time_dependent
@@ -61,17 +60,21 @@ def test_variant_parity(name, dim, cells, p, kind, params, dt, periodic, init):
     else:
         prob = ShallowWaterProblem(Phi=params["Phi"], f0=params["f0"], gamma=params.get("gamma", 0.0))
         oprob = OracleProblem("sw", dim, Phi=params["Phi"], f_cor=params["f0"], gamma=params.get("gamma", 0.0))
-    S = OracleSolver(oprob, cells, p, periodic=[periodic] * dim, dt=dt)
+    S = OracleSolver(oprob, cells, p, periodic=[periodic] * dim, dt=dt, scheme="I" if scheme == "iHDG-I" else "II")
     if getattr(prob, "forcing", None) is not None:
         S.set_forcing(prob.forcing)
-    cfg = IterationConfig(tol=1e-10)
+    cfg = IterationConfig(tol=1e-10, scheme=scheme)
     if dt is None:
         rep = run(mesh, prob, ops, cfg)
         ref = S.run(tol=1e-10)
         assert rep.iterations == ref["iterations"]
-        assert rep.status == ref["status"] == "converged"
+        assert rep.status == ref["status"]
+        if scheme == "iHDG-I" and ref["status"] == "diverged":
+            return None   # same divergence sweep as the oracle (1e6 x first norm)
+        assert ref["status"] == "converged"
         assert rel_l2(rep.state.data.reshape(S.nel, -1), ref["u"]) < 1e-10
         assert rel_l2(rep.trace, S.trace(ref["u"])) < 1e-10
+        return [rep.iterations]
     else:
         labels = prob.labels(dim)
         reps = run_time_dependent(mesh, prob, ops, cfg, dt, n_steps=2, initial={init: f}, keep_states=True)
@@ -79,8 +82,37 @@ def test_variant_parity(name, dim, cells, p, kind, params, dt, periodic, init):
         u0[:, labels.index(init), :] = S.interpolate(f)
         _, refs = S.run_time_dependent(u0.reshape(S.nel, -1), 2, tol=1e-10)
         assert [r.iterations for r in reps] == [r["iterations"] for r in refs]
+        assert [r.status for r in reps] == [r["status"] for r in refs]
+        if refs[-1]["status"] != "converged":
+            return None
         for r, o in zip(reps, refs):
             assert rel_l2(r.state.data.reshape(S.nel, -1), o["u"]) < 1e-10
+        return [r.iterations for r in reps]
+
+
+@pytest.mark.parametrize("name,dim,cells,p,kind,params,dt,periodic,init", CASES, ids=[c[0] for c in CASES])
+def test_variant_parity(name, dim, cells, p, kind, params, dt, periodic, init):
+    _check(name, dim, cells, p, kind, params, dt, periodic, init)
+
+
+IHDG1_CASES = [c for c in CASES if c[0] in ("transport2d_negbeta_p3", "transport3d_p2_generic", "cd2d_steady_p2",
+                                             "cd2d_be_p3", "sw_walls_p3", "sw_periodic_p2")] + [
+    ("cd2d_conv_p1", 2, [4, 4], 1, "cd", dict(kappa=1e-3, beta=[1.0, 1.0], nu=1.0), None, False, None),
+    ("sw_walls_p1_small_dt", 2, [4, 4], 1, "sw", dict(Phi=1.0, f0=0.0), 1e-2, False, "phi"),
+]
+
+
+@pytest.mark.parametrize("name,dim,cells,p,kind,params,dt,periodic,init", IHDG1_CASES,
+                         ids=[c[0] for c in IHDG1_CASES])
+def test_ihdg1_parity_and_dominance(name, dim, cells, p, kind, params, dt, periodic, init):
+    """iHDG-I (all-iterate-k trace) through the same C-ABI matches the oracle's
+    iHDG-I, and iHDG-II never needs more sweeps (Tables 6-7)."""
+    it1 = _check(name, dim, cells, p, kind, params, dt, periodic, init, scheme="iHDG-I")
+    it2 = _check(name, dim, cells, p, kind, params, dt, periodic, init, scheme="iHDG-II")
+    if it1 is not None:   # both converge (a diverging iHDG-I is checked against the oracle above)
+        assert all(b <= a for a, b in zip(it1, it2)), (it1, it2)
+
+
 
 
 def test_unsupported_order_raises():
