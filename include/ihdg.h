@@ -105,6 +105,7 @@ typedef struct {
   double first_norm;
   double last_norm;
   double diverge_factor;/* 1e6 */
+  double last_err;      /* exact-solution rule: ||u^k - u^e||_{L2} of the latest iterate */
 } ihdg_iter_state;
 
 /* K1: assemble A (and the neighbour-coupling B, time-level R) per operator
@@ -218,6 +219,31 @@ typedef struct {
   int32_t pad1;
 } ihdg_sweep_args;
 
+/* K5: ||u - u^e||_{L2(Omega)}^2 per tile by (p+2)^d Gauss quadrature
+ * (l2_error), fixed-order tile partials.  mode 0: the
+ * initial iterate (state->last_err := error, status untouched).  mode 1:
+ * after a sweep with finalize = 0; the last CTA reduces the sweep's
+ * successive partials and the error partials and applies the exact-solution
+ * stopping rule |e_k - e_{k-1}| < tol; divergence and
+ * NaN stay on the successive norm. */
+typedef struct {
+  ihdg_geom g;
+  const double* u;            /* ghost-padded state */
+  const double* ue_q;         /* [Nel_local][ncomp][nq^dim] exact solution at the Gauss points */
+  const double* vq;           /* [nq][N1] nodal basis at the Gauss points */
+  const double* wq;           /* [nq] Gauss weights on [-1,1] */
+  double* err_partials;       /* [ihdg_error_tile_count(g)] */
+  const double* succ_partials;/* the sweep's tile partials (mode 1) */
+  int64_t n_succ;             /* their count */
+  ihdg_iter_state* state;
+  double* norm_hist;          /* successive norms [max_iters] or NULL */
+  double* err_hist;           /* errors [max_iters] or NULL */
+  double comp_w[IHDG_MAX_COMP];
+  double jac;
+  int32_t nq;
+  int32_t mode;
+} ihdg_error_args;
+
 /* K3 (multi-rank): reduce globally gathered tile partials, update *state. */
 typedef struct {
   const double* tile_partials; /* [n_tiles_global] in global tile order */
@@ -273,6 +299,16 @@ int ihdg_copy_state(const ihdg_geom* g, const double* src, double* dst, void* st
  * NULL) receives the number of sweep kernels launched. */
 int ihdg_iterate(const ihdg_sweep_args* a, double* buf0, double* buf1, int32_t batch,
                  void* stream, ihdg_iter_state* state_out, int64_t* n_launched);
+
+/* K5 (see ihdg_error_args) and its tile count */
+int ihdg_error_norm(const ihdg_error_args* e, void* stream);
+int64_t ihdg_error_tile_count(const ihdg_geom* g);
+/* ihdg_iterate with the exact-solution stopping rule: every sweep runs with
+ * finalize = 0 and is followed by K5 (mode 1) on its output; e->u is set per
+ * sweep, e->mode forced to 1.  The caller runs K5 in mode 0 on the initial
+ * iterate first (state->last_err). */
+int ihdg_iterate_exact(const ihdg_sweep_args* a, const ihdg_error_args* e, double* buf0, double* buf1,
+                       int32_t batch, void* stream, ihdg_iter_state* state_out, int64_t* n_launched);
 
 #ifdef __cplusplus
 }

@@ -433,9 +433,19 @@ class OracleSolver:
     """Factor-once local systems + the iHDG-II iteration on the CPU."""
 
     def __init__(self, prob: OracleProblem, cells, p: int, box=None, periodic=None, dt=None,
-                 scheme: str = "II"):
+                 scheme: str = "II", time_scheme: str = "BE"):
+        """time_scheme "BE" (backward Euler) or "CN" (Crank-Nicolson):
+        with the spatial operator S = A - R of the local system, theta = 1/2 on
+        rows with a time derivative and 1 on algebraic rows (sigma, CD):
+            LHS = R + Theta S,   iterate-k couplings Theta N_f (Theta Own),
+            RHS = f + (R - (1-Theta) S) u^m + (1-Theta) (sum_f N_f u^m_nbr + Own u^m)."""
         d = prob.dim
         self.prob, self.p, self.dt, self.scheme = prob, p, dt, scheme
+        if time_scheme not in ("BE", "CN"):
+            raise ValueError(time_scheme)
+        if time_scheme == "CN" and dt is None:
+            raise ValueError("Crank-Nicolson needs a time step")
+        self.time_scheme = time_scheme
         self.cells = [int(c) for c in cells]
         self.periodic = [False] * d if periodic is None else [bool(x) for x in periodic]
         lo = np.zeros(d) if box is None else np.asarray(box[0], float)
@@ -460,8 +470,21 @@ class OracleSolver:
         for ci, mk in enumerate(masks):
             A, Nf, R, Ho, Hn, Own = local_operators(prob, self.el, mk if prob.kind != "transport" else 0, dt,
                                                     scheme)
+            Nx, Ownx = None, None
+            if time_scheme == "CN":
+                th = np.ones(prob.m)
+                th[prob.time_comps] = 0.5
+                th = np.repeat(th, self.el.np)[:, None]
+                S = A - R
+                A = R + th * S
+                R = R - (1.0 - th) * S
+                Nx = [(1.0 - th) * x for x in Nf]
+                Ownx = (1.0 - th) * Own
+                Nf = [th * x for x in Nf]
+                Own = th * Own
             lu, piv = sla.lu_factor(A)
-            self.classes[mk] = dict(idx=ci, A=A, N=Nf, R=R, lu=lu, piv=piv, Hown=Ho, Hnbr=Hn, Own=Own)
+            self.classes[mk] = dict(idx=ci, A=A, N=Nf, R=R, lu=lu, piv=piv, Hown=Ho, Hnbr=Hn, Own=Own,
+                                    Nx=Nx, Ownx=Ownx)
         if prob.kind == "transport":
             self.cls[:] = 0
             self.class_list = [self.classes[0]]
@@ -509,9 +532,17 @@ class OracleSolver:
     def rhs_static(self, u_prev=None):
         rhs = self.b_static.copy()
         if u_prev is not None and self.dt is not None:
+            d = self.prob.dim
             for ci, C in enumerate(self.class_list):
-                sel = self.cls == ci
+                sel = np.nonzero(self.cls == ci)[0]
                 rhs[sel] += u_prev[sel] @ C["R"].T
+                if self.time_scheme == "CN":   # explicit half of the neighbour / own trace terms
+                    rhs[sel] += u_prev[sel] @ C["Ownx"].T
+                    for f in range(2 * d):
+                        nb = self.nbr[sel, f]
+                        ok = nb != BOUNDARY
+                        if np.any(ok):
+                            rhs[sel[ok]] += u_prev[nb[ok]] @ C["Nx"][f].T
         return rhs
 
     def sweep(self, u_old, rhs):
@@ -530,6 +561,28 @@ class OracleSolver:
                     r[ok] += u_old[nb[ok]] @ C["N"][f].T
             u_new[sel] = sla.lu_solve((C["lu"], C["piv"]), r.T).T
         return u_new
+
+    def set_exact(self, exact, t=None):
+        """u^e at the Gauss points for the exact-solution rule:
+        exact(x[, t]) -> (n,) (the primary component) or (n, m) (all)."""
+        pts = self.element_points(self.b.qx).reshape(-1, self.prob.dim)
+        vals = np.asarray(exact(pts) if t is None else exact(pts, t), float)
+        nq = self.el.W.size
+        self.ue_q = np.zeros((self.nel, self.m, nq))
+        self.err_w = np.zeros(self.m)
+        if vals.ndim == 1:
+            c = self.prob.forcing_comp
+            self.ue_q[:, c, :] = vals.reshape(self.nel, nq)
+            self.err_w[c] = 1.0
+        else:
+            self.ue_q[:] = vals.reshape(self.nel, nq, self.m).transpose(0, 2, 1)
+            self.err_w[:] = 1.0
+
+    def err_norm(self, u):
+        """||u - u^e||_{L2} by quadrature, element sums in order."""
+        vals = u.reshape(self.nel, self.m, self.npn) @ self.el.Phi.T - self.ue_q
+        per = np.einsum("emq,q,m->e", vals * vals, self.el.W, self.err_w)
+        return float(np.sqrt(np.add.accumulate(per)[-1]))
 
     def vol_norm(self, delta):
         """||delta||_{L2} by quadrature, element sums in lexicographic order."""
@@ -556,14 +609,19 @@ class OracleSolver:
         u = np.zeros((self.nel, self.nv)) if u0 is None else np.array(u0, float).reshape(self.nel, self.nv)
         rhs = self.rhs_static(u_prev)
         norms = []
+        errs = []
         status = "max-iter"
         first = None
+        e_prev = self.err_norm(u) if norm == "exact" else None
         hist = [u.copy()] if keep_history else None
         for k in range(1, max_iters + 1):
             un = self.sweep(u, rhs)
             delta = un - u
             nrm = self.trace_norm(delta) if norm == "trace" else self.vol_norm(delta)
             norms.append(nrm)
+            if norm == "exact":
+                e = self.err_norm(un)
+                errs.append(e)
             u = un
             if keep_history:
                 hist.append(u.copy())
@@ -572,21 +630,29 @@ class OracleSolver:
             if not np.isfinite(nrm):
                 status = "diverged"
                 break
-            if nrm < tol:
+            if norm == "exact":
+                done = abs(e - e_prev) < tol
+                e_prev = e
+                if done:
+                    status = "converged"
+                    break
+            elif nrm < tol:
                 status = "converged"
                 break
             if k > 1 and nrm > diverge_factor * first:
                 status = "diverged"
                 break
-        out = dict(u=u, iterations=len(norms), status=status, norms=np.array(norms))
+        out = dict(u=u, iterations=len(norms), status=status, norms=np.array(norms), errors=np.array(errs))
         if keep_history:
             out["history"] = hist
         return out
 
-    def run_time_dependent(self, u0, nsteps, tol=1e-10, max_iters=10000, norm="volume"):
+    def run_time_dependent(self, u0, nsteps, tol=1e-10, max_iters=10000, norm="volume", exact=None):
         u = np.array(u0, float).reshape(self.nel, self.nv)
         reports = []
-        for _ in range(nsteps):
+        for step in range(nsteps):
+            if norm == "exact":
+                self.set_exact(exact, (step + 1) * self.dt)
             r = self.run(u0=u, tol=tol, max_iters=max_iters, norm=norm, u_prev=u)
             reports.append(r)
             u = r["u"]

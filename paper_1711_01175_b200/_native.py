@@ -42,7 +42,7 @@ class Geom(C.Structure):
 class IterState(C.Structure):
     _fields_ = [("status", _i32), ("iters", _i32), ("max_iters", _i32), ("ticket", C.c_uint32),
                 ("tol", _f64), ("first_norm", _f64), ("last_norm", _f64),
-                ("diverge_factor", _f64)]
+                ("diverge_factor", _f64), ("last_err", _f64)]
 
 
 class AssemblyArgs(C.Structure):
@@ -89,8 +89,14 @@ class TraceArgs(C.Structure):
                 ("w_int_nbr", (_f64 * 4) * 3), ("w_lo", (_f64 * 4) * 3), ("w_hi", (_f64 * 4) * 3)]
 
 
+class ErrorArgs(C.Structure):
+    _fields_ = [("g", Geom), ("u", _p), ("ue_q", _p), ("vq", _p), ("wq", _p), ("err_partials", _p),
+                ("succ_partials", _p), ("n_succ", _i64), ("state", _p), ("norm_hist", _p), ("err_hist", _p),
+                ("comp_w", _f64 * 4), ("jac", _f64), ("nq", _i32), ("mode", _i32)]
+
+
 _STRUCTS = [Geom, IterState, AssemblyArgs, ClassApplyArgs, FieldArgs, QuadArgs, SweepArgs,
-            FinalizeArgs, TraceArgs]
+            FinalizeArgs, TraceArgs, ErrorArgs]
 
 # exported symbol -> (restype, argtypes)
 SIGNATURES = {
@@ -111,6 +117,10 @@ SIGNATURES = {
     "ihdg_copy_state": (_i32, [C.POINTER(Geom), _p, _p, _p]),
     "ihdg_iterate": (_i32, [C.POINTER(SweepArgs), _p, _p, _i32, _p, C.POINTER(IterState),
                             C.POINTER(_i64)]),
+    "ihdg_error_norm": (_i32, [C.POINTER(ErrorArgs), _p]),
+    "ihdg_error_tile_count": (_i64, [C.POINTER(Geom)]),
+    "ihdg_iterate_exact": (_i32, [C.POINTER(SweepArgs), C.POINTER(ErrorArgs), _p, _p, _i32, _p,
+                                  C.POINTER(IterState), C.POINTER(_i64)]),
 }
 
 _lib = None

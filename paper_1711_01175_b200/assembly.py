@@ -56,6 +56,7 @@ B column as iHDG-II:
 from __future__ import annotations
 
 from dataclasses import dataclass, field
+from typing import Optional
 
 import numpy as np
 
@@ -101,6 +102,9 @@ class OperatorSpec:
     periodic: tuple
     boundary_rhs: list = field(default_factory=list)
     scheme: str = "iHDG-II"
+    time_scheme: str = "BE"
+    terms_expl: Optional[np.ndarray] = None   # CN: A terms + (1 - theta) B terms (L_expl)
+    coefs_expl: Optional[np.ndarray] = None
 
     @property
     def n1(self):
@@ -124,19 +128,57 @@ class _Terms:
         self.dim = dim
         self.rows = []
         self.coefs = []
+        self.time = []    # True: a 1/dt mass term (not part of the spatial operator)
 
-    def add(self, cls, target, rc, cb, axis_ops, coef):
+    def add(self, cls, target, rc, cb, axis_ops, coef, time=False):
         if coef == 0.0:
             return
         ops = list(axis_ops) + [MASS] * (3 - len(axis_ops))
         self.rows.append([cls, target, rc, cb, ops[0], ops[1], ops[2], 0])
         self.coefs.append(float(coef))
+        self.time.append(bool(time or target == R_T))
 
-    def vol(self, cls, target, rc, cb, coef, axis=None, op=None):
+    def vol(self, cls, target, rc, cb, coef, axis=None, op=None, time=False):
         ops = [MASS] * self.dim
         if axis is not None:
             ops[axis] = op
-        self.add(cls, target, rc, cb, ops, coef)
+        self.add(cls, target, rc, cb, ops, coef, time)
+
+    def crank_nicolson(self, theta, time_comp0):
+        """Trapezoidal split of the spatial operator S:
+        rows of component c get theta_c S on the LHS (and theta_c B for the
+        iterate-k couplings) and -(1 - theta_c) S in the explicit operator R,
+        whose columns become absolute components.  Returns the term list of
+        the explicit couplings (1 - theta_c) B (with the same A) for L_expl."""
+        rows, coefs = [], []
+        ex_rows, ex_coefs = [], []
+        for r, c, t in zip(self.rows, self.coefs, self.time):
+            cls, target, rc, cb = r[:4]
+            th = theta[rc]
+            if target == R_T:
+                rows.append([cls, R_T, rc, cb + time_comp0] + r[4:])
+                coefs.append(c)
+            elif target == A_T and t:
+                rows.append(r)
+                coefs.append(c)
+                ex_rows.append(r)
+                ex_coefs.append(c)
+            elif target == A_T:
+                rows.append(r)
+                coefs.append(th * c)
+                ex_rows.append(r)
+                ex_coefs.append(th * c)
+                if th != 1.0:
+                    rows.append([cls, R_T, rc, cb] + r[4:])
+                    coefs.append(-(1.0 - th) * c)
+            else:  # B_T
+                rows.append(r)
+                coefs.append(th * c)
+                if th != 1.0:
+                    ex_rows.append(r)
+                    ex_coefs.append((1.0 - th) * c)
+        self.rows, self.coefs = rows, coefs
+        return (np.asarray(ex_rows, dtype=np.int32).reshape(-1, 8), np.asarray(ex_coefs, dtype=float))
 
 
 def _ops_table(ops: ElementOperators) -> tuple[np.ndarray, np.ndarray]:
@@ -177,9 +219,17 @@ def _class_masks(mesh) -> list[int]:
 SCHEMES = ("iHDG-II", "iHDG-I")
 
 
-def build_spec(mesh, problem, ops: ElementOperators, dt=None, norm="auto", scheme: str = "iHDG-II") -> OperatorSpec:
+TIME_SCHEMES = ("BE", "CN")
+
+
+def build_spec(mesh, problem, ops: ElementOperators, dt=None, norm="auto", scheme: str = "iHDG-II",
+               time_scheme: str = "BE") -> OperatorSpec:
     if scheme not in SCHEMES:
         raise ValueError(f"unknown scheme {scheme!r}")
+    if time_scheme not in TIME_SCHEMES:
+        raise ValueError(f"unknown time scheme {time_scheme!r} (BE or CN)")
+    if time_scheme == "CN" and dt is None:
+        raise ValueError("Crank-Nicolson needs a time step")
     one = scheme == "iHDG-I"
     d = mesh.dim
     if ops.dim != d:
@@ -218,7 +268,8 @@ def build_spec(mesh, problem, ops: ElementOperators, dt=None, norm="auto", schem
         cls = 0
         for a in range(d):
             terms.vol(cls, A_T, 0, 0, -beta[a] * Jf[a], axis=a, op=CONVT)
-        terms.vol(cls, A_T, 0, 0, (problem.reaction + inv_dt) * J)
+        terms.vol(cls, A_T, 0, 0, problem.reaction * J)
+        terms.vol(cls, A_T, 0, 0, inv_dt * J, time=True)
         for f in range(2 * d):
             a, s = divmod(f, 2)
             sgn = 1.0 if s else -1.0
@@ -271,7 +322,8 @@ def build_spec(mesh, problem, ops: ElementOperators, dt=None, norm="auto", schem
                 terms.vol(ci, A_T, a, U, -Jf[a], axis=a, op=CONVT)
                 terms.vol(ci, A_T, U, a, -Jf[a], axis=a, op=CONVT)
                 terms.vol(ci, A_T, U, U, -beta[a] * Jf[a], axis=a, op=CONVT)
-            terms.vol(ci, A_T, U, U, (problem.nu + inv_dt) * J)
+            terms.vol(ci, A_T, U, U, problem.nu * J)
+            terms.vol(ci, A_T, U, U, inv_dt * J, time=True)
             for f in range(2 * d):
                 a, s = divmod(f, 2)
                 sgn = 1.0 if s else -1.0
@@ -335,12 +387,13 @@ def build_spec(mesh, problem, ops: ElementOperators, dt=None, norm="auto", schem
         for ci, mk in enumerate(masks):
             class_of_mask[mk] = ci
         for ci, mk in enumerate(masks):
-            terms.vol(ci, A_T, 0, 0, J * inv_dt)
+            terms.vol(ci, A_T, 0, 0, J * inv_dt, time=True)
             for a in range(2):
                 th = 1 + a
                 terms.vol(ci, A_T, 0, th, -P * Jf[a], axis=a, op=CONVT)
                 terms.vol(ci, A_T, th, 0, -P * Jf[a], axis=a, op=CONVT)
-                terms.vol(ci, A_T, th, th, (P * inv_dt + problem.gamma * P) * J)
+                terms.vol(ci, A_T, th, th, P * inv_dt * J, time=True)
+                terms.vol(ci, A_T, th, th, problem.gamma * P * J)
             terms.vol(ci, A_T, 1, 2, -fc * P * J)
             terms.vol(ci, A_T, 2, 1, fc * P * J)
             for f in range(4):
@@ -391,6 +444,13 @@ def build_spec(mesh, problem, ops: ElementOperators, dt=None, norm="auto", schem
     else:
         raise TypeError(f"unsupported problem type {type(problem).__name__}")
 
+    terms_expl = coefs_expl = None
+    if time_scheme == "CN":
+        # theta = 1/2 on rows with a time derivative, 1 on algebraic rows (sigma)
+        theta = np.ones(m)
+        theta[tc0:tc0 + ntc] = 0.5
+        terms_expl, coefs_expl = terms.crank_nicolson(theta, tc0)
+        nr, tc0, ntc = m * ops.n_nodes, 0, m
     terms_arr = np.asarray(terms.rows, dtype=np.int32).reshape(-1, 8)
     return OperatorSpec(
         dim=d, order=ops.p, ncomp=m, labels=tuple(labels), n_class=len(masks),
@@ -398,11 +458,13 @@ def build_spec(mesh, problem, ops: ElementOperators, dt=None, norm="auto", schem
         terms=terms_arr, coefs=np.asarray(terms.coefs, dtype=float), nr=nr,
         time_comp0=tc0, n_time_comp=ntc, forcing_comp=fcomp, face_w=face_w, coupled=coupled,
         out_face=out_face, out_w=out_w, own_w=own_w, comp_w=comp_w, trace_w=tw, jac=J, jac_face=jac_face,
-        periodic=tuple(mesh.periodic), scheme=scheme)
+        periodic=tuple(mesh.periodic), scheme=scheme, time_scheme=time_scheme, terms_expl=terms_expl,
+        coefs_expl=coefs_expl)
 
 
-def evaluate_terms(spec: OperatorSpec):
-    """Host evaluation of the term list -> (A, B, R) per class.
+def evaluate_terms(spec: OperatorSpec, expl: bool = False):
+    """Host evaluation of the term list -> (A, B, R) per class (expl: the
+    Crank-Nicolson explicit-coupling list, B = (1 - theta) B).
 
     Mirror of the first stage of K1 (k_assemble_build), used by the CPU tests
     to check the physics against the oracle without a GPU.  Not on the
@@ -413,7 +475,8 @@ def evaluate_terms(spec: OperatorSpec):
     A = np.zeros((spec.n_class, nv, nv))
     B = np.zeros((spec.n_class, nv, kin))
     R = np.zeros((spec.n_class, nv, max(spec.nr, 1)))
-    for row, coef in zip(spec.terms, spec.coefs):
+    rows, coefs = (spec.terms_expl, spec.coefs_expl) if expl else (spec.terms, spec.coefs)
+    for row, coef in zip(rows, coefs):
         cls, target, rc, cb = (int(x) for x in row[:4])
         mats = []
         for a in range(d):

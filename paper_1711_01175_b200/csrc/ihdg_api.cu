@@ -154,6 +154,7 @@ int64_t ihdg_struct_size(int32_t which) {
     case 6: return sizeof(ihdg_sweep_args);
     case 7: return sizeof(ihdg_finalize_args);
     case 8: return sizeof(ihdg_trace_args);
+    case 9: return sizeof(ihdg_error_args);
     default: return -1;
   }
 }
@@ -295,6 +296,8 @@ int ihdg_copy_state(const ihdg_geom* g, const double* src, double* dst, void* st
 // the buffer parity of every replay at buf0 -> buf1.
 struct SweepGraph {
   ihdg_sweep_args a;
+  ihdg_error_args e;
+  bool has_e = false;
   double* b0 = nullptr;
   double* b1 = nullptr;
   int nb = 0;
@@ -311,11 +314,15 @@ static bool graphs_enabled() {
   return on == 1;
 }
 
-static cudaGraphExec_t sweep_graph(const Entry* e, const ihdg_sweep_args& a, double* b0, double* b1, int nb,
-                                   cudaStream_t st) {
+static int do_error(const ihdg_error_args* e, cudaStream_t st);
+
+static cudaGraphExec_t sweep_graph(const Entry* e, const ihdg_sweep_args& a, const ihdg_error_args* ea, double* b0,
+                                   double* b1, int nb, cudaStream_t st) {
   static thread_local SweepGraph cache;
+  const bool has_e = ea != nullptr;
   if (cache.exec != nullptr && cache.b0 == b0 && cache.b1 == b1 && cache.nb == nb && cache.st == st &&
-      std::memcmp(&cache.a, &a, sizeof(a)) == 0)
+      std::memcmp(&cache.a, &a, sizeof(a)) == 0 && cache.has_e == has_e &&
+      (!has_e || std::memcmp(&cache.e, ea, sizeof(*ea)) == 0))
     return cache.exec;
   if (cache.exec != nullptr) {
     cudaGraphExecDestroy(cache.exec);
@@ -331,12 +338,19 @@ static cudaGraphExec_t sweep_graph(const Entry* e, const ihdg_sweep_args& a, dou
     s.u_old = (j & 1) ? b1 : b0;
     s.u_new = (j & 1) ? b0 : b1;
     ok = do_sweep(e, &s, st) == IHDG_OK;
+    if (ok && has_e) {
+      ihdg_error_args x = *ea;
+      x.u = s.u_new;
+      ok = do_error(&x, st) == IHDG_OK;
+    }
   }
   cudaGraph_t g = nullptr;
   const cudaError_t ce = cudaStreamEndCapture(st, &g);
   cudaGraphExec_t ex = nullptr;
   if (ok && ce == cudaSuccess && g != nullptr && cudaGraphInstantiate(&ex, g, 0) == cudaSuccess) {
     cache.a = a;
+    if (has_e) cache.e = *ea;
+    cache.has_e = has_e;
     cache.b0 = b0;
     cache.b1 = b1;
     cache.nb = nb;
@@ -350,8 +364,48 @@ static cudaGraphExec_t sweep_graph(const Entry* e, const ihdg_sweep_args& a, dou
   return ex;
 }
 
+static int64_t error_tiles(const ihdg_geom& g) {
+  Geo geo;
+  geo.init(g, ERR_TE);
+  return geo.ntiles;
+}
+
+static int do_error(const ihdg_error_args* e, cudaStream_t st) {
+  const int64_t nt = error_tiles(e->g);
+  int64_t grid = nt < 4 * num_sms() ? nt : 4 * num_sms();
+  if (grid < 1) grid = 1;
+  k_error_norm<<<(unsigned)grid, 256, 0, st>>>(*e);
+  return check_launch("k_error_norm");
+}
+
+int ihdg_error_norm(const ihdg_error_args* e, void* stream) {
+  if (e == nullptr || e->u == nullptr || e->ue_q == nullptr || e->state == nullptr)
+    return set_err(IHDG_ERR_ARG, "null args");
+  int rc = check_geom(e->g);
+  if (rc) return rc;
+  if (e->nq < 1 || e->nq > 16 || e->g.order + 1 > 8) return set_err(IHDG_ERR_ARG, "nq / order out of range");
+  if (e->mode == 1 && e->succ_partials == nullptr) return set_err(IHDG_ERR_ARG, "mode 1 needs the sweep partials");
+  return do_error(e, (cudaStream_t)stream);
+}
+
+int64_t ihdg_error_tile_count(const ihdg_geom* g) { return g == nullptr ? -1 : error_tiles(*g); }
+
+static int iterate_impl(const ihdg_sweep_args* a0, const ihdg_error_args* e0, double* buf0, double* buf1,
+                        int32_t batch, void* stream, ihdg_iter_state* state_out, int64_t* n_launched);
+
 int ihdg_iterate(const ihdg_sweep_args* a0, double* buf0, double* buf1, int32_t batch, void* stream,
                  ihdg_iter_state* state_out, int64_t* n_launched) {
+  return iterate_impl(a0, nullptr, buf0, buf1, batch, stream, state_out, n_launched);
+}
+
+int ihdg_iterate_exact(const ihdg_sweep_args* a0, const ihdg_error_args* e0, double* buf0, double* buf1,
+                       int32_t batch, void* stream, ihdg_iter_state* state_out, int64_t* n_launched) {
+  if (e0 == nullptr) return set_err(IHDG_ERR_ARG, "null error args");
+  return iterate_impl(a0, e0, buf0, buf1, batch, stream, state_out, n_launched);
+}
+
+static int iterate_impl(const ihdg_sweep_args* a0, const ihdg_error_args* e0, double* buf0, double* buf1,
+                        int32_t batch, void* stream, ihdg_iter_state* state_out, int64_t* n_launched) {
   if (a0 == nullptr || buf0 == nullptr || buf1 == nullptr || state_out == nullptr)
     return set_err(IHDG_ERR_ARG, "null args");
   if (batch < 1) batch = 1;
@@ -376,16 +430,25 @@ int ihdg_iterate(const ihdg_sweep_args* a0, double* buf0, double* buf1, int32_t 
     st = own;
   }
   ihdg_sweep_args a = *a0;
-  a.finalize = 1;
+  a.finalize = e0 == nullptr ? 1 : 0;   // exact rule: K5 finalizes
   a.u_old = a.u_new = nullptr;
+  ihdg_error_args ex{};
+  if (e0 != nullptr) {
+    ex = *e0;
+    ex.mode = 1;
+    ex.u = nullptr;
+    ex.succ_partials = a.tile_partials;
+    ex.state = a.state;
+  }
+  const ihdg_error_args* ep = e0 != nullptr ? &ex : nullptr;
   int64_t launched = 0;
   // sweeps after the stop are no-ops on the device, so a batch rounded up to
   // an even count changes nothing but the launch count
   const int nb = batch + (batch & 1);
-  cudaGraphExec_t ex = graphs_enabled() ? sweep_graph(e, a, buf0, buf1, nb, st) : nullptr;
+  cudaGraphExec_t gx = graphs_enabled() ? sweep_graph(e, a, ep, buf0, buf1, nb, st) : nullptr;
   for (;;) {
-    if (ex != nullptr) {
-      IHDG_CUDA_TRY(cudaGraphLaunch(ex, st));
+    if (gx != nullptr) {
+      IHDG_CUDA_TRY(cudaGraphLaunch(gx, st));
       launched += nb;
     } else {
       for (int j = 0; j < batch; ++j) {
@@ -393,6 +456,11 @@ int ihdg_iterate(const ihdg_sweep_args* a0, double* buf0, double* buf1, int32_t 
         a.u_new = (launched & 1) ? buf0 : buf1;
         rc = do_sweep(e, &a, st);
         if (rc) return rc;
+        if (ep != nullptr) {
+          ex.u = a.u_new;
+          rc = do_error(&ex, st);
+          if (rc) return rc;
+        }
         ++launched;
       }
     }

@@ -346,4 +346,117 @@ __global__ void k_finalize(const ihdg_finalize_args a) {
   finalize_block(a.tile_partials, a.n_tiles, a.state, a.norm_hist);
 }
 
+// Fixed-order sum of n partials (256 virtual lanes, then a fixed tree), the
+// same order as finalize_block.  Every thread of the CTA must call it.
+__device__ inline double fixed_sum(const double* parts, int64_t n) {
+  __shared__ double red[256];
+  __syncthreads();
+  for (int v = threadIdx.x; v < 256; v += blockDim.x) {
+    double s = 0.0;
+    for (int64_t i = v; i < n; i += 256) s += __ldcg(parts + i);
+    red[v] = s;
+  }
+  __syncthreads();
+  for (int w = 128; w > 0; w >>= 1) {
+    for (int v = threadIdx.x; v < w; v += blockDim.x) red[v] += red[v + w];
+    __syncthreads();
+  }
+  return red[0];
+}
+
+constexpr int ERR_TE = 8;   // elements per error tile
+
+// K5: ||u - u^e||^2 per tile by Gauss quadrature, then
+// (mode 1) the exact-solution stopping rule in the last CTA.
+__global__ void k_error_norm(const ihdg_error_args a) {
+  ihdg_iter_state* st = a.state;
+  if (a.mode == 1 && st->status != IHDG_RUNNING) return;   // later sweeps are no-ops
+  __shared__ double vq_s[16 * 8];
+  __shared__ double wq_s[16];
+  __shared__ double red[256];
+  __shared__ int last_s;
+  const int d = a.g.dim, n1 = a.g.order + 1, m = a.g.ncomp, nq = a.nq;
+  for (int i = threadIdx.x; i < nq * n1; i += blockDim.x) vq_s[i] = a.vq[i];
+  for (int i = threadIdx.x; i < nq; i += blockDim.x) wq_s[i] = a.wq[i];
+  int np = 1, nqd = 1;
+  for (int i = 0; i < d; ++i) {
+    np *= n1;
+    nqd *= nq;
+  }
+  const int nv = m * np;
+  Geo geo;
+  geo.init(a.g, ERR_TE);
+  const double* u = a.u + geo.ls * nv;
+  __syncthreads();
+  for (int64_t tile = blockIdx.x; tile < geo.ntiles; tile += gridDim.x) {
+    int64_t e0;
+    int nt;
+    geo.tile_range(tile, ERR_TE, e0, nt);
+    double acc = 0.0;
+    const int items = nt * m * nqd;
+    for (int it = threadIdx.x; it < items; it += blockDim.x) {
+      const int t = it / (m * nqd), rem = it - t * m * nqd, c = rem / nqd, q = rem - c * nqd;
+      int qa[3] = {q % nq, (q / nq) % nq, q / (nq * nq)};
+      const double* ue = u + (e0 + t) * nv + c * np;
+      double v = 0.0;
+      for (int n = 0; n < np; ++n) {
+        double w = vq_s[qa[0] * n1 + n % n1];
+        if (d > 1) w *= vq_s[qa[1] * n1 + (n / n1) % n1];
+        if (d > 2) w *= vq_s[qa[2] * n1 + n / (n1 * n1)];
+        v = fma(w, ue[n], v);
+      }
+      double wt = wq_s[qa[0]];
+      if (d > 1) wt *= wq_s[qa[1]];
+      if (d > 2) wt *= wq_s[qa[2]];
+      const double diff = v - a.ue_q[((e0 + t) * m + c) * (int64_t)nqd + q];
+      acc = fma(a.comp_w[c] * wt * diff, diff, acc);
+    }
+    red[threadIdx.x] = acc;
+    __syncthreads();
+    for (int w = 128; w > 0; w >>= 1) {
+      if ((int)threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) a.err_partials[tile] = a.jac * red[0];
+    __syncthreads();
+  }
+  // last CTA: reduce (mode 0: initial error; mode 1: stop rule)
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned tk = atomicAdd(&st->ticket, 1u);
+    last_s = (tk == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (!last_s) return;
+  __threadfence();
+  const double err = sqrt(fixed_sum(a.err_partials, geo.ntiles));
+  if (a.mode == 0) {
+    if (threadIdx.x == 0) {
+      st->last_err = err;
+      st->ticket = 0u;
+      __threadfence();
+    }
+    return;
+  }
+  const double norm = sqrt(fixed_sum(a.succ_partials, a.n_succ));
+  if (threadIdx.x == 0) {
+    const int it = st->iters + 1;
+    st->iters = it;
+    if (a.norm_hist != nullptr && it <= st->max_iters) a.norm_hist[it - 1] = norm;
+    if (a.err_hist != nullptr && it <= st->max_iters) a.err_hist[it - 1] = err;
+    if (it == 1) st->first_norm = norm;
+    st->last_norm = norm;
+    int status = IHDG_RUNNING;
+    if (!(norm == norm) || !(err == err)) status = IHDG_NAN;
+    else if (fabs(err - st->last_err) < st->tol) status = IHDG_CONVERGED;
+    else if (it > 1 && norm > st->diverge_factor * st->first_norm) status = IHDG_DIVERGED;
+    else if (it >= st->max_iters) status = IHDG_MAXITER;
+    st->last_err = err;
+    st->status = status;
+    st->ticket = 0u;
+    __threadfence();
+  }
+}
+
 }  // namespace ihdg

@@ -26,8 +26,9 @@ __all__ = ["IterationConfig", "IterationReport", "run", "run_time_dependent", "d
 @dataclass
 class IterationConfig:
     """SPEC.md:315-318.  ``stop``: "successive" (||u^k - u^{k-1}||_{L2} < tol,
-    PAPER.md:1308-1311) or "trace" (skeleton L2 norm of the trace update,
-    SURVEY.md App. B.2; transport only)."""
+    PAPER.md:1308-1311), "exact" (| ||u^k - u^e|| - ||u^{k-1} - u^e|| | < tol,
+    PAPER.md:1303-1306, needs problem.exact) or "trace" (skeleton L2 norm of
+    the trace update; transport only)."""
 
     scheme: str = "iHDG-II"
     stop: str = "successive"
@@ -45,7 +46,9 @@ class IterationConfig:
             raise ValueError("max_iters must be >= 1")
         if self.scheme not in ("iHDG-II", "iHDG-I"):
             raise ValueError(f"unknown scheme {self.scheme!r} (iHDG-I or iHDG-II)")
-        if self.stop not in ("successive", "trace"):
+        if self.stop == "exact-solution":
+            self.stop = "exact"
+        if self.stop not in ("successive", "trace", "exact"):
             raise NotImplementedError(f"stopping rule {self.stop!r} not on the device path")
 
 
@@ -73,9 +76,20 @@ def default_max_iters(mesh) -> int:
     return max(int(10 * (n * mesh.dim) + 100), 100000)
 
 
+def _exact_at(exact, t):
+    """exact(x) (steady) or exact(x, t) at the new time level -> a function of x."""
+    if t is None:
+        return lambda x: exact(x)
+    return lambda x: exact(x, t)
+
+
 def _norm_name(cfg: IterationConfig, problem) -> str:
     if cfg.stop == "trace" and not isinstance(problem, TransportProblem):
         raise NotImplementedError("the trace stopping rule is defined for transport")
+    if cfg.stop == "exact":
+        if getattr(problem, "exact", None) is None:
+            raise ValueError("the exact-solution stopping rule needs problem.exact")
+        return "exact"
     return "trace" if cfg.stop == "trace" else "volume"
 
 
@@ -110,6 +124,8 @@ def run(mesh, problem, ops: ElementOperators, cfg: Optional[IterationConfig] = N
         solver.set_forcing(forcing)
     solver.prepare_steady()
     _set_initial(solver, cfg.initial_guess)
+    if cfg.stop == "exact":
+        solver.set_exact(_exact_at(problem.exact, None))
     res = solver.iterate(tol=cfg.tol, max_iters=cfg.max_iters or default_max_iters(mesh),
                          norm=_norm_name(cfg, problem), batch=cfg.check_every)
     state = FieldState(solver.get_state(), solver.spec.labels, k=res.iterations) if return_state else None
@@ -117,23 +133,29 @@ def run(mesh, problem, ops: ElementOperators, cfg: Optional[IterationConfig] = N
                             and solver.layers[1] == mesh.cells[-1]) else None
     return IterationReport(res.iterations, res.status, res.norms, time.perf_counter() - t0,
                            state, tr, res.first_norm, res.last_norm, res.launched,
-                           extra={"device_seconds": res.seconds})
+                           extra={"device_seconds": res.seconds, "l2_errors": res.errors})
 
 
 def run_time_dependent(mesh, problem, ops: ElementOperators, cfg: Optional[IterationConfig],
                        dt: float, T: Optional[float] = None, n_steps: Optional[int] = None,
                        initial=None, solver: Optional[DeviceSolver] = None,
-                       keep_states: bool = False) -> list:
-    """Backward-Euler steps; each step iterates from u^m.
-    Divergence at any step aborts the run (the last report says which step)."""
+                       keep_states: bool = False, time_scheme: str = "backward-euler") -> list:
+    """Time steps; each step iterates from u^m.
+    ``time_scheme``: "backward-euler" or "crank-nicolson" (trapezoidal split of
+    the spatial operator).  Divergence at any step aborts
+    the run (the last report says which step)."""
     cfg = cfg or IterationConfig()
+    ts = {"backward-euler": "BE", "be": "BE", "crank-nicolson": "CN", "cn": "CN"}.get(time_scheme.lower())
+    if ts is None:
+        raise ValueError(f"unknown time scheme {time_scheme!r}")
     if n_steps is None:
         if T is None:
             raise ValueError("give T or n_steps")
         n_steps = int(round(T / dt))
     if solver is None:
         solver = DeviceSolver(mesh, problem, ops, dt=dt,
-                              max_iters=cfg.max_iters or default_max_iters(mesh), scheme=cfg.scheme)
+                              max_iters=cfg.max_iters or default_max_iters(mesh), scheme=cfg.scheme,
+                              time_scheme=ts)
     forcing = getattr(problem, "forcing", None)
     if forcing is not None and solver.s_static is None:
         solver.set_forcing(forcing)
@@ -142,6 +164,8 @@ def run_time_dependent(mesh, problem, ops: ElementOperators, cfg: Optional[Itera
     for m in range(n_steps):
         t0 = time.perf_counter()
         solver.begin_step()
+        if cfg.stop == "exact":
+            solver.set_exact(_exact_at(problem.exact, (m + 1) * dt))
         res = solver.iterate(tol=cfg.tol, max_iters=cfg.max_iters or default_max_iters(mesh),
                              norm=_norm_name(cfg, problem), batch=cfg.check_every)
         last = m == n_steps - 1 or res.status != "converged"
@@ -150,7 +174,8 @@ def run_time_dependent(mesh, problem, ops: ElementOperators, cfg: Optional[Itera
         reports.append(IterationReport(res.iterations, res.status, res.norms,
                                        time.perf_counter() - t0, st, None, res.first_norm,
                                        res.last_norm, res.launched,
-                                       extra={"step": m + 1, "device_seconds": res.seconds}))
+                                       extra={"step": m + 1, "device_seconds": res.seconds,
+                                              "l2_errors": res.errors}))
         if res.status != "converged":
             break
     return reports

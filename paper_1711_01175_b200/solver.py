@@ -47,6 +47,7 @@ class IterResult:
     last_norm: float
     launched: int
     seconds: float
+    errors: Optional[np.ndarray] = None   # exact-solution rule: ||u^k - u^e||_{L2} per sweep
 
 
 class DeviceSolver:
@@ -58,13 +59,14 @@ class DeviceSolver:
 
     def __init__(self, mesh, problem, ops: ElementOperators, dt=None, layers=None,
                  device=None, max_iters: int = 100000, spec: Optional[OperatorSpec] = None,
-                 scheme: str = "iHDG-II"):
+                 scheme: str = "iHDG-II", time_scheme: str = "BE"):
         torch = _torch()
         L = N.lib()
         self.torch = torch
         self.L = L
         self.mesh, self.problem, self.ops, self.dt = mesh, problem, ops, dt
-        self.spec = spec if spec is not None else build_spec(mesh, problem, ops, dt, scheme=scheme)
+        self.spec = spec if spec is not None else build_spec(mesh, problem, ops, dt, scheme=scheme,
+                                                             time_scheme=time_scheme)
         sp = self.spec
         d = mesh.dim
         if not L.ihdg_supported(d, ops.p, sp.ncomp):
@@ -135,6 +137,24 @@ class DeviceSolver:
         a.PT = _ptr(self.PT) if nr > 0 else 0
         a.min_pivot = _ptr(self.min_pivot)
         N.check(self.L.ihdg_assemble(C.byref(a), self._sptr), "ihdg_assemble")
+        self.LT_expl = None
+        if sp.time_scheme == "CN":
+            # L_expl = A^-1 (1 - theta) B: the explicit half of the trace couplings
+            self._terms_x = torch.as_tensor(sp.terms_expl, device=dev).contiguous()
+            self._coefs_x = torch.as_tensor(sp.coefs_expl, dtype=f64, device=dev)
+            A2, Ai2, AiT2 = torch.zeros_like(self.A), torch.zeros_like(self.A), torch.zeros_like(self.A)
+            B2 = torch.zeros_like(self.B)
+            self.LT_expl = torch.zeros_like(self.LT)
+            mp2 = torch.zeros_like(self.min_pivot)
+            b = N.AssemblyArgs()
+            b.dim, b.order, b.ncomp, b.n_class = sp.dim, sp.order, sp.ncomp, nc
+            b.n_ops, b.n_terms, b.nr = sp.ops1d.shape[0], sp.terms_expl.shape[0], 0
+            b.ops1d, b.op_ncols = _ptr(self._ops1d), _ptr(self._opn)
+            b.terms, b.coefs = _ptr(self._terms_x), _ptr(self._coefs_x)
+            b.A, b.Ainv, b.AinvT, b.B = _ptr(A2), _ptr(Ai2), _ptr(AiT2), _ptr(B2)
+            b.R, b.LT, b.PT, b.min_pivot = 0, _ptr(self.LT_expl), 0, _ptr(mp2)
+            N.check(self.L.ihdg_assemble(C.byref(b), self._sptr), "ihdg_assemble (CN explicit)")
+            del A2, Ai2, AiT2, B2, mp2
         piv = self.min_pivot.cpu().numpy()
         scale = self.A.abs().amax(dim=(1, 2)).cpu().numpy()
         bad = np.nonzero(~(piv > 1e-13 * scale))[0]
@@ -237,8 +257,13 @@ class DeviceSolver:
         else:
             self.s.copy_(self.s_static)
 
-    def begin_step(self) -> None:
-        """Backward-Euler RHS of the next step from the current state u^m (K4)."""
+    def begin_step(self, exchange=None) -> None:
+        """RHS of the next step from the current state u^m.
+
+        Backward Euler: s = P u^m (+ A^-1 f) (K4).  Crank-Nicolson adds the
+        explicit half of the trace couplings, A^-1 (1-theta) B q(u^m): one
+        sweep with L_expl from u^m into the spare buffer, which becomes s
+        (``exchange`` refreshes the ghost layers of u^m first, multi-rank)."""
         sp = self.spec
         if sp.nr == 0:
             raise RuntimeError("problem was assembled without a time step")
@@ -248,6 +273,15 @@ class DeviceSolver:
         else:
             acc = 0
         self._apply(self.PT, sp.nr, self.u[self.cur], self.nv, sp.time_comp0 * self.np_, 1, self.s, acc)
+        if sp.time_scheme == "CN":
+            if exchange is not None:
+                exchange()
+            self.reset_state(0.0, 1)
+            a = self.sweep_args("volume", finalize=0)
+            a.LT = _ptr(self.LT_expl)
+            a.u_old, a.u_new = _ptr(self.u[self.cur]), _ptr(self.u[1 - self.cur])
+            N.check(self.L.ihdg_sweep(C.byref(a), self._sptr), "ihdg_sweep (CN explicit half)")
+            self.s.copy_(self.interior(1 - self.cur))
 
     # -- iteration ---------------------------------------------------------
     def sweep_args(self, norm: str, finalize: int = 1) -> N.SweepArgs:
@@ -291,10 +325,52 @@ class DeviceSolver:
         raw = bytes(self.state_dev.cpu().numpy().tobytes())
         return N.IterState.from_buffer_copy(raw)
 
+    def set_exact(self, exact, t: Optional[float] = None) -> None:
+        """Exact solution u^e for the exact-solution stopping rule
+        (PAPER.md:1303-1306), evaluated at the Gauss points of every local
+        element: ``exact(x)`` or ``exact(x, t)`` -> (n,) for the problem's
+        primary component or (n, m) for all components."""
+        torch, sp, ops = self.torch, self.spec, self.ops
+        d = self.mesh.dim
+        pts = self._local_points(ops.quad_points).reshape(-1, d)
+        vals = np.asarray(exact(pts) if t is None else exact(pts, t), dtype=float)
+        nqd = ops.quad_points.size ** d
+        ue = np.zeros((self.nloc, sp.ncomp, nqd))
+        w = np.zeros(4)
+        if vals.ndim == 1:
+            c = sp.forcing_comp
+            ue[:, c, :] = vals.reshape(self.nloc, nqd)
+            w[c] = 1.0
+        else:
+            ue[:] = vals.reshape(self.nloc, nqd, sp.ncomp).transpose(0, 2, 1)
+            w[: sp.ncomp] = 1.0
+        self.ue_q = torch.as_tensor(ue, dtype=torch.float64, device=self.device).contiguous()
+        self._err_w = w
+        if getattr(self, "_vq", None) is None:
+            self._vq = torch.as_tensor(ops.interp, dtype=torch.float64, device=self.device).contiguous()
+            self._wq = torch.as_tensor(ops.quad_weights, dtype=torch.float64, device=self.device).contiguous()
+            self.err_partials = torch.zeros(int(self.L.ihdg_error_tile_count(C.byref(self.geom))),
+                                            dtype=torch.float64, device=self.device)
+            self.err_hist = torch.zeros(self.max_iters, dtype=torch.float64, device=self.device)
+
+    def _error_args(self, mode: int) -> N.ErrorArgs:
+        e = N.ErrorArgs()
+        e.g = self.geom
+        e.u, e.ue_q, e.vq, e.wq = _ptr(self.u[self.cur]), _ptr(self.ue_q), _ptr(self._vq), _ptr(self._wq)
+        e.err_partials, e.succ_partials, e.n_succ = _ptr(self.err_partials), _ptr(self.partials), self.ntiles
+        e.state, e.norm_hist, e.err_hist = _ptr(self.state_dev), _ptr(self.norm_hist), _ptr(self.err_hist)
+        for c in range(4):
+            e.comp_w[c] = float(self._err_w[c])
+        e.jac, e.nq, e.mode = self.spec.jac, self.ops.quad_points.size, mode
+        return e
+
     def iterate(self, tol: float = 1e-10, max_iters: int = 10000, norm: str = "volume",
                 batch: int = 16) -> IterResult:
         """Algorithm 1 from the current iterate until the
-        stopping rule holds; the latest iterate becomes current."""
+        stopping rule holds; the latest iterate becomes current.  norm
+        "volume" / "trace" (successive) or "exact" (set_exact first)."""
+        if norm == "exact":
+            return self._iterate_exact(tol, max_iters, batch)
         self.reset_state(tol, max_iters)
         a = self.sweep_args(norm, finalize=1)
         out = N.IterState()
@@ -309,6 +385,29 @@ class DeviceSolver:
         norms = self.norm_hist[:it].cpu().numpy().copy()
         return IterResult(it, N.STATUS_NAMES[out.status], norms, out.first_norm, out.last_norm,
                           int(nl.value), sec)
+
+    def _iterate_exact(self, tol, max_iters, batch) -> IterResult:
+        if getattr(self, "ue_q", None) is None:
+            raise RuntimeError("exact-solution rule: call set_exact() first")
+        if self.layers != (0, self.mesh.cells[self.mesh.dim - 1]):
+            raise NotImplementedError("exact-solution rule on a partitioned mesh")
+        self.reset_state(tol, max_iters)
+        N.check(self.L.ihdg_error_norm(C.byref(self._error_args(0)), self._sptr), "ihdg_error_norm")
+        a = self.sweep_args("volume", finalize=0)
+        e = self._error_args(1)
+        out = N.IterState()
+        nl = C.c_int64(0)
+        b0, b1 = self.u[self.cur], self.u[1 - self.cur]
+        t0 = time.perf_counter()
+        N.check(self.L.ihdg_iterate_exact(C.byref(a), C.byref(e), _ptr(b0), _ptr(b1), int(batch), self._sptr,
+                                          C.byref(out), C.byref(nl)), "ihdg_iterate_exact")
+        sec = time.perf_counter() - t0
+        self.cur = (self.cur + out.iters) % 2
+        it = out.iters
+        norms = self.norm_hist[:it].cpu().numpy().copy()
+        errs = self.err_hist[:it].cpu().numpy().copy()
+        return IterResult(it, N.STATUS_NAMES[out.status], norms, out.first_norm, out.last_norm,
+                          int(nl.value), sec, errs)
 
     def sweep_once(self, norm: str = "volume", finalize: int = 1, a: Optional[N.SweepArgs] = None):
         """One sweep from the current iterate (used by the bench and multi-rank driver)."""
@@ -386,6 +485,9 @@ class DistributedSweeper:
         f.state, f.norm_hist = _ptr(sv.state_dev), _ptr(sv.norm_hist)
         N.check(sv.L.ihdg_finalize(C.byref(f), sv._sptr), "ihdg_finalize")
         sv.cur = 1 - sv.cur
+
+    def begin_step(self) -> None:
+        self.sv.begin_step(exchange=self._exchange)
 
     def iterate(self, tol=1e-10, max_iters=10000, norm="volume", batch=16) -> IterResult:
         sv = self.sv

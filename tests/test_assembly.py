@@ -73,6 +73,38 @@ def test_ihdg1_operators_match_oracle(name, dim, cells, p, prob, dt, periodic):
         assert np.isfinite(np.linalg.cond(A[ci]))
 
 
+CN_CASES = [c for c in CASES if c[5] is not None]
+
+
+@pytest.mark.parametrize("scheme", ["iHDG-II", "iHDG-I"])
+@pytest.mark.parametrize("name,dim,cells,p,prob,dt,periodic", CN_CASES, ids=[c[0] for c in CN_CASES])
+def test_crank_nicolson_operators_match_oracle(name, dim, cells, p, prob, dt, periodic, scheme):
+    """Crank-Nicolson split: LHS R + Theta S, iterate-k
+    couplings Theta B, explicit R - (1-Theta) S and (1-Theta) B, against the
+    oracle's trapezoidal operators."""
+    mesh = build_mesh(dim, cells, periodic=periodic)
+    ops = build_operators(p, dim, mesh.h)
+    spec = build_spec(mesh, prob, ops, dt, scheme=scheme, time_scheme="CN")
+    A, B, R = evaluate_terms(spec)
+    Ax, Bx, _ = evaluate_terms(spec, expl=True)
+    S = OracleSolver(oracle_problem(prob, dim), cells, p, periodic=[periodic] * dim, dt=dt,
+                     scheme="I" if scheme == "iHDG-I" else "II", time_scheme="CN")
+    assert spec.nr == spec.nv and spec.time_comp0 == 0
+    for ci, mk in enumerate(spec.class_masks):
+        C = S.classes[mk if prob.kind != "transport" else 0]
+        scale = max(np.max(np.abs(C["A"])), 1.0)
+        assert np.max(np.abs(A[ci] - C["A"])) <= 1e-12 * scale
+        assert np.max(np.abs(Ax[ci] - C["A"])) <= 1e-12 * scale
+        assert np.max(np.abs(R[ci][:, : spec.nr] - C["R"])) <= 1e-12 * scale
+        for f in range(2 * dim):
+            if mk & (1 << f):
+                continue
+            assert np.max(np.abs(neighbor_coupling(spec, B[ci], f) - C["N"][f])) <= 1e-12 * scale
+            assert np.max(np.abs(neighbor_coupling(spec, Bx[ci], f) - C["Nx"][f])) <= 1e-12 * scale
+        assert np.max(np.abs(own_coupling(spec, B[ci], mk) - C["Own"])) <= 1e-12 * scale
+        assert np.max(np.abs(own_coupling(spec, Bx[ci], mk) - C["Ownx"])) <= 1e-12 * scale
+
+
 def test_class_enumeration():
     mesh = build_mesh(2, [5, 5])
     ops = build_operators(1, 2, mesh.h)

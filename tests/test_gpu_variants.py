@@ -38,7 +38,7 @@ CASES = [
 ]
 
 
-def _check(name, dim, cells, p, kind, params, dt, periodic, init, scheme="iHDG-II"):
+def _check(name, dim, cells, p, kind, params, dt, periodic, init, scheme="iHDG-II", time_scheme="BE"):
     from oracle.ihdg_oracle import OracleProblem, OracleSolver
     from paper_1711_01175_b200.basis import build_operators
     from paper_1711_01175_b200.iteration import IterationConfig, run, run_time_dependent
@@ -60,7 +60,8 @@ def _check(name, dim, cells, p, kind, params, dt, periodic, init, scheme="iHDG-I
     else:
         prob = ShallowWaterProblem(Phi=params["Phi"], f0=params["f0"], gamma=params.get("gamma", 0.0))
         oprob = OracleProblem("sw", dim, Phi=params["Phi"], f_cor=params["f0"], gamma=params.get("gamma", 0.0))
-    S = OracleSolver(oprob, cells, p, periodic=[periodic] * dim, dt=dt, scheme="I" if scheme == "iHDG-I" else "II")
+    S = OracleSolver(oprob, cells, p, periodic=[periodic] * dim, dt=dt, scheme="I" if scheme == "iHDG-I" else "II",
+                     time_scheme=time_scheme)
     if getattr(prob, "forcing", None) is not None:
         S.set_forcing(prob.forcing)
     cfg = IterationConfig(tol=1e-10, scheme=scheme)
@@ -77,7 +78,8 @@ def _check(name, dim, cells, p, kind, params, dt, periodic, init, scheme="iHDG-I
         return [rep.iterations]
     else:
         labels = prob.labels(dim)
-        reps = run_time_dependent(mesh, prob, ops, cfg, dt, n_steps=2, initial={init: f}, keep_states=True)
+        reps = run_time_dependent(mesh, prob, ops, cfg, dt, n_steps=2, initial={init: f}, keep_states=True,
+                                  time_scheme=time_scheme)
         u0 = np.zeros((S.nel, S.m, S.npn))
         u0[:, labels.index(init), :] = S.interpolate(f)
         _, refs = S.run_time_dependent(u0.reshape(S.nel, -1), 2, tol=1e-10)
@@ -115,6 +117,38 @@ def test_ihdg1_parity_and_dominance(name, dim, cells, p, kind, params, dt, perio
 
 
 
+CN_CASES = [c for c in CASES if c[6] is not None] + [
+    ("transport2d_be_p2", 2, [6, 5], 2, "transport", dict(beta=[1.0, -0.5]), 0.05, False, "u"),
+]
+
+
+@pytest.mark.parametrize("scheme", ["iHDG-II", "iHDG-I"])
+@pytest.mark.parametrize("name,dim,cells,p,kind,params,dt,periodic,init", CN_CASES, ids=[c[0] for c in CN_CASES])
+def test_crank_nicolson_parity(name, dim, cells, p, kind, params, dt, periodic, init, scheme):
+    """Crank-Nicolson steps (explicit half by one L_expl sweep from u^m) vs the
+    oracle's trapezoidal local solves: same sweep counts / statuses, fields."""
+    _check(name, dim, cells, p, kind, params, dt, periodic, init, scheme=scheme, time_scheme="CN")
+
+
+def test_table6_sw_crank_nicolson_ihdg1_diverges():
+    """SW, Nel=64, p=1, dt=0.1, Crank-Nicolson -> iHDG-I diverges
+    while iHDG-II converges (Table 6, standing wave, mirror walls)."""
+    from paper_1711_01175_b200.basis import build_operators
+    from paper_1711_01175_b200.iteration import IterationConfig, run_time_dependent
+    from paper_1711_01175_b200.mesh import build_mesh
+    from paper_1711_01175_b200.pde import ShallowWaterProblem
+
+    mesh = build_mesh(2, [8, 8])
+    ops = build_operators(1, 2, mesh.h)
+    phi0 = lambda x: np.cos(np.pi * x[:, 0]) * np.cos(np.pi * x[:, 1])  # noqa: E731
+    out = {}
+    for scheme in ("iHDG-I", "iHDG-II"):
+        reps = run_time_dependent(mesh, ShallowWaterProblem(Phi=1.0), ops, IterationConfig(scheme=scheme, tol=1e-10),
+                                  0.1, n_steps=1, initial={"phi": phi0}, time_scheme="crank-nicolson")
+        out[scheme] = reps[-1].status
+    assert out == {"iHDG-I": "diverged", "iHDG-II": "converged"}, out
+
+
 def test_unsupported_order_raises():
     from paper_1711_01175_b200.basis import build_operators
     from paper_1711_01175_b200.iteration import run
@@ -124,3 +158,44 @@ def test_unsupported_order_raises():
     mesh = build_mesh(2, [4, 4])
     with pytest.raises(NotImplementedError):
         run(mesh, TransportProblem(beta=np.array([1.0, 1.0])), build_operators(8, 2, mesh.h))
+
+
+EXACT_CASES = [
+    # name, preset, cells, p, dt, steps, time scheme
+    ("sw_standing_wave_cn_p2", "sw_standing_wave", [8, 8], 2, 0.01, 2, "CN"),
+    ("sw_standing_wave_be_p1", "sw_standing_wave", [6, 6], 1, 0.05, 1, "BE"),
+    ("transport3d_timedep_cn_p2", "transport3d_timedep", [4, 4, 4], 2, 0.05, 2, "CN"),
+]
+
+
+@pytest.mark.parametrize("name,preset,cells,p,dt,steps,ts", EXACT_CASES, ids=[c[0] for c in EXACT_CASES])
+def test_exact_solution_rule_parity(name, preset, cells, p, dt, steps, ts):
+    """Exact-solution stopping rule on the device (K5 +
+    fused finalize) vs the oracle: same sweep counts, errors, fields."""
+    from oracle.ihdg_oracle import OracleSolver
+    from paper_1711_01175_b200.basis import build_operators
+    from paper_1711_01175_b200.iteration import IterationConfig, run_time_dependent
+    from paper_1711_01175_b200.mesh import build_mesh
+    from paper_1711_01175_b200.pde import preset_problems
+    from tests.oracle_bridge import oracle_problem, rel_l2
+
+    prob = preset_problems()[preset]
+    dim = len(cells)
+    mesh = build_mesh(dim, cells)
+    ops = build_operators(p, dim, mesh.h)
+    labels = prob.labels(dim)
+    init = {lab: (lambda x, c=c: np.atleast_2d(np.asarray(prob.exact(x, 0.0)).T).T[:, c])
+            for c, lab in enumerate(labels)}
+    reps = run_time_dependent(mesh, prob, ops, IterationConfig(tol=1e-10, stop="exact"), dt, n_steps=steps,
+                              initial=init, keep_states=True,
+                              time_scheme="crank-nicolson" if ts == "CN" else "backward-euler")
+    S = OracleSolver(oracle_problem(prob, dim), cells, p, dt=dt, time_scheme=ts)
+    u0 = np.zeros((S.nel, S.m, S.npn))
+    for c in range(S.m):
+        u0[:, c, :] = S.interpolate(init[labels[c]])
+    _, refs = S.run_time_dependent(u0.reshape(S.nel, -1), steps, tol=1e-10, norm="exact", exact=prob.exact)
+    assert [r.iterations for r in reps] == [o["iterations"] for o in refs]
+    assert all(r.status == "converged" for r in reps)
+    for r, o in zip(reps, refs):
+        assert rel_l2(r.state.data.reshape(S.nel, -1), o["u"]) < 1e-10
+        assert np.allclose(r.extra["l2_errors"], o["errors"], rtol=1e-9, atol=1e-14)
