@@ -194,3 +194,27 @@ def test_sweep_impl_parity(impl):
     r = subprocess.run([sys.executable, os.path.join(root, "tests", "_impl_child.py"), "1e-1"], env=env,
                        capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout + r.stderr
+
+
+# PAPER.md:1349-1395 (Table 2) / SPEC.md acceptance 1: 2D N x N -> {9, 17, 33, 65} for N = 4..32,
+# 3D N^3 -> {6, 12, 23, 47} for N = 2..16, within +-2 (any p)
+TABLE2 = [(2, 4, 9), (2, 8, 17), (2, 16, 33), (2, 32, 65), (3, 2, 6), (3, 4, 12), (3, 8, 23), (3, 16, 47)]
+
+
+@pytest.mark.parametrize("dim,n,paper", TABLE2, ids=[f"{d}d_{n}" for d, n, _ in TABLE2])
+def test_table2_transport_counts(dim, n, paper):
+    """Steady diagonal transport (transport2d_diag / transport3d_diag) on the
+    device: iteration counts within +-2 of Table 2 for p = 1..4 (p <= 3 in 3D)."""
+    from paper_1711_01175_b200.basis import build_operators
+    from paper_1711_01175_b200.iteration import IterationConfig, run
+    from paper_1711_01175_b200.mesh import build_mesh
+    from paper_1711_01175_b200.pde import TransportProblem
+    from paper_1711_01175_b200.workloads import fourier_modes
+
+    mesh = build_mesh(dim, [n] * dim)
+    f = fourier_modes(np.random.default_rng(3), dim)
+    for p in (1, 2, 3, 4) if dim == 2 else (1, 2, 3):
+        rep = run(mesh, TransportProblem(beta=np.ones(dim), forcing=f), build_operators(p, dim, mesh.h),
+                  IterationConfig(stop="trace", tol=1e-10), return_trace=False)
+        assert rep.status == "converged"
+        assert abs(rep.iterations - paper) <= 2, (p, rep.iterations, paper)
