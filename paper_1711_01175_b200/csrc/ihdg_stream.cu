@@ -8,6 +8,7 @@
 #include "ihdg_v3.cuh"
 #include "ihdg_ws2.cuh"
 #include "ihdg_ws3.cuh"
+#include "ihdg_ws4.cuh"
 
 namespace ihdg {
 
@@ -57,6 +58,25 @@ int launch_ws3_t(const ihdg_sweep_args* a, cudaStream_t st) {
   int64_t grid = geo.ntiles < stream_sms() ? geo.ntiles : stream_sms();
   if (grid < 1) grid = 1;
   k_sweep_ws3<N1, M, NCF, NWC, E, NS><<<(unsigned)grid, C::NT, C::BYTES, st>>>(*a);
+  return cudaGetLastError() == cudaSuccess ? 0 : -2;
+}
+
+template <int N1, int M, int NCF, int NWC, int NS>
+int launch_ws4_t(const ihdg_sweep_args* a, cudaStream_t st) {
+  using C = W4Cfg<N1, M, NCF, NWC, NS>;
+  static_assert(C::EL == Cfg<2, N1, M>::TE, "ws4 logical tile must equal the generic tile (tile partial count)");
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(k_sweep_ws4<N1, M, NCF, NWC, NS>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::BYTES);
+    if (e != cudaSuccess) return -2;
+    configured = true;
+  }
+  Geo geo;
+  geo.init(a->g, C::EL);
+  int64_t grid = geo.ntiles < stream_sms() ? geo.ntiles : stream_sms();
+  if (grid < 1) grid = 1;
+  k_sweep_ws4<N1, M, NCF, NWC, NS><<<(unsigned)grid, C::NT, C::BYTES, st>>>(*a);
   return cudaGetLastError() == cudaSuccess ? 0 : -2;
 }
 
@@ -121,7 +141,7 @@ struct StreamEntry {
   int D, N1, M, NCF, NWC, E, NV;
   int (*launch)(const ihdg_sweep_args*, cudaStream_t);
   int v3;  // version-3 kernel (physical 8-element tiles)
-  int ws3; // k_sweep_ws3 (skipped under IHDG_SWEEP_IMPL=ws)
+  int ws3; // opt-in kernels: 1 k_sweep_ws3 (IHDG_SWEEP_IMPL=ws3), 2 k_sweep_ws4 (=ws4)
 };
 
 #define IHDG_V3(D, N1, M, NCF, NWC, NS, NCW, PF, NQW) \
@@ -133,6 +153,9 @@ struct StreamEntry {
 #endif
 #define IHDG_WS(N1, M, NCF, NWC, E, NS) \
   {2, N1, M, NCF, NWC, E, M * N1 * N1, launch_ws_t<N1, M, NCF, NWC, E, NS>, 0, 0},
+#ifndef IHDG_WS4_NS
+#define IHDG_WS4_NS 6
+#endif
 #ifndef IHDG_WS3_NS
 #define IHDG_WS3_NS 3
 #endif
@@ -146,6 +169,7 @@ const StreamEntry kStream[] = {
     IHDG_V3(3, 4, 1, 3, 1, 16, 6, 4, 4)    // config 4: transport 3D p=3
     IHDG_WS2(7, 3, 4, 2, 16, 6)            // config 5: CD 2D p=6 (ws2: s / u^{k+1} bypass smem)
     IHDG_WS3(7, 3, 4, 2, 16, IHDG_WS3_NS)  // config 5: CD 2D p=6 (ws3: q in the consumers, DFMA norm warps)
+    {2, 7, 3, 4, 2, 16, 147, launch_ws4_t<7, 3, 4, 2, IHDG_WS4_NS>, 0, 2},  // config 5 (ws4: two consumer teams)
     IHDG_WS(7, 3, 4, 2, 16, IHDG_WS5_NS)   // config 5: CD 2D p=6 (warp-specialised)
     IHDG_WS(5, 3, 4, 2, 16, 4)             // configs 2/3: CD / SW 2D p=4
     IHDG_STREAM(3, 4, 1, 3, 1, 32, 3, 4)   // config 4: transport 3D p=3
@@ -172,6 +196,11 @@ const StreamEntry* stream_entry(const ihdg_sweep_args* a) {
     want_ws2 = (s != nullptr && std::strcmp(s, "ws2") == 0) ? 1 : 0;
   }
   // "ws3" opts in to k_sweep_ws3 (slower than ws on config 5)
+  static int want_ws4 = -1;
+  if (want_ws4 < 0) {
+    const char* s = std::getenv("IHDG_SWEEP_IMPL");
+    want_ws4 = (s != nullptr && std::strcmp(s, "ws4") == 0) ? 1 : 0;
+  }
   static int want_ws3 = -1;
   if (want_ws3 < 0) {
     const char* s = std::getenv("IHDG_SWEEP_IMPL");
@@ -192,7 +221,8 @@ const StreamEntry* stream_entry(const ihdg_sweep_args* a) {
     if (e.D != g.dim || e.N1 != g.order + 1 || e.M != g.ncomp) continue;
     if (e.NCF != ncf || maxw > e.NWC) continue;
     if (e.v3 && no_v3) continue;
-    if (e.ws3 && !want_ws3) continue;
+    if (e.ws3 == 1 && !want_ws3) continue;
+    if (e.ws3 == 2 && !want_ws4) continue;
     if (e.launch == (int (*)(const ihdg_sweep_args*, cudaStream_t))launch_ws2_t<7, 3, 4, 2, 16, 6> && !want_ws2)
       continue;
     Geo geo;
