@@ -244,6 +244,42 @@ typedef struct {
   int32_t mode;
 } ihdg_error_args;
 
+/* K6: diagnostics of iteration.run in diagnostic mode (SPEC.md:320-323,
+ * 341-349, 398); not on the sweep path.
+ * ihdg_elem_error: per local element e,
+ *   err2[e] = J sum_c comp_w[c] ||u_{e,c} - r_{e,c}||^2_{M}  (consistent mass,
+ *             M1 = C C^T), flags[e] = (err2[e] < tol^2),
+ *   *total  = fixed-order sum of err2 (256 virtual lanes).
+ * The element convergence map of SPEC.md:321 / layer_convergence_map
+ * is flags with r = the converged HDG solution. */
+typedef struct {
+  ihdg_geom g;
+  const double* u;            /* ghost-padded state */
+  const double* r;            /* ghost-padded reference state, same layout */
+  const double* chol1d;       /* [N1][N1] lower factor C, row-major */
+  double* err2;               /* [Nel_local] */
+  uint8_t* flags;             /* [Nel_local] or NULL */
+  double* total;              /* [1] or NULL */
+  double comp_w[IHDG_MAX_COMP];
+  double jac;
+  double tol;
+} ihdg_elem_error_args;
+
+/* Skeleton energy of a face array t[n_faces][(p+1)^(d-1)] (mesh.py face order,
+ * e.g. written by ihdg_extract_trace): e2[f] = Jf_axis(f) ||t_f - t_ref_f||^2_{M_f},
+ * M_f = M1 x .. x M1 over the tangential axes; *total = fixed-order sum.
+ * Trace energy and the skeleton jump norm are this applied to
+ * the trace of u^k - r and to the interior-face jump of u^k. */
+typedef struct {
+  ihdg_geom g;                /* single rank: layer range = whole axis */
+  const double* t;
+  const double* t_ref;        /* same shape as t, or NULL (= 0) */
+  const double* chol1d;
+  double* e2;                 /* [n_faces] */
+  double* total;              /* [1] or NULL */
+  double jac_face[IHDG_MAX_DIM];
+} ihdg_face_energy_args;
+
 /* K3 (multi-rank): reduce globally gathered tile partials, update *state. */
 typedef struct {
   const double* tile_partials; /* [n_tiles_global] in global tile order */
@@ -309,6 +345,9 @@ int64_t ihdg_error_tile_count(const ihdg_geom* g);
  * iterate first (state->last_err). */
 int ihdg_iterate_exact(const ihdg_sweep_args* a, const ihdg_error_args* e, double* buf0, double* buf1,
                        int32_t batch, void* stream, ihdg_iter_state* state_out, int64_t* n_launched);
+/* K6 diagnostics (see ihdg_elem_error_args / ihdg_face_energy_args) */
+int ihdg_elem_error(const ihdg_elem_error_args* a, void* stream);
+int ihdg_face_energy(const ihdg_face_energy_args* a, void* stream);
 
 #ifdef __cplusplus
 }

@@ -10,7 +10,8 @@ import ctypes as C
 import os
 
 __all__ = ["NativeUnavailable", "lib", "Geom", "IterState", "AssemblyArgs", "ClassApplyArgs",
-           "FieldArgs", "QuadArgs", "SweepArgs", "FinalizeArgs", "TraceArgs", "check",
+           "FieldArgs", "QuadArgs", "SweepArgs", "FinalizeArgs", "TraceArgs", "ElemErrorArgs",
+           "FaceEnergyArgs", "check",
            "LIB_PATH", "STATUS_NAMES"]
 
 LIB_PATH = os.environ.get("IHDG_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)),
@@ -95,8 +96,18 @@ class ErrorArgs(C.Structure):
                 ("comp_w", _f64 * 4), ("jac", _f64), ("nq", _i32), ("mode", _i32)]
 
 
+class ElemErrorArgs(C.Structure):
+    _fields_ = [("g", Geom), ("u", _p), ("r", _p), ("chol1d", _p), ("err2", _p), ("flags", _p),
+                ("total", _p), ("comp_w", _f64 * 4), ("jac", _f64), ("tol", _f64)]
+
+
+class FaceEnergyArgs(C.Structure):
+    _fields_ = [("g", Geom), ("t", _p), ("t_ref", _p), ("chol1d", _p), ("e2", _p), ("total", _p),
+                ("jac_face", _f64 * 3)]
+
+
 _STRUCTS = [Geom, IterState, AssemblyArgs, ClassApplyArgs, FieldArgs, QuadArgs, SweepArgs,
-            FinalizeArgs, TraceArgs, ErrorArgs]
+            FinalizeArgs, TraceArgs, ErrorArgs, ElemErrorArgs, FaceEnergyArgs]
 
 # exported symbol -> (restype, argtypes)
 SIGNATURES = {
@@ -121,6 +132,8 @@ SIGNATURES = {
     "ihdg_error_tile_count": (_i64, [C.POINTER(Geom)]),
     "ihdg_iterate_exact": (_i32, [C.POINTER(SweepArgs), C.POINTER(ErrorArgs), _p, _p, _i32, _p,
                                   C.POINTER(IterState), C.POINTER(_i64)]),
+    "ihdg_elem_error": (_i32, [C.POINTER(ElemErrorArgs), _p]),
+    "ihdg_face_energy": (_i32, [C.POINTER(FaceEnergyArgs), _p]),
 }
 
 _lib = None

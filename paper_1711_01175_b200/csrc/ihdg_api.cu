@@ -155,6 +155,8 @@ int64_t ihdg_struct_size(int32_t which) {
     case 7: return sizeof(ihdg_finalize_args);
     case 8: return sizeof(ihdg_trace_args);
     case 9: return sizeof(ihdg_error_args);
+    case 10: return sizeof(ihdg_elem_error_args);
+    case 11: return sizeof(ihdg_face_energy_args);
     default: return -1;
   }
 }
@@ -389,6 +391,49 @@ int ihdg_error_norm(const ihdg_error_args* e, void* stream) {
 }
 
 int64_t ihdg_error_tile_count(const ihdg_geom* g) { return g == nullptr ? -1 : error_tiles(*g); }
+
+int ihdg_elem_error(const ihdg_elem_error_args* a, void* stream) {
+  if (a == nullptr || a->u == nullptr || a->r == nullptr || a->chol1d == nullptr || a->err2 == nullptr)
+    return set_err(IHDG_ERR_ARG, "null args");
+  int rc = check_geom(a->g);
+  if (rc) return rc;
+  if (a->g.order + 1 > 8) return set_err(IHDG_ERR_ARG, "order out of range (p <= 7)");
+  Geo geo;
+  geo.init(a->g, 1);
+  if (geo.nloc == 0) return IHDG_OK;
+  const int64_t grid = geo.nloc < 8 * num_sms() ? geo.nloc : 8 * num_sms();
+  k_elem_error<<<(unsigned)grid, 128, 0, (cudaStream_t)stream>>>(*a);
+  rc = check_launch("k_elem_error");
+  if (rc || a->total == nullptr) return rc;
+  k_fixed_total<<<1, 256, 0, (cudaStream_t)stream>>>(a->err2, geo.nloc, a->total);
+  return check_launch("k_fixed_total");
+}
+
+int ihdg_face_energy(const ihdg_face_energy_args* a, void* stream) {
+  if (a == nullptr || a->t == nullptr || a->chol1d == nullptr || a->e2 == nullptr)
+    return set_err(IHDG_ERR_ARG, "null args");
+  int rc = check_geom(a->g);
+  if (rc) return rc;
+  if (a->g.order + 1 > 8) return set_err(IHDG_ERR_ARG, "order out of range (p <= 7)");
+  Geo geo;
+  geo.init(a->g, 1);
+  if (geo.lb != 0 || geo.le != geo.c[geo.D - 1]) return set_err(IHDG_ERR_ARG, "face energy needs the whole mesh");
+  int64_t nfaces = 0;
+  for (int ax = 0; ax < geo.D; ++ax) {
+    int64_t ntan = 1;
+    for (int b = 0; b < geo.D; ++b)
+      if (b != ax) ntan *= geo.c[b];
+    nfaces += (geo.c[ax] + (geo.per[ax] ? 0 : 1)) * ntan;
+  }
+  int64_t grid = (nfaces + 127) / 128;
+  if (grid > 8 * num_sms()) grid = 8 * num_sms();
+  if (grid < 1) grid = 1;
+  k_face_energy<<<(unsigned)grid, 128, 0, (cudaStream_t)stream>>>(*a);
+  rc = check_launch("k_face_energy");
+  if (rc || a->total == nullptr) return rc;
+  k_fixed_total<<<1, 256, 0, (cudaStream_t)stream>>>(a->e2, nfaces, a->total);
+  return check_launch("k_fixed_total");
+}
 
 static int iterate_impl(const ihdg_sweep_args* a0, const ihdg_error_args* e0, double* buf0, double* buf1,
                         int32_t batch, void* stream, ihdg_iter_state* state_out, int64_t* n_launched);

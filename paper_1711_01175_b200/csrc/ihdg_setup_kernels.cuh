@@ -459,4 +459,125 @@ __global__ void k_error_norm(const ihdg_error_args a) {
   }
 }
 
+
+// ---------------------------------------------------------------------------
+// K6: per-iteration diagnostics of iteration.run (SPEC.md:320-323, 341-349,
+// 398).  Diagnostic mode only (the reference computes them single-threaded
+// after the barrier); not on the sweep path.
+// ---------------------------------------------------------------------------
+
+// err2[e] = J sum_c comp_w[c] |(C^T x .. x C^T)(u - r)_{e,c}|^2, one element
+// per CTA pass: the difference is staged in shared memory and one exact
+// triangular pass per axis runs over the node lines (same factorisation as
+// the sweep's stopping norm, M1 = C C^T).
+__global__ void k_elem_error(const ihdg_elem_error_args a) {
+  __shared__ double x_s[IHDG_MAX_COMP * 512];
+  __shared__ double c_s[64];
+  __shared__ double red[128];
+  const int d = a.g.dim, n1 = a.g.order + 1, m = a.g.ncomp;
+  int np = 1;
+  for (int i = 0; i < d; ++i) np *= n1;
+  const int nv = m * np, lpl = np / n1;
+  for (int i = threadIdx.x; i < n1 * n1; i += blockDim.x) c_s[i] = a.chol1d[i];
+  Geo geo;
+  geo.init(a.g, 1);
+  const double* u = a.u + geo.ls * nv;
+  const double* r = a.r + geo.ls * nv;
+  __syncthreads();
+  for (int64_t e = blockIdx.x; e < geo.nloc; e += gridDim.x) {
+    for (int i = threadIdx.x; i < nv; i += blockDim.x) x_s[i] = u[e * nv + i] - r[e * nv + i];
+    __syncthreads();
+    double acc = 0.0;
+    int mul = 1;
+    for (int ax = 0; ax < d; ++ax) {
+      const bool last_ax = ax == d - 1;
+      for (int ln = threadIdx.x; ln < m * lpl; ln += blockDim.x) {
+        const int c = ln / lpl;
+        int rem = ln - c * lpl, base = c * np, mb = 1;
+        for (int b = 0; b < d; ++b) {
+          if (b != ax) {
+            base += (rem % n1) * mb;
+            rem /= n1;
+          }
+          mb *= n1;
+        }
+        double xv[8];
+        for (int i = 0; i < n1; ++i) xv[i] = x_s[base + i * mul];
+        for (int i = 0; i < n1; ++i) {
+          double y = 0.0;
+          for (int ip = i; ip < n1; ++ip) y = fma(c_s[ip * n1 + i], xv[ip], y);
+          if (last_ax) acc = fma(a.comp_w[c] * y, y, acc);
+          else x_s[base + i * mul] = y;
+        }
+      }
+      __syncthreads();
+      mul *= n1;
+    }
+    red[threadIdx.x] = acc;
+    __syncthreads();
+    for (int w = 64; w > 0; w >>= 1) {
+      if ((int)threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+      const double e2 = a.jac * red[0];
+      a.err2[e] = e2;
+      if (a.flags != nullptr) a.flags[e] = (uint8_t)(e2 < a.tol * a.tol ? 1 : 0);
+    }
+    __syncthreads();
+  }
+}
+
+// e2[f] = Jf_axis |(C^T x .. x C^T) t_f|^2 for every face of t (mesh.py face
+// order, as written by k_extract_trace)
+__global__ void k_face_energy(const ihdg_face_energy_args a) {
+  Geo geo;
+  geo.init(a.g, 1);
+  const int D = geo.D, n1 = a.g.order + 1;
+  int nf = 1;
+  for (int i = 0; i < D - 1; ++i) nf *= n1;
+  int64_t off[4] = {0, 0, 0, 0};
+  for (int ax = 0; ax < D; ++ax) {
+    int64_t ntan = 1;
+    for (int b = 0; b < D; ++b)
+      if (b != ax) ntan *= geo.c[b];
+    off[ax + 1] = off[ax] + (geo.c[ax] + (geo.per[ax] ? 0 : 1)) * ntan;
+  }
+  for (int64_t f = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; f < off[D];
+       f += (int64_t)gridDim.x * blockDim.x) {
+    int ax = 0;
+    while (f >= off[ax + 1]) ++ax;
+    double x[64];
+    for (int i = 0; i < nf; ++i) x[i] = a.t[f * nf + i] - (a.t_ref != nullptr ? a.t_ref[f * nf + i] : 0.0);
+    // tangential passes: axis 0 of the face (fastest), then axis 1
+    double acc = 0.0;
+    if (D == 1) {
+      acc = x[0] * x[0];
+    } else {
+      const int nt = D - 1;
+      int mul = 1;
+      for (int b = 0; b < nt; ++b) {
+        const bool last_b = b == nt - 1;
+        for (int ln = 0; ln < nf / n1; ++ln) {
+          const int base = (b == 0) ? ln * n1 : ln;
+          for (int i = 0; i < n1; ++i) {
+            double y = 0.0;
+            for (int ip = i; ip < n1; ++ip) y = fma(a.chol1d[ip * n1 + i], x[base + ip * mul], y);
+            if (last_b) acc = fma(y, y, acc);
+            else x[base + i * mul] = y;  // in place: later rows read only ip >= i' > i
+          }
+        }
+        mul *= n1;
+      }
+    }
+    a.e2[f] = a.jac_face[ax] * acc;
+  }
+}
+
+// *out = fixed-order sum of n values (one CTA)
+__global__ void k_fixed_total(const double* v, int64_t n, double* out) {
+  const double s = fixed_sum(v, n);
+  if (threadIdx.x == 0) *out = s;
+}
+
 }  // namespace ihdg

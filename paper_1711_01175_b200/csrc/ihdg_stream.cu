@@ -164,9 +164,20 @@ struct StreamEntry {
 #define IHDG_STREAM(D, N1, M, NCF, NWC, E, NS, G) \
   {D, N1, M, NCF, NWC, E, M * Pow<N1, D>::v, launch_stream_t<D, N1, M, NCF, NWC, E, NS, G>, 0, 0},
 
+// config-4 v3 shape (A/B builds override it): stages, consumer warps, prep warps
+#ifndef IHDG_C4_NS
+#define IHDG_C4_NS 16
+#endif
+#ifndef IHDG_C4_NCW
+#define IHDG_C4_NCW 6
+#endif
+#ifndef IHDG_C4_NQW
+#define IHDG_C4_NQW 4
+#endif
+
 const StreamEntry kStream[] = {
     IHDG_V3(2, 5, 3, 4, 2, 16, 8, 2, 2)    // configs 2/3: CD / SW 2D p=4
-    IHDG_V3(3, 4, 1, 3, 1, 16, 6, 4, 4)    // config 4: transport 3D p=3
+    IHDG_V3(3, 4, 1, 3, 1, IHDG_C4_NS, IHDG_C4_NCW, 4, IHDG_C4_NQW)  // config 4: transport 3D p=3
     IHDG_WS2(7, 3, 4, 2, 16, 6)            // config 5: CD 2D p=6 (ws2: s / u^{k+1} bypass smem)
     IHDG_WS3(7, 3, 4, 2, 16, IHDG_WS3_NS)  // config 5: CD 2D p=6 (ws3: q in the consumers, DFMA norm warps)
     {2, 7, 3, 4, 2, 16, 147, launch_ws4_t<7, 3, 4, 2, IHDG_WS4_NS>, 0, 2},  // config 5 (ws4: two consumer teams)

@@ -418,24 +418,93 @@ class DeviceSolver:
         self.cur = 1 - self.cur
 
     # -- output ------------------------------------------------------------
-    def trace(self) -> np.ndarray:
-        """Single-valued trace (n_faces, 1, N_f) in mesh.py face order."""
+    def _whole_mesh(self, what: str) -> None:
         if self.layers != (0, self.mesh.cells[self.mesh.dim - 1]):
-            raise NotImplementedError("trace of a partitioned mesh: gather the state first")
+            raise NotImplementedError(f"{what} of a partitioned mesh: gather the state first")
+
+    @property
+    def primary_comp(self) -> int:
+        """Component carrying the single-valued trace (phi for shallow water, u otherwise)."""
+        labels = self.spec.labels
+        return labels.index("phi") if "phi" in labels else labels.index("u")
+
+    def trace_of(self, buf=None, jump: bool = False):
+        """Face array (n_faces, N_f) on the device, mesh.py face order, of the
+        ghost-padded state ``buf`` (default: the current iterate).  jump=False:
+        the single-valued trace; jump=True: u^- - u^+ of the primary component on
+        interior faces (0 on boundary faces)."""
+        self._whole_mesh("trace")
         sp = self.spec
         nf = sp.n1 ** (self.mesh.dim - 1)
         out = self.torch.zeros((self.mesh.n_faces, nf), dtype=self.torch.float64, device=self.device)
         a = N.TraceArgs()
         a.g = self.geom
-        a.u, a.trace = _ptr(self.u[self.cur]), _ptr(out)
+        a.u, a.trace = _ptr(self.u[self.cur] if buf is None else buf), _ptr(out)
+        pc = self.primary_comp
         for ax in range(3):
             for c in range(4):
-                a.w_int_own[ax][c] = float(sp.trace_w["int_own"][ax, c])
-                a.w_int_nbr[ax][c] = float(sp.trace_w["int_nbr"][ax, c])
-                a.w_lo[ax][c] = float(sp.trace_w["lo"][ax, c])
-                a.w_hi[ax][c] = float(sp.trace_w["hi"][ax, c])
+                if jump:
+                    a.w_int_own[ax][c] = 1.0 if c == pc else 0.0
+                    a.w_int_nbr[ax][c] = -1.0 if c == pc else 0.0
+                    a.w_lo[ax][c] = a.w_hi[ax][c] = 0.0
+                else:
+                    a.w_int_own[ax][c] = float(sp.trace_w["int_own"][ax, c])
+                    a.w_int_nbr[ax][c] = float(sp.trace_w["int_nbr"][ax, c])
+                    a.w_lo[ax][c] = float(sp.trace_w["lo"][ax, c])
+                    a.w_hi[ax][c] = float(sp.trace_w["hi"][ax, c])
         N.check(self.L.ihdg_extract_trace(C.byref(a), self._sptr), "ihdg_extract_trace")
-        return out.cpu().numpy().reshape(self.mesh.n_faces, 1, nf)
+        return out
+
+    def trace(self) -> np.ndarray:
+        """Single-valued trace (n_faces, 1, N_f) in mesh.py face order."""
+        t = self.trace_of()
+        return t.cpu().numpy().reshape(self.mesh.n_faces, 1, t.shape[1])
+
+    # -- diagnostics (K6; SPEC.md:320-323, 341-349, 398) ---------------------
+    def padded_copy(self, data=None):
+        """Ghost-padded device copy of the current iterate, or of a host
+        FieldState array (Nel, m, Np) / (Nel, nv)."""
+        if data is None:
+            return self.u[self.cur].clone()
+        out = self.torch.zeros_like(self.u[0])
+        arr = np.ascontiguousarray(np.asarray(data, dtype=np.float64).reshape(self.nloc, self.nv))
+        out[self.ls: self.ls + self.nloc].copy_(self.torch.from_numpy(arr))
+        return out
+
+    def element_errors(self, ref, tol: float, buf=None):
+        """Per-element ||u_K - r_K||^2_{L2(K)} (all components, the successive
+        norm's weights) and the converged flags (< tol) on the device;
+        returns (err2, flags, total)."""
+        torch = self.torch
+        if getattr(self, "_diag_err2", None) is None:
+            self._diag_err2 = torch.zeros(self.nloc, dtype=torch.float64, device=self.device)
+            self._diag_flags = torch.zeros(self.nloc, dtype=torch.uint8, device=self.device)
+            self._diag_tot = torch.zeros(2, dtype=torch.float64, device=self.device)
+        a = N.ElemErrorArgs()
+        a.g = self.geom
+        a.u = _ptr(self.u[self.cur] if buf is None else buf)
+        a.r, a.chol1d = _ptr(ref), _ptr(self.chol)
+        a.err2, a.flags, a.total = _ptr(self._diag_err2), _ptr(self._diag_flags), _ptr(self._diag_tot)
+        for c in range(4):
+            a.comp_w[c] = float(self.spec.comp_w[c])
+        a.jac, a.tol = self.spec.jac, float(tol)
+        N.check(self.L.ihdg_elem_error(C.byref(a), self._sptr), "ihdg_elem_error")
+        return self._diag_err2, self._diag_flags, float(self._diag_tot[0].item())
+
+    def face_energy(self, t, t_ref=None) -> float:
+        """sum_f ||t_f - t_ref_f||^2_{L2(f)} over the skeleton (face arrays from trace_of)."""
+        torch = self.torch
+        if getattr(self, "_diag_e2", None) is None:
+            self._diag_e2 = torch.zeros(self.mesh.n_faces, dtype=torch.float64, device=self.device)
+            self._diag_etot = torch.zeros(2, dtype=torch.float64, device=self.device)
+        a = N.FaceEnergyArgs()
+        a.g = self.geom
+        a.t, a.t_ref = _ptr(t), (_ptr(t_ref) if t_ref is not None else None)
+        a.chol1d, a.e2, a.total = _ptr(self.chol), _ptr(self._diag_e2), _ptr(self._diag_etot)
+        for i in range(3):
+            a.jac_face[i] = float(self.spec.jac_face[i])
+        N.check(self.L.ihdg_face_energy(C.byref(a), self._sptr), "ihdg_face_energy")
+        return float(self._diag_etot[0].item())
 
 
 class DistributedSweeper:
