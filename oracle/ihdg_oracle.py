@@ -698,6 +698,72 @@ class OracleSolver:
                 out.append(tr)
         return np.concatenate(out, axis=0)[:, None, :]
 
+    # -- diagnostics ------------------------
+    def elem_errors(self, u, ref):
+        """Per-element ||u_K - r_K||^2_{L2(K)} by quadrature, all components."""
+        vals = (np.asarray(u) - np.asarray(ref)).reshape(self.nel, self.m, self.npn) @ self.el.Phi.T
+        return np.einsum("emq,q->e", vals * vals, self.el.W)
+
+    def face_energy(self, t, t_ref=None):
+        """sum_f ||t_f - t_ref_f||^2_{L2(f)} for face-node arrays in mesh.py face
+        order (as returned by trace()), by face Gauss quadrature."""
+        d = self.prob.dim
+        t = np.asarray(t, float).reshape(t.shape[0], -1)
+        if t_ref is not None:
+            t = t - np.asarray(t_ref, float).reshape(t.shape)
+        b = self.b
+        Vf = _kron_axes([b.V] * (d - 1)) if d > 1 else np.ones((1, 1))
+        wf = _kron_axes([b.qw[:, None]] * (d - 1))[:, 0] if d > 1 else np.ones(1)
+        tot, off = 0.0, 0
+        for a in range(d):
+            ntan = int(np.prod([self.cells[c] for c in range(d) if c != a])) if d > 1 else 1
+            nfa = (self.cells[a] + (0 if self.periodic[a] else 1)) * ntan
+            Jf = float(np.prod([self.h[c] / 2 for c in range(d) if c != a]))
+            v = t[off: off + nfa] @ Vf.T
+            tot += Jf * float(np.sum((v * v) @ wf))
+            off += nfa
+        return tot
+
+    def jump_faces(self, u, comp):
+        """u^- - u^+ of component ``comp`` at the face nodes of every face
+        (0 on boundary faces), mesh.py face order."""
+        d = self.prob.dim
+        cells = self.cells
+        u = np.asarray(u, float).reshape(self.nel, self.m, self.npn)[:, comp, :]
+        strides = [int(np.prod(cells[:a])) for a in range(d)]
+        out = []
+        for a in range(d):
+            tang = [b for b in range(d) if b != a]
+            ntan = int(np.prod([cells[b] for b in tang])) if tang else 1
+            planes = cells[a] + (0 if self.periodic[a] else 1)
+            base = np.zeros(ntan, dtype=np.int64)
+            rem = np.arange(ntan)
+            for b in tang:
+                base += (rem % cells[b]) * strides[b]
+                rem //= cells[b]
+            Phi_hi, Phi_lo = self.el.Pn[2 * a + 1], self.el.Pn[2 * a]
+            for pl in range(planes):
+                if self.periodic[a] or 0 < pl < cells[a]:
+                    lower = pl - 1 if pl > 0 else cells[a] - 1
+                    eo = base + lower * strides[a]
+                    en = base + (pl % cells[a]) * strides[a]
+                    out.append(u[eo] @ Phi_hi.T - u[en] @ Phi_lo.T)
+                else:
+                    out.append(np.zeros((ntan, Phi_hi.shape[0])))
+        return np.concatenate(out, axis=0)
+
+    def diagnostics(self, hist, ref, tol=1e-10):
+        """Per-iteration trace energy, jump norm and converged-element map of
+        a run(keep_history=True) history against the reference state."""
+        comp = 0 if self.prob.kind != "cd" else self.prob.dim
+        t_ref = self.trace(ref)
+        energy, jump, maps = [], [], []
+        for u in hist[1:]:
+            energy.append(np.sqrt(self.face_energy(self.trace(u), t_ref)))
+            jump.append(np.sqrt(self.face_energy(self.jump_faces(u, comp))))
+            maps.append(self.elem_errors(u, ref) < tol * tol)
+        return dict(trace_energy=np.array(energy), jump_norm=np.array(jump), maps=maps)
+
     # -- C sweep (CPU baseline / `_sweep_cy` role) --------------------------
     def c_sweep_data(self):
         """Compressed neighbour blocks + LU factors for oracle/sweep.c."""

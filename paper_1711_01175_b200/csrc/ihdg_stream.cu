@@ -172,7 +172,7 @@ struct StreamEntry {
 #define IHDG_C4_NCW 6
 #endif
 #ifndef IHDG_C4_NQW
-#define IHDG_C4_NQW 4
+#define IHDG_C4_NQW 8
 #endif
 
 const StreamEntry kStream[] = {

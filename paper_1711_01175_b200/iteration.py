@@ -20,7 +20,11 @@ from .basis import ElementOperators, FieldState
 from .pde import ConvectionDiffusionProblem, FourierModes, GaussianBump, ShallowWaterProblem, TransportProblem
 from .solver import DeviceSolver
 
-__all__ = ["IterationConfig", "IterationReport", "run", "run_time_dependent", "default_max_iters"]
+__all__ = ["IterationConfig", "IterationReport", "run", "run_time_dependent", "default_max_iters",
+           "layer_convergence_map", "write_history_csv", "HISTORY_COLUMNS"]
+
+HISTORY_COLUMNS = ("iteration", "l2_error", "successive_norm", "trace_energy", "converged_elements",
+                   "elapsed_ms")
 
 
 @dataclass
@@ -38,6 +42,11 @@ class IterationConfig:
     workers: Optional[int] = None      # API parity; the device owns parallelism
     check_every: int = 16              # sweeps per host poll of the device flag
     diverge_factor: float = 1e6
+    # per-iteration diagnostics: sweep-by-sweep,
+    # against ``reference`` (the converged HDG solution; computed by a first
+    # solve from the same initial guess when None)
+    diagnostics: bool = False
+    reference: object = None
 
     def __post_init__(self):
         if not self.tol > 0:
@@ -109,6 +118,107 @@ def _set_initial(solver: DeviceSolver, init):
         raise TypeError(f"unsupported initial guess {type(init).__name__}")
 
 
+def _diagnostic_iterate(solver: DeviceSolver, cfg: IterationConfig, norm: str, max_iters: int) -> dict:
+    """Algorithm 1 one sweep at a time with the per-iteration diagnostics of
+    SPEC.md:321 on the device (K6): successive norm, L2 error vs exact (when
+    known), trace energy ||u_hat(u^k) - u_hat(r)||_{L2(E_h)}, skeleton jump
+    norm ||u^- - u^+||_{L2(E_h)} of the trace variable, and the element
+    convergence map {K : ||u^k - r||_{L2(K)} < tol}.  r is cfg.reference or the
+    converged solution of a first (batched) solve from the same iterate."""
+    import ctypes as C
+    from . import _native as N
+    torch = solver.torch
+    start = solver.padded_copy()
+    cur0 = solver.cur
+    if cfg.reference is not None:
+        ref_data = cfg.reference.data if isinstance(cfg.reference, FieldState) else cfg.reference
+        ref = solver.padded_copy(ref_data)
+    else:
+        pre = solver.iterate(tol=cfg.tol, max_iters=max_iters, norm=norm, batch=cfg.check_every)
+        if pre.status != "converged":
+            raise RuntimeError(f"diagnostics: the reference solve did not converge ({pre.status})")
+        ref = solver.padded_copy()
+        solver.cur = cur0
+        solver.u[cur0].copy_(start)
+    t_ref = solver.trace_of(ref)
+    has_exact = getattr(solver, "ue_q", None) is not None
+    solver.reset_state(cfg.tol, max_iters, cfg.diverge_factor)
+    if norm == "exact":
+        N.check(solver.L.ihdg_error_norm(C.byref(solver._error_args(0)), solver._sptr), "ihdg_error_norm")
+        a = solver.sweep_args("volume", finalize=0)
+    else:
+        a = solver.sweep_args(norm, finalize=1)
+    cols = {k: [] for k in HISTORY_COLUMNS}
+    maps = []
+    t0 = time.perf_counter()
+    status = "running"
+    for k in range(1, max_iters + 1):
+        solver.sweep_once(a=a)
+        if norm == "exact":
+            e = solver._error_args(1)
+            N.check(solver.L.ihdg_error_norm(C.byref(e), solver._sptr), "ihdg_error_norm")
+        st = solver.read_state()
+        err = float("nan")
+        if norm == "exact":
+            err = st.last_err
+        elif has_exact:
+            e = solver._error_args(0)
+            N.check(solver.L.ihdg_error_norm(C.byref(e), solver._sptr), "ihdg_error_norm")
+            err = solver.read_state().last_err
+        energy = np.sqrt(solver.face_energy(solver.trace_of(), t_ref))
+        _, flags, _ = solver.element_errors(ref, cfg.tol)
+        fl = flags.cpu().numpy().astype(bool)
+        maps.append(fl)
+        cols["iteration"].append(k)
+        cols["l2_error"].append(err)
+        cols["successive_norm"].append(st.last_norm)
+        cols["trace_energy"].append(energy)
+        cols["converged_elements"].append(int(fl.sum()))
+        cols["elapsed_ms"].append((time.perf_counter() - t0) * 1e3)
+        cols.setdefault("jump_norm", []).append(np.sqrt(solver.face_energy(solver.trace_of(jump=True))))
+        status = N.STATUS_NAMES[st.status]
+        if st.status != N.RUNNING:
+            break
+    hist = {k: np.asarray(v) for k, v in cols.items()}
+    return dict(iterations=len(maps), status=status, history=hist, maps=maps, first_norm=st.first_norm,
+                last_norm=st.last_norm, contraction=contraction_factor(hist["trace_energy"], cfg.tol),
+                seconds=time.perf_counter() - t0)
+
+
+def contraction_factor(energy, tol: float = 1e-10) -> float:
+    """Measured contraction factor: geometric mean of the
+    successive trace-energy ratios E_{k+1}/E_k after the first iteration,
+    over the energies above 1e3 * tol (below that the reference solution's
+    own stopping error dominates)."""
+    e = np.asarray(energy, dtype=float)
+    r = [e[k + 1] / e[k] for k in range(1, len(e) - 1) if e[k] > 0 and e[k + 1] > 1e3 * tol]
+    return float(np.exp(np.mean(np.log(r)))) if r else float("nan")
+
+
+def layer_convergence_map(report: "IterationReport") -> list:
+    """per-iteration converged-element sets (element ids in
+    mesh order) of a run with cfg.diagnostics=True."""
+    maps = report.extra.get("convergence_map")
+    if maps is None:
+        raise ValueError("layer_convergence_map needs a run with IterationConfig(diagnostics=True)")
+    return [set(np.flatnonzero(m).tolist()) for m in maps]
+
+
+def write_history_csv(report: "IterationReport", path) -> None:
+    """Per-iteration CSV rows: iteration, l2_error,
+    successive_norm, trace_energy, converged_elements, elapsed_ms."""
+    import csv
+    hist = report.extra.get("history")
+    if hist is None:
+        raise ValueError("write_history_csv needs a run with IterationConfig(diagnostics=True)")
+    with open(path, "w", newline="") as fh:
+        w = csv.writer(fh)
+        w.writerow(HISTORY_COLUMNS)
+        for i in range(len(hist["iteration"])):
+            w.writerow([int(hist["iteration"][i])] + [repr(float(hist[c][i])) for c in HISTORY_COLUMNS[1:4]]
+                       + [int(hist["converged_elements"][i]), f"{hist['elapsed_ms'][i]:.3f}"])
+
+
 def run(mesh, problem, ops: ElementOperators, cfg: Optional[IterationConfig] = None,
         solver: Optional[DeviceSolver] = None, return_state: bool = True,
         return_trace: bool = True) -> IterationReport:
@@ -124,8 +234,11 @@ def run(mesh, problem, ops: ElementOperators, cfg: Optional[IterationConfig] = N
         solver.set_forcing(forcing)
     solver.prepare_steady()
     _set_initial(solver, cfg.initial_guess)
-    if cfg.stop == "exact":
+    if cfg.stop == "exact" or (cfg.diagnostics and getattr(problem, "exact", None) is not None):
         solver.set_exact(_exact_at(problem.exact, None))
+    if cfg.diagnostics:
+        return _diagnostic_report(solver, cfg, _norm_name(cfg, problem), cfg.max_iters or default_max_iters(mesh),
+                                  t0, return_state, return_trace)
     res = solver.iterate(tol=cfg.tol, max_iters=cfg.max_iters or default_max_iters(mesh),
                          norm=_norm_name(cfg, problem), batch=cfg.check_every)
     state = FieldState(solver.get_state(), solver.spec.labels, k=res.iterations) if return_state else None
@@ -134,6 +247,19 @@ def run(mesh, problem, ops: ElementOperators, cfg: Optional[IterationConfig] = N
     return IterationReport(res.iterations, res.status, res.norms, time.perf_counter() - t0,
                            state, tr, res.first_norm, res.last_norm, res.launched,
                            extra={"device_seconds": res.seconds, "l2_errors": res.errors})
+
+
+def _diagnostic_report(solver, cfg, norm, max_iters, t0, return_state, return_trace, extra=None):
+    d = _diagnostic_iterate(solver, cfg, norm, max_iters)
+    h = d["history"]
+    state = FieldState(solver.get_state(), solver.spec.labels, k=d["iterations"]) if return_state else None
+    tr = solver.trace() if return_trace else None
+    ex = {"device_seconds": d["seconds"], "l2_errors": h["l2_error"], "history": h,
+          "convergence_map": d["maps"], "contraction_factor": d["contraction"],
+          "trace_energy": h["trace_energy"], "jump_norm": h["jump_norm"]}
+    ex.update(extra or {})
+    return IterationReport(d["iterations"], d["status"], h["successive_norm"], time.perf_counter() - t0,
+                           state, tr, d["first_norm"], d["last_norm"], d["iterations"], extra=ex)
 
 
 def run_time_dependent(mesh, problem, ops: ElementOperators, cfg: Optional[IterationConfig],
@@ -164,8 +290,18 @@ def run_time_dependent(mesh, problem, ops: ElementOperators, cfg: Optional[Itera
     for m in range(n_steps):
         t0 = time.perf_counter()
         solver.begin_step()
-        if cfg.stop == "exact":
+        if cfg.stop == "exact" or (cfg.diagnostics and getattr(problem, "exact", None) is not None):
             solver.set_exact(_exact_at(problem.exact, (m + 1) * dt))
+        if cfg.diagnostics:
+            rep = _diagnostic_report(solver, cfg, _norm_name(cfg, problem),
+                                     cfg.max_iters or default_max_iters(mesh), t0,
+                                     keep_states or m == n_steps - 1, False, extra={"step": m + 1})
+            if rep.state is not None:
+                rep.state.m = m + 1
+            reports.append(rep)
+            if rep.status != "converged":
+                break
+            continue
         res = solver.iterate(tol=cfg.tol, max_iters=cfg.max_iters or default_max_iters(mesh),
                              norm=_norm_name(cfg, problem), batch=cfg.check_every)
         last = m == n_steps - 1 or res.status != "converged"

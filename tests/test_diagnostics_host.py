@@ -1,0 +1,80 @@
+"""Host side of the per-iteration diagnostics (no GPU): the oracle's layer
+map against SPEC.md:346-348, its trace-energy / jump restatement against
+direct quadrature, and the report helpers (contraction factor, CSV, map)."""
+
+import csv
+
+import numpy as np
+import pytest
+
+
+def _oracle_transport(dim, cells, p, beta, seed=5):
+    from oracle.ihdg_oracle import OracleProblem, OracleSolver
+    from paper_1711_01175_b200.workloads import fourier_modes
+
+    S = OracleSolver(OracleProblem("transport", dim, beta=np.array(beta, float)), cells, p)
+    S.set_forcing(fourier_modes(np.random.default_rng(seed), dim))
+    return S
+
+
+def test_oracle_layer_map_4x4():
+    """SPEC.md:346-347 on the oracle: 7 layers to coverage, corner first."""
+    S = _oracle_transport(2, [4, 4], 2, [1.0, 1.0])
+    o = S.run(tol=1e-10, keep_history=True)
+    maps = S.diagnostics(o["history"], o["u"])["maps"]
+    assert np.flatnonzero(maps[0]).tolist() == [0]
+    assert next(j for j, m in enumerate(maps, 1) if m.all()) == 7
+
+
+def test_oracle_layer_map_1d():
+    """element j converged at iteration j."""
+    S = _oracle_transport(1, [5], 2, [1.0])
+    o = S.run(tol=1e-10, keep_history=True)
+    maps = S.diagnostics(o["history"], o["u"])["maps"]
+    for j in range(1, 6):
+        assert np.flatnonzero(maps[j - 1]).tolist() == list(range(j))
+
+
+def test_oracle_face_energy_of_constant_trace():
+    """||1||^2 over the skeleton = total face measure (2D: 2 N (N+1) h)."""
+    S = _oracle_transport(2, [3, 3], 3, [1.0, 1.0])
+    t = S.trace(np.zeros((S.nel, S.nv)))
+    ones = np.ones_like(t)
+    n, h = 3, 1.0 / 3
+    assert np.isclose(S.face_energy(ones), 2 * n * (n + 1) * h, rtol=1e-13)
+    assert S.face_energy(ones, ones) == 0.0
+
+
+def test_oracle_jump_of_continuous_field_is_zero():
+    """A globally continuous polynomial (degree <= p) has no skeleton jump."""
+    S = _oracle_transport(2, [3, 2], 2, [1.0, 1.0])
+    u = S.interpolate(lambda x: 1.0 + x[:, 0] * x[:, 1] - x[:, 1] ** 2)
+    assert np.max(np.abs(S.jump_faces(u.reshape(S.nel, -1), 0))) < 1e-13
+
+
+def test_contraction_factor_geometric_mean():
+    from paper_1711_01175_b200.iteration import contraction_factor
+
+    e = 3.0 * 0.5 ** np.arange(12)
+    assert np.isclose(contraction_factor(e), 0.5, rtol=1e-12)
+    assert np.isnan(contraction_factor([1.0]))
+
+
+def test_history_csv_and_map_helpers(tmp_path):
+    from paper_1711_01175_b200.iteration import (HISTORY_COLUMNS, IterationReport, layer_convergence_map,
+                                                 write_history_csv)
+
+    hist = {"iteration": np.array([1, 2]), "l2_error": np.array([np.nan, np.nan]),
+            "successive_norm": np.array([1.0, 1e-11]), "trace_energy": np.array([0.5, 0.0]),
+            "converged_elements": np.array([1, 2]), "elapsed_ms": np.array([0.1, 0.2])}
+    maps = [np.array([True, False]), np.array([True, True])]
+    rep = IterationReport(2, "converged", hist["successive_norm"], 0.0,
+                          extra={"history": hist, "convergence_map": maps})
+    assert layer_convergence_map(rep) == [{0}, {0, 1}]
+    p = tmp_path / "h.csv"
+    write_history_csv(rep, p)
+    rows = list(csv.reader(open(p)))
+    assert tuple(rows[0]) == HISTORY_COLUMNS and len(rows) == 3
+    assert float(rows[2][2]) == 1e-11 and rows[2][4] == "2"
+    with pytest.raises(ValueError):
+        layer_convergence_map(IterationReport(1, "converged", np.zeros(1), 0.0))
