@@ -187,7 +187,7 @@ __global__ void __launch_bounds__(V3Cfg<D, N1, M, NCF, NWC, NS, NCW, PF, NQW_>::
       V3_T0(tl);
       if (lane == 0) {
         STile<D> ti;
-        ti.init(a.g, phys_of(it), E, nlay, lsi);
+        ti.e0 = phys_of(it) * E;   // tiles are E consecutive elements of a row, c0 % E == 0
         constexpr uint32_t bytes = (uint32_t)(E * NV * sizeof(double));
         mbar_arrive_expect_tx(&full_bar[stage], bytes);
         if constexpr (C::ES == NV) {
@@ -213,25 +213,45 @@ __global__ void __launch_bounds__(V3Cfg<D, N1, M, NCF, NWC, NS, NCW, PF, NQW_>::
     const int c0 = (int)a.g.cells[0];
     const int per0 = a.g.periodic[0];
     constexpr int QM = (E * KC + 31) / 32;
+    // per-lane entry constants, hoisted out of the item loop: entry m of this
+    // lane is (element t, column k) with k's face f and its gather offsets /
+    // weights (TraceSnapshot layout, fixed for the launch)
+    int ent_t[QM], ent_f[QM], ent_q[QM][NWC];
+#pragma unroll
+    for (int m = 0; m < QM; ++m) {
+      const int idx = lane + 32 * m;
+      const int t = idx < E * KC ? idx / KC : 0, k = idx < E * KC ? idx - (idx / KC) * KC : 0;
+      ent_t[m] = idx < E * KC ? t : -1;
+      ent_f[m] = qf_s[k];
+#pragma unroll
+      for (int j = 0; j < NWC; ++j) ent_q[m][j] = qt_s[k][j];
+    }
     double gv[QM][NWC], gvn[QM][NWC];
     int qsn = 0;      // bit m: entry m of the next item is an in-tile neighbour
     int qln = 0;      // bit m: entry m of the next item was loaded from global
     int qs = 0, ql = 0;
+    STile<D> tnext;
     auto gather = [&](int itg, double (&dst)[QM][NWC], int& in_tile_bits, int& load_bits) {
       in_tile_bits = 0;
       load_bits = 0;
       if (itg >= n_items) return;
-      STile<D> tg;
+      STile<D>& tg = tnext;
       tg.init(a.g, phys_of(itg), E, nlay, lsi);
+      // missing neighbours: faces of axes >= 1 are tile-uniform, x faces only
+      // at the tile ends
+      int hm = 0;
+#pragma unroll
+      for (int f = 2; f < NFACE; ++f)
+        if (!tg.has[f]) hm |= 1 << f;
+      const bool xlo = !per0 && tg.i0 == 0, xhi = !per0 && tg.i0 + E == c0;
 #pragma unroll
       for (int m = 0; m < QM; ++m) {
-        const int idx = lane + 32 * m;
 #pragma unroll
         for (int j = 0; j < NWC; ++j) dst[m][j] = 0.0;
-        if (idx < E * KC) {
-          const int t = idx / KC, k = idx - (idx / KC) * KC;
-          const int f = qf_s[k];
-          if (!(tg.mask(t, c0, per0) & (1 << f))) {
+        const int t = ent_t[m], f = ent_f[m];
+        if (t >= 0) {
+          const bool miss = f >= 2 ? ((hm >> f) & 1) : (f == 0 ? (t == 0 && xlo) : (t == E - 1 && xhi));
+          if (!miss) {
             const bool in_tile = (f >> 1) == 0 && !((f == 0 && t == 0) || (f == 1 && t == E - 1));
             if (in_tile) {
               in_tile_bits |= 1 << m;
@@ -246,7 +266,7 @@ __global__ void __launch_bounds__(V3Cfg<D, N1, M, NCF, NWC, NS, NCW, PF, NQW_>::
               }
               const double* src = uo + (int64_t)nb * NV;
 #pragma unroll
-              for (int j = 0; j < NWC; ++j) dst[m][j] = __ldg(src + qt_s[k][j]);
+              for (int j = 0; j < NWC; ++j) dst[m][j] = __ldg(src + ent_q[m][j]);
             }
           }
         }
@@ -255,9 +275,8 @@ __global__ void __launch_bounds__(V3Cfg<D, N1, M, NCF, NWC, NS, NCW, PF, NQW_>::
     gather(pw, gv, qs, ql);
     for (int it = pw; it < n_items; it += NQW) {
       const int stage = it % NS;
+      const STile<D> ti = tnext;   // geometry of item it (computed by its gather)
       gather(it + NQW, gvn, qsn, qln);
-      STile<D> ti;
-      ti.init(a.g, phys_of(it), E, nlay, lsi);
       V3_T0(tp);
       mbar_wait(&full_bar[stage], (it / NS) & 1);
       V3_ACC(1, tp);
@@ -283,19 +302,18 @@ __global__ void __launch_bounds__(V3Cfg<D, N1, M, NCF, NWC, NS, NCW, PF, NQW_>::
       double* qst = sm + stage * C::STAGE + TILE;
 #pragma unroll
       for (int m = 0; m < QM; ++m) {
-        const int idx = lane + 32 * m;
-        if (idx < E * KC) {
-          const int t = idx / KC, k = idx - (idx / KC) * KC;
-          const int ci = k / NF;
+        const int t = ent_t[m];
+        if (t >= 0) {
+          const int k = lane + 32 * m - t * KC;
+          const double* w = ww_s[k / NF];
           double v = 0.0;
           if (qs & (1 << m)) {
-            const int f = qf_s[k];
-            const double* src = ust + (t + (f == 0 ? -1 : 1)) * C::ES;
+            const double* src = ust + (t + (ent_f[m] == 0 ? -1 : 1)) * C::ES;
 #pragma unroll
-            for (int j = 0; j < NWC; ++j) v = fma(ww_s[ci][j], src[qt_s[k][j]], v);
+            for (int j = 0; j < NWC; ++j) v = fma(w[j], src[ent_q[m][j]], v);
           } else if (ql & (1 << m)) {
 #pragma unroll
-            for (int j = 0; j < NWC; ++j) v = fma(ww_s[ci][j], gv[m][j], v);
+            for (int j = 0; j < NWC; ++j) v = fma(w[j], gv[m][j], v);
           }
           qst[t * C::KCP + k] = v;
         }
@@ -319,9 +337,7 @@ __global__ void __launch_bounds__(V3Cfg<D, N1, M, NCF, NWC, NS, NCW, PF, NQW_>::
     double acc[NRT][2], accn[C::PREF ? NRT : 1][2];
     auto load_s = [&](int it_load, double (&dst)[NRT][2]) {
       if (it_load < n_items) {
-        STile<D> tl;
-        tl.init(a.g, phys_of(it_load), E, nlay, lsi);
-        const double* sg = a.s + (int64_t)tl.e0 * NV;
+        const double* sg = a.s + (int64_t)(phys_of(it_load) * E) * NV;
 #pragma unroll
         for (int rt = 0; rt < NRT; ++rt) {
           const int row = rt * 8 + rsub;
@@ -333,9 +349,7 @@ __global__ void __launch_bounds__(V3Cfg<D, N1, M, NCF, NWC, NS, NCW, PF, NQW_>::
     if constexpr (C::PREF) load_s(warp, acc);
     for (int it = warp; it < n_items; it += NCW) {
       const int stage = it % NS;
-      STile<D> ti;
-      ti.init(a.g, phys_of(it), E, nlay, lsi);
-      const int e0 = ti.e0;
+      const int e0 = phys_of(it) * E;
       if constexpr (C::PREF) load_s(it + NCW, *reinterpret_cast<double(*)[NRT][2]>(&accn[0][0]));
       else load_s(it, acc);
       V3_T0(tc);
