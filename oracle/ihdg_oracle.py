@@ -528,9 +528,43 @@ class OracleSolver:
         c = self.prob.forcing_comp
         self.b_static[:, c * self.npn:(c + 1) * self.npn] = bvals
 
+    def _face_node_ids(self, f):
+        """Volume node indices of local face f (tangential axes increasing,
+        smallest fastest; mesh.py:166-187)."""
+        d, n1 = self.prob.dim, self.p + 1
+        a, s = divmod(f, 2)
+        grid = np.indices([n1] * d).reshape(d, -1)[::-1]   # grid[b] = index along axis b, axis 0 fastest
+        keep = grid[a] == (n1 - 1 if s else 0)
+        return np.flatnonzero(keep)
+
+    def set_inflow(self, g):
+        """Transport inflow data u_ext = g, taken in the
+        trace space: g at the face GLL nodes, interpolated over the face.
+        RHS += <(|b.n| - b.n)/2 g_h, v> on every inflow boundary face."""
+        d = self.prob.dim
+        self.b_inflow = np.zeros((self.nel, self.nv))
+        self.inflow_nodes = {}
+        if g is None:
+            return
+        pts = self.element_points(self.b.nodes)
+        Vf = _kron_axes([self.b.V] * (d - 1)) if d > 1 else np.ones((1, 1))
+        for f in range(2 * d):
+            a, s = divmod(f, 2)
+            bn = self.prob.beta[a] * (1.0 if s else -1.0)
+            if bn >= 0 or self.periodic[a]:
+                continue
+            on = np.flatnonzero(self.nbr[:, f] == BOUNDARY)
+            ids = self._face_node_ids(f)
+            gv = np.asarray(g(pts[on][:, ids, :].reshape(-1, d)), float).reshape(on.size, -1)
+            M = self.el.fmass(f, self.el.Pf[f], Vf)          # (Np, N_f)
+            self.b_inflow[on, :self.npn] += 0.5 * (abs(bn) - bn) * gv @ M.T
+            self.inflow_nodes[f] = (on, gv)
+
     # -- sweep -------------------------------------------------------------
     def rhs_static(self, u_prev=None):
         rhs = self.b_static.copy()
+        if getattr(self, "b_inflow", None) is not None:
+            rhs += self.b_inflow
         if u_prev is not None and self.dt is not None:
             d = self.prob.dim
             for ci, C in enumerate(self.class_list):
@@ -695,6 +729,10 @@ class OracleSolver:
                     else:
                         H = self.class_list[self.cls[eo[0]]]["Hown"][f]
                     tr = u[eo] @ H.T
+                    data = getattr(self, "inflow_nodes", {}).get(f)
+                    if data is not None:   # inflow boundary: u_hat = g
+                        pos = {int(e): i for i, e in enumerate(data[0])}
+                        tr = tr + np.stack([data[1][pos[int(e)]] for e in eo])
                 out.append(tr)
         return np.concatenate(out, axis=0)[:, None, :]
 

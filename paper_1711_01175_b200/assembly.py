@@ -300,9 +300,7 @@ def build_spec(mesh, problem, ops: ElementOperators, dt=None, norm="auto", schem
         nr = ops.n_nodes if dt is not None else 0
         tc0, ntc, fcomp = 0, 1, 0
         comp_w[0] = 1.0
-        if problem.inflow is not None:
-            raise NotImplementedError("non-zero inflow data is not wired to the device path yet")
-        labels = ("u",)
+        labels = ("u",)   # inflow data g enters s as L q_g (DeviceSolver.set_inflow)
     elif isinstance(problem, ConvectionDiffusionProblem):
         beta = problem.beta_const(d)
         if beta is None:

@@ -293,21 +293,40 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS>::NT, 1)
     // global (L2) into registers one tile ahead
     double gv[QM][NWC], gvn[QM][NWC];
     int qs = 0, ql = 0, qsn = 0, qln = 0;
+    // per-lane entry constants, hoisted out of the tile loop: entry m of this
+    // lane is (element t, column k) with k's face f and its gather offsets
+    int ent_t[QM], ent_f[QM], ent_q[QM][NWC];
+#pragma unroll
+    for (int m = 0; m < QM; ++m) {
+      const int idx = lane + 32 * m;
+      const bool ok = idx < HALF * KC;
+      const int k = ok ? idx - (idx / KC) * KC : 0;
+      ent_t[m] = ok ? pw * HALF + idx / KC : -1;
+      ent_f[m] = qf_s[k];
+#pragma unroll
+      for (int j = 0; j < NWC; ++j) ent_q[m][j] = qt_s[k][j];
+    }
     auto gather = [&](int itg, double (&dst)[QM][NWC], int& in_bits, int& ld_bits) {
       in_bits = 0;
       ld_bits = 0;
       if (itg >= n_my) return;
       STile<D> tg;
       tg.init(a.g, (int)blockIdx.x + itg * (int)gridDim.x, E, nlay, lsi);
+      // missing neighbours: faces of axes >= 1 are tile-uniform, x faces only
+      // at the tile ends
+      int hm = 0;
+#pragma unroll
+      for (int f = 2; f < 2 * D; ++f)
+        if (!tg.has[f]) hm |= 1 << f;
+      const bool xlo = !per0 && tg.i0 == 0, xhi = !per0 && tg.i0 + E == c0;
 #pragma unroll
       for (int m = 0; m < QM; ++m) {
-        const int idx = lane + 32 * m;
 #pragma unroll
         for (int j = 0; j < NWC; ++j) dst[m][j] = 0.0;
-        if (idx < HALF * KC) {
-          const int t = pw * HALF + idx / KC, k = idx - (idx / KC) * KC;
-          const int f = qf_s[k];
-          if (!(tg.mask(t, c0, per0) & (1 << f))) {
+        const int t = ent_t[m], f = ent_f[m];
+        if (t >= 0) {
+          const bool miss = f >= 2 ? ((hm >> f) & 1) : (f == 0 ? (t == 0 && xlo) : (t == E - 1 && xhi));
+          if (!miss) {
             const bool in_tile = (f >> 1) == 0 && !((f == 0 && t == 0) || (f == 1 && t == E - 1));
             if (in_tile) {
               in_bits |= 1 << m;
@@ -322,7 +341,7 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS>::NT, 1)
               }
               const double* src = uo + (int64_t)nb * NV;
 #pragma unroll
-              for (int j = 0; j < NWC; ++j) dst[m][j] = __ldg(src + qt_s[k][j]);
+              for (int j = 0; j < NWC; ++j) dst[m][j] = __ldg(src + ent_q[m][j]);
             }
           }
         }
@@ -346,19 +365,18 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS>::NT, 1)
       double* qst = const_cast<double*>(ust) + TILE + C::HALO;
 #pragma unroll
       for (int m = 0; m < QM; ++m) {
-        const int idx = lane + 32 * m;
-        if (idx < HALF * KC) {
-          const int t = pw * HALF + idx / KC, k = idx - (idx / KC) * KC;
-          const int ci = k / NF;
+        const int t = ent_t[m];
+        if (t >= 0) {
+          const int k = lane + 32 * m - (t - pw * HALF) * KC;
+          const double* w = ww_s[k / NF];
           double v = 0.0;
           if (qs & (1 << m)) {
-            const int f = qf_s[k];
-            const double* src = ust + (t + (f == 0 ? -1 : 1)) * NV;
+            const double* src = ust + (t + (ent_f[m] == 0 ? -1 : 1)) * NV;
 #pragma unroll
-            for (int j = 0; j < NWC; ++j) v = fma(ww_s[ci][j], src[qt_s[k][j]], v);
+            for (int j = 0; j < NWC; ++j) v = fma(w[j], src[ent_q[m][j]], v);
           } else if (ql & (1 << m)) {
 #pragma unroll
-            for (int j = 0; j < NWC; ++j) v = fma(ww_s[ci][j], gv[m][j], v);
+            for (int j = 0; j < NWC; ++j) v = fma(w[j], gv[m][j], v);
           }
           qst[ws_qcol<C::NEG>(t) * KC + k] = v;
         }

@@ -21,7 +21,8 @@ from .pde import ConvectionDiffusionProblem, FourierModes, GaussianBump, Shallow
 from .solver import DeviceSolver
 
 __all__ = ["IterationConfig", "IterationReport", "run", "run_time_dependent", "default_max_iters",
-           "layer_convergence_map", "write_history_csv", "HISTORY_COLUMNS"]
+           "layer_convergence_map", "write_history_csv", "HISTORY_COLUMNS", "cfl_number",
+           "contraction_factor"]
 
 HISTORY_COLUMNS = ("iteration", "l2_error", "successive_norm", "trace_energy", "converged_elements",
                    "elapsed_ms")
@@ -90,6 +91,17 @@ def _exact_at(exact, t):
     if t is None:
         return lambda x: exact(x)
     return lambda x: exact(x, t)
+
+
+def _takes_time(fn) -> bool:
+    """True for a data callable of (x, t) (time-dependent forcing / boundary data)."""
+    if fn is None or isinstance(fn, (FourierModes, GaussianBump)):
+        return False
+    import inspect
+    try:
+        return len(inspect.signature(fn).parameters) >= 2
+    except (TypeError, ValueError):
+        return False
 
 
 def _norm_name(cfg: IterationConfig, problem) -> str:
@@ -232,6 +244,8 @@ def run(mesh, problem, ops: ElementOperators, cfg: Optional[IterationConfig] = N
     forcing = getattr(problem, "forcing", None)
     if forcing is not None and solver.s_static is None:
         solver.set_forcing(forcing)
+    if getattr(problem, "inflow", None) is not None:
+        solver.set_inflow(problem.inflow)
     solver.prepare_steady()
     _set_initial(solver, cfg.initial_guess)
     if cfg.stop == "exact" or (cfg.diagnostics and getattr(problem, "exact", None) is not None):
@@ -247,6 +261,19 @@ def run(mesh, problem, ops: ElementOperators, cfg: Optional[IterationConfig] = N
     return IterationReport(res.iterations, res.status, res.norms, time.perf_counter() - t0,
                            state, tr, res.first_norm, res.last_norm, res.launched,
                            extra={"device_seconds": res.seconds, "l2_errors": res.errors})
+
+
+def cfl_number(problem, mesh, p: int, dt: float) -> float:
+    """CFL = |beta|_max dt (p+1)^2 / h (the DG estimate of
+    PAPER.md section 4.4); |beta| is the Euclidean speed, h the smallest
+    element size.  Shallow water uses the gravity-wave speed sqrt(Phi)."""
+    if hasattr(problem, "beta"):
+        speed = float(np.linalg.norm(np.asarray(problem.beta, float)))
+    elif hasattr(problem, "Phi"):
+        speed = float(np.sqrt(problem.Phi))
+    else:
+        speed = 0.0
+    return speed * dt * (p + 1) ** 2 / float(np.min(mesh.h))
 
 
 def _diagnostic_report(solver, cfg, norm, max_iters, t0, return_state, return_trace, extra=None):
@@ -267,11 +294,15 @@ def run_time_dependent(mesh, problem, ops: ElementOperators, cfg: Optional[Itera
                        initial=None, solver: Optional[DeviceSolver] = None,
                        keep_states: bool = False, time_scheme: str = "backward-euler") -> list:
     """Time steps; each step iterates from u^m.
-    ``time_scheme``: "backward-euler" or "crank-nicolson" (trapezoidal split of
-    the spatial operator).  Divergence at any step aborts
-    the run (the last report says which step)."""
+    ``time_scheme``: "backward-euler" (= "locally-implicit": the implicit
+    Euler HDG step solved by iHDG from the initial guess u^m, PAPER.md:593-653,
+    SPEC.md:248) or "crank-nicolson" (trapezoidal split of the spatial
+    operator).  Each report records the step's CFL number
+    (SPEC.md:355, 400).  Divergence at any step aborts the run (the last report
+    says which step)."""
     cfg = cfg or IterationConfig()
-    ts = {"backward-euler": "BE", "be": "BE", "crank-nicolson": "CN", "cn": "CN"}.get(time_scheme.lower())
+    ts = {"backward-euler": "BE", "be": "BE", "locally-implicit": "BE", "crank-nicolson": "CN",
+          "cn": "CN"}.get(time_scheme.lower())
     if ts is None:
         raise ValueError(f"unknown time scheme {time_scheme!r}")
     if n_steps is None:
@@ -283,19 +314,27 @@ def run_time_dependent(mesh, problem, ops: ElementOperators, cfg: Optional[Itera
                               max_iters=cfg.max_iters or default_max_iters(mesh), scheme=cfg.scheme,
                               time_scheme=ts)
     forcing = getattr(problem, "forcing", None)
-    if forcing is not None and solver.s_static is None:
+    f_t = _takes_time(forcing)
+    if forcing is not None and solver.s_static is None and not f_t:
         solver.set_forcing(forcing)
+    inflow = getattr(problem, "inflow", None)
     _set_initial(solver, initial if initial is not None else cfg.initial_guess)
     reports = []
+    cfl = cfl_number(problem, mesh, ops.p, dt)
     for m in range(n_steps):
         t0 = time.perf_counter()
+        t_new = (m + 1) * dt
+        if f_t:        # time-dependent forcing / inflow data at the new level (implicit Euler)
+            solver.set_forcing(_exact_at(forcing, t_new))
+        if inflow is not None:
+            solver.set_inflow(_exact_at(inflow, t_new) if _takes_time(inflow) else inflow)
         solver.begin_step()
         if cfg.stop == "exact" or (cfg.diagnostics and getattr(problem, "exact", None) is not None):
             solver.set_exact(_exact_at(problem.exact, (m + 1) * dt))
         if cfg.diagnostics:
             rep = _diagnostic_report(solver, cfg, _norm_name(cfg, problem),
                                      cfg.max_iters or default_max_iters(mesh), t0,
-                                     keep_states or m == n_steps - 1, False, extra={"step": m + 1})
+                                     keep_states or m == n_steps - 1, False, extra={"step": m + 1, "cfl": cfl})
             if rep.state is not None:
                 rep.state.m = m + 1
             reports.append(rep)
@@ -311,7 +350,7 @@ def run_time_dependent(mesh, problem, ops: ElementOperators, cfg: Optional[Itera
                                        time.perf_counter() - t0, st, None, res.first_norm,
                                        res.last_norm, res.launched,
                                        extra={"step": m + 1, "device_seconds": res.seconds,
-                                              "l2_errors": res.errors}))
+                                              "l2_errors": res.errors, "cfl": cfl}))
         if res.status != "converged":
             break
     return reports

@@ -208,16 +208,24 @@ def upwind_flux_matrix(problem, n, beta=None):
     return np.array([[bn]]), np.array([[abs(bn)]])
 
 
+def _gauss_timedep(x, t):
+    x = np.asarray(x, dtype=float)
+    return np.exp(-5.0 * np.sum((x - 0.35 * t) ** 2, axis=1))
+
+
 def preset_problems():
     """Named presets usable through the same API."""
     s2 = np.sqrt(2.0)
     cat = {
         "transport2d_diag": TransportProblem(beta=np.array([1.0, 1.0])),
         "transport3d_diag": TransportProblem(beta=np.array([1.0, 1.0, 1.0])),
+        # u^e = exp(-5 |x - 0.35 t|^2) (SPEC.md:198); f = u_t + beta . grad u
+        # = 1.5 u sum_i (x_i - 0.35 t) manufactured, inflow data g = u^e
         "transport3d_timedep": TransportProblem(
             beta=np.array([0.2, 0.2, 0.2]),
-            exact=lambda x, t=0.0: np.exp(-5 * ((x[:, 0] - 0.35 * t) ** 2 + (x[:, 1] - 0.35 * t) ** 2
-                                                 + (x[:, 2] - 0.35 * t) ** 2))),
+            exact=lambda x, t=0.0: _gauss_timedep(x, t),
+            forcing=lambda x, t=0.0: 1.5 * np.sum(np.asarray(x) - 0.35 * t, axis=1) * _gauss_timedep(x, t),
+            inflow=lambda x, t=0.0: _gauss_timedep(x, t)),
         "sw_standing_wave": ShallowWaterProblem(
             Phi=1.0,
             exact=lambda x, t=0.0: np.stack([

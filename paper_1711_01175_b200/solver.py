@@ -15,9 +15,9 @@ from typing import Optional
 import numpy as np
 
 from . import _native as N
-from .assembly import OperatorSpec, build_spec
+from .assembly import OperatorSpec, build_spec, face_node_indices
 from .basis import ElementOperators
-from .pde import FourierModes, GaussianBump
+from .pde import FourierModes, GaussianBump, TransportProblem
 
 __all__ = ["DeviceSolver", "IterResult"]
 
@@ -250,12 +250,57 @@ class DeviceSolver:
         a.in_ghost, a.out_ghost, a.accumulate = in_ghost, 0, accumulate
         N.check(self.L.ihdg_class_apply(C.byref(a), self._sptr), "ihdg_class_apply")
 
+    def set_inflow(self, g) -> None:
+        """Inflow boundary data u_ext = g,
+        transport: the inflow faces' neighbour scalar on the boundary is
+        q = face_w g instead of 0, so the static RHS gains s_g = L q_g (K4 with
+        the lifted operator).  ``g(x)`` -> (n,) is evaluated at the boundary
+        face nodes; None clears it."""
+        torch, sp, d = self.torch, self.spec, self.mesh.dim
+        if g is None:
+            self.s_inflow, self._inflow_faces = None, None
+            return
+        if not isinstance(self.problem, TransportProblem) or sp.n_class != 1:
+            raise NotImplementedError("inflow data is defined for transport (one operator class)")
+        nf = sp.n1 ** (d - 1)
+        nfc = 2 * d * nf
+        pts = self._local_points(self.ops.nodes)               # (nloc, Np, d)
+        qg = np.zeros((self.nloc, nfc))
+        lb = self.layers[0]
+        e = np.arange(self.nloc, dtype=np.int64)
+        idx = [(e // int(np.prod(self.mesh.cells[:a]))) % self.mesh.cells[a] for a in range(d - 1)]
+        idx.append(lb + e // self.ls)
+        faces = {}
+        for f in range(2 * d):
+            a, side = divmod(f, 2)
+            w = float(sp.face_w[f, 0])
+            if not sp.coupled[f] or w == 0.0 or self.mesh.periodic[a]:
+                continue
+            on = np.flatnonzero(idx[a] == (self.mesh.cells[a] - 1 if side else 0))
+            if on.size == 0:
+                continue
+            fn = face_node_indices(d, sp.n1, f)
+            vals = np.asarray(g(pts[on][:, fn, :].reshape(-1, d)), dtype=float).reshape(on.size, nf)
+            qg[on, f * nf:(f + 1) * nf] = w * vals
+            faces[f] = (on, vals)
+        q = torch.as_tensor(qg, dtype=torch.float64, device=self.device)
+        self.s_inflow = torch.zeros((self.nloc, self.nv), dtype=torch.float64, device=self.device)
+        # one K4 pass per inflow face with that face's column block of L
+        # (transport has a single operator class, so the block is contiguous)
+        for f in faces:
+            blk = self.LT.view(-1)[f * nf * self.nv:]
+            self._apply(blk, nf, q, nfc, f * nf, 0, self.s_inflow, 1)
+        self._inflow_faces = faces
+        self.stream.synchronize()
+
     def prepare_steady(self) -> None:
-        """s = A^-1 b (forcing) or 0."""
+        """s = A^-1 b (forcing) or 0, plus the inflow-data part L q_g."""
         if self.s_static is None:
             self.s.zero_()
         else:
             self.s.copy_(self.s_static)
+        if getattr(self, "s_inflow", None) is not None:
+            self.s.add_(self.s_inflow)
 
     def begin_step(self, exchange=None) -> None:
         """RHS of the next step from the current state u^m.
@@ -272,8 +317,16 @@ class DeviceSolver:
             acc = 1
         else:
             acc = 0
+        if getattr(self, "s_inflow", None) is not None:
+            if acc:
+                self.s.add_(self.s_inflow)
+            else:
+                self.s.copy_(self.s_inflow)
+            acc = 1
         self._apply(self.PT, sp.nr, self.u[self.cur], self.nv, sp.time_comp0 * self.np_, 1, self.s, acc)
         if sp.time_scheme == "CN":
+            if getattr(self, "s_inflow", None) is not None:
+                raise NotImplementedError("inflow data with Crank-Nicolson")
             if exchange is not None:
                 exchange()
             self.reset_state(0.0, 1)
@@ -455,9 +508,30 @@ class DeviceSolver:
         N.check(self.L.ihdg_extract_trace(C.byref(a), self._sptr), "ihdg_extract_trace")
         return out
 
+    def _face_ids(self, elems, f) -> np.ndarray:
+        """mesh.py face id (mesh.py:89-125) of local face f of the given elements."""
+        d, cells = self.mesh.dim, self.mesh.cells
+        e = np.asarray(elems, dtype=np.int64) + self.layers[0] * self.ls
+        idx = [(e // int(np.prod(cells[:b]))) % cells[b] for b in range(d)]
+        a, side = divmod(f, 2)
+        off = 0
+        for b in range(a):
+            off += (cells[b] + (0 if self.mesh.periodic[b] else 1)) * int(np.prod([cells[c] for c in range(d) if c != b]))
+        ntan = int(np.prod([cells[c] for c in range(d) if c != a]))
+        tl, mul = np.zeros_like(e), 1
+        for b in range(d):
+            if b != a:
+                tl += idx[b] * mul
+                mul *= cells[b]
+        return off + (idx[a] + side) * ntan + tl
+
     def trace(self) -> np.ndarray:
-        """Single-valued trace (n_faces, 1, N_f) in mesh.py face order."""
+        """Single-valued trace (n_faces, 1, N_f) in mesh.py face order; on
+        inflow boundary faces with data it is g at the face nodes."""
         t = self.trace_of()
+        for f, (on, vals) in (getattr(self, "_inflow_faces", None) or {}).items():
+            t[self.torch.as_tensor(self._face_ids(on, f), device=self.device)] = self.torch.as_tensor(
+                vals, dtype=self.torch.float64, device=self.device)
         return t.cpu().numpy().reshape(self.mesh.n_faces, 1, t.shape[1])
 
     # -- diagnostics (K6; SPEC.md:320-323, 341-349, 398) ---------------------

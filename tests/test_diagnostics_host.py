@@ -78,3 +78,42 @@ def test_history_csv_and_map_helpers(tmp_path):
     assert float(rows[2][2]) == 1e-11 and rows[2][4] == "2"
     with pytest.raises(ValueError):
         layer_convergence_map(IterationReport(1, "converged", np.zeros(1), 0.0))
+
+
+def test_cfl_number_definition():
+    """CFL = |beta|_max dt (p+1)^2 / h."""
+    from paper_1711_01175_b200.iteration import cfl_number
+    from paper_1711_01175_b200.mesh import build_mesh
+    from paper_1711_01175_b200.pde import ShallowWaterProblem, TransportProblem
+
+    mesh = build_mesh(3, [8, 8, 8])
+    prob = TransportProblem(beta=np.array([0.2, 0.2, 0.2]))
+    assert np.isclose(cfl_number(prob, mesh, 4, 0.01), np.sqrt(3) * 0.2 * 0.01 * 25 * 8)
+    mesh2 = build_mesh(2, [4, 8])
+    assert np.isclose(cfl_number(ShallowWaterProblem(Phi=4.0), mesh2, 1, 0.1), 2.0 * 0.1 * 4 * 8)
+
+
+def test_oracle_inflow_constant_is_transported():
+    """1D, beta = 1, p = 1, f = 0, inflow value 1 -> solution 1."""
+    from oracle.ihdg_oracle import OracleProblem, OracleSolver
+
+    S = OracleSolver(OracleProblem("transport", 1, beta=np.array([1.0])), [4], 1)
+    S.set_inflow(lambda x: np.ones(len(x)))
+    o = S.run(tol=1e-12)
+    assert o["status"] == "converged"
+    assert np.max(np.abs(o["u"] - 1.0)) < 1e-13
+    assert np.allclose(S.trace(o["u"]), 1.0, atol=1e-13)
+
+
+def test_oracle_manufactured_transport3d_timedep_forcing():
+    """The preset's manufactured forcing is the strong residual of u^e."""
+    from paper_1711_01175_b200.pde import preset_problems
+
+    pr = preset_problems()["transport3d_timedep"]
+    rng = np.random.default_rng(0)
+    x, t, eps = rng.random((20, 3)), 0.3, 1e-6
+    ut = (pr.exact(x, t + eps) - pr.exact(x, t - eps)) / (2 * eps)
+    grad = np.stack([(pr.exact(x + eps * np.eye(3)[a], t) - pr.exact(x - eps * np.eye(3)[a], t)) / (2 * eps)
+                     for a in range(3)], axis=1)
+    res = ut + grad @ pr.beta - pr.forcing(x, t)
+    assert np.max(np.abs(res)) < 1e-8
