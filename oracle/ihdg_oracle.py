@@ -537,14 +537,29 @@ class OracleSolver:
         keep = grid[a] == (n1 - 1 if s else 0)
         return np.flatnonzero(keep)
 
-    def set_inflow(self, g):
+    def set_inflow(self, g, g_old=None):
         """Transport inflow data u_ext = g, taken in the
         trace space: g at the face GLL nodes, interpolated over the face.
-        RHS += <(|b.n| - b.n)/2 g_h, v> on every inflow boundary face."""
+        RHS += <(|b.n| - b.n)/2 g_h, v> on every inflow boundary face.
+        Crank-Nicolson (theta = 1/2 on the transport row): half of the term at
+        the new level g, half at the old level g_old."""
         d = self.prob.dim
         self.b_inflow = np.zeros((self.nel, self.nv))
         self.inflow_nodes = {}
         if g is None:
+            return
+        if self.time_scheme == "CN":
+            if g_old is None:
+                raise ValueError("Crank-Nicolson inflow data needs g_old")
+            self.set_inflow(g)
+            b_new, nodes = self.b_inflow, self.inflow_nodes
+            self.time_scheme = "BE"
+            try:
+                self.set_inflow(g_old)
+            finally:
+                self.time_scheme = "CN"
+            self.b_inflow = 0.5 * (b_new + self.b_inflow)
+            self.inflow_nodes = nodes
             return
         pts = self.element_points(self.b.nodes)
         Vf = _kron_axes([self.b.V] * (d - 1)) if d > 1 else np.ones((1, 1))
@@ -681,10 +696,21 @@ class OracleSolver:
             out["history"] = hist
         return out
 
-    def run_time_dependent(self, u0, nsteps, tol=1e-10, max_iters=10000, norm="volume", exact=None):
+    def run_time_dependent(self, u0, nsteps, tol=1e-10, max_iters=10000, norm="volume", exact=None,
+                           forcing=None, inflow=None):
+        """forcing(x, t) / inflow(x, t): time-dependent data, taken at the new
+        level (BE) or averaged / split between the levels (CN)."""
         u = np.array(u0, float).reshape(self.nel, self.nv)
         reports = []
         for step in range(nsteps):
+            t0, t1 = step * self.dt, (step + 1) * self.dt
+            if forcing is not None:
+                if self.time_scheme == "CN":
+                    self.set_forcing(lambda x: 0.5 * (forcing(x, t0) + forcing(x, t1)))
+                else:
+                    self.set_forcing(lambda x: forcing(x, t1))
+            if inflow is not None:
+                self.set_inflow(lambda x: inflow(x, t1), lambda x: inflow(x, t0))
             if norm == "exact":
                 self.set_exact(exact, (step + 1) * self.dt)
             r = self.run(u0=u, tol=tol, max_iters=max_iters, norm=norm, u_prev=u)

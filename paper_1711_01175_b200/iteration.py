@@ -323,11 +323,20 @@ def run_time_dependent(mesh, problem, ops: ElementOperators, cfg: Optional[Itera
     cfl = cfl_number(problem, mesh, ops.p, dt)
     for m in range(n_steps):
         t0 = time.perf_counter()
-        t_new = (m + 1) * dt
-        if f_t:        # time-dependent forcing / inflow data at the new level (implicit Euler)
-            solver.set_forcing(_exact_at(forcing, t_new))
+        t_old, t_new = m * dt, (m + 1) * dt
+        # time-dependent forcing / inflow data: the new level (implicit Euler);
+        # Crank-Nicolson averages the forcing and splits the boundary coupling
+        # between the levels like the trace couplings
+        if f_t:
+            if ts == "CN":
+                solver.set_forcing(lambda x, a=t_old, b=t_new: 0.5 * (np.asarray(forcing(x, a))
+                                                                      + np.asarray(forcing(x, b))))
+            else:
+                solver.set_forcing(_exact_at(forcing, t_new))
         if inflow is not None:
-            solver.set_inflow(_exact_at(inflow, t_new) if _takes_time(inflow) else inflow)
+            g_t = _takes_time(inflow)
+            solver.set_inflow(_exact_at(inflow, t_new) if g_t else inflow,
+                              (_exact_at(inflow, t_old) if g_t else inflow) if ts == "CN" else None)
         solver.begin_step()
         if cfg.stop == "exact" or (cfg.diagnostics and getattr(problem, "exact", None) is not None):
             solver.set_exact(_exact_at(problem.exact, (m + 1) * dt))

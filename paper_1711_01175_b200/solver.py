@@ -250,7 +250,7 @@ class DeviceSolver:
         a.in_ghost, a.out_ghost, a.accumulate = in_ghost, 0, accumulate
         N.check(self.L.ihdg_class_apply(C.byref(a), self._sptr), "ihdg_class_apply")
 
-    def set_inflow(self, g) -> None:
+    def set_inflow(self, g, g_explicit=None) -> None:
         """Inflow boundary data u_ext = g,
         transport: the inflow faces' neighbour scalar on the boundary is
         q = face_w g instead of 0, so the static RHS gains s_g = L q_g (K4 with
@@ -265,31 +265,42 @@ class DeviceSolver:
         nf = sp.n1 ** (d - 1)
         nfc = 2 * d * nf
         pts = self._local_points(self.ops.nodes)               # (nloc, Np, d)
-        qg = np.zeros((self.nloc, nfc))
         lb = self.layers[0]
         e = np.arange(self.nloc, dtype=np.int64)
         idx = [(e // int(np.prod(self.mesh.cells[:a]))) % self.mesh.cells[a] for a in range(d - 1)]
         idx.append(lb + e // self.ls)
-        faces = {}
-        for f in range(2 * d):
-            a, side = divmod(f, 2)
-            w = float(sp.face_w[f, 0])
-            if not sp.coupled[f] or w == 0.0 or self.mesh.periodic[a]:
-                continue
-            on = np.flatnonzero(idx[a] == (self.mesh.cells[a] - 1 if side else 0))
-            if on.size == 0:
-                continue
-            fn = face_node_indices(d, sp.n1, f)
-            vals = np.asarray(g(pts[on][:, fn, :].reshape(-1, d)), dtype=float).reshape(on.size, nf)
-            qg[on, f * nf:(f + 1) * nf] = w * vals
-            faces[f] = (on, vals)
-        q = torch.as_tensor(qg, dtype=torch.float64, device=self.device)
+
+        def face_data(fn):
+            qg = np.zeros((self.nloc, nfc))
+            faces = {}
+            for f in range(2 * d):
+                a, side = divmod(f, 2)
+                w = float(sp.face_w[f, 0])
+                if not sp.coupled[f] or w == 0.0 or self.mesh.periodic[a]:
+                    continue
+                on = np.flatnonzero(idx[a] == (self.mesh.cells[a] - 1 if side else 0))
+                if on.size == 0:
+                    continue
+                fn_ids = face_node_indices(d, sp.n1, f)
+                vals = np.asarray(fn(pts[on][:, fn_ids, :].reshape(-1, d)), dtype=float).reshape(on.size, nf)
+                qg[on, f * nf:(f + 1) * nf] = w * vals
+                faces[f] = (on, vals)
+            return torch.as_tensor(qg, dtype=torch.float64, device=self.device), faces
+
         self.s_inflow = torch.zeros((self.nloc, self.nv), dtype=torch.float64, device=self.device)
         # one K4 pass per inflow face with that face's column block of L
         # (transport has a single operator class, so the block is contiguous)
-        for f in faces:
-            blk = self.LT.view(-1)[f * nf * self.nv:]
-            self._apply(blk, nf, q, nfc, f * nf, 0, self.s_inflow, 1)
+        parts = [(g, self.LT)]
+        if sp.time_scheme == "CN":
+            if g_explicit is None:
+                raise ValueError("Crank-Nicolson inflow data needs the old-level data g_explicit")
+            parts.append((g_explicit, self.LT_expl))
+        faces = None
+        for fn, LT in parts:
+            q, fc = face_data(fn)
+            faces = fc if faces is None else faces
+            for f in fc:
+                self._apply(LT.view(-1)[f * nf * self.nv:], nf, q, nfc, f * nf, 0, self.s_inflow, 1)
         self._inflow_faces = faces
         self.stream.synchronize()
 
@@ -325,8 +336,6 @@ class DeviceSolver:
             acc = 1
         self._apply(self.PT, sp.nr, self.u[self.cur], self.nv, sp.time_comp0 * self.np_, 1, self.s, acc)
         if sp.time_scheme == "CN":
-            if getattr(self, "s_inflow", None) is not None:
-                raise NotImplementedError("inflow data with Crank-Nicolson")
             if exchange is not None:
                 exchange()
             self.reset_state(0.0, 1)

@@ -193,7 +193,8 @@ def test_exact_solution_rule_parity(name, preset, cells, p, dt, steps, ts):
     u0 = np.zeros((S.nel, S.m, S.npn))
     for c in range(S.m):
         u0[:, c, :] = S.interpolate(init[labels[c]])
-    _, refs = S.run_time_dependent(u0.reshape(S.nel, -1), steps, tol=1e-10, norm="exact", exact=prob.exact)
+    _, refs = S.run_time_dependent(u0.reshape(S.nel, -1), steps, tol=1e-10, norm="exact", exact=prob.exact,
+                                   forcing=getattr(prob, "forcing", None), inflow=getattr(prob, "inflow", None))
     assert [r.iterations for r in reps] == [o["iterations"] for o in refs]
     assert all(r.status == "converged" for r in reps)
     for r, o in zip(reps, refs):

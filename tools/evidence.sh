@@ -22,3 +22,10 @@ if timeout 300 $CMD3 > $O/${TAG}_bench_short3.json 2>&1; then
     -o $O/${TAG}_ws_full -f $CMD3 > $O/${TAG}_ncu_full.log 2>&1
 fi
 echo done
+# config-4 evidence: role counters (profiling build) and one full capture of k_sweep_v3
+IHDG_LIB=paper_1711_01175_b200/libihdg_cuda_prof.so timeout 300 python tools/ws_roles.py 4 > $O/${TAG}_cfg4_roles.txt 2>&1
+if timeout 300 python tools/sweep_cfg.py 4 20 3 > $O/${TAG}_cfg4_plain.txt 2>&1; then
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_sweep_v3 -s 3 -c 1 \
+    -o $O/${TAG}_cfg4_v3_full -f python tools/sweep_cfg.py 4 5 3 > $O/${TAG}_cfg4_ncu.log 2>&1
+fi
+echo done-cfg4
