@@ -551,10 +551,10 @@ class OracleSolver:
         if self.time_scheme == "CN":
             if g_old is None:
                 raise ValueError("Crank-Nicolson inflow data needs g_old")
-            self.set_inflow(g)
-            b_new, nodes = self.b_inflow, self.inflow_nodes
             self.time_scheme = "BE"
             try:
+                self.set_inflow(g)
+                b_new, nodes = self.b_inflow, self.inflow_nodes
                 self.set_inflow(g_old)
             finally:
                 self.time_scheme = "CN"

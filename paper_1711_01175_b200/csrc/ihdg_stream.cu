@@ -169,7 +169,7 @@ struct StreamEntry {
 #define IHDG_C4_NS 16
 #endif
 #ifndef IHDG_C4_NCW
-#define IHDG_C4_NCW 6
+#define IHDG_C4_NCW 7
 #endif
 #ifndef IHDG_C4_NQW
 #define IHDG_C4_NQW 8

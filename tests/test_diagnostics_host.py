@@ -117,3 +117,18 @@ def test_oracle_manufactured_transport3d_timedep_forcing():
                      for a in range(3)], axis=1)
     res = ut + grad @ pr.beta - pr.forcing(x, t)
     assert np.max(np.abs(res)) < 1e-8
+
+
+def test_oracle_cn_inflow_is_the_level_average():
+    """Crank-Nicolson inflow term = half new-level + half old-level data."""
+    from oracle.ihdg_oracle import OracleProblem, OracleSolver
+
+    pr = OracleProblem("transport", 2, beta=np.array([1.0, 0.5]))
+    S = OracleSolver(pr, [3, 3], 2, dt=0.1, time_scheme="CN")
+    B = OracleSolver(pr, [3, 3], 2, dt=0.1)
+    g1, g0 = (lambda x: 1.0 + x[:, 0]), (lambda x: x[:, 1] ** 2)
+    S.set_inflow(g1, g0)
+    B.set_inflow(g1)
+    b1 = B.b_inflow.copy()
+    B.set_inflow(g0)
+    assert np.allclose(S.b_inflow, 0.5 * (b1 + B.b_inflow), rtol=0, atol=1e-15)
