@@ -175,8 +175,19 @@ struct StreamEntry {
 #define IHDG_C4_NQW 8
 #endif
 
+// configs 2/3 v3 shape (A/B builds override it)
+#ifndef IHDG_C23_NS
+#define IHDG_C23_NS 16
+#endif
+#ifndef IHDG_C23_NCW
+#define IHDG_C23_NCW 8
+#endif
+#ifndef IHDG_C23_NQW
+#define IHDG_C23_NQW 2
+#endif
+
 const StreamEntry kStream[] = {
-    IHDG_V3(2, 5, 3, 4, 2, 16, 8, 2, 2)    // configs 2/3: CD / SW 2D p=4
+    IHDG_V3(2, 5, 3, 4, 2, IHDG_C23_NS, IHDG_C23_NCW, 2, IHDG_C23_NQW)  // configs 2/3: CD / SW 2D p=4
     IHDG_V3(3, 4, 1, 3, 1, IHDG_C4_NS, IHDG_C4_NCW, 4, IHDG_C4_NQW)  // config 4: transport 3D p=3
     IHDG_WS2(7, 3, 4, 2, 16, 6)            // config 5: CD 2D p=6 (ws2: s / u^{k+1} bypass smem)
     IHDG_WS3(7, 3, 4, 2, 16, IHDG_WS3_NS)  // config 5: CD 2D p=6 (ws3: q in the consumers, DFMA norm warps)
