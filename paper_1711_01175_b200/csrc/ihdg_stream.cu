@@ -166,7 +166,7 @@ struct StreamEntry {
 
 // config-4 v3 shape (A/B builds override it): stages, consumer warps, prep warps
 #ifndef IHDG_C4_NS
-#define IHDG_C4_NS 16
+#define IHDG_C4_NS 12
 #endif
 #ifndef IHDG_C4_NCW
 #define IHDG_C4_NCW 7
@@ -180,10 +180,10 @@ struct StreamEntry {
 #define IHDG_C23_NS 16
 #endif
 #ifndef IHDG_C23_NCW
-#define IHDG_C23_NCW 8
+#define IHDG_C23_NCW 7
 #endif
 #ifndef IHDG_C23_NQW
-#define IHDG_C23_NQW 2
+#define IHDG_C23_NQW 8
 #endif
 
 const StreamEntry kStream[] = {
