@@ -100,10 +100,18 @@ struct WCfg {
   static constexpr int NRT = (NV + 7) / 8;
   static constexpr int KS = KC / 4;
   static constexpr int NEG = E / 8;
+#ifdef IHDG_WS_NCW
+  static constexpr int NCW = IHDG_WS_NCW;                          // A/B builds
+#else
   static constexpr int NCW = NRT >= 16 ? 10 : (NRT >= 8 ? 8 : 4);  // consumer warps
+#endif
   static constexpr int RTW = (NRT + NCW - 1) / NCW;
   static constexpr int UPW = (E * M + NCW - 1) / NCW;
+#ifdef IHDG_WS_NQW
+  static constexpr int NQW = IHDG_WS_NQW;                          // A/B builds
+#else
   static constexpr int NQW = 4;                                    // prep warps
+#endif
   static constexpr int NT = 32 * (NCW + NQW + 1);
   static constexpr int TILE = E * NV;
   static constexpr int HALO = 0;   // out-of-tile faces: prep warps load them into registers
