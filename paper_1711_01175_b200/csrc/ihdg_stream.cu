@@ -141,7 +141,7 @@ struct StreamEntry {
   int D, N1, M, NCF, NWC, E, NV;
   int (*launch)(const ihdg_sweep_args*, cudaStream_t);
   int v3;  // version-3 kernel (physical 8-element tiles)
-  int ws3; // opt-in kernels: 1 k_sweep_ws3 (IHDG_SWEEP_IMPL=ws3), 2 k_sweep_ws4 (=ws4)
+  int ws3; // opt-in kernels: 1 k_sweep_ws3 (IHDG_SWEEP_IMPL=ws3), 2 k_sweep_ws4 (=ws4), 3 k_sweep_v3 on config 5 (=v3)
 };
 
 #define IHDG_V3(D, N1, M, NCF, NWC, NS, NCW, PF, NQW) \
@@ -186,12 +186,24 @@ struct StreamEntry {
 #define IHDG_C23_NQW 8
 #endif
 
+// config-5 v3 (opt-in, IHDG_SWEEP_IMPL=v3) shape
+#ifndef IHDG_C5V3_NS
+#define IHDG_C5V3_NS 16
+#endif
+#ifndef IHDG_C5V3_NCW
+#define IHDG_C5V3_NCW 7
+#endif
+#ifndef IHDG_C5V3_NQW
+#define IHDG_C5V3_NQW 8
+#endif
+
 const StreamEntry kStream[] = {
     IHDG_V3(2, 5, 3, 4, 2, IHDG_C23_NS, IHDG_C23_NCW, 2, IHDG_C23_NQW)  // configs 2/3: CD / SW 2D p=4
     IHDG_V3(3, 4, 1, 3, 1, IHDG_C4_NS, IHDG_C4_NCW, 4, IHDG_C4_NQW)  // config 4: transport 3D p=3
     IHDG_WS2(7, 3, 4, 2, 16, 6)            // config 5: CD 2D p=6 (ws2: s / u^{k+1} bypass smem)
     IHDG_WS3(7, 3, 4, 2, 16, IHDG_WS3_NS)  // config 5: CD 2D p=6 (ws3: q in the consumers, DFMA norm warps)
     {2, 7, 3, 4, 2, 16, 147, launch_ws4_t<7, 3, 4, 2, IHDG_WS4_NS>, 0, 2},  // config 5 (ws4: two consumer teams)
+    {2, 7, 3, 4, 2, 16, 147, launch_v3_t<2, 7, 3, 4, 2, IHDG_C5V3_NS, IHDG_C5V3_NCW, 2, IHDG_C5V3_NQW>, 1, 3},  // config 5 (v3)
     IHDG_WS(7, 3, 4, 2, 16, IHDG_WS5_NS)   // config 5: CD 2D p=6 (warp-specialised)
     IHDG_WS(5, 3, 4, 2, 16, 4)             // configs 2/3: CD / SW 2D p=4
     IHDG_STREAM(3, 4, 1, 3, 1, 32, 3, 4)   // config 4: transport 3D p=3
@@ -223,6 +235,11 @@ const StreamEntry* stream_entry(const ihdg_sweep_args* a) {
     const char* s = std::getenv("IHDG_SWEEP_IMPL");
     want_ws4 = (s != nullptr && std::strcmp(s, "ws4") == 0) ? 1 : 0;
   }
+  static int want_v3 = -1;
+  if (want_v3 < 0) {
+    const char* s = std::getenv("IHDG_SWEEP_IMPL");
+    want_v3 = (s != nullptr && std::strcmp(s, "v3") == 0) ? 1 : 0;
+  }
   static int want_ws3 = -1;
   if (want_ws3 < 0) {
     const char* s = std::getenv("IHDG_SWEEP_IMPL");
@@ -245,6 +262,7 @@ const StreamEntry* stream_entry(const ihdg_sweep_args* a) {
     if (e.v3 && no_v3) continue;
     if (e.ws3 == 1 && !want_ws3) continue;
     if (e.ws3 == 2 && !want_ws4) continue;
+    if (e.ws3 == 3 && !want_v3) continue;
     if (e.launch == (int (*)(const ihdg_sweep_args*, cudaStream_t))launch_ws2_t<7, 3, 4, 2, 16, 6> && !want_ws2)
       continue;
     Geo geo;
