@@ -181,7 +181,7 @@ def test_config4_full_size_layer_count():
     assert np.array_equal(r1.state.data, r2.state.data)
 
 
-@pytest.mark.parametrize("impl", ["ws4", "ws3", "ws2", "ws", "generic", "nograph"])
+@pytest.mark.parametrize("impl", ["v3", "ws4", "ws3", "ws2", "ws", "generic", "nograph"])
 def test_sweep_impl_parity(impl):
     """Every selectable sweep kernel (IHDG_SWEEP_IMPL) on config 5 reduced,
     and the stream-launched (not graph-replayed) iterate loop."""
