@@ -133,9 +133,11 @@ def _set_initial(solver: DeviceSolver, init):
 def _diagnostic_iterate(solver: DeviceSolver, cfg: IterationConfig, norm: str, max_iters: int) -> dict:
     """Algorithm 1 one sweep at a time with the per-iteration diagnostics of
     SPEC.md:321 on the device (K6): successive norm, L2 error vs exact (when
-    known), trace energy ||u_hat(u^k) - u_hat(r)||_{L2(E_h)}, skeleton jump
-    norm ||u^- - u^+||_{L2(E_h)} of the trace variable, and the element
-    convergence map {K : ||u^k - r||_{L2(K)} < tol}.  r is cfg.reference or the
+    known), trace energy ||(phi, theta.n)(u^k - r)||^2_{E_h} (shallow water;
+    (sigma.n, u) for convection-diffusion, u for transport) -- the skeleton
+    norm the contraction theorems bound --,
+    skeleton jump norm ||u^- - u^+||_{L2(E_h)} of the trace variable, and the
+    element convergence map {K : ||u^k - r||_{L2(K)} < tol}.  r is cfg.reference or the
     converged solution of a first (batched) solve from the same iterate."""
     import ctypes as C
     from . import _native as N
@@ -152,7 +154,7 @@ def _diagnostic_iterate(solver: DeviceSolver, cfg: IterationConfig, norm: str, m
         ref = solver.padded_copy()
         solver.cur = cur0
         solver.u[cur0].copy_(start)
-    t_ref = solver.trace_of(ref)
+    side_refs = [solver.trace_of(ref, weights=w) for w in solver.energy_sides()]
     has_exact = getattr(solver, "ue_q", None) is not None
     solver.reset_state(cfg.tol, max_iters, cfg.diverge_factor)
     if norm == "exact":
@@ -177,7 +179,7 @@ def _diagnostic_iterate(solver: DeviceSolver, cfg: IterationConfig, norm: str, m
             e = solver._error_args(0)
             N.check(solver.L.ihdg_error_norm(C.byref(e), solver._sptr), "ihdg_error_norm")
             err = solver.read_state().last_err
-        energy = np.sqrt(solver.face_energy(solver.trace_of(), t_ref))
+        energy = solver.skeleton_energy(side_refs)
         _, flags, _ = solver.element_errors(ref, cfg.tol)
         fl = flags.cpu().numpy().astype(bool)
         maps.append(fl)
@@ -199,11 +201,12 @@ def _diagnostic_iterate(solver: DeviceSolver, cfg: IterationConfig, norm: str, m
 
 def contraction_factor(energy, tol: float = 1e-10) -> float:
     """Measured contraction factor: geometric mean of the
-    successive trace-energy ratios E_{k+1}/E_k after the first iteration,
-    over the energies above 1e3 * tol (below that the reference solution's
-    own stopping error dominates)."""
+    successive trace-energy ratios E_{k+1}/E_k after the first iteration
+    (E is the squared skeleton norm, so this is comparable with the C / D of
+    the theorems), over the energies above (1e3 tol)^2 (below that the
+    reference solution's own stopping error dominates)."""
     e = np.asarray(energy, dtype=float)
-    r = [e[k + 1] / e[k] for k in range(1, len(e) - 1) if e[k] > 0 and e[k + 1] > 1e3 * tol]
+    r = [e[k + 1] / e[k] for k in range(1, len(e) - 1) if e[k] > 0 and e[k + 1] > (1e3 * tol) ** 2]
     return float(np.exp(np.mean(np.log(r)))) if r else float("nan")
 
 

@@ -490,7 +490,7 @@ class DeviceSolver:
         labels = self.spec.labels
         return labels.index("phi") if "phi" in labels else labels.index("u")
 
-    def trace_of(self, buf=None, jump: bool = False):
+    def trace_of(self, buf=None, jump: bool = False, weights=None):
         """Face array (n_faces, N_f) on the device, mesh.py face order, of the
         ghost-padded state ``buf`` (default: the current iterate).  jump=False:
         the single-valued trace; jump=True: u^- - u^+ of the primary component on
@@ -505,7 +505,12 @@ class DeviceSolver:
         pc = self.primary_comp
         for ax in range(3):
             for c in range(4):
-                if jump:
+                if weights is not None:      # explicit face-side weights (int_own, int_nbr, lo, hi)
+                    a.w_int_own[ax][c] = float(weights["int_own"][ax, c])
+                    a.w_int_nbr[ax][c] = float(weights["int_nbr"][ax, c])
+                    a.w_lo[ax][c] = float(weights["lo"][ax, c])
+                    a.w_hi[ax][c] = float(weights["hi"][ax, c])
+                elif jump:
                     a.w_int_own[ax][c] = 1.0 if c == pc else 0.0
                     a.w_int_nbr[ax][c] = -1.0 if c == pc else 0.0
                     a.w_lo[ax][c] = a.w_hi[ax][c] = 0.0
@@ -573,6 +578,41 @@ class DeviceSolver:
         a.jac, a.tol = self.spec.jac, float(tol)
         N.check(self.L.ihdg_elem_error(C.byref(a), self._sptr), "ihdg_elem_error")
         return self._diag_err2, self._diag_flags, float(self._diag_tot[0].item())
+
+    def energy_sides(self) -> list:
+        """Face-side extraction weights of the skeleton energy of the theorems
+        (PAPER.md ThmConvergenceShallowWater / ThmUpwindDDM):
+        ||(phi, theta.n)||^2_{E_h} with the Phi weight on theta.n (shallow
+        water), ||(sigma.n, u)||^2_{E_h} (convection-diffusion), ||u||^2_{E_h}
+        (transport).  Every element's own face values over its whole boundary:
+        one weight set for the owner side and one for the neighbour side of
+        every face."""
+        d, labels = self.mesh.dim, self.spec.labels
+        fields = []   # (component per axis, weight)
+        if "phi" in labels:
+            fields.append(([0] * d, 1.0))
+            fields.append(([1 + a for a in range(d)], float(np.sqrt(self.problem.Phi))))
+        elif len(labels) > 1:   # convection-diffusion: sigma_a on axis-a faces, u
+            fields.append(([labels.index("u")] * d, 1.0))
+            fields.append(([a for a in range(d)], 1.0))
+        else:
+            fields.append(([0] * d, 1.0))
+        out = []
+        for comps, w in fields:
+            own = {k: np.zeros((3, 4)) for k in ("int_own", "int_nbr", "lo", "hi")}
+            nbr = {k: np.zeros((3, 4)) for k in ("int_own", "int_nbr", "lo", "hi")}
+            for ax in range(d):
+                c = comps[ax]
+                own["int_own"][ax, c] = own["lo"][ax, c] = own["hi"][ax, c] = w
+                nbr["int_nbr"][ax, c] = w
+            out += [own, nbr]
+        return out
+
+    def skeleton_energy(self, ref_traces, buf=None) -> float:
+        """sum over the energy_sides() of ||t(u) - t(r)||^2_{L2(E_h)} (K6);
+        ref_traces = [trace_of(r, weights=w) for w in energy_sides()]."""
+        return sum(self.face_energy(self.trace_of(buf, weights=w), tr)
+                   for w, tr in zip(self.energy_sides(), ref_traces))
 
     def face_energy(self, t, t_ref=None) -> float:
         """sum_f ||t_f - t_ref_f||^2_{L2(f)} over the skeleton (face arrays from trace_of)."""
