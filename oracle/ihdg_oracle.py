@@ -575,6 +575,37 @@ class OracleSolver:
             self.b_inflow[on, :self.npn] += 0.5 * (abs(bn) - bn) * gv @ M.T
             self.inflow_nodes[f] = (on, gv)
 
+    def set_dirichlet(self, g):
+        """Convection-diffusion Dirichlet data u_hat := g_D on the boundary
+        (SPEC.md:214, 269), in the trace space (g at the face GLL nodes):
+        the sigma_a rows gain -<g_h, tau.n> = -sgn <g_h, phi>_f and the u row
+        +tau <g_h, v>_f, tau = (alpha - beta.n)/2 (PAPER.md:1060)."""
+        d = self.prob.dim
+        self.b_inflow = np.zeros((self.nel, self.nv))
+        self.inflow_nodes = {}
+        if g is None:
+            return
+        if self.prob.kind != "cd" or self.time_scheme == "CN":
+            raise NotImplementedError("Dirichlet data: convection-diffusion, backward Euler / steady")
+        pts = self.element_points(self.b.nodes)
+        Vf = _kron_axes([self.b.V] * (d - 1)) if d > 1 else np.ones((1, 1))
+        U = d
+        for f in range(2 * d):
+            a, s = divmod(f, 2)
+            if self.periodic[a]:
+                continue
+            sgn = 1.0 if s else -1.0
+            bn = self.prob.beta[a] * sgn
+            tau = 0.5 * (np.sqrt(bn * bn + 4.0) - bn)
+            on = np.flatnonzero(self.nbr[:, f] == BOUNDARY)
+            ids = self._face_node_ids(f)
+            gv = np.asarray(g(pts[on][:, ids, :].reshape(-1, d)), float).reshape(on.size, -1)
+            M = self.el.fmass(f, self.el.Pf[f], Vf)          # (Np, N_f)
+            val = gv @ M.T
+            self.b_inflow[on, a * self.npn:(a + 1) * self.npn] += -sgn * val
+            self.b_inflow[on, U * self.npn:(U + 1) * self.npn] += tau * val
+            self.inflow_nodes[f] = (on, gv)
+
     # -- sweep -------------------------------------------------------------
     def rhs_static(self, u_prev=None):
         rhs = self.b_static.copy()

@@ -105,6 +105,8 @@ class OperatorSpec:
     time_scheme: str = "BE"
     terms_expl: Optional[np.ndarray] = None   # CN: A terms + (1 - theta) B terms (L_expl)
     coefs_expl: Optional[np.ndarray] = None
+    terms_dir: Optional[np.ndarray] = None    # CD Dirichlet data: A terms + B_D terms (L_D = A^-1 B_D)
+    coefs_dir: Optional[np.ndarray] = None
 
     @property
     def n1(self):
@@ -305,8 +307,9 @@ def build_spec(mesh, problem, ops: ElementOperators, dt=None, norm="auto", schem
         beta = problem.beta_const(d)
         if beta is None:
             raise NotImplementedError("device path needs a constant beta (shared operator)")
-        if problem.dirichlet is not None:
-            raise NotImplementedError("non-zero Dirichlet data is not wired to the device path yet")
+        if problem.dirichlet is not None and time_scheme == "CN":
+            raise NotImplementedError("Dirichlet data with Crank-Nicolson")
+        dterms = _Terms(d) if problem.dirichlet is not None else None
         m = d + 1
         U = d
         masks = _class_masks(mesh)
@@ -332,6 +335,12 @@ def build_spec(mesh, problem, ops: ElementOperators, dt=None, norm="auto", schem
                 if mk & (1 << f):
                     terms.vol(ci, A_T, U, a, sgn * Jf[a], axis=a, op=E(s))
                     terms.vol(ci, A_T, U, U, (bn + tau) * Jf[a], axis=a, op=E(s))
+                    if dterms is not None:
+                        # u_hat := g_D: -<g, tau.n> (sigma rows)
+                        # and +tau <g, v> (u row) move to the RHS; g lives at
+                        # the face nodes, coupled like a neighbour scalar
+                        dterms.vol(ci, B_T, a, f, -sgn * Jf[a], axis=a, op=Cc(s))
+                        dterms.vol(ci, B_T, U, f, tau * Jf[a], axis=a, op=Cc(s))
                 elif one:
                     terms.vol(ci, A_T, U, a, sgn * Jf[a], axis=a, op=E(s))
                     terms.vol(ci, A_T, U, U, (bn + tau) * Jf[a], axis=a, op=E(s))
@@ -449,6 +458,11 @@ def build_spec(mesh, problem, ops: ElementOperators, dt=None, norm="auto", schem
         theta[tc0:tc0 + ntc] = 0.5
         terms_expl, coefs_expl = terms.crank_nicolson(theta, tc0)
         nr, tc0, ntc = m * ops.n_nodes, 0, m
+    terms_dir = coefs_dir = None
+    if isinstance(problem, ConvectionDiffusionProblem) and dterms is not None:
+        keep = [i for i, r in enumerate(terms.rows) if r[1] == A_T]
+        terms_dir = np.asarray([terms.rows[i] for i in keep] + dterms.rows, dtype=np.int32).reshape(-1, 8)
+        coefs_dir = np.asarray([terms.coefs[i] for i in keep] + dterms.coefs, dtype=float)
     terms_arr = np.asarray(terms.rows, dtype=np.int32).reshape(-1, 8)
     return OperatorSpec(
         dim=d, order=ops.p, ncomp=m, labels=tuple(labels), n_class=len(masks),
@@ -457,12 +471,13 @@ def build_spec(mesh, problem, ops: ElementOperators, dt=None, norm="auto", schem
         time_comp0=tc0, n_time_comp=ntc, forcing_comp=fcomp, face_w=face_w, coupled=coupled,
         out_face=out_face, out_w=out_w, own_w=own_w, comp_w=comp_w, trace_w=tw, jac=J, jac_face=jac_face,
         periodic=tuple(mesh.periodic), scheme=scheme, time_scheme=time_scheme, terms_expl=terms_expl,
-        coefs_expl=coefs_expl)
+        coefs_expl=coefs_expl, terms_dir=terms_dir, coefs_dir=coefs_dir)
 
 
-def evaluate_terms(spec: OperatorSpec, expl: bool = False):
-    """Host evaluation of the term list -> (A, B, R) per class (expl: the
-    Crank-Nicolson explicit-coupling list, B = (1 - theta) B).
+def evaluate_terms(spec: OperatorSpec, expl: bool = False, which: str = "main"):
+    """Host evaluation of the term list -> (A, B, R) per class (expl /
+    which="expl": the Crank-Nicolson explicit-coupling list, B = (1 - theta) B;
+    which="dir": the Dirichlet-data list, B = B_D).
 
     Mirror of the first stage of K1 (k_assemble_build), used by the CPU tests
     to check the physics against the oracle without a GPU.  Not on the
@@ -473,7 +488,10 @@ def evaluate_terms(spec: OperatorSpec, expl: bool = False):
     A = np.zeros((spec.n_class, nv, nv))
     B = np.zeros((spec.n_class, nv, kin))
     R = np.zeros((spec.n_class, nv, max(spec.nr, 1)))
-    rows, coefs = (spec.terms_expl, spec.coefs_expl) if expl else (spec.terms, spec.coefs)
+    if expl:
+        which = "expl"
+    rows, coefs = {"main": (spec.terms, spec.coefs), "expl": (spec.terms_expl, spec.coefs_expl),
+                   "dir": (spec.terms_dir, spec.coefs_dir)}[which]
     for row, coef in zip(rows, coefs):
         cls, target, rc, cb = (int(x) for x in row[:4])
         mats = []

@@ -249,6 +249,8 @@ def run(mesh, problem, ops: ElementOperators, cfg: Optional[IterationConfig] = N
         solver.set_forcing(forcing)
     if getattr(problem, "inflow", None) is not None:
         solver.set_inflow(problem.inflow)
+    if getattr(problem, "dirichlet", None) is not None:
+        solver.set_dirichlet(problem.dirichlet)
     solver.prepare_steady()
     _set_initial(solver, cfg.initial_guess)
     if cfg.stop == "exact" or (cfg.diagnostics and getattr(problem, "exact", None) is not None):
@@ -336,6 +338,9 @@ def run_time_dependent(mesh, problem, ops: ElementOperators, cfg: Optional[Itera
                                                                       + np.asarray(forcing(x, b))))
             else:
                 solver.set_forcing(_exact_at(forcing, t_new))
+        dirichlet = getattr(problem, "dirichlet", None)
+        if dirichlet is not None:
+            solver.set_dirichlet(_exact_at(dirichlet, t_new) if _takes_time(dirichlet) else dirichlet)
         if inflow is not None:
             g_t = _takes_time(inflow)
             solver.set_inflow(_exact_at(inflow, t_new) if g_t else inflow,

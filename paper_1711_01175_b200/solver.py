@@ -155,6 +155,10 @@ class DeviceSolver:
             b.R, b.LT, b.PT, b.min_pivot = 0, _ptr(self.LT_expl), 0, _ptr(mp2)
             N.check(self.L.ihdg_assemble(C.byref(b), self._sptr), "ihdg_assemble (CN explicit)")
             del A2, Ai2, AiT2, B2, mp2
+        self.LT_dir = None
+        if sp.terms_dir is not None:
+            # L_D = A^-1 B_D: the Dirichlet-data couplings (convection-diffusion)
+            self.LT_dir = self._assemble_lifted(sp.terms_dir, sp.coefs_dir, "ihdg_assemble (Dirichlet data)")
         piv = self.min_pivot.cpu().numpy()
         scale = self.A.abs().amax(dim=(1, 2)).cpu().numpy()
         bad = np.nonzero(~(piv > 1e-13 * scale))[0]
@@ -163,6 +167,26 @@ class DeviceSolver:
             raise np.linalg.LinAlgError(
                 f"singular local matrix in operator class {c} (boundary mask {sp.class_masks[c]}): "
                 f"min pivot {piv[c]:.3e}, max |A| {scale[c]:.3e}")
+
+    def _assemble_lifted(self, terms, coefs, what):
+        """A^-1 B of another term list with the same A (K1), as LT [class][kin][nv]."""
+        torch, sp = self.torch, self.spec
+        tt = torch.as_tensor(terms, device=self.device).contiguous()
+        cc = torch.as_tensor(coefs, dtype=torch.float64, device=self.device)
+        A2, Ai2, AiT2 = torch.zeros_like(self.A), torch.zeros_like(self.A), torch.zeros_like(self.A)
+        B2 = torch.zeros_like(self.B)
+        LT = torch.zeros_like(self.LT)
+        mp2 = torch.zeros_like(self.min_pivot)
+        b = N.AssemblyArgs()
+        b.dim, b.order, b.ncomp, b.n_class = sp.dim, sp.order, sp.ncomp, sp.n_class
+        b.n_ops, b.n_terms, b.nr = sp.ops1d.shape[0], terms.shape[0], 0
+        b.ops1d, b.op_ncols = _ptr(self._ops1d), _ptr(self._opn)
+        b.terms, b.coefs = _ptr(tt), _ptr(cc)
+        b.A, b.Ainv, b.AinvT, b.B = _ptr(A2), _ptr(Ai2), _ptr(AiT2), _ptr(B2)
+        b.R, b.LT, b.PT, b.min_pivot = 0, _ptr(LT), 0, _ptr(mp2)
+        N.check(self.L.ihdg_assemble(C.byref(b), self._sptr), what)
+        self.stream.synchronize()
+        return LT
 
     # -- state -------------------------------------------------------------
     def interior(self, which=None):
@@ -258,7 +282,7 @@ class DeviceSolver:
         face nodes; None clears it."""
         torch, sp, d = self.torch, self.spec, self.mesh.dim
         if g is None:
-            self.s_inflow, self._inflow_faces = None, None
+            self.s_bdata, self._bdata_faces = None, None
             return
         if not isinstance(self.problem, TransportProblem) or sp.n_class != 1:
             raise NotImplementedError("inflow data is defined for transport (one operator class)")
@@ -287,7 +311,7 @@ class DeviceSolver:
                 faces[f] = (on, vals)
             return torch.as_tensor(qg, dtype=torch.float64, device=self.device), faces
 
-        self.s_inflow = torch.zeros((self.nloc, self.nv), dtype=torch.float64, device=self.device)
+        self.s_bdata = torch.zeros((self.nloc, self.nv), dtype=torch.float64, device=self.device)
         # one K4 pass per inflow face with that face's column block of L
         # (transport has a single operator class, so the block is contiguous)
         parts = [(g, self.LT)]
@@ -300,8 +324,53 @@ class DeviceSolver:
             q, fc = face_data(fn)
             faces = fc if faces is None else faces
             for f in fc:
-                self._apply(LT.view(-1)[f * nf * self.nv:], nf, q, nfc, f * nf, 0, self.s_inflow, 1)
-        self._inflow_faces = faces
+                self._apply(LT.view(-1)[f * nf * self.nv:], nf, q, nfc, f * nf, 0, self.s_bdata, 1)
+        self._bdata_faces = faces
+        self.stream.synchronize()
+
+    def _boundary_face_data(self, fn, face_ok):
+        """(q, faces): fn at the face nodes of every boundary face f of the
+        local elements with face_ok(f) (non-periodic axes), as a
+        [nloc][2d N_f] face-node array and {f: (elements, values)}."""
+        torch, sp, d = self.torch, self.spec, self.mesh.dim
+        nf = sp.n1 ** (d - 1)
+        nfc = 2 * d * nf
+        pts = self._local_points(self.ops.nodes)
+        e = np.arange(self.nloc, dtype=np.int64)
+        idx = [(e // int(np.prod(self.mesh.cells[:a]))) % self.mesh.cells[a] for a in range(d - 1)]
+        idx.append(self.layers[0] + e // self.ls)
+        qg = np.zeros((self.nloc, nfc))
+        faces = {}
+        for f in range(2 * d):
+            a, side = divmod(f, 2)
+            if self.mesh.periodic[a] or not face_ok(f):
+                continue
+            on = np.flatnonzero(idx[a] == (self.mesh.cells[a] - 1 if side else 0))
+            if on.size == 0:
+                continue
+            ids = face_node_indices(d, sp.n1, f)
+            vals = np.asarray(fn(pts[on][:, ids, :].reshape(-1, d)), dtype=float).reshape(on.size, nf)
+            qg[on, f * nf:(f + 1) * nf] = vals
+            faces[f] = (on, vals)
+        return torch.as_tensor(qg, dtype=torch.float64, device=self.device), faces
+
+    def set_dirichlet(self, g) -> None:
+        """Dirichlet data u_hat := g_D on the boundary,
+        convection-diffusion: s gains L_D q_g (K4), L_D = A^-1 B_D assembled by
+        K1 from the Dirichlet-data term list; g at the boundary face nodes
+        (the trace space).  The returned trace is g on the boundary."""
+        if g is None:
+            self.s_bdata, self._bdata_faces = None, None
+            return
+        if self.LT_dir is None:
+            raise NotImplementedError("Dirichlet data needs a ConvectionDiffusionProblem built with dirichlet=")
+        sp = self.spec
+        q, faces = self._boundary_face_data(g, lambda f: True)
+        nfc = q.shape[1]
+        assert sp.kin == nfc, "Dirichlet data: every face slot is coupled for convection-diffusion"
+        self.s_bdata = self.torch.zeros((self.nloc, self.nv), dtype=self.torch.float64, device=self.device)
+        self._apply(self.LT_dir, nfc, q, nfc, 0, 0, self.s_bdata, 0)
+        self._bdata_faces = faces
         self.stream.synchronize()
 
     def prepare_steady(self) -> None:
@@ -310,8 +379,8 @@ class DeviceSolver:
             self.s.zero_()
         else:
             self.s.copy_(self.s_static)
-        if getattr(self, "s_inflow", None) is not None:
-            self.s.add_(self.s_inflow)
+        if getattr(self, "s_bdata", None) is not None:
+            self.s.add_(self.s_bdata)
 
     def begin_step(self, exchange=None) -> None:
         """RHS of the next step from the current state u^m.
@@ -328,11 +397,11 @@ class DeviceSolver:
             acc = 1
         else:
             acc = 0
-        if getattr(self, "s_inflow", None) is not None:
+        if getattr(self, "s_bdata", None) is not None:
             if acc:
-                self.s.add_(self.s_inflow)
+                self.s.add_(self.s_bdata)
             else:
-                self.s.copy_(self.s_inflow)
+                self.s.copy_(self.s_bdata)
             acc = 1
         self._apply(self.PT, sp.nr, self.u[self.cur], self.nv, sp.time_comp0 * self.np_, 1, self.s, acc)
         if sp.time_scheme == "CN":
@@ -543,7 +612,7 @@ class DeviceSolver:
         """Single-valued trace (n_faces, 1, N_f) in mesh.py face order; on
         inflow boundary faces with data it is g at the face nodes."""
         t = self.trace_of()
-        for f, (on, vals) in (getattr(self, "_inflow_faces", None) or {}).items():
+        for f, (on, vals) in (getattr(self, "_bdata_faces", None) or {}).items():
             t[self.torch.as_tensor(self._face_ids(on, f), device=self.device)] = self.torch.as_tensor(
                 vals, dtype=self.torch.float64, device=self.device)
         return t.cpu().numpy().reshape(self.mesh.n_faces, 1, t.shape[1])

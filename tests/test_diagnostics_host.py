@@ -132,3 +132,34 @@ def test_oracle_cn_inflow_is_the_level_average():
     b1 = B.b_inflow.copy()
     B.set_inflow(g0)
     assert np.allclose(S.b_inflow, 0.5 * (b1 + B.b_inflow), rtol=0, atol=1e-15)
+
+
+@pytest.mark.parametrize("dim,cells,p", [(2, [3, 4], 2), (3, [2, 2, 3], 1), (1, [5], 3)])
+def test_dirichlet_data_terms_match_oracle(dim, cells, p):
+    """The product's Dirichlet-data couplings B_D (term lists, K1's input)
+    applied to g at the boundary face nodes = the oracle's quadrature of
+    -<g, tau.n> and +tau <g, v>, for every element."""
+    from oracle.ihdg_oracle import OracleProblem, OracleSolver
+    from paper_1711_01175_b200.assembly import build_spec, evaluate_terms, face_node_indices
+    from paper_1711_01175_b200.basis import build_operators
+    from paper_1711_01175_b200.mesh import build_mesh
+    from paper_1711_01175_b200.pde import ConvectionDiffusionProblem
+
+    beta = np.array([1.0, -0.5, 0.3])[:dim]
+    g = lambda x: 1.0 + np.sin(2 * x[:, 0]) + (x[:, -1] ** 2 if x.shape[1] > 1 else 0.0)  # noqa: E731
+    mesh = build_mesh(dim, cells)
+    ops = build_operators(p, dim, mesh.h)
+    prob = ConvectionDiffusionProblem(kappa=0.1, beta=beta, dirichlet=g)
+    sp = build_spec(mesh, prob, ops, 0.05)
+    _, BD, _ = evaluate_terms(sp, which="dir")
+    S = OracleSolver(OracleProblem("cd", dim, beta=beta, kappa=0.1), cells, p, dt=0.05)
+    S.set_dirichlet(g)
+    pts = S.element_points(S.b.nodes)
+    nf = (p + 1) ** (dim - 1)
+    for e in range(S.nel):
+        q = np.zeros(2 * dim * nf)
+        for f in range(2 * dim):
+            if S.nbr[e, f] == -1:
+                q[f * nf:(f + 1) * nf] = g(pts[e][face_node_indices(dim, p + 1, f)])
+        c = sp.class_of_mask[S.mask[e]]
+        assert np.allclose(BD[c] @ q, S.b_inflow[e], rtol=1e-12, atol=1e-13)

@@ -131,3 +131,75 @@ def test_inflow_constant_transported_1d():
     assert rep.status == "converged"
     assert np.max(np.abs(rep.state.data - 1.0)) < 1e-13
     assert np.allclose(rep.trace, 1.0, atol=1e-13)
+
+
+def _cd_manufactured():
+    """u^e = exp(x) sin(y) + 0.5 (harmonic part), kappa = 0.1, beta = (1, 0.5),
+    nu = 1: f = beta . grad u + nu u, g_D = u^e."""
+    from paper_1711_01175_b200.pde import ConvectionDiffusionProblem
+
+    ue = lambda x: np.exp(x[:, 0]) * np.sin(x[:, 1]) + 0.5   # noqa: E731
+    f = lambda x: (np.exp(x[:, 0]) * (1.0 * np.sin(x[:, 1]) + 0.5 * np.cos(x[:, 1]))  # noqa: E731
+                   + ue(x))
+    return ConvectionDiffusionProblem(kappa=0.1, beta=np.array([1.0, 0.5]), nu=1.0, forcing=f, dirichlet=ue,
+                                      exact=ue), ue
+
+
+def test_dirichlet_data_steady_parity_and_accuracy():
+    """Steady convection-diffusion with Dirichlet data g_D = u^e and the
+    manufactured forcing: same count as the oracle, volume and trace (g on
+    the boundary) within 1e-10 relative L2, and the solution is u^e to the
+    discretisation error."""
+    from oracle.ihdg_oracle import OracleProblem, OracleSolver
+    from paper_1711_01175_b200.basis import build_operators
+    from paper_1711_01175_b200.iteration import IterationConfig, run
+    from paper_1711_01175_b200.mesh import build_mesh
+    from tests.oracle_bridge import rel_l2
+
+    prob, ue = _cd_manufactured()
+    mesh = build_mesh(2, [6, 5])
+    ops = build_operators(3, 2, mesh.h)
+    rep = run(mesh, prob, ops, IterationConfig(tol=1e-10))
+    S = OracleSolver(OracleProblem("cd", 2, beta=prob.beta, kappa=0.1, nu=1.0), [6, 5], 3)
+    S.set_forcing(prob.forcing)
+    S.set_dirichlet(ue)
+    o = S.run(tol=1e-10)
+    assert rep.iterations == o["iterations"] and rep.status == o["status"] == "converged"
+    assert rel_l2(rep.state.data.reshape(S.nel, -1), o["u"]) < 1e-10
+    assert rel_l2(rep.trace, S.trace(o["u"])) < 1e-10
+    S.set_exact(ue)
+    u_only = np.zeros_like(o["u"]).reshape(S.nel, S.m, S.npn)
+    u_only[:, 2, :] = o["u"].reshape(S.nel, S.m, S.npn)[:, 2, :]
+    assert S.err_norm(u_only.reshape(S.nel, -1)) < 1e-4
+
+
+def test_dirichlet_data_backward_euler_parity():
+    """Two backward-Euler steps with time-dependent Dirichlet data g(x, t):
+    iterations per step and fields as the oracle."""
+    from oracle.ihdg_oracle import OracleProblem, OracleSolver
+    from paper_1711_01175_b200.basis import build_operators
+    from paper_1711_01175_b200.iteration import IterationConfig, run_time_dependent
+    from paper_1711_01175_b200.mesh import build_mesh
+    from paper_1711_01175_b200.pde import ConvectionDiffusionProblem
+    from paper_1711_01175_b200.workloads import fourier_modes
+    from tests.oracle_bridge import rel_l2
+
+    g = lambda x, t=0.0: np.cos(x[:, 0] + 2 * t) * (1 + x[:, 1])   # noqa: E731
+    prob = ConvectionDiffusionProblem(kappa=0.02, beta=np.array([1.0, 1.0]), dirichlet=g)
+    mesh = build_mesh(2, [8, 8])
+    ops = build_operators(2, 2, mesh.h)
+    f0 = fourier_modes(np.random.default_rng(6), 2)
+    dt = 0.02
+    reps = run_time_dependent(mesh, prob, ops, IterationConfig(tol=1e-10), dt, n_steps=2, initial={"u": f0},
+                              keep_states=True)
+    S = OracleSolver(OracleProblem("cd", 2, beta=prob.beta, kappa=0.02), [8, 8], 2, dt=dt)
+    u = np.zeros((S.nel, S.m, S.npn))
+    u[:, 2, :] = S.interpolate(f0)
+    u = u.reshape(S.nel, -1)
+    for m, r in enumerate(reps):
+        t = (m + 1) * dt
+        S.set_dirichlet(lambda x: g(x, t))
+        o = S.run(u0=u, u_prev=u, tol=1e-10)
+        assert r.iterations == o["iterations"] and r.status == o["status"] == "converged"
+        assert rel_l2(r.state.data.reshape(S.nel, -1), o["u"]) < 1e-10
+        u = o["u"]

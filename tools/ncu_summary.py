@@ -29,6 +29,8 @@ def main(path):
     want = ("dram__bytes_read.sum", "dram__bytes_write.sum", "gpu__time_duration.sum",
             "sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active",
             "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active",
+            "sm__inst_executed_pipe_tensor_subpipe_dmma.avg.pct_of_peak_sustained_active",
+            "sm__ops_path_tensor_src_fp64.avg.pct_of_peak_sustained_elapsed",
             "smsp__inst_executed.sum", "lts__t_bytes.sum")
     for i, n in enumerate(h):
         if n in want:
