@@ -575,7 +575,7 @@ class OracleSolver:
             self.b_inflow[on, :self.npn] += 0.5 * (abs(bn) - bn) * gv @ M.T
             self.inflow_nodes[f] = (on, gv)
 
-    def set_dirichlet(self, g):
+    def set_dirichlet(self, g, g_old=None):
         """Convection-diffusion Dirichlet data u_hat := g_D on the boundary
         (SPEC.md:214, 269), in the trace space (g at the face GLL nodes):
         the sigma_a rows gain -<g_h, tau.n> = -sgn <g_h, phi>_f and the u row
@@ -585,8 +585,10 @@ class OracleSolver:
         self.inflow_nodes = {}
         if g is None:
             return
-        if self.prob.kind != "cd" or self.time_scheme == "CN":
-            raise NotImplementedError("Dirichlet data: convection-diffusion, backward Euler / steady")
+        if self.prob.kind != "cd":
+            raise NotImplementedError("Dirichlet data: convection-diffusion")
+        if self.time_scheme == "CN" and g_old is None:
+            raise ValueError("Crank-Nicolson Dirichlet data needs g_old")
         pts = self.element_points(self.b.nodes)
         Vf = _kron_axes([self.b.V] * (d - 1)) if d > 1 else np.ones((1, 1))
         U = d
@@ -602,8 +604,14 @@ class OracleSolver:
             gv = np.asarray(g(pts[on][:, ids, :].reshape(-1, d)), float).reshape(on.size, -1)
             M = self.el.fmass(f, self.el.Pf[f], Vf)          # (Np, N_f)
             val = gv @ M.T
+            # Crank-Nicolson: the algebraic sigma rows take the new level only,
+            # the u row (time derivative) the average of the two levels
+            val_u = val
+            if self.time_scheme == "CN":
+                g0 = np.asarray(g_old(pts[on][:, ids, :].reshape(-1, d)), float).reshape(on.size, -1)
+                val_u = 0.5 * (val + g0 @ M.T)
             self.b_inflow[on, a * self.npn:(a + 1) * self.npn] += -sgn * val
-            self.b_inflow[on, U * self.npn:(U + 1) * self.npn] += tau * val
+            self.b_inflow[on, U * self.npn:(U + 1) * self.npn] += tau * val_u
             self.inflow_nodes[f] = (on, gv)
 
     # -- sweep -------------------------------------------------------------
@@ -728,7 +736,7 @@ class OracleSolver:
         return out
 
     def run_time_dependent(self, u0, nsteps, tol=1e-10, max_iters=10000, norm="volume", exact=None,
-                           forcing=None, inflow=None):
+                           forcing=None, inflow=None, dirichlet=None):
         """forcing(x, t) / inflow(x, t): time-dependent data, taken at the new
         level (BE) or averaged / split between the levels (CN)."""
         u = np.array(u0, float).reshape(self.nel, self.nv)
@@ -742,6 +750,8 @@ class OracleSolver:
                     self.set_forcing(lambda x: forcing(x, t1))
             if inflow is not None:
                 self.set_inflow(lambda x: inflow(x, t1), lambda x: inflow(x, t0))
+            if dirichlet is not None:
+                self.set_dirichlet(lambda x: dirichlet(x, t1), lambda x: dirichlet(x, t0))
             if norm == "exact":
                 self.set_exact(exact, (step + 1) * self.dt)
             r = self.run(u0=u, tol=tol, max_iters=max_iters, norm=norm, u_prev=u)

@@ -107,6 +107,8 @@ class OperatorSpec:
     coefs_expl: Optional[np.ndarray] = None
     terms_dir: Optional[np.ndarray] = None    # CD Dirichlet data: A terms + B_D terms (L_D = A^-1 B_D)
     coefs_dir: Optional[np.ndarray] = None
+    terms_dir_expl: Optional[np.ndarray] = None   # CN: A terms + (1 - theta) B_D terms (old-level data)
+    coefs_dir_expl: Optional[np.ndarray] = None
 
     @property
     def n1(self):
@@ -307,8 +309,6 @@ def build_spec(mesh, problem, ops: ElementOperators, dt=None, norm="auto", schem
         beta = problem.beta_const(d)
         if beta is None:
             raise NotImplementedError("device path needs a constant beta (shared operator)")
-        if problem.dirichlet is not None and time_scheme == "CN":
-            raise NotImplementedError("Dirichlet data with Crank-Nicolson")
         dterms = _Terms(d) if problem.dirichlet is not None else None
         m = d + 1
         U = d
@@ -452,17 +452,30 @@ def build_spec(mesh, problem, ops: ElementOperators, dt=None, norm="auto", schem
         raise TypeError(f"unsupported problem type {type(problem).__name__}")
 
     terms_expl = coefs_expl = None
+    theta_rows = None
     if time_scheme == "CN":
+        theta_rows = np.ones(m)
+        theta_rows[tc0:tc0 + ntc] = 0.5
         # theta = 1/2 on rows with a time derivative, 1 on algebraic rows (sigma)
         theta = np.ones(m)
         theta[tc0:tc0 + ntc] = 0.5
         terms_expl, coefs_expl = terms.crank_nicolson(theta, tc0)
         nr, tc0, ntc = m * ops.n_nodes, 0, m
-    terms_dir = coefs_dir = None
+    terms_dir = coefs_dir = terms_dir_expl = coefs_dir_expl = None
     if isinstance(problem, ConvectionDiffusionProblem) and dterms is not None:
+        # the A terms after the (possible) Crank-Nicolson split; the data
+        # couplings split like the trace couplings: theta_c B_D on the new
+        # level, (1 - theta_c) B_D on the old one
         keep = [i for i, r in enumerate(terms.rows) if r[1] == A_T]
-        terms_dir = np.asarray([terms.rows[i] for i in keep] + dterms.rows, dtype=np.int32).reshape(-1, 8)
-        coefs_dir = np.asarray([terms.coefs[i] for i in keep] + dterms.coefs, dtype=float)
+        a_rows = [terms.rows[i] for i in keep]
+        a_coefs = [terms.coefs[i] for i in keep]
+        th = [1.0 if theta_rows is None else float(theta_rows[r[2]]) for r in dterms.rows]
+        terms_dir = np.asarray(a_rows + dterms.rows, dtype=np.int32).reshape(-1, 8)
+        coefs_dir = np.asarray(a_coefs + [t * c for t, c in zip(th, dterms.coefs)], dtype=float)
+        if theta_rows is not None:
+            ex = [(r, (1.0 - t) * c) for r, t, c in zip(dterms.rows, th, dterms.coefs) if t != 1.0]
+            terms_dir_expl = np.asarray(a_rows + [r for r, _ in ex], dtype=np.int32).reshape(-1, 8)
+            coefs_dir_expl = np.asarray(a_coefs + [c for _, c in ex], dtype=float)
     terms_arr = np.asarray(terms.rows, dtype=np.int32).reshape(-1, 8)
     return OperatorSpec(
         dim=d, order=ops.p, ncomp=m, labels=tuple(labels), n_class=len(masks),
@@ -471,7 +484,8 @@ def build_spec(mesh, problem, ops: ElementOperators, dt=None, norm="auto", schem
         time_comp0=tc0, n_time_comp=ntc, forcing_comp=fcomp, face_w=face_w, coupled=coupled,
         out_face=out_face, out_w=out_w, own_w=own_w, comp_w=comp_w, trace_w=tw, jac=J, jac_face=jac_face,
         periodic=tuple(mesh.periodic), scheme=scheme, time_scheme=time_scheme, terms_expl=terms_expl,
-        coefs_expl=coefs_expl, terms_dir=terms_dir, coefs_dir=coefs_dir)
+        coefs_expl=coefs_expl, terms_dir=terms_dir, coefs_dir=coefs_dir, terms_dir_expl=terms_dir_expl,
+        coefs_dir_expl=coefs_dir_expl)
 
 
 def evaluate_terms(spec: OperatorSpec, expl: bool = False, which: str = "main"):
@@ -491,7 +505,8 @@ def evaluate_terms(spec: OperatorSpec, expl: bool = False, which: str = "main"):
     if expl:
         which = "expl"
     rows, coefs = {"main": (spec.terms, spec.coefs), "expl": (spec.terms_expl, spec.coefs_expl),
-                   "dir": (spec.terms_dir, spec.coefs_dir)}[which]
+                   "dir": (spec.terms_dir, spec.coefs_dir),
+                   "dir_expl": (spec.terms_dir_expl, spec.coefs_dir_expl)}[which]
     for row, coef in zip(rows, coefs):
         cls, target, rc, cb = (int(x) for x in row[:4])
         mats = []

@@ -340,7 +340,9 @@ def run_time_dependent(mesh, problem, ops: ElementOperators, cfg: Optional[Itera
                 solver.set_forcing(_exact_at(forcing, t_new))
         dirichlet = getattr(problem, "dirichlet", None)
         if dirichlet is not None:
-            solver.set_dirichlet(_exact_at(dirichlet, t_new) if _takes_time(dirichlet) else dirichlet)
+            d_t = _takes_time(dirichlet)
+            solver.set_dirichlet(_exact_at(dirichlet, t_new) if d_t else dirichlet,
+                                 (_exact_at(dirichlet, t_old) if d_t else dirichlet) if ts == "CN" else None)
         if inflow is not None:
             g_t = _takes_time(inflow)
             solver.set_inflow(_exact_at(inflow, t_new) if g_t else inflow,

@@ -155,10 +155,13 @@ class DeviceSolver:
             b.R, b.LT, b.PT, b.min_pivot = 0, _ptr(self.LT_expl), 0, _ptr(mp2)
             N.check(self.L.ihdg_assemble(C.byref(b), self._sptr), "ihdg_assemble (CN explicit)")
             del A2, Ai2, AiT2, B2, mp2
-        self.LT_dir = None
+        self.LT_dir = self.LT_dir_expl = None
         if sp.terms_dir is not None:
             # L_D = A^-1 B_D: the Dirichlet-data couplings (convection-diffusion)
             self.LT_dir = self._assemble_lifted(sp.terms_dir, sp.coefs_dir, "ihdg_assemble (Dirichlet data)")
+        if sp.terms_dir_expl is not None:
+            self.LT_dir_expl = self._assemble_lifted(sp.terms_dir_expl, sp.coefs_dir_expl,
+                                                     "ihdg_assemble (Dirichlet data, CN old level)")
         piv = self.min_pivot.cpu().numpy()
         scale = self.A.abs().amax(dim=(1, 2)).cpu().numpy()
         bad = np.nonzero(~(piv > 1e-13 * scale))[0]
@@ -354,11 +357,13 @@ class DeviceSolver:
             faces[f] = (on, vals)
         return torch.as_tensor(qg, dtype=torch.float64, device=self.device), faces
 
-    def set_dirichlet(self, g) -> None:
+    def set_dirichlet(self, g, g_explicit=None) -> None:
         """Dirichlet data u_hat := g_D on the boundary,
         convection-diffusion: s gains L_D q_g (K4), L_D = A^-1 B_D assembled by
         K1 from the Dirichlet-data term list; g at the boundary face nodes
-        (the trace space).  The returned trace is g on the boundary."""
+        (the trace space).  The returned trace is g on the boundary.
+        Crank-Nicolson: g at the new level, g_explicit at the old one, split
+        like the trace couplings (theta = 1 on the sigma rows, 1/2 on u)."""
         if g is None:
             self.s_bdata, self._bdata_faces = None, None
             return
@@ -370,6 +375,11 @@ class DeviceSolver:
         assert sp.kin == nfc, "Dirichlet data: every face slot is coupled for convection-diffusion"
         self.s_bdata = self.torch.zeros((self.nloc, self.nv), dtype=self.torch.float64, device=self.device)
         self._apply(self.LT_dir, nfc, q, nfc, 0, 0, self.s_bdata, 0)
+        if self.LT_dir_expl is not None:
+            if g_explicit is None:
+                raise ValueError("Crank-Nicolson Dirichlet data needs the old-level data g_explicit")
+            q0, _ = self._boundary_face_data(g_explicit, lambda f: True)
+            self._apply(self.LT_dir_expl, nfc, q0, nfc, 0, 0, self.s_bdata, 1)
         self._bdata_faces = faces
         self.stream.synchronize()
 

@@ -163,3 +163,38 @@ def test_dirichlet_data_terms_match_oracle(dim, cells, p):
                 q[f * nf:(f + 1) * nf] = g(pts[e][face_node_indices(dim, p + 1, f)])
         c = sp.class_of_mask[S.mask[e]]
         assert np.allclose(BD[c] @ q, S.b_inflow[e], rtol=1e-12, atol=1e-13)
+
+
+def test_dirichlet_data_terms_crank_nicolson_match_oracle():
+    """Crank-Nicolson split of the Dirichlet-data couplings (theta = 1 on the
+    sigma rows, 1/2 on the u row): theta B_D q(g_new) + (1 - theta) B_D q(g_old)
+    equals the oracle's CN data term for every element."""
+    from oracle.ihdg_oracle import OracleProblem, OracleSolver
+    from paper_1711_01175_b200.assembly import build_spec, evaluate_terms, face_node_indices
+    from paper_1711_01175_b200.basis import build_operators
+    from paper_1711_01175_b200.mesh import build_mesh
+    from paper_1711_01175_b200.pde import ConvectionDiffusionProblem
+
+    dim, cells, p = 2, [3, 3], 2
+    beta = np.array([1.0, -0.5])
+    g1 = lambda x: 1.0 + x[:, 0] * x[:, 1]   # noqa: E731
+    g0 = lambda x: np.cos(x[:, 1])           # noqa: E731
+    mesh = build_mesh(dim, cells)
+    ops = build_operators(p, dim, mesh.h)
+    sp = build_spec(mesh, ConvectionDiffusionProblem(kappa=0.1, beta=beta, dirichlet=g1), ops, 0.05,
+                    time_scheme="CN")
+    _, B1, _ = evaluate_terms(sp, which="dir")
+    _, B0, _ = evaluate_terms(sp, which="dir_expl")
+    S = OracleSolver(OracleProblem("cd", dim, beta=beta, kappa=0.1), cells, p, dt=0.05, time_scheme="CN")
+    S.set_dirichlet(g1, g0)
+    pts = S.element_points(S.b.nodes)
+    nf = p + 1
+    for e in range(S.nel):
+        q1, q0 = np.zeros(4 * nf), np.zeros(4 * nf)
+        for f in range(4):
+            if S.nbr[e, f] == -1:
+                ids = face_node_indices(dim, p + 1, f)
+                q1[f * nf:(f + 1) * nf] = g1(pts[e][ids])
+                q0[f * nf:(f + 1) * nf] = g0(pts[e][ids])
+        c = sp.class_of_mask[S.mask[e]]
+        assert np.allclose(B1[c] @ q1 + B0[c] @ q0, S.b_inflow[e], rtol=1e-12, atol=1e-13)

@@ -173,9 +173,10 @@ def test_dirichlet_data_steady_parity_and_accuracy():
     assert S.err_norm(u_only.reshape(S.nel, -1)) < 1e-4
 
 
-def test_dirichlet_data_backward_euler_parity():
-    """Two backward-Euler steps with time-dependent Dirichlet data g(x, t):
-    iterations per step and fields as the oracle."""
+@pytest.mark.parametrize("ts", ["BE", "CN"])
+def test_dirichlet_data_time_dependent_parity(ts):
+    """Two backward-Euler / Crank-Nicolson steps with time-dependent Dirichlet
+    data g(x, t): iterations per step and fields as the oracle."""
     from oracle.ihdg_oracle import OracleProblem, OracleSolver
     from paper_1711_01175_b200.basis import build_operators
     from paper_1711_01175_b200.iteration import IterationConfig, run_time_dependent
@@ -191,14 +192,14 @@ def test_dirichlet_data_backward_euler_parity():
     f0 = fourier_modes(np.random.default_rng(6), 2)
     dt = 0.02
     reps = run_time_dependent(mesh, prob, ops, IterationConfig(tol=1e-10), dt, n_steps=2, initial={"u": f0},
-                              keep_states=True)
-    S = OracleSolver(OracleProblem("cd", 2, beta=prob.beta, kappa=0.02), [8, 8], 2, dt=dt)
+                              keep_states=True, time_scheme="crank-nicolson" if ts == "CN" else "backward-euler")
+    S = OracleSolver(OracleProblem("cd", 2, beta=prob.beta, kappa=0.02), [8, 8], 2, dt=dt, time_scheme=ts)
     u = np.zeros((S.nel, S.m, S.npn))
     u[:, 2, :] = S.interpolate(f0)
     u = u.reshape(S.nel, -1)
     for m, r in enumerate(reps):
         t = (m + 1) * dt
-        S.set_dirichlet(lambda x: g(x, t))
+        S.set_dirichlet(lambda x: g(x, t), lambda x: g(x, t - dt))
         o = S.run(u0=u, u_prev=u, tol=1e-10)
         assert r.iterations == o["iterations"] and r.status == o["status"] == "converged"
         assert rel_l2(r.state.data.reshape(S.nel, -1), o["u"]) < 1e-10
