@@ -90,6 +90,10 @@ __global__ void __launch_bounds__(V3Cfg<D, N1, M, NCF, NWC, NS, NCW, PF, NQW_>::
   __shared__ int qf_s[KC], qh_s[KC];
   __shared__ int qt_s[KC][NWC];
   __shared__ int mfast_s[NS];
+  // item ids of the stage's current load / q (phase-aliasing guard: a warp
+  // that waits on stage s for item it first sees it published, so the
+  // barrier is at most one phase behind its parity wait)
+  __shared__ int mload_s[NS], mq_s[NS];
   __shared__ unsigned mcset_s[NS];
   __shared__ int mcls_s[NS][E];
   __shared__ double part_s[NS];
@@ -138,6 +142,8 @@ __global__ void __launch_bounds__(V3Cfg<D, N1, M, NCF, NWC, NS, NCW, PF, NQW_>::
       qh_s[k] = ci * NWC * NF + nn;
     }
     for (int s = 0; s < NS; ++s) {
+      mload_s[s] = -1;
+      mq_s[s] = -1;
       mbar_init(&full_bar[s], 1);
       mbar_init(&qready_bar[s], 1);
       mbar_init(&done_bar[s], 1);
@@ -189,6 +195,7 @@ __global__ void __launch_bounds__(V3Cfg<D, N1, M, NCF, NWC, NS, NCW, PF, NQW_>::
         STile<D> ti;
         ti.e0 = phys_of(it) * E;   // tiles are E consecutive elements of a row, c0 % E == 0
         constexpr uint32_t bytes = (uint32_t)(E * NV * sizeof(double));
+        *(volatile int*)&mload_s[stage] = it;   // stage free: item it - NS retired
         mbar_arrive_expect_tx(&full_bar[stage], bytes);
         if constexpr (C::ES == NV) {
           bulk_g2s(sm + stage * C::STAGE, uo + (int64_t)ti.e0 * NV, bytes, &full_bar[stage]);
@@ -278,6 +285,8 @@ __global__ void __launch_bounds__(V3Cfg<D, N1, M, NCF, NWC, NS, NCW, PF, NQW_>::
       const STile<D> ti = tnext;   // geometry of item it (computed by its gather)
       gather(it + NQW, gvn, qsn, qln);
       V3_T0(tp);
+      while (*(volatile int*)&mload_s[stage] != it) {
+      }
       mbar_wait(&full_bar[stage], (it / NS) & 1);
       V3_ACC(1, tp);
       V3_T0(tq);
@@ -320,7 +329,10 @@ __global__ void __launch_bounds__(V3Cfg<D, N1, M, NCF, NWC, NS, NCW, PF, NQW_>::
       }
       __syncwarp();
       V3_ACC(2, tq);
-      if (lane == 0) mbar_arrive(&qready_bar[stage]);
+      if (lane == 0) {
+        *(volatile int*)&mq_s[stage] = it;
+        mbar_arrive(&qready_bar[stage]);
+      }
 #pragma unroll
       for (int m = 0; m < QM; ++m)
 #pragma unroll
@@ -353,6 +365,8 @@ __global__ void __launch_bounds__(V3Cfg<D, N1, M, NCF, NWC, NS, NCW, PF, NQW_>::
       if constexpr (C::PREF) load_s(it + NCW, *reinterpret_cast<double(*)[NRT][2]>(&accn[0][0]));
       else load_s(it, acc);
       V3_T0(tc);
+      while (*(volatile int*)&mq_s[stage] != it) {
+      }
       mbar_wait(&qready_bar[stage], (it / NS) & 1);
       V3_ACC(3, tc);
       V3_T0(tm);
