@@ -166,7 +166,7 @@ struct StreamEntry {
 
 // config-4 v3 shape (A/B builds override it): stages, consumer warps, prep warps
 #ifndef IHDG_C4_NS
-#define IHDG_C4_NS 12
+#define IHDG_C4_NS 10
 #endif
 #ifndef IHDG_C4_NCW
 #define IHDG_C4_NCW 7
