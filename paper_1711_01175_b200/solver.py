@@ -291,28 +291,13 @@ class DeviceSolver:
             raise NotImplementedError("inflow data is defined for transport (one operator class)")
         nf = sp.n1 ** (d - 1)
         nfc = 2 * d * nf
-        pts = self._local_points(self.ops.nodes)               # (nloc, Np, d)
-        lb = self.layers[0]
-        e = np.arange(self.nloc, dtype=np.int64)
-        idx = [(e // int(np.prod(self.mesh.cells[:a]))) % self.mesh.cells[a] for a in range(d - 1)]
-        idx.append(lb + e // self.ls)
+
+        def inflow_face(f):
+            return bool(sp.coupled[f]) and float(sp.face_w[f, 0]) != 0.0
 
         def face_data(fn):
-            qg = np.zeros((self.nloc, nfc))
-            faces = {}
-            for f in range(2 * d):
-                a, side = divmod(f, 2)
-                w = float(sp.face_w[f, 0])
-                if not sp.coupled[f] or w == 0.0 or self.mesh.periodic[a]:
-                    continue
-                on = np.flatnonzero(idx[a] == (self.mesh.cells[a] - 1 if side else 0))
-                if on.size == 0:
-                    continue
-                fn_ids = face_node_indices(d, sp.n1, f)
-                vals = np.asarray(fn(pts[on][:, fn_ids, :].reshape(-1, d)), dtype=float).reshape(on.size, nf)
-                qg[on, f * nf:(f + 1) * nf] = w * vals
-                faces[f] = (on, vals)
-            return torch.as_tensor(qg, dtype=torch.float64, device=self.device), faces
+            # q = face_w g on the inflow boundary faces (the neighbour scalar)
+            return self._boundary_face_data(fn, inflow_face, weight=lambda f: float(sp.face_w[f, 0]))
 
         self.s_bdata = torch.zeros((self.nloc, self.nv), dtype=torch.float64, device=self.device)
         # one K4 pass per inflow face with that face's column block of L
@@ -331,7 +316,7 @@ class DeviceSolver:
         self._bdata_faces = faces
         self.stream.synchronize()
 
-    def _boundary_face_data(self, fn, face_ok):
+    def _boundary_face_data(self, fn, face_ok, weight=None):
         """(q, faces): fn at the face nodes of every boundary face f of the
         local elements with face_ok(f) (non-periodic axes), as a
         [nloc][2d N_f] face-node array and {f: (elements, values)}."""
@@ -353,7 +338,7 @@ class DeviceSolver:
                 continue
             ids = face_node_indices(d, sp.n1, f)
             vals = np.asarray(fn(pts[on][:, ids, :].reshape(-1, d)), dtype=float).reshape(on.size, nf)
-            qg[on, f * nf:(f + 1) * nf] = vals
+            qg[on, f * nf:(f + 1) * nf] = vals if weight is None else weight(f) * vals
             faces[f] = (on, vals)
         return torch.as_tensor(qg, dtype=torch.float64, device=self.device), faces
 
