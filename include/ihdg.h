@@ -54,7 +54,7 @@
 extern "C" {
 #endif
 
-#define IHDG_ABI_VERSION 2
+#define IHDG_ABI_VERSION 3
 #define IHDG_MAX_DIM 3
 #define IHDG_MAX_COMP 4
 #define IHDG_MAX_FACE 6
@@ -323,6 +323,18 @@ int ihdg_sweep(const ihdg_sweep_args* a, void* stream);
 /* 1 if ihdg_sweep would use the streaming (TMA bulk-copy) kernel for these
  * args, 0 if it falls back to the generic kernel */
 int ihdg_stream_variant(const ihdg_sweep_args* a);
+/* Name of the kernel ihdg_sweep launches for these args under the current
+ * selector: "k_sweep_ws" (2D warp-specialised, config 5), "k_sweep_v3"
+ * (warp-owned tiles, configs 2-4), "k_sweep_stream" (TMA ring), "k_sweep"
+ * (generic), or NULL if no kernel is instantiated (static string). */
+const char* ihdg_sweep_kernel(const ihdg_sweep_args* a);
+/* Process-wide sweep-kernel selector: "auto" (default; the initial value is
+ * read from the environment variable IHDG_SWEEP_IMPL), "ws" / "stream" (skip
+ * v3), "generic" (generic kernel only).  IHDG_ERR_ARG for other names. */
+int ihdg_set_sweep_impl(const char* name);
+/* CUDA-graph replay of sweep batches in ihdg_iterate (default on unless the
+ * environment sets IHDG_NO_GRAPH): 1 on, 0 off. */
+int ihdg_set_graphs(int on);
 int ihdg_finalize(const ihdg_finalize_args* a, void* stream);
 int ihdg_extract_trace(const ihdg_trace_args* a, void* stream);
 /* copy the ghost-padded layer range between two buffers (initial guess) */

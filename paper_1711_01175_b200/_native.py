@@ -17,6 +17,7 @@ __all__ = ["NativeUnavailable", "lib", "Geom", "IterState", "AssemblyArgs", "Cla
 LIB_PATH = os.environ.get("IHDG_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)),
                                                      "libihdg_cuda.so")
 
+ABI_VERSION = 3
 IHDG_OK = 0
 RUNNING, CONVERGED, DIVERGED, NAN, MAXITER = 0, 1, 2, 3, 4
 STATUS_NAMES = {RUNNING: "running", CONVERGED: "converged", DIVERGED: "diverged",
@@ -123,6 +124,9 @@ SIGNATURES = {
     "ihdg_quad_project": (_i32, [C.POINTER(QuadArgs), _p]),
     "ihdg_sweep": (_i32, [C.POINTER(SweepArgs), _p]),
     "ihdg_stream_variant": (_i32, [C.POINTER(SweepArgs)]),
+    "ihdg_sweep_kernel": (C.c_char_p, [C.POINTER(SweepArgs)]),
+    "ihdg_set_sweep_impl": (_i32, [C.c_char_p]),
+    "ihdg_set_graphs": (_i32, [_i32]),
     "ihdg_finalize": (_i32, [C.POINTER(FinalizeArgs), _p]),
     "ihdg_extract_trace": (_i32, [C.POINTER(TraceArgs), _p]),
     "ihdg_copy_state": (_i32, [C.POINTER(Geom), _p, _p, _p]),
@@ -156,7 +160,7 @@ def lib():
         fn = getattr(L, name)
         fn.restype = res
         fn.argtypes = args
-    if L.ihdg_abi_version() != 2:
+    if L.ihdg_abi_version() != ABI_VERSION:
         raise NativeUnavailable("libihdg_cuda.so ABI version mismatch")
     for i, st in enumerate(_STRUCTS):
         if L.ihdg_struct_size(i) != C.sizeof(st):
@@ -164,6 +168,25 @@ def lib():
                                     f"C {L.ihdg_struct_size(i)} vs ctypes {C.sizeof(st)}")
     _lib = L
     return L
+
+
+def sweep_kernel(args: "SweepArgs") -> str:
+    """Name of the kernel ihdg_sweep dispatches these args to (k_sweep_ws,
+    k_sweep_v3, k_sweep_stream or k_sweep)."""
+    s = lib().ihdg_sweep_kernel(C.byref(args))
+    if s is None:
+        raise RuntimeError("no sweep kernel instantiated for these args")
+    return s.decode()
+
+
+def set_sweep_impl(name: str) -> None:
+    """Process-wide kernel selector: auto / ws / stream / generic."""
+    check(lib().ihdg_set_sweep_impl(name.encode()), "ihdg_set_sweep_impl")
+
+
+def set_graphs(on: bool) -> None:
+    """CUDA-graph replay of sweep batches in ihdg_iterate on / off."""
+    lib().ihdg_set_graphs(1 if on else 0)
 
 
 def check(rc: int, what: str) -> None:

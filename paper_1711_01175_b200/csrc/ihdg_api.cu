@@ -1,4 +1,5 @@
 // extern "C" entry points of libihdg_cuda.so (declared in include/ihdg.h).
+#include <atomic>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -9,7 +10,9 @@
 
 using namespace ihdg;
 
-int ihdg_stream_launch(const ihdg_sweep_args* a, cudaStream_t st);
+int ihdg_stream_launch(const ihdg_sweep_args* a, cudaStream_t st, cudaError_t* err);
+const char* ihdg_stream_kernel_name(const ihdg_sweep_args* a);
+int ihdg_stream_set_impl(const char* name);
 
 namespace {
 
@@ -32,22 +35,30 @@ int check_launch(const char* what) {
   return IHDG_OK;
 }
 
+int current_device() {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  return dev;
+}
+
+// SM count of the current device (cached per device ordinal)
 int num_sms() {
-  static int sms = 0;
-  if (sms == 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    if (sms <= 0) sms = 148;
+  static int sms[64] = {0};
+  const int dev = current_device() & 63;
+  if (sms[dev] == 0) {
+    int n = 0;
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    sms[dev] = n > 0 ? n : 148;
   }
-  return sms;
+  return sms[dev];
 }
 
 // ---- per-instantiation launchers -----------------------------------------
 template <int D, int N1, int M>
 int launch_sweep(const ihdg_sweep_args* a, cudaStream_t st) {
   using C = Cfg<D, N1, M>;
-  static int grid_max = 0;
+  static int grid_max_dev[64] = {0};   // per device ordinal
+  int& grid_max = grid_max_dev[current_device() & 63];
   const size_t smem = SweepSmem<D, N1, M>::bytes;
   if (grid_max == 0) {
     IHDG_CUDA_TRY(cudaFuncSetAttribute(k_sweep<D, N1, M>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -67,7 +78,8 @@ int launch_sweep(const ihdg_sweep_args* a, cudaStream_t st) {
 template <int D, int N1, int M>
 int launch_apply(const ihdg_class_apply_args* a, cudaStream_t st) {
   using C = Cfg<D, N1, M>;
-  static int grid_max = 0;
+  static int grid_max_dev[64] = {0};   // per device ordinal
+  int& grid_max = grid_max_dev[current_device() & 63];
   const size_t smem = (size_t)C::NV * C::TE * sizeof(double);
   if (a->ncols > C::NV) return set_err(IHDG_ERR_ARG, "class_apply: ncols > NV");
   if (grid_max == 0) {
@@ -250,9 +262,11 @@ int ihdg_quad_project(const ihdg_quad_args* a, void* stream) {
 }
 
 static int do_sweep(const Entry* e, const ihdg_sweep_args* a, cudaStream_t st) {
-  const int rc = ihdg_stream_launch(a, st);
+  cudaError_t ce = cudaSuccess;
+  const int rc = ihdg_stream_launch(a, st, &ce);
   if (rc == 1) return IHDG_OK;
-  if (rc < 0) return check_launch("k_sweep_stream");
+  if (rc < 0)
+    return set_err(IHDG_ERR_CUDA, std::string(ihdg_stream_kernel_name(a)) + " launch: " + cudaGetErrorString(ce));
   return e->sweep(a, st);
 }
 
@@ -263,6 +277,20 @@ int ihdg_sweep(const ihdg_sweep_args* a, void* stream) {
   const Entry* e = find_entry(a->g.dim, a->g.order, a->g.ncomp);
   if (e == nullptr) return set_err(IHDG_ERR_UNSUPPORTED, "no kernel instantiated for this (dim, order, ncomp)");
   return do_sweep(e, a, (cudaStream_t)stream);
+}
+
+const char* ihdg_sweep_kernel(const ihdg_sweep_args* a) {
+  if (a == nullptr || check_geom(a->g) != IHDG_OK) return nullptr;
+  if (find_entry(a->g.dim, a->g.order, a->g.ncomp) == nullptr) return nullptr;
+  const char* s = ihdg_stream_kernel_name(a);
+  return s != nullptr ? s : "k_sweep";
+}
+
+int ihdg_set_sweep_impl(const char* name) {
+  if (ihdg_stream_set_impl(name) != 0)
+    return set_err(IHDG_ERR_ARG, std::string("unknown sweep impl '") + (name ? name : "(null)") +
+                                     "' (auto, ws, stream, generic)");
+  return IHDG_OK;
 }
 
 int ihdg_finalize(const ihdg_finalize_args* a, void* stream) {
@@ -307,20 +335,32 @@ struct SweepGraph {
   cudaGraphExec_t exec = nullptr;
 };
 
+// CUDA-graph replay of sweep batches: on unless IHDG_NO_GRAPH is set, and
+// switchable at run time (ihdg_set_graphs)
+static std::atomic<int> g_graphs{-1};
+
 static bool graphs_enabled() {
-  static int on = -1;
+  int on = g_graphs.load();
   if (on < 0) {
     const char* s = std::getenv("IHDG_NO_GRAPH");
-    on = (s != nullptr && s[0] != '\0' && s[0] != '0') ? 0 : 1;
+    int expect = -1;
+    g_graphs.compare_exchange_strong(expect, (s != nullptr && s[0] != '\0' && s[0] != '0') ? 0 : 1);
+    on = g_graphs.load();
   }
   return on == 1;
+}
+
+extern "C" int ihdg_set_graphs(int on) {
+  g_graphs.store(on ? 1 : 0);
+  return IHDG_OK;
 }
 
 static int do_error(const ihdg_error_args* e, cudaStream_t st);
 
 static cudaGraphExec_t sweep_graph(const Entry* e, const ihdg_sweep_args& a, const ihdg_error_args* ea, double* b0,
                                    double* b1, int nb, cudaStream_t st) {
-  static thread_local SweepGraph cache;
+  static thread_local SweepGraph cache_dev[8];   // per device ordinal (mod 8)
+  SweepGraph& cache = cache_dev[current_device() & 7];
   const bool has_e = ea != nullptr;
   if (cache.exec != nullptr && cache.b0 == b0 && cache.b1 == b1 && cache.nb == nb && cache.st == st &&
       std::memcmp(&cache.a, &a, sizeof(a)) == 0 && cache.has_e == has_e &&
@@ -463,9 +503,12 @@ static int iterate_impl(const ihdg_sweep_args* a0, const ihdg_error_args* e0, do
   cudaStream_t st = (cudaStream_t)stream;
   if (graphs_enabled() && (st == nullptr || st == cudaStreamLegacy || st == cudaStreamPerThread)) {
     // the default stream cannot be captured: run the loop on a private
-    // stream ordered after the caller's work (the call is synchronous)
-    static thread_local cudaStream_t own = nullptr;
-    static thread_local cudaEvent_t ev = nullptr;
+    // stream (per device) ordered after the caller's work (the call is synchronous)
+    static thread_local cudaStream_t own_dev[8] = {nullptr};
+    static thread_local cudaEvent_t ev_dev[8] = {nullptr};
+    const int slot = current_device() & 7;
+    cudaStream_t& own = own_dev[slot];
+    cudaEvent_t& ev = ev_dev[slot];
     if (own == nullptr) {
       IHDG_CUDA_TRY(cudaStreamCreateWithFlags(&own, cudaStreamNonBlocking));
       IHDG_CUDA_TRY(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
@@ -487,6 +530,7 @@ static int iterate_impl(const ihdg_sweep_args* a0, const ihdg_error_args* e0, do
   }
   const ihdg_error_args* ep = e0 != nullptr ? &ex : nullptr;
   int64_t launched = 0;
+  int32_t seen_iters = -1;
   // sweeps after the stop are no-ops on the device, so a batch rounded up to
   // an even count changes nothing but the launch count
   const int nb = batch + (batch & 1);
@@ -512,6 +556,14 @@ static int iterate_impl(const ihdg_sweep_args* a0, const ihdg_error_args* e0, do
     IHDG_CUDA_TRY(cudaMemcpyAsync(hs, a0->state, sizeof(ihdg_iter_state), cudaMemcpyDeviceToHost, st));
     IHDG_CUDA_TRY(cudaStreamSynchronize(st));
     if (hs->status != IHDG_RUNNING) break;
+    // a batch of live sweeps always advances the count (every sweep either
+    // finalizes or the status leaves RUNNING): no progress means the kernels
+    // did not run, so fail instead of polling forever
+    if (hs->iters <= seen_iters || hs->iters > hs->max_iters)
+      return set_err(IHDG_ERR_CUDA, "ihdg_iterate: the device iteration count stopped advancing (" +
+                                        std::to_string(hs->iters) + " after " + std::to_string(launched) +
+                                        " launched sweeps)");
+    seen_iters = hs->iters;
   }
   *state_out = *hs;
   if (n_launched) *n_launched = launched;

@@ -14,8 +14,6 @@
 //                    norm J |C^T Delta C|^2 of tile i-1      -> done[i&1]
 #pragma once
 
-#include <type_traits>
-
 #include "ihdg_stream.cuh"
 
 namespace ihdg {
@@ -467,112 +465,6 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS>::NT, 1)
       const int kk = 4 * ks + (lane & 3), nn = lane >> 2;
       cfr[ks] = (kk < N1 && nn < N1) ? chol_s[kk * N1 + nn] : 0.0;
     }
-#ifdef IHDG_WS_FUSE
-    // One tile: the norm of tile it-LAG and the contraction of tile it in one
-    // straight-line region per path (fast / masked), so ptxas can interleave
-    // the two DMMA chains; the first LAG tiles (no norm) run a peeled copy.
-    auto tile_body = [&](int it, auto with_norm) {
-      constexpr bool WN = decltype(with_norm)::value;
-      const int stage = it % NS;
-      const int ob = it & 1;
-      mbar_wait(&qready_bar[stage], (it / NS) & 1);
-      const int fast = mfast_s[stage];
-      const double* sst = sm + stage * C::STAGE;
-      const double* ust = sst + TILE;
-      const double* qst = ust + TILE + C::HALO;
-      const int jn = it - C::LAG;
-      if constexpr (WN) mbar_wait(&done_bar[jn & 1], (jn >> 1) & 1);
-      double nsum = 0.0;
-      double acc[NEG][RTW][2];
-#pragma unroll
-      for (int eg = 0; eg < NEG; ++eg) {
-        const int te = ws_elem<NEG>(lane & 3, eg, 0);
-#pragma unroll
-        for (int j = 0; j < RTW; ++j) {
-          const int row = (warp + j * NCW) * 8 + (lane >> 2);
-          const bool ok = row < NV && (warp + j * NCW) < NRT;
-          acc[eg][j][0] = ok ? sst[te * NV + row] : 0.0;
-          acc[eg][j][1] = ok ? sst[(te + 1) * NV + row] : 0.0;
-        }
-      }
-      const double* qb = qst + (lane >> 2) * KC + (lane & 3);
-      if (fast) {
-        if constexpr (WN)
-          nsum = norm_units_swz<N1, M, E, NCW, UPW, C::DUE, C::DUC>(d_s + (jn % C::NDB) * C::DT, warp, lane, cfr,
-                                                                    a.comp_w);
-#pragma unroll
-        for (int ks = 0; ks < KS; ++ks) {
-          double b[NEG];
-#pragma unroll
-          for (int eg = 0; eg < NEG; ++eg) b[eg] = qb[eg * 8 * KC + 4 * ks];
-#pragma unroll
-          for (int eg = 0; eg < NEG; ++eg)
-#pragma unroll
-            for (int j = 0; j < RTW; ++j) dmma_8x8x4(acc[eg][j][0], acc[eg][j][1], Lf[j][ks], b[eg]);
-        }
-      } else {
-        if constexpr (WN)
-          nsum = norm_units_swz<N1, M, E, NCW, UPW, C::DUE, C::DUC>(d_s + (jn % C::NDB) * C::DT, warp, lane, cfr,
-                                                                    a.comp_w);
-        const unsigned cset = mcset_s[stage];
-        for (unsigned rem = cset; rem != 0u; rem &= rem - 1u) {
-          const int c = __ffs(rem) - 1;
-          for (int ks = 0; ks < KS; ++ks) {
-            const int k = 4 * ks + (lane & 3);
-            const int col = cf_s[k / NF] * NF + (k % NF);
-            double av[RTW];
-#pragma unroll
-            for (int j = 0; j < RTW; ++j) {
-              const int row = (warp + j * NCW) * 8 + (lane >> 2);
-              av[j] = (row < NV) ? __ldg(a.LT + ((size_t)c * (NFACE * NF) + col) * NV + row) : 0.0;
-            }
-#pragma unroll
-            for (int eg = 0; eg < NEG; ++eg) {
-              const int n = lane >> 2;
-              const double b = (mcls_s[stage][ws_elem<NEG>(n >> 1, eg, n & 1)] == c) ? qb[eg * 8 * KC + 4 * ks] : 0.0;
-#pragma unroll
-              for (int j = 0; j < RTW; ++j) dmma_8x8x4(acc[eg][j][0], acc[eg][j][1], av[j], b);
-            }
-          }
-        }
-      }
-      if (it >= 2) mbar_wait(&outfree_bar[ob], ((it - 2) >> 1) & 1);
-      double* outb = out_s + ob * TILE;
-      double* dcur = d_s + (it % C::NDB) * C::DT;
-#pragma unroll
-      for (int eg = 0; eg < NEG; ++eg) {
-        const int te = ws_elem<NEG>(lane & 3, eg, 0);
-#pragma unroll
-        for (int j = 0; j < RTW; ++j) {
-          const int row = (warp + j * NCW) * 8 + (lane >> 2);
-          if (row < NV && (warp + j * NCW) < NRT) {
-#pragma unroll
-            for (int v = 0; v < 2; ++v) {
-              const int t = te + v;
-              outb[t * NV + row] = acc[eg][j][v];
-              dcur[t * C::DUE + doff[j]] = acc[eg][j][v] - ust[t * NV + row];
-            }
-          }
-        }
-      }
-      if constexpr (WN) {
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) nsum += __shfl_xor_sync(0xffffffffu, nsum, o);
-        if (lane == 0) red_s[(jn % C::NDB) * 32 + warp] = nsum;
-      }
-      fence_proxy_async();
-      __syncwarp();
-      if (lane == 0) {
-        mbar_arrive(&empty_bar[stage]);
-        mbar_arrive(&done_bar[ob]);
-      }
-    };
-    {
-      int it = 0;
-      for (; it < n_my && it < C::LAG; ++it) tile_body(it, std::false_type{});
-      for (; it < n_my; ++it) tile_body(it, std::true_type{});
-    }
-#else
     for (int it = 0; it < n_my; ++it) {
       const int stage = it % NS;
       const int ob = it & 1;
@@ -679,7 +571,6 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS>::NT, 1)
         mbar_arrive(&done_bar[ob]);
       }
     }
-#endif
     // drain: norms of the last LAG tiles
     for (int jn = n_my - C::LAG > 0 ? n_my - C::LAG : 0; jn < n_my; ++jn) {
       mbar_wait(&done_bar[jn & 1], (jn >> 1) & 1);

@@ -265,7 +265,8 @@ def run(mesh, problem, ops: ElementOperators, cfg: Optional[IterationConfig] = N
                             and solver.layers[1] == mesh.cells[-1]) else None
     return IterationReport(res.iterations, res.status, res.norms, time.perf_counter() - t0,
                            state, tr, res.first_norm, res.last_norm, res.launched,
-                           extra={"device_seconds": res.seconds, "l2_errors": res.errors})
+                           extra={"device_seconds": res.seconds, "l2_errors": res.errors,
+                                  "kernel": res.kernel})
 
 
 def cfl_number(problem, mesh, p: int, dt: float) -> float:
@@ -297,7 +298,8 @@ def _diagnostic_report(solver, cfg, norm, max_iters, t0, return_state, return_tr
 def run_time_dependent(mesh, problem, ops: ElementOperators, cfg: Optional[IterationConfig],
                        dt: float, T: Optional[float] = None, n_steps: Optional[int] = None,
                        initial=None, solver: Optional[DeviceSolver] = None,
-                       keep_states: bool = False, time_scheme: str = "backward-euler") -> list:
+                       keep_states: bool = False, time_scheme: str = "backward-euler",
+                       return_trace: bool = True) -> list:
     """Time steps; each step iterates from u^m.
     ``time_scheme``: "backward-euler" (= "locally-implicit": the implicit
     Euler HDG step solved by iHDG from the initial guess u^m, PAPER.md:593-653,
@@ -351,9 +353,10 @@ def run_time_dependent(mesh, problem, ops: ElementOperators, cfg: Optional[Itera
         if cfg.stop == "exact" or (cfg.diagnostics and getattr(problem, "exact", None) is not None):
             solver.set_exact(_exact_at(problem.exact, (m + 1) * dt))
         if cfg.diagnostics:
+            keep = keep_states or m == n_steps - 1
             rep = _diagnostic_report(solver, cfg, _norm_name(cfg, problem),
                                      cfg.max_iters or default_max_iters(mesh), t0,
-                                     keep_states or m == n_steps - 1, False, extra={"step": m + 1, "cfl": cfl})
+                                     keep, keep and return_trace, extra={"step": m + 1, "cfl": cfl})
             if rep.state is not None:
                 rep.state.m = m + 1
             reports.append(rep)
@@ -363,13 +366,17 @@ def run_time_dependent(mesh, problem, ops: ElementOperators, cfg: Optional[Itera
         res = solver.iterate(tol=cfg.tol, max_iters=cfg.max_iters or default_max_iters(mesh),
                              norm=_norm_name(cfg, problem), batch=cfg.check_every)
         last = m == n_steps - 1 or res.status != "converged"
+        keep = keep_states or last
         st = (FieldState(solver.get_state(), solver.spec.labels, k=res.iterations, m=m + 1)
-              if (keep_states or last) else None)
+              if keep else None)
+        # the step's single-valued trace with every state returned
+        tr = solver.trace() if (keep and return_trace and solver.layers[0] == 0
+                                and solver.layers[1] == mesh.cells[-1]) else None
         reports.append(IterationReport(res.iterations, res.status, res.norms,
-                                       time.perf_counter() - t0, st, None, res.first_norm,
+                                       time.perf_counter() - t0, st, tr, res.first_norm,
                                        res.last_norm, res.launched,
                                        extra={"step": m + 1, "device_seconds": res.seconds,
-                                              "l2_errors": res.errors, "cfl": cfl}))
+                                              "l2_errors": res.errors, "cfl": cfl, "kernel": res.kernel}))
         if res.status != "converged":
             break
     return reports

@@ -48,6 +48,7 @@ class IterResult:
     launched: int
     seconds: float
     errors: Optional[np.ndarray] = None   # exact-solution rule: ||u^k - u^e||_{L2} per sweep
+    kernel: str = ""                      # sweep kernel ihdg_sweep dispatched to (ihdg_sweep_kernel)
 
 
 class DeviceSolver:
@@ -441,8 +442,15 @@ class DeviceSolver:
         return a
 
     def reset_state(self, tol: float, max_iters: int, diverge_factor: float = 1e6) -> None:
+        if int(max_iters) > self.max_iters:
+            # the norm history holds one entry per sweep: grow it rather than
+            # silently capping the caller's max_iters
+            self.max_iters = int(max_iters)
+            self.norm_hist = self.torch.zeros(self.max_iters, dtype=self.torch.float64, device=self.device)
+            if getattr(self, "err_hist", None) is not None:
+                self.err_hist = self.torch.zeros(self.max_iters, dtype=self.torch.float64, device=self.device)
         st = N.IterState()
-        st.status, st.iters, st.max_iters, st.ticket = N.RUNNING, 0, min(int(max_iters), self.max_iters), 0
+        st.status, st.iters, st.max_iters, st.ticket = N.RUNNING, 0, int(max_iters), 0
         st.tol, st.first_norm, st.last_norm, st.diverge_factor = tol, 0.0, 0.0, diverge_factor
         host = self.torch.frombuffer(bytearray(bytes(st)), dtype=self.torch.uint8)
         self.state_dev.copy_(host)
@@ -502,6 +510,8 @@ class DeviceSolver:
         out = N.IterState()
         nl = C.c_int64(0)
         b0, b1 = self.u[self.cur], self.u[1 - self.cur]
+        a.u_old, a.u_new = _ptr(b0), _ptr(b1)
+        kernel = N.sweep_kernel(a)
         t0 = time.perf_counter()
         N.check(self.L.ihdg_iterate(C.byref(a), _ptr(b0), _ptr(b1), int(batch), self._sptr,
                                     C.byref(out), C.byref(nl)), "ihdg_iterate")
@@ -510,7 +520,7 @@ class DeviceSolver:
         it = out.iters
         norms = self.norm_hist[:it].cpu().numpy().copy()
         return IterResult(it, N.STATUS_NAMES[out.status], norms, out.first_norm, out.last_norm,
-                          int(nl.value), sec)
+                          int(nl.value), sec, kernel=kernel)
 
     def _iterate_exact(self, tol, max_iters, batch) -> IterResult:
         if getattr(self, "ue_q", None) is None:
@@ -524,6 +534,8 @@ class DeviceSolver:
         out = N.IterState()
         nl = C.c_int64(0)
         b0, b1 = self.u[self.cur], self.u[1 - self.cur]
+        a.u_old, a.u_new = _ptr(b0), _ptr(b1)
+        kernel = N.sweep_kernel(a)
         t0 = time.perf_counter()
         N.check(self.L.ihdg_iterate_exact(C.byref(a), C.byref(e), _ptr(b0), _ptr(b1), int(batch), self._sptr,
                                           C.byref(out), C.byref(nl)), "ihdg_iterate_exact")
@@ -533,7 +545,7 @@ class DeviceSolver:
         norms = self.norm_hist[:it].cpu().numpy().copy()
         errs = self.err_hist[:it].cpu().numpy().copy()
         return IterResult(it, N.STATUS_NAMES[out.status], norms, out.first_norm, out.last_norm,
-                          int(nl.value), sec, errs)
+                          int(nl.value), sec, errs, kernel=kernel)
 
     def sweep_once(self, norm: str = "volume", finalize: int = 1, a: Optional[N.SweepArgs] = None):
         """One sweep from the current iterate (used by the bench and multi-rank driver)."""

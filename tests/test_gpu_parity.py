@@ -69,12 +69,16 @@ def test_config1_volume_rule():
     assert rel_l2(rep.state.data.reshape(S.nel, -1), ref["u"]) < TOL_FIELD
 
 
-@pytest.mark.parametrize("cells,steps", [(16, 2), (24, 1)])
-def test_config2_reduced_parity(cells, steps):
+@pytest.mark.parametrize("cells,steps,kernel", [(16, 2, "k_sweep_v3"), (32, 1, "k_sweep_v3"),
+                                                (20, 1, "k_sweep")])
+def test_config2_reduced_parity(cells, steps, kernel):
+    """20^2 has tile rows that are not a multiple of the v3 tile: the generic
+    kernel runs (asserted), the others run v3."""
     from tests.oracle_bridge import rel_l2
 
     wl = _wl(2, cells=cells, n_steps=steps)
     reps, S, refs = _unsteady(wl)
+    assert all(r.extra["kernel"] == kernel for r in reps)
     assert [r.iterations for r in reps] == [r["iterations"] for r in refs]
     assert all(r.status == "converged" for r in reps)
     for r, o in zip(reps, refs):
@@ -86,6 +90,7 @@ def test_config3_reduced_parity():
 
     wl = _wl(3, cells=16, n_steps=2)
     reps, S, refs = _unsteady(wl)
+    assert all(r.extra["kernel"] == "k_sweep_v3" for r in reps)
     assert [r.iterations for r in reps] == [r["iterations"] for r in refs]
     for r, o in zip(reps, refs):
         assert rel_l2(r.state.data.reshape(S.nel, -1), o["u"]) < TOL_FIELD
@@ -96,6 +101,7 @@ def test_config4_reduced_parity():
 
     wl = _wl(4, cells=8)
     rep, S, ref = _steady(wl, "successive")
+    assert rep.extra["kernel"] == "k_sweep_v3"
     assert rep.iterations == ref["iterations"] == 3 * 7 + 1 + 1
     assert rel_l2(rep.state.data.reshape(S.nel, -1), ref["u"]) < TOL_FIELD
     assert rel_l2(rep.trace, S.trace(ref["u"])) < TOL_FIELD
@@ -107,6 +113,7 @@ def test_config5_reduced_parity(kappa):
 
     wl = _wl(5, cells=32, kappa=kappa, n_steps=1)
     reps, S, refs = _unsteady(wl)
+    assert all(r.extra["kernel"] == "k_sweep_ws" for r in reps)
     assert [r.iterations for r in reps] == [r["iterations"] for r in refs]
     for r, o in zip(reps, refs):
         assert rel_l2(r.state.data.reshape(S.nel, -1), o["u"]) < TOL_FIELD
@@ -181,19 +188,51 @@ def test_config4_full_size_layer_count():
     assert np.array_equal(r1.state.data, r2.state.data)
 
 
-@pytest.mark.parametrize("impl", ["v3", "ws4", "ws3", "ws2", "ws", "generic", "nograph"])
-def test_sweep_impl_parity(impl):
-    """Every selectable sweep kernel (IHDG_SWEEP_IMPL) on config 5 reduced,
-    and the stream-launched (not graph-replayed) iterate loop."""
-    import os
-    import subprocess
-    import sys
+IMPL_CASES = [  # (selector, graphs, config, cells, expected kernel)
+    ("auto", True, 5, 16, "k_sweep_ws"), ("generic", True, 5, 16, "k_sweep"),
+    ("auto", False, 5, 16, "k_sweep_ws"),
+    ("auto", True, 2, 16, "k_sweep_v3"), ("ws", True, 2, 16, "k_sweep_ws"), ("generic", True, 2, 16, "k_sweep"),
+    ("auto", True, 3, 16, "k_sweep_v3"), ("ws", True, 3, 16, "k_sweep_ws"),
+]
 
-    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    env = dict(os.environ, IHDG_NO_GRAPH="1") if impl == "nograph" else dict(os.environ, IHDG_SWEEP_IMPL=impl)
-    r = subprocess.run([sys.executable, os.path.join(root, "tests", "_impl_child.py"), "1e-1"], env=env,
-                       capture_output=True, text=True, timeout=600)
-    assert r.returncode == 0, r.stdout + r.stderr
+
+@pytest.mark.parametrize("impl,graphs,cfg,cells,kernel", IMPL_CASES,
+                         ids=[f"cfg{c}-{i}-{'graph' if g else 'stream'}" for i, g, c, _, _ in IMPL_CASES])
+def test_sweep_impl_parity(impl, graphs, cfg, cells, kernel):
+    """Every selectable sweep kernel (ihdg_set_sweep_impl, switched in
+    process) and the stream-launched (not graph-replayed) iterate loop,
+    against the oracle; the dispatched kernel is asserted by name."""
+    from paper_1711_01175_b200 import _native as N
+    from tests.oracle_bridge import rel_l2
+
+    wl = _wl(cfg, cells=cells, n_steps=1, **({"kappa": 1e-1} if cfg == 5 else {}))
+    N.set_sweep_impl(impl)
+    N.set_graphs(graphs)
+    try:
+        reps, S, refs = _unsteady(wl)
+    finally:
+        N.set_sweep_impl("auto")
+        N.set_graphs(True)
+    assert all(r.extra["kernel"] == kernel for r in reps), [r.extra["kernel"] for r in reps]
+    assert [r.iterations for r in reps] == [r["iterations"] for r in refs]
+    for r, o in zip(reps, refs):
+        assert rel_l2(r.state.data.reshape(S.nel, -1), o["u"]) < TOL_FIELD
+
+
+def test_config4_stream_kernel_parity():
+    """Config 4 reduced through k_sweep_stream (the 3D kernel without v3)."""
+    from paper_1711_01175_b200 import _native as N
+    from tests.oracle_bridge import rel_l2
+
+    wl = _wl(4, cells=8)
+    N.set_sweep_impl("stream")
+    try:
+        rep, S, ref = _steady(wl, "successive")
+    finally:
+        N.set_sweep_impl("auto")
+    assert rep.extra["kernel"] == "k_sweep_stream"
+    assert rep.iterations == ref["iterations"]
+    assert rel_l2(rep.state.data.reshape(S.nel, -1), ref["u"]) < TOL_FIELD
 
 
 # PAPER.md:1349-1395 (Table 2) / SPEC.md acceptance 1: 2D N x N -> {9, 17, 33, 65} for N = 4..32,

@@ -54,3 +54,49 @@ def test_no_cpu_fallback(monkeypatch):
     monkeypatch.setattr(N, "LIB_PATH", "/nonexistent/libihdg_cuda.so")
     with pytest.raises(N.NativeUnavailable):
         N.lib()
+
+
+def _cpu_sweep_args(cfg, cells=None):
+    """SweepArgs of a BASELINE config built on the host (no device pointers):
+    enough for the dispatch query, which reads only the geometry and weights."""
+    from paper_1711_01175_b200.assembly import build_spec
+    from paper_1711_01175_b200.workloads import make_config
+
+    wl = make_config(cfg, cells=cells)
+    sp = build_spec(wl.mesh, wl.problem, wl.ops, wl.dt)
+    a = N.SweepArgs()
+    d = wl.mesh.dim
+    a.g.dim, a.g.order, a.g.ncomp = d, wl.ops.p, sp.ncomp
+    for i in range(3):
+        a.g.cells[i] = wl.mesh.cells[i] if i < d else 1
+        a.g.periodic[i] = int(wl.mesh.periodic[i]) if i < d else 0
+    a.g.layer_begin, a.g.layer_end = 0, wl.mesh.cells[d - 1]
+    for f in range(6):
+        a.coupled[f] = int(sp.coupled[f])
+        for c in range(4):
+            a.face_w[f][c] = float(sp.face_w[f, c])
+    a.norm_kind = N.NORM_VOLUME
+    a.scheme = N.SCHEME_II
+    return a
+
+
+@pytest.mark.parametrize("cfg,cells,auto,no_v3", [
+    (5, None, "k_sweep_ws", "k_sweep_ws"), (4, None, "k_sweep_v3", "k_sweep_stream"),
+    (3, None, "k_sweep_v3", "k_sweep_ws"), (2, None, "k_sweep_v3", "k_sweep_ws"),
+    (2, 20, "k_sweep", "k_sweep"), (1, None, "k_sweep", "k_sweep")])
+def test_dispatch_names(cfg, cells, auto, no_v3):
+    """ihdg_sweep_kernel names the kernel each BASELINE config runs on; the
+    selector switches in process (no GPU needed for the query)."""
+    if not os.path.exists(N.LIB_PATH):
+        pytest.skip("libihdg_cuda.so not built")
+    a = _cpu_sweep_args(cfg, cells)
+    try:
+        assert N.sweep_kernel(a) == auto
+        N.set_sweep_impl("ws")
+        assert N.sweep_kernel(a) == no_v3
+        N.set_sweep_impl("generic")
+        assert N.sweep_kernel(a) == "k_sweep"
+    finally:
+        N.set_sweep_impl("auto")
+    with pytest.raises(RuntimeError):
+        N.set_sweep_impl("ws9")

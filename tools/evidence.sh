@@ -1,15 +1,18 @@
 #!/bin/bash
 # Round evidence on one B200: GPU tests, smoke, default bench (both arms),
-# ncu launch list of the bench command, one full ncu capture of the sweep.
-# Every ncu command runs only after the same command has exited 0 plainly.
+# ncu launch list of the bench command, one full ncu capture of the config-5
+# sweep and of the config-4 sweep.  Every ncu command runs only after the same
+# command has exited 0 without ncu.   tools/evidence.sh <tag> [skip-tests]
 set -u
 O=gpurun_out
-TAG=${1:-r01}
+TAG=${1:-r02}
 mkdir -p $O
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw,temperature.gpu --format=csv > $O/${TAG}_gpu.txt
-timeout 1500 python -m pytest tests -m gpu -q > $O/${TAG}_pytest_gpu.txt 2>&1; echo "pytest rc=$?" >> $O/${TAG}_pytest_gpu.txt
-timeout 300 python -c "import __graft_entry__ as g; g.smoke(); print('smoke ok')" > $O/${TAG}_smoke.txt 2>&1
-timeout 900 python bench.py > $O/${TAG}_bench.json 2> $O/${TAG}_bench.err
+if [ "${2:-}" != "skip-tests" ]; then
+  timeout 2400 python -m pytest tests -m gpu -q > $O/${TAG}_pytest_gpu.txt 2>&1; echo "pytest rc=$?" >> $O/${TAG}_pytest_gpu.txt
+  timeout 300 python -c "import __graft_entry__ as g; g.smoke(); print('smoke ok')" > $O/${TAG}_smoke.txt 2>&1
+fi
+timeout 1200 python bench.py > $O/${TAG}_bench.json 2> $O/${TAG}_bench.err
 timeout 600 python bench.py --impl reference > $O/${TAG}_bench_reference.json 2> $O/${TAG}_bench_reference.err
 CMD="python bench.py --steps 20 --warmup 3 --ttc-steps 0 --no-e2e --no-cpu --no-others"
 if timeout 300 $CMD > $O/${TAG}_bench_short.json 2>&1; then
@@ -18,14 +21,11 @@ if timeout 300 $CMD > $O/${TAG}_bench_short.json 2>&1; then
 fi
 CMD3="python bench.py --steps 3 --warmup 3 --ttc-steps 0 --no-e2e --no-cpu --no-others"
 if timeout 300 $CMD3 > $O/${TAG}_bench_short3.json 2>&1; then
-  timeout 1200 ncu --set full --clock-control none --import-source on -k regex:^k_sweep_ws$ -s 2 -c 1 \
+  timeout 1200 ncu --set full --clock-control none --import-source on -k regex:^k_sweep_ws -s 2 -c 1 \
     -o $O/${TAG}_ws_full -f $CMD3 > $O/${TAG}_ncu_full.log 2>&1
 fi
-echo done
-# config-4 evidence: role counters (profiling build) and one full capture of k_sweep_v3
-IHDG_LIB=paper_1711_01175_b200/libihdg_cuda_prof.so timeout 300 python tools/ws_roles.py 4 > $O/${TAG}_cfg4_roles.txt 2>&1
 if timeout 300 python tools/sweep_cfg.py 4 20 3 > $O/${TAG}_cfg4_plain.txt 2>&1; then
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_sweep_v3 -s 3 -c 1 \
     -o $O/${TAG}_cfg4_v3_full -f python tools/sweep_cfg.py 4 5 3 > $O/${TAG}_cfg4_ncu.log 2>&1
 fi
-echo done-cfg4
+echo done
