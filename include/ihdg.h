@@ -217,6 +217,22 @@ typedef struct {
                                  (all-iterate-k trace); zero for iHDG-II */
   int32_t scheme;             /* IHDG_SCHEME_II / IHDG_SCHEME_I */
   int32_t pad1;
+  /* Gram-form stopping norm (k_sweep_ws only; both NULL = the direct norm).
+   * Within one solve, u^k = s + L q^{k-1} for k >= 1, so the successive
+   * difference of an interior-class element is delta = L (q^k - q^{k-1}) and
+   *   ||delta||^2_M = J ||R (q^k - q^{k-1})||^2,  R^T R = L^T (W (x) M1 (x) M1) L
+   * (W = diag(comp_w), M1 the 1D reference mass): a gram_kc x gram_kc
+   * triangle instead of the two sum-factorised mass passes over the volume.
+   * q_store keeps every element's neighbour face scalars q (gram_kc per
+   * element, tile-major) and is rewritten by every sweep; the kernel uses the
+   * stored q^{k-1} only when state->iters > 0, i.e. from the second sweep of
+   * a solve on (the first sweep, and tiles with a boundary-class element,
+   * take the direct norm).  Contract: between two sweeps of one solve the
+   * caller changes neither s nor the operators. */
+  double* q_store;            /* [n_tiles_local][tile elems][gram_kc] or NULL */
+  const double* gram_R;       /* [gram_kc][gram_kc] row-major upper-triangular R of the interior class, kernel column order (coupled faces ascending, face nodes) */
+  int32_t gram_kc;            /* ihdg_sweep_gram_kc(args), 0 = off */
+  int32_t pad2;
 } ihdg_sweep_args;
 
 /* K5: ||u - u^e||_{L2(Omega)}^2 per tile by (p+2)^d Gauss quadrature
@@ -225,7 +241,9 @@ typedef struct {
  * after a sweep with finalize = 0; the last CTA reduces the sweep's
  * successive partials and the error partials and applies the exact-solution
  * stopping rule |e_k - e_{k-1}| < tol; divergence and
- * NaN stay on the successive norm. */
+ * NaN stay on the successive norm.  mode 2: as mode 1 with the
+ * vs-direct rule e_k < tol (section 6.3), ue_q = a direct HDG
+ * solution at the Gauss points. */
 typedef struct {
   ihdg_geom g;
   const double* u;            /* ghost-padded state */
@@ -332,6 +350,10 @@ const char* ihdg_sweep_kernel(const ihdg_sweep_args* a);
  * read from the environment variable IHDG_SWEEP_IMPL), "ws" / "stream" (skip
  * v3), "generic" (generic kernel only).  IHDG_ERR_ARG for other names. */
 int ihdg_set_sweep_impl(const char* name);
+/* Columns of the Gram factor R the dispatched kernel takes for these args
+ * (q scalars per element, see ihdg_sweep_args.q_store), or 0 if the kernel
+ * has no Gram-form norm. */
+int ihdg_sweep_gram_kc(const ihdg_sweep_args* a);
 /* CUDA-graph replay of sweep batches in ihdg_iterate (default on unless the
  * environment sets IHDG_NO_GRAPH): 1 on, 0 off. */
 int ihdg_set_graphs(int on);
@@ -353,8 +375,8 @@ int ihdg_error_norm(const ihdg_error_args* e, void* stream);
 int64_t ihdg_error_tile_count(const ihdg_geom* g);
 /* ihdg_iterate with the exact-solution stopping rule: every sweep runs with
  * finalize = 0 and is followed by K5 (mode 1) on its output; e->u is set per
- * sweep, e->mode forced to 1.  The caller runs K5 in mode 0 on the initial
- * iterate first (state->last_err). */
+ * sweep, e->mode forced to 1 (2 kept).  The caller runs K5 in mode 0 on the initial
+ * iterate first (state->last_err).  e->mode 2 selects the vs-direct rule. */
 int ihdg_iterate_exact(const ihdg_sweep_args* a, const ihdg_error_args* e, double* buf0, double* buf1,
                        int32_t batch, void* stream, ihdg_iter_state* state_out, int64_t* n_launched);
 /* K6 diagnostics (see ihdg_elem_error_args / ihdg_face_energy_args) */

@@ -692,8 +692,13 @@ class OracleSolver:
         return float(np.sqrt(np.add.accumulate(tot)[-1]))
 
     def run(self, u0=None, tol=1e-10, max_iters=10000, norm="volume", u_prev=None,
-            diverge_factor=1e6, keep_history=False):
-        """Algorithm 1; returns (u, iterations, status, norms)."""
+            diverge_factor=1e6, keep_history=False, engine="numpy", threads=0, reference=None):
+        """Algorithm 1; returns (u, iterations, status, norms).  engine
+        "numpy": scipy LU solves + quadrature norms; "c": the C/OpenMP map
+        (oracle/sweep.c: the same LU solve per element, norm sum_K delta^T M
+        delta) for full-size parity runs (volume rule, iHDG-II, BE/steady).
+        norm "vs-direct": stop when ||u^k - reference||_{L2} < tol (SPEC.md:316;
+        reference = the direct HDG solution, oracle/reference_hdg.py)."""
         u = np.zeros((self.nel, self.nv)) if u0 is None else np.array(u0, float).reshape(self.nel, self.nv)
         rhs = self.rhs_static(u_prev)
         norms = []
@@ -701,14 +706,34 @@ class OracleSolver:
         status = "max-iter"
         first = None
         e_prev = self.err_norm(u) if norm == "exact" else None
+        if norm == "vs-direct":
+            if reference is None:
+                raise ValueError("vs-direct needs the reference (direct HDG) solution")
+            reference = np.asarray(reference, float).reshape(self.nel, self.nv)
         hist = [u.copy()] if keep_history else None
+        if engine == "c":
+            if norm != "volume" or self.scheme != "II" or self.time_scheme != "BE":
+                raise NotImplementedError("engine='c': volume rule, iHDG-II, steady / backward Euler")
+            if getattr(self, "_cdata", None) is None:
+                self._cdata = self.c_sweep_data()
+            u = np.ascontiguousarray(u)
+            rhs = np.ascontiguousarray(rhs)
+            spare = np.empty_like(u)
         for k in range(1, max_iters + 1):
-            un = self.sweep(u, rhs)
-            delta = un - u
-            nrm = self.trace_norm(delta) if norm == "trace" else self.vol_norm(delta)
+            if engine == "c":
+                total = self.c_sweep(self._cdata, u, rhs, spare, threads)
+                un, spare = spare, u
+                nrm = float(np.sqrt(total))
+            else:
+                un = self.sweep(u, rhs)
+                delta = un - u
+                nrm = self.trace_norm(delta) if norm == "trace" else self.vol_norm(delta)
             norms.append(nrm)
             if norm == "exact":
                 e = self.err_norm(un)
+                errs.append(e)
+            elif norm == "vs-direct":
+                e = self.vol_norm(un - reference)
                 errs.append(e)
             u = un
             if keep_history:
@@ -724,6 +749,10 @@ class OracleSolver:
                 if done:
                     status = "converged"
                     break
+            elif norm == "vs-direct":
+                if e < tol:
+                    status = "converged"
+                    break
             elif nrm < tol:
                 status = "converged"
                 break
@@ -736,7 +765,7 @@ class OracleSolver:
         return out
 
     def run_time_dependent(self, u0, nsteps, tol=1e-10, max_iters=10000, norm="volume", exact=None,
-                           forcing=None, inflow=None, dirichlet=None):
+                           forcing=None, inflow=None, dirichlet=None, engine="numpy", threads=0):
         """forcing(x, t) / inflow(x, t): time-dependent data, taken at the new
         level (BE) or averaged / split between the levels (CN)."""
         u = np.array(u0, float).reshape(self.nel, self.nv)
@@ -754,7 +783,7 @@ class OracleSolver:
                 self.set_dirichlet(lambda x: dirichlet(x, t1), lambda x: dirichlet(x, t0))
             if norm == "exact":
                 self.set_exact(exact, (step + 1) * self.dt)
-            r = self.run(u0=u, tol=tol, max_iters=max_iters, norm=norm, u_prev=u)
+            r = self.run(u0=u, tol=tol, max_iters=max_iters, norm=norm, u_prev=u, engine=engine, threads=threads)
             reports.append(r)
             u = r["u"]
             if r["status"] != "converged":

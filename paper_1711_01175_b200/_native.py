@@ -79,7 +79,8 @@ class SweepArgs(C.Structure):
                 ("out_w", (_f64 * 4) * 6), ("jac", _f64), ("jac_face", _f64 * 3),
                 ("coupled", _i32 * 6), ("out_face", _i32 * 6), ("norm_kind", _i32),
                 ("finalize", _i32), ("tile_offset", _i64), ("chol", _f64 * 64),
-                ("own_w", (_f64 * 4) * 6), ("scheme", _i32), ("pad1", _i32)]
+                ("own_w", (_f64 * 4) * 6), ("scheme", _i32), ("pad1", _i32),
+                ("q_store", _p), ("gram_R", _p), ("gram_kc", _i32), ("pad2", _i32)]
 
 
 class FinalizeArgs(C.Structure):
@@ -125,6 +126,7 @@ SIGNATURES = {
     "ihdg_sweep": (_i32, [C.POINTER(SweepArgs), _p]),
     "ihdg_stream_variant": (_i32, [C.POINTER(SweepArgs)]),
     "ihdg_sweep_kernel": (C.c_char_p, [C.POINTER(SweepArgs)]),
+    "ihdg_sweep_gram_kc": (_i32, [C.POINTER(SweepArgs)]),
     "ihdg_set_sweep_impl": (_i32, [C.c_char_p]),
     "ihdg_set_graphs": (_i32, [_i32]),
     "ihdg_finalize": (_i32, [C.POINTER(FinalizeArgs), _p]),

@@ -13,6 +13,7 @@ using namespace ihdg;
 int ihdg_stream_launch(const ihdg_sweep_args* a, cudaStream_t st, cudaError_t* err);
 const char* ihdg_stream_kernel_name(const ihdg_sweep_args* a);
 int ihdg_stream_set_impl(const char* name);
+int ihdg_stream_gram_kc(const ihdg_sweep_args* a);
 
 namespace {
 
@@ -286,6 +287,11 @@ const char* ihdg_sweep_kernel(const ihdg_sweep_args* a) {
   return s != nullptr ? s : "k_sweep";
 }
 
+int ihdg_sweep_gram_kc(const ihdg_sweep_args* a) {
+  if (a == nullptr || check_geom(a->g) != IHDG_OK) return 0;
+  return ihdg_stream_gram_kc(a);
+}
+
 int ihdg_set_sweep_impl(const char* name) {
   if (ihdg_stream_set_impl(name) != 0)
     return set_err(IHDG_ERR_ARG, std::string("unknown sweep impl '") + (name ? name : "(null)") +
@@ -426,7 +432,8 @@ int ihdg_error_norm(const ihdg_error_args* e, void* stream) {
   int rc = check_geom(e->g);
   if (rc) return rc;
   if (e->nq < 1 || e->nq > 16 || e->g.order + 1 > 8) return set_err(IHDG_ERR_ARG, "nq / order out of range");
-  if (e->mode == 1 && e->succ_partials == nullptr) return set_err(IHDG_ERR_ARG, "mode 1 needs the sweep partials");
+  if (e->mode < 0 || e->mode > 2) return set_err(IHDG_ERR_ARG, "mode must be 0, 1 or 2");
+  if (e->mode != 0 && e->succ_partials == nullptr) return set_err(IHDG_ERR_ARG, "modes 1/2 need the sweep partials");
   return do_error(e, (cudaStream_t)stream);
 }
 
@@ -523,7 +530,7 @@ static int iterate_impl(const ihdg_sweep_args* a0, const ihdg_error_args* e0, do
   ihdg_error_args ex{};
   if (e0 != nullptr) {
     ex = *e0;
-    ex.mode = 1;
+    ex.mode = e0->mode == 2 ? 2 : 1;   // 2: vs-direct rule, else the exact-solution rule
     ex.u = nullptr;
     ex.succ_partials = a.tile_partials;
     ex.state = a.state;

@@ -370,7 +370,7 @@ constexpr int ERR_TE = 8;   // elements per error tile
 // (mode 1) the exact-solution stopping rule in the last CTA.
 __global__ void k_error_norm(const ihdg_error_args a) {
   ihdg_iter_state* st = a.state;
-  if (a.mode == 1 && st->status != IHDG_RUNNING) return;   // later sweeps are no-ops
+  if (a.mode != 0 && st->status != IHDG_RUNNING) return;   // later sweeps are no-ops
   __shared__ double vq_s[16 * 8];
   __shared__ double wq_s[16];
   __shared__ double red[256];
@@ -449,7 +449,7 @@ __global__ void k_error_norm(const ihdg_error_args a) {
     st->last_norm = norm;
     int status = IHDG_RUNNING;
     if (!(norm == norm) || !(err == err)) status = IHDG_NAN;
-    else if (fabs(err - st->last_err) < st->tol) status = IHDG_CONVERGED;
+    else if (a.mode == 2 ? (err < st->tol) : (fabs(err - st->last_err) < st->tol)) status = IHDG_CONVERGED;
     else if (it > 1 && norm > st->diverge_factor * st->first_norm) status = IHDG_DIVERGED;
     else if (it >= st->max_iters) status = IHDG_MAXITER;
     st->last_err = err;

@@ -186,6 +186,14 @@ const char* ihdg_stream_kernel_name(const ihdg_sweep_args* a) {
   return e == nullptr ? nullptr : ihdg::kKindName[e->kind];
 }
 
+// Gram-form norm columns (q scalars per element) of the kernel these args
+// dispatch to: k_sweep_ws only (ihdg.h, ihdg_sweep_args.q_store)
+int ihdg_stream_gram_kc(const ihdg_sweep_args* a) {
+  const ihdg::StreamEntry* e = ihdg::stream_entry(a);
+  if (e == nullptr || e->kind != ihdg::KIND_WS) return 0;
+  return e->NCF * e->N1;
+}
+
 // 0 ok, -1 unknown name
 int ihdg_stream_set_impl(const char* name) {
   const int v = ihdg::parse_impl(name);

@@ -116,7 +116,14 @@ struct WCfg {
   static constexpr int TILE = E * NV;
   static constexpr int HALO = 0;   // out-of-tile faces: prep warps load them into registers
   static constexpr int QT = E * KC;
-  static constexpr int STAGE = 2 * TILE + HALO + QT;
+  // stage: s tile, u^k tile, q (neighbour face scalars), dq = q^k - q^{k-1}
+  // (Gram-form norm), the last two in the consumers' column order
+  static constexpr int STAGE = 2 * TILE + HALO + 2 * QT;
+  // Gram-form norm ||R dq||^2: R is KC x KC upper triangular, so row tile rt
+  // of R touches k-steps 2 rt .. KS-1; one (row tile, element group) item per
+  // consumer warp, the heavy items on the last warps (lightest contraction)
+  static constexpr int GRT = (KC + 7) / 8;
+  static constexpr int NGI = GRT * NEG;
   static constexpr int OFF_OUT = NS * STAGE;
   // delta tiles: bank-conflict-free swizzled layout (node row stride 8,
   // column XOR 4 on every other pair of rows; component stride DUC, element
@@ -131,12 +138,19 @@ struct WCfg {
   static constexpr int NDB = 2 * LAG;
   static constexpr int OFF_D = OFF_OUT + 2 * TILE;
   static constexpr int OFF_RED = OFF_D + NDB * DT;
-  static constexpr int N_DBL = OFF_RED + 32 * NDB;
+  // per-warp norm partials: slot = tile % NRED.  A Gram partial of tile j is
+  // written in iteration j, a direct one in j + 1, and prep warp 0 reads it in
+  // its iteration j + 2; consumers reach iteration j + NRED only after prep
+  // iteration j + NRED started, so NRED = 4 slots never overwrite an unread one
+  static constexpr int NRED = 4;
+  static constexpr int N_DBL = OFF_RED + 32 * NRED;
   static constexpr int NBAR = 3 * NS + 4;
   static constexpr size_t BYTES = (size_t)N_DBL * sizeof(double) + NBAR * sizeof(uint64_t);
   static_assert(KC % 4 == 0 && E % 8 == 0 && E <= 32 && N1 <= 8, "ws config");
   static_assert((TILE * sizeof(double)) % 16 == 0, "tile bytes must be 16-byte multiples");
   static_assert(E % NQW == 0, "prep warps split the tile");
+  static_assert(NGI <= NCW, "one Gram item per consumer warp");
+  static_assert(BYTES + 4096 <= 232448, "shared memory (dynamic + static) over the sm_100a opt-in limit");
 };
 
 template <int N1, int M, int NCF, int NWC, int E, int NS>
@@ -227,6 +241,12 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS>::NT, 1)
 
   const int fast_class = a.class_of_mask[0];
   const int ntiles = (int)geo.ntiles;
+  // Gram-form norm (ihdg.h, q_store): q of every tile is stored each sweep;
+  // the stored q^{k-1} is used from the second sweep of a solve on (the
+  // last CTA's finalize of the previous launch wrote iters; no CTA of this
+  // launch can finalize before every CTA has read it)
+  const bool qsave = a.q_store != nullptr && a.gram_kc == KC;
+  const bool gram = qsave && a.gram_R != nullptr && st->iters > 0;
   V3_T0(tk0);
   int n_my = 0;  // tiles of this CTA
   for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) ++n_my;
@@ -300,6 +320,8 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS>::NT, 1)
     // out-of-tile neighbour face nodes of this warp's entries, loaded from
     // global (L2) into registers one tile ahead
     double gv[QM][NWC], gvn[QM][NWC];
+    // stored q^{k-1} of this warp's entries (Gram-form norm), one tile ahead
+    double qo[QM], qon[QM];
     int qs = 0, ql = 0, qsn = 0, qln = 0;
     // per-lane entry constants, hoisted out of the tile loop: entry m of this
     // lane is (element t, column k) with k's face f and its gather offsets
@@ -314,12 +336,18 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS>::NT, 1)
 #pragma unroll
       for (int j = 0; j < NWC; ++j) ent_q[m][j] = qt_s[k][j];
     }
-    auto gather = [&](int itg, double (&dst)[QM][NWC], int& in_bits, int& ld_bits) {
+    auto gather = [&](int itg, double (&dst)[QM][NWC], double (&qdst)[QM], int& in_bits, int& ld_bits) {
       in_bits = 0;
       ld_bits = 0;
       if (itg >= n_my) return;
       STile<D> tg;
-      tg.init(a.g, (int)blockIdx.x + itg * (int)gridDim.x, E, nlay, lsi);
+      const int tgi = (int)blockIdx.x + itg * (int)gridDim.x;
+      tg.init(a.g, tgi, E, nlay, lsi);
+      if (gram) {
+        const double* qsrc = a.q_store + (int64_t)tgi * C::QT + pw * HALF * KC + lane;
+#pragma unroll
+        for (int m = 0; m < QM; ++m) qdst[m] = ent_t[m] >= 0 ? __ldcs(qsrc + 32 * m) : 0.0;
+      }
       // missing neighbours: faces of axes >= 1 are tile-uniform, x faces only
       // at the tile ends
       int hm = 0;
@@ -355,10 +383,10 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS>::NT, 1)
         }
       }
     };
-    gather(0, gv, qs, ql);
+    gather(0, gv, qo, qs, ql);
     for (int it = 0; it < n_my; ++it) {
       const int stage = it % NS;
-      gather(it + 1, gvn, qsn, qln);
+      gather(it + 1, gvn, qon, qsn, qln);
       V3_T0(tp);
       mbar_wait(&full_bar[stage], (it / NS) & 1);
       V3_ACC(1, tp);
@@ -371,6 +399,8 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS>::NT, 1)
       const double* sst = sm + stage * C::STAGE;
       const double* ust = sst + TILE;
       double* qst = const_cast<double*>(ust) + TILE + C::HALO;
+      double* dqst = qst + C::QT;
+      double* qdst = qsave ? a.q_store + (int64_t)cur_tile * C::QT + pw * HALF * KC + lane : nullptr;
 #pragma unroll
       for (int m = 0; m < QM; ++m) {
         const int t = ent_t[m];
@@ -387,6 +417,8 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS>::NT, 1)
             for (int j = 0; j < NWC; ++j) v = fma(w[j], gv[m][j], v);
           }
           qst[ws_qcol<C::NEG>(t) * KC + k] = v;
+          if (gram) dqst[ws_qcol<C::NEG>(t) * KC + k] = v - qo[m];
+          if (qsave) __stcs(qdst + 32 * m, v);
         }
       }
       __syncwarp();
@@ -401,7 +433,7 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS>::NT, 1)
           const int jt = it - 1 - C::LAG;   // every warp has reduced tile jt by done(it-1)
           if (jt >= 0) {
             double s = 0.0;
-            for (int w = 0; w < NCW; ++w) s += red_s[(jt % C::NDB) * 32 + w];
+            for (int w = 0; w < NCW; ++w) s += red_s[(jt % C::NRED) * 32 + w];
             a.tile_partials[hist[jt & 3]] = a.jac * s;
           }
           if (it >= 2) {
@@ -416,9 +448,11 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS>::NT, 1)
       // the gathers of tile it+1 are consumed only here (a register move
       // waits on the load), i.e. after qready(it) and the done wait
 #pragma unroll
-      for (int m = 0; m < QM; ++m)
+      for (int m = 0; m < QM; ++m) {
 #pragma unroll
         for (int j = 0; j < NWC; ++j) gv[m][j] = gvn[m][j];
+        qo[m] = qon[m];
+      }
       qs = qsn;
       ql = qln;
     }
@@ -432,7 +466,7 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS>::NT, 1)
         const int jt = L - C::LAG;
         if (jt >= 0) {
           double s = 0.0;
-          for (int w = 0; w < NCW; ++w) s += red_s[(jt % C::NDB) * 32 + w];
+          for (int w = 0; w < NCW; ++w) s += red_s[(jt % C::NRED) * 32 + w];
           a.tile_partials[hist[jt & 3]] = a.jac * s;
         }
         bulk_wait<0>();
@@ -465,6 +499,18 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS>::NT, 1)
       const int kk = 4 * ks + (lane & 3), nn = lane >> 2;
       cfr[ks] = (kk < N1 && nn < N1) ? chol_s[kk * N1 + nn] : 0.0;
     }
+    // Gram-form norm item of this warp: R row tile grt x element group geg
+    static_assert(C::LAG == 1, "the Gram / direct norm schedule assumes LAG = 1");
+    const int gi = NCW - 1 - warp;
+    const bool has_gi = gi >= 0 && gi < C::NGI;
+    const int grt = has_gi ? gi / NEG : 0, geg = has_gi ? gi - (gi / NEG) * NEG : 0;
+    double Rf[KS];
+#pragma unroll
+    for (int ks = 0; ks < KS; ++ks) {
+      const int row = grt * 8 + (lane >> 2), col = 4 * ks + (lane & 3);
+      Rf[ks] = (gram && has_gi && row < KC) ? __ldg(a.gram_R + row * KC + col) : 0.0;
+    }
+    int prev_direct = 0;   // tile it-1 took the direct norm (its delta is in d_s)
     for (int it = 0; it < n_my; ++it) {
       const int stage = it % NS;
       const int ob = it & 1;
@@ -472,19 +518,20 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS>::NT, 1)
       mbar_wait(&qready_bar[stage], (it / NS) & 1);
       V3_ACC(3, tc);
       const int fast = mfast_s[stage];
+      const bool gtile = gram && fast;   // tile it: Gram-form norm
       const double* sst = sm + stage * C::STAGE;
       const double* ust = sst + TILE;
       const double* qst = ust + TILE + C::HALO;
-      // norm of the previous tile (needs every warp's delta of tile it-1)
-      double nsum = 0.0;
-      if (it >= C::LAG) {
-        const int jn = it - C::LAG;
+      // direct norm of the previous tile (needs every warp's delta of tile it-1)
+      double nprev = 0.0;
+      if (it >= 1 && prev_direct) {
+        const int jn = it - 1;
         V3_T0(td);
         mbar_wait(&done_bar[jn & 1], (jn >> 1) & 1);
         V3_ACC(8, td);
         V3_T0(tn);
-        nsum = norm_units_swz<N1, M, E, NCW, UPW, C::DUE, C::DUC>(d_s + (jn % C::NDB) * C::DT, warp, lane, cfr,
-                                                                  a.comp_w);
+        nprev = norm_units_swz<N1, M, E, NCW, UPW, C::DUE, C::DUC>(d_s + (jn % C::NDB) * C::DT, warp, lane, cfr,
+                                                                   a.comp_w);
         V3_ACC(7, tn);
       }
       V3_T0(tm);
@@ -535,7 +582,22 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS>::NT, 1)
           }
         }
       }
+      // Gram-form norm of tile it: Y = R dq for this warp's item, ||Y||_F^2
+      // (comp_w and the reference mass are inside R, the Jacobian is applied
+      // with the tile partial)
+      double ng = 0.0;
+      if (gtile && has_gi) {
+        const double* dqb = qst + C::QT + (lane >> 2) * KC + (lane & 3) + geg * 8 * KC;
+        double y0 = 0.0, y1 = 0.0;
+#pragma unroll
+        for (int ks = 0; ks < KS; ++ks)
+          if (ks >= 2 * grt) dmma_8x8x4(y0, y1, Rf[ks], dqb[4 * ks]);
+        ng = fma(y0, y0, y1 * y1);
+      }
       V3_ACC(4, tm);
+      // a direct tile rewrites the d_s slot of tile it-2: every warp finished
+      // that tile's norm by done(it-1)
+      if (!gtile && it >= 1 && !prev_direct) mbar_wait(&done_bar[(it - 1) & 1], ((it - 1) >> 1) & 1);
       V3_T0(to);
       if (it >= 2) mbar_wait(&outfree_bar[ob], ((it - 2) >> 1) & 1);
       V3_ACC(5, to);
@@ -553,16 +615,21 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS>::NT, 1)
             for (int v = 0; v < 2; ++v) {
               const int t = te + v;
               outb[t * NV + row] = acc[eg][j][v];
-              dcur[t * C::DUE + doff[j]] = acc[eg][j][v] - ust[t * NV + row];
+              if (!gtile) dcur[t * C::DUE + doff[j]] = acc[eg][j][v] - ust[t * NV + row];
             }
           }
         }
       }
       V3_ACC(10, te);
-      if (it >= C::LAG) {
+      if (it >= 1 && prev_direct) {
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) nsum += __shfl_xor_sync(0xffffffffu, nsum, o);
-        if (lane == 0) red_s[((it - C::LAG) % C::NDB) * 32 + warp] = nsum;
+        for (int o = 16; o > 0; o >>= 1) nprev += __shfl_xor_sync(0xffffffffu, nprev, o);
+        if (lane == 0) red_s[((it - 1) % C::NRED) * 32 + warp] = nprev;
+      }
+      if (gtile) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) ng += __shfl_xor_sync(0xffffffffu, ng, o);
+        if (lane == 0) red_s[(it % C::NRED) * 32 + warp] = ng;
       }
       fence_proxy_async();
       __syncwarp();
@@ -570,15 +637,17 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS>::NT, 1)
         mbar_arrive(&empty_bar[stage]);
         mbar_arrive(&done_bar[ob]);
       }
+      prev_direct = gtile ? 0 : 1;
     }
-    // drain: norms of the last LAG tiles
-    for (int jn = n_my - C::LAG > 0 ? n_my - C::LAG : 0; jn < n_my; ++jn) {
+    // drain: direct norm of the last tile
+    if (n_my >= 1 && prev_direct) {
+      const int jn = n_my - 1;
       mbar_wait(&done_bar[jn & 1], (jn >> 1) & 1);
       double nsum = norm_units_swz<N1, M, E, NCW, UPW, C::DUE, C::DUC>(d_s + (jn % C::NDB) * C::DT, warp, lane, cfr,
                                                                        a.comp_w);
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) nsum += __shfl_xor_sync(0xffffffffu, nsum, o);
-      if (lane == 0) red_s[(jn % C::NDB) * 32 + warp] = nsum;
+      if (lane == 0) red_s[(jn % C::NRED) * 32 + warp] = nsum;
     }
   }
 
@@ -588,7 +657,7 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS>::NT, 1)
     for (int jn = n_my - C::LAG > 0 ? n_my - C::LAG : 0; jn < n_my; ++jn) {
       if (jn <= n_my - 1 - C::LAG) continue;
       double s = 0.0;
-      for (int w = 0; w < NCW; ++w) s += red_s[(jn % C::NDB) * 32 + w];
+      for (int w = 0; w < NCW; ++w) s += red_s[(jn % C::NRED) * 32 + w];
       a.tile_partials[blockIdx.x + jn * gridDim.x] = a.jac * s;
     }
   }

@@ -32,8 +32,10 @@ HISTORY_COLUMNS = ("iteration", "l2_error", "successive_norm", "trace_energy", "
 class IterationConfig:
     """SPEC.md:315-318.  ``stop``: "successive" (||u^k - u^{k-1}||_{L2} < tol,
     PAPER.md:1308-1311), "exact" (| ||u^k - u^e|| - ||u^{k-1} - u^e|| | < tol,
-    PAPER.md:1303-1306, needs problem.exact) or "trace" (skeleton L2 norm of
-    the trace update; transport only)."""
+    PAPER.md:1303-1306, needs problem.exact), "vs-direct" (||u^k - u_direct||
+    < tol, SPEC.md:316 / PAPER.md section 6.3, ``reference`` = the direct HDG
+    solution) or "trace" (skeleton L2 norm of the trace update, SURVEY.md
+    App. B.2; transport only)."""
 
     scheme: str = "iHDG-II"
     stop: str = "successive"
@@ -58,8 +60,10 @@ class IterationConfig:
             raise ValueError(f"unknown scheme {self.scheme!r} (iHDG-I or iHDG-II)")
         if self.stop == "exact-solution":
             self.stop = "exact"
-        if self.stop not in ("successive", "trace", "exact"):
+        if self.stop not in ("successive", "trace", "exact", "vs-direct"):
             raise NotImplementedError(f"stopping rule {self.stop!r} not on the device path")
+        if self.stop == "vs-direct" and self.reference is None:
+            raise ValueError("the vs-direct stopping rule needs IterationConfig(reference=<direct HDG solution>)")
 
 
 @dataclass
@@ -111,6 +115,8 @@ def _norm_name(cfg: IterationConfig, problem) -> str:
         if getattr(problem, "exact", None) is None:
             raise ValueError("the exact-solution stopping rule needs problem.exact")
         return "exact"
+    if cfg.stop == "vs-direct":
+        return "vs-direct"
     return "trace" if cfg.stop == "trace" else "volume"
 
 
@@ -157,7 +163,8 @@ def _diagnostic_iterate(solver: DeviceSolver, cfg: IterationConfig, norm: str, m
     side_refs = [solver.trace_of(ref, weights=w) for w in solver.energy_sides()]
     has_exact = getattr(solver, "ue_q", None) is not None
     solver.reset_state(cfg.tol, max_iters, cfg.diverge_factor)
-    if norm == "exact":
+    err_rule = {"exact": 1, "vs-direct": 2}.get(norm, 0)   # K5 mode of the stop rule
+    if err_rule:
         N.check(solver.L.ihdg_error_norm(C.byref(solver._error_args(0)), solver._sptr), "ihdg_error_norm")
         a = solver.sweep_args("volume", finalize=0)
     else:
@@ -168,12 +175,12 @@ def _diagnostic_iterate(solver: DeviceSolver, cfg: IterationConfig, norm: str, m
     status = "running"
     for k in range(1, max_iters + 1):
         solver.sweep_once(a=a)
-        if norm == "exact":
-            e = solver._error_args(1)
+        if err_rule:
+            e = solver._error_args(err_rule)
             N.check(solver.L.ihdg_error_norm(C.byref(e), solver._sptr), "ihdg_error_norm")
         st = solver.read_state()
         err = float("nan")
-        if norm == "exact":
+        if err_rule:
             err = st.last_err
         elif has_exact:
             e = solver._error_args(0)
@@ -255,6 +262,8 @@ def run(mesh, problem, ops: ElementOperators, cfg: Optional[IterationConfig] = N
     _set_initial(solver, cfg.initial_guess)
     if cfg.stop == "exact" or (cfg.diagnostics and getattr(problem, "exact", None) is not None):
         solver.set_exact(_exact_at(problem.exact, None))
+    if cfg.stop == "vs-direct":
+        solver.set_reference(cfg.reference.data if isinstance(cfg.reference, FieldState) else cfg.reference)
     if cfg.diagnostics:
         return _diagnostic_report(solver, cfg, _norm_name(cfg, problem), cfg.max_iters or default_max_iters(mesh),
                                   t0, return_state, return_trace)
@@ -352,6 +361,9 @@ def run_time_dependent(mesh, problem, ops: ElementOperators, cfg: Optional[Itera
         solver.begin_step()
         if cfg.stop == "exact" or (cfg.diagnostics and getattr(problem, "exact", None) is not None):
             solver.set_exact(_exact_at(problem.exact, (m + 1) * dt))
+        if cfg.stop == "vs-direct":   # one direct solution per step (a list), or one for all
+            r = cfg.reference[m] if isinstance(cfg.reference, (list, tuple)) else cfg.reference
+            solver.set_reference(r.data if isinstance(r, FieldState) else r)
         if cfg.diagnostics:
             keep = keep_states or m == n_steps - 1
             rep = _diagnostic_report(solver, cfg, _norm_name(cfg, problem),

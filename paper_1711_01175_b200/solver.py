@@ -106,6 +106,7 @@ class DeviceSolver:
             self.norm_hist = torch.zeros(self.max_iters, dtype=f64, device=dev)
             self.chol = torch.as_tensor(ops.chol1d.copy(), dtype=f64, device=dev)
             self.class_of_mask = torch.as_tensor(sp.class_of_mask, device=dev)
+            self._setup_gram()
 
     # -- setup -------------------------------------------------------------
     @property
@@ -191,6 +192,43 @@ class DeviceSolver:
         N.check(self.L.ihdg_assemble(C.byref(b), self._sptr), what)
         self.stream.synchronize()
         return LT
+
+    def _setup_gram(self) -> None:
+        """Gram-form stopping norm of the interior operator class (ihdg.h,
+        ihdg_sweep_args.q_store): R upper triangular with
+        R^T R = L^T (W (x) M1 (x) .. (x) M1) L over the kernel's q columns,
+        so that ||u^{k+1} - u^k||^2_M = J ||R (q^k - q^{k-1})||^2 within a
+        solve; plus the per-element q store.  Only for kernels that take it
+        (ihdg_sweep_gram_kc > 0); otherwise the direct norm runs."""
+        self.gram_R = self.q_store = None
+        self.gram_kc = 0
+        a = self.sweep_args("volume", gram=False)
+        a.u_old, a.u_new = _ptr(self.u[0]), _ptr(self.u[1])
+        kc = int(self.L.ihdg_sweep_gram_kc(C.byref(a)))
+        if kc <= 0:
+            return
+        sp, d = self.spec, self.mesh.dim
+        nf = sp.n1 ** (d - 1)
+        cols = [f * nf + n for f in range(2 * d) if sp.coupled[f] for n in range(nf)]
+        if len(cols) != kc:
+            return
+        c = int(sp.class_of_mask[0])
+        Lc = self.LT[c].cpu().numpy().T[:, cols]                   # (nv, kc)
+        m1 = self.ops.chol1d @ self.ops.chol1d.T
+        mref = m1
+        for _ in range(d - 1):
+            mref = np.kron(m1, mref)
+        W = np.kron(np.diag(np.asarray(sp.comp_w[: sp.ncomp], dtype=float)), mref)
+        G = Lc.T @ W @ Lc
+        G = 0.5 * (G + G.T)
+        try:
+            R = np.linalg.cholesky(G).T                            # upper: G = R^T R
+        except np.linalg.LinAlgError:
+            return                                                 # singular: direct norm
+        torch = self.torch
+        self.gram_R = torch.as_tensor(np.ascontiguousarray(R), dtype=torch.float64, device=self.device)
+        self.q_store = torch.zeros((self.nloc, kc), dtype=torch.float64, device=self.device)
+        self.gram_kc = kc
 
     # -- state -------------------------------------------------------------
     def interior(self, which=None):
@@ -404,14 +442,17 @@ class DeviceSolver:
             if exchange is not None:
                 exchange()
             self.reset_state(0.0, 1)
-            a = self.sweep_args("volume", finalize=0)
+            a = self.sweep_args("volume", finalize=0, gram=False)
             a.LT = _ptr(self.LT_expl)
             a.u_old, a.u_new = _ptr(self.u[self.cur]), _ptr(self.u[1 - self.cur])
             N.check(self.L.ihdg_sweep(C.byref(a), self._sptr), "ihdg_sweep (CN explicit half)")
             self.s.copy_(self.interior(1 - self.cur))
 
     # -- iteration ---------------------------------------------------------
-    def sweep_args(self, norm: str, finalize: int = 1) -> N.SweepArgs:
+    def sweep_args(self, norm: str, finalize: int = 1, gram: bool = True) -> N.SweepArgs:
+        """Sweep arguments of the current operators; ``gram``: pass the
+        Gram-form norm data when the kernel takes it (the caller keeps s and
+        the operators fixed between the sweeps of one solve)."""
         sp = self.spec
         a = N.SweepArgs()
         a.g = self.geom
@@ -439,6 +480,8 @@ class DeviceSolver:
         a.finalize = finalize
         a.tile_offset = 0
         a.scheme = N.SCHEME_I if sp.scheme == "iHDG-I" else N.SCHEME_II
+        if gram and getattr(self, "gram_kc", 0) > 0:
+            a.q_store, a.gram_R, a.gram_kc = _ptr(self.q_store), _ptr(self.gram_R), self.gram_kc
         return a
 
     def reset_state(self, tol: float, max_iters: int, diverge_factor: float = 1e6) -> None:
@@ -487,6 +530,29 @@ class DeviceSolver:
                                             dtype=torch.float64, device=self.device)
             self.err_hist = torch.zeros(self.max_iters, dtype=torch.float64, device=self.device)
 
+    def set_reference(self, ref) -> None:
+        """Reference field of the vs-direct stopping rule: a
+        direct HDG solution (FieldState data (Nel, m, Np) of the local strip),
+        interpolated to the Gauss points; the rule is ||u^k - u_ref||_{L2} < tol
+        over all components."""
+        torch, sp, ops = self.torch, self.spec, self.ops
+        d = self.mesh.dim
+        r = np.asarray(ref, dtype=np.float64).reshape(self.nloc, sp.ncomp, self.np_)
+        vq = np.asarray(ops.interp, dtype=np.float64)          # (nq, N1)
+        phi = vq
+        for _ in range(d - 1):
+            phi = np.kron(vq, phi)                               # (nq^d, Np), axis 0 fastest
+        ue = r @ phi.T                                           # (nloc, m, nq^d)
+        self.ue_q = torch.as_tensor(np.ascontiguousarray(ue), dtype=torch.float64, device=self.device)
+        self._err_w = np.zeros(4)
+        self._err_w[: sp.ncomp] = 1.0
+        if getattr(self, "_vq", None) is None:
+            self._vq = torch.as_tensor(ops.interp, dtype=torch.float64, device=self.device).contiguous()
+            self._wq = torch.as_tensor(ops.quad_weights, dtype=torch.float64, device=self.device).contiguous()
+            self.err_partials = torch.zeros(int(self.L.ihdg_error_tile_count(C.byref(self.geom))),
+                                            dtype=torch.float64, device=self.device)
+            self.err_hist = torch.zeros(self.max_iters, dtype=torch.float64, device=self.device)
+
     def _error_args(self, mode: int) -> N.ErrorArgs:
         e = N.ErrorArgs()
         e.g = self.geom
@@ -503,8 +569,8 @@ class DeviceSolver:
         """Algorithm 1 from the current iterate until the
         stopping rule holds; the latest iterate becomes current.  norm
         "volume" / "trace" (successive) or "exact" (set_exact first)."""
-        if norm == "exact":
-            return self._iterate_exact(tol, max_iters, batch)
+        if norm in ("exact", "vs-direct"):
+            return self._iterate_exact(tol, max_iters, batch, mode=2 if norm == "vs-direct" else 1)
         self.reset_state(tol, max_iters)
         a = self.sweep_args(norm, finalize=1)
         out = N.IterState()
@@ -522,15 +588,15 @@ class DeviceSolver:
         return IterResult(it, N.STATUS_NAMES[out.status], norms, out.first_norm, out.last_norm,
                           int(nl.value), sec, kernel=kernel)
 
-    def _iterate_exact(self, tol, max_iters, batch) -> IterResult:
+    def _iterate_exact(self, tol, max_iters, batch, mode: int = 1) -> IterResult:
         if getattr(self, "ue_q", None) is None:
-            raise RuntimeError("exact-solution rule: call set_exact() first")
+            raise RuntimeError("exact-solution / vs-direct rule: call set_exact() / set_reference() first")
         if self.layers != (0, self.mesh.cells[self.mesh.dim - 1]):
             raise NotImplementedError("exact-solution rule on a partitioned mesh")
         self.reset_state(tol, max_iters)
         N.check(self.L.ihdg_error_norm(C.byref(self._error_args(0)), self._sptr), "ihdg_error_norm")
         a = self.sweep_args("volume", finalize=0)
-        e = self._error_args(1)
+        e = self._error_args(mode)
         out = N.IterState()
         nl = C.c_int64(0)
         b0, b1 = self.u[self.cur], self.u[1 - self.cur]

@@ -224,12 +224,17 @@ def test_config4_stream_kernel_parity():
     from paper_1711_01175_b200 import _native as N
     from tests.oracle_bridge import rel_l2
 
-    wl = _wl(4, cells=8)
+    from paper_1711_01175_b200.iteration import IterationConfig, run
+    from tests.oracle_bridge import oracle_solver
+
+    wl = _wl(4, cells=32)   # k_sweep_stream tiles are 32 elements of one axis-0 row
     N.set_sweep_impl("stream")
     try:
-        rep, S, ref = _steady(wl, "successive")
+        rep = run(wl.mesh, wl.problem, wl.ops, IterationConfig(tol=1e-10))
     finally:
         N.set_sweep_impl("auto")
+    S = oracle_solver(wl)
+    ref = S.run(tol=1e-10, engine="c")
     assert rep.extra["kernel"] == "k_sweep_stream"
     assert rep.iterations == ref["iterations"]
     assert rel_l2(rep.state.data.reshape(S.nel, -1), ref["u"]) < TOL_FIELD
@@ -257,3 +262,39 @@ def test_table2_transport_counts(dim, n, paper):
                   IterationConfig(stop="trace", tol=1e-10), return_trace=False)
         assert rep.status == "converged"
         assert abs(rep.iterations - paper) <= 2, (p, rep.iterations, paper)
+
+
+@pytest.mark.parametrize("cfg,cells,kw", [(5, 32, {"kappa": 1e-1}), (5, 32, {"kappa": 1e-3}), (2, 32, {})])
+def test_gram_norm_matches_direct(cfg, cells, kw):
+    """The Gram-form norm of k_sweep_ws (ihdg_sweep_args.q_store) against the
+    direct mass-norm of the same kernel: identical counts, identical first
+    sweep (direct in both), later norms equal to the rounding of the
+    successive difference (relative to |u|, so looser as it shrinks)."""
+    from paper_1711_01175_b200 import _native as N
+    from paper_1711_01175_b200.solver import DeviceSolver
+
+    wl = _wl(cfg, cells=cells, n_steps=1, **kw)
+    if cfg == 2:
+        N.set_sweep_impl("ws")
+    try:
+        out = []
+        for gram in (True, False):
+            sv = DeviceSolver(wl.mesh, wl.problem, wl.ops, dt=wl.dt)
+            assert sv.gram_kc == 4 * (wl.ops.p + 1)
+            if not gram:
+                sv.gram_kc = 0
+            for name, fld in wl.initial.items():
+                sv.set_state_component(fld, sv.spec.labels.index(name))
+            sv.begin_step()
+            r = sv.iterate(tol=1e-10, max_iters=100000)
+            assert r.kernel == "k_sweep_ws"
+            out.append((r, sv.get_state()))
+    finally:
+        N.set_sweep_impl("auto")
+    (rg, ug), (rd, ud) = out
+    assert rg.iterations == rd.iterations and rg.status == rd.status == "converged"
+    assert rg.norms[0] == rd.norms[0]
+    assert np.array_equal(ug, ud)          # the norm never feeds back into the fields
+    big = rd.norms > 1e-6 * rd.norms[0]
+    assert np.allclose(rg.norms[big], rd.norms[big], rtol=1e-9, atol=0)
+    assert np.allclose(rg.norms, rd.norms, rtol=1e-4, atol=0)
