@@ -216,7 +216,7 @@ def run_ours(args):
     setup_s = time.perf_counter() - t_setup
     dofs_rank = sv.nloc * sv.nv
     dofs_total = mesh.n_elements * sv.nv
-    dsw = DistributedSweeper(sv, rank, world, group) if world > 1 else None
+    dsw = DistributedSweeper(sv, rank, world, group, overlap=not args.no_overlap) if world > 1 else None
     # a large tolerance-free run: status stays RUNNING for K+W sweeps
     sv.reset_state(tol=0.0, max_iters=args.steps + args.warmup + 10)
     a = sv.sweep_args("volume", finalize=1 if world == 1 else 0)
@@ -377,7 +377,7 @@ def run_ours(args):
                          "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
                          "bytes_per_dof": BYTES_PER_DOF, "kernel_ms": sweep_ms},
             "clocks": clk.summary(),
-            "gpu_launches": args.steps * (1 if world == 1 else 2),
+            "gpu_launches": args.steps * (1 if world == 1 else dsw.launches_per_sweep()),
             "setup_seconds": setup_s,
             "time_to_converge": ttc or None,
             "e2e": e2e,
@@ -389,6 +389,20 @@ def run_ours(args):
         print(json.dumps(line), flush=True)
     if world > 1:
         torch.distributed.destroy_process_group()
+
+
+def _self_launch(args) -> int:
+    """--gpus N without a torchrun environment: start N ranks (one per GPU)
+    through torch.distributed.run on 127.0.0.1 and return their exit code."""
+    import socket
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
 
 
 def main():
@@ -411,9 +425,16 @@ def main():
     ap.add_argument("--no-others", dest="other_configs", action="store_false")
     ap.add_argument("--cpu-rows", type=int, default=64)
     ap.add_argument("--cpu-reps", type=int, default=3)
+    ap.add_argument("--no-overlap", action="store_true",
+                    help="multi-GPU: halo before the whole sweep instead of under the interior layers")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(_self_launch(args))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
     if args.impl == "reference":
         run_reference(args)
     else:

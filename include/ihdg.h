@@ -229,7 +229,7 @@ typedef struct {
    * a solve on (the first sweep, and tiles with a boundary-class element,
    * take the direct norm).  Contract: between two sweeps of one solve the
    * caller changes neither s nor the operators. */
-  double* q_store;            /* [n_tiles_local][tile elems][gram_kc] or NULL */
+  double* q_store;            /* [n_tiles_local][tile elems * gram_kc] or NULL (kernel-internal order within a tile) */
   const double* gram_R;       /* [gram_kc][gram_kc] row-major upper-triangular R of the interior class, kernel column order (coupled faces ascending, face nodes) */
   int32_t gram_kc;            /* ihdg_sweep_gram_kc(args), 0 = off */
   int32_t pad2;
@@ -298,13 +298,35 @@ typedef struct {
   double jac_face[IHDG_MAX_DIM];
 } ihdg_face_energy_args;
 
-/* K3 (multi-rank): reduce globally gathered tile partials, update *state. */
+/* K3 (multi-rank): reduce the gathered partials, update *state.  The
+ * partials are n_tiles values in rows of row_len (one row per element layer
+ * of the slowest axis, tile order): each row is summed sequentially, the row
+ * sums in a fixed order (256 virtual lanes + a fixed tree) -- the order the
+ * fused single-rank finalize uses, so a strip partition (which splits only
+ * between layers) gives bit-identical norms.  Multi-rank callers pass the
+ * all-reduced layer sums of ihdg_layer_sums with row_len 1. */
 typedef struct {
-  const double* tile_partials; /* [n_tiles_global] in global tile order */
+  const double* tile_partials; /* [n_tiles] */
   int64_t n_tiles;
   ihdg_iter_state* state;
   double* norm_hist;
+  int64_t row_len;             /* tiles per row (<= 0: 1) */
 } ihdg_finalize_args;
+
+/* Halo pack / unpack of a strip partition: only the face-node
+ * entries a neighbouring rank's sweep reads cross the wire, not whole layers.
+ * For every element of one layer of the ghost-padded state, the element-local
+ * DOF entries idx[0..n_idx) (component * (p+1)^d + node of the face the
+ * neighbour reads, components with a nonzero face weight) are copied to /
+ * from packed[element][n_idx]. */
+typedef struct {
+  ihdg_geom g;
+  double* buf;                /* ghost-padded state */
+  double* packed;             /* [layer elems][n_idx] */
+  const int32_t* idx;         /* [n_idx] element-local entries (device) */
+  int32_t n_idx;
+  int32_t layer;              /* 0 ghost_lo, 1 first local, 2 last local, 3 ghost_hi */
+} ihdg_halo_args;
 
 /* Single-valued trace on every face, mesh.py face order (mesh.py:89-125).
  * Per axis a: interior face (owner = lower element, normal +e_a)
@@ -324,7 +346,8 @@ typedef struct {
 int ihdg_abi_version(void);
 /* sizeof the ABI structs, for binding self-checks: 0 geom, 1 iter_state,
  * 2 assembly_args, 3 class_apply_args, 4 field_args, 5 quad_args,
- * 6 sweep_args, 7 finalize_args, 8 trace_args; -1 otherwise */
+ * 6 sweep_args, 7 finalize_args, 8 trace_args, 9 error_args, 10 elem_error_args,
+ * 11 face_energy_args, 12 halo_args; -1 otherwise */
 int64_t ihdg_struct_size(int32_t which);
 const char* ihdg_last_error(void);
 /* 1 if the sweep/apply kernels are instantiated for (dim, order, ncomp) */
@@ -358,6 +381,12 @@ int ihdg_sweep_gram_kc(const ihdg_sweep_args* a);
  * environment sets IHDG_NO_GRAPH): 1 on, 0 off. */
 int ihdg_set_graphs(int on);
 int ihdg_finalize(const ihdg_finalize_args* a, void* stream);
+/* out[r] = sequential sum of row r of the tile partials [n_rows][row_len]
+ * (a rank's layer sums, the inner sums of ihdg_finalize) */
+int ihdg_layer_sums(const double* tile_partials, int64_t n_rows, int64_t row_len, double* out, void* stream);
+/* halo pack (layer 1/2 -> packed) and unpack (packed -> layer 0/3) */
+int ihdg_halo_pack(const ihdg_halo_args* a, void* stream);
+int ihdg_halo_unpack(const ihdg_halo_args* a, void* stream);
 int ihdg_extract_trace(const ihdg_trace_args* a, void* stream);
 /* copy the ghost-padded layer range between two buffers (initial guess) */
 int ihdg_copy_state(const ihdg_geom* g, const double* src, double* dst, void* stream);

@@ -84,7 +84,11 @@ class SweepArgs(C.Structure):
 
 
 class FinalizeArgs(C.Structure):
-    _fields_ = [("tile_partials", _p), ("n_tiles", _i64), ("state", _p), ("norm_hist", _p)]
+    _fields_ = [("tile_partials", _p), ("n_tiles", _i64), ("state", _p), ("norm_hist", _p), ("row_len", _i64)]
+
+
+class HaloArgs(C.Structure):
+    _fields_ = [("g", Geom), ("buf", _p), ("packed", _p), ("idx", _p), ("n_idx", _i32), ("layer", _i32)]
 
 
 class TraceArgs(C.Structure):
@@ -109,7 +113,7 @@ class FaceEnergyArgs(C.Structure):
 
 
 _STRUCTS = [Geom, IterState, AssemblyArgs, ClassApplyArgs, FieldArgs, QuadArgs, SweepArgs,
-            FinalizeArgs, TraceArgs, ErrorArgs, ElemErrorArgs, FaceEnergyArgs]
+            FinalizeArgs, TraceArgs, ErrorArgs, ElemErrorArgs, FaceEnergyArgs, HaloArgs]
 
 # exported symbol -> (restype, argtypes)
 SIGNATURES = {
@@ -130,6 +134,9 @@ SIGNATURES = {
     "ihdg_set_sweep_impl": (_i32, [C.c_char_p]),
     "ihdg_set_graphs": (_i32, [_i32]),
     "ihdg_finalize": (_i32, [C.POINTER(FinalizeArgs), _p]),
+    "ihdg_layer_sums": (_i32, [_p, _i64, _i64, _p, _p]),
+    "ihdg_halo_pack": (_i32, [C.POINTER(HaloArgs), _p]),
+    "ihdg_halo_unpack": (_i32, [C.POINTER(HaloArgs), _p]),
     "ihdg_extract_trace": (_i32, [C.POINTER(TraceArgs), _p]),
     "ihdg_copy_state": (_i32, [C.POINTER(Geom), _p, _p, _p]),
     "ihdg_iterate": (_i32, [C.POINTER(SweepArgs), _p, _p, _i32, _p, C.POINTER(IterState),

@@ -170,6 +170,7 @@ int64_t ihdg_struct_size(int32_t which) {
     case 9: return sizeof(ihdg_error_args);
     case 10: return sizeof(ihdg_elem_error_args);
     case 11: return sizeof(ihdg_face_energy_args);
+    case 12: return sizeof(ihdg_halo_args);
     default: return -1;
   }
 }
@@ -304,6 +305,32 @@ int ihdg_finalize(const ihdg_finalize_args* a, void* stream) {
   k_finalize<<<1, 256, 0, (cudaStream_t)stream>>>(*a);
   return check_launch("k_finalize");
 }
+
+int ihdg_layer_sums(const double* tile_partials, int64_t n_rows, int64_t row_len, double* out, void* stream) {
+  if (tile_partials == nullptr || out == nullptr || n_rows < 0 || row_len < 1) return set_err(IHDG_ERR_ARG, "bad args");
+  if (n_rows == 0) return IHDG_OK;
+  int64_t grid = (n_rows + 3) / 4;   // 4 warps (rows) per CTA
+  if (grid > 8 * num_sms()) grid = 8 * num_sms();
+  k_layer_sums<<<(unsigned)grid, 128, 0, (cudaStream_t)stream>>>(tile_partials, n_rows, row_len, out);
+  return check_launch("k_layer_sums");
+}
+
+static int halo_copy(const ihdg_halo_args* a, int unpack, cudaStream_t st) {
+  if (a == nullptr || a->buf == nullptr || a->packed == nullptr || a->idx == nullptr || a->n_idx < 1)
+    return set_err(IHDG_ERR_ARG, "null / empty halo args");
+  int rc = check_geom(a->g);
+  if (rc) return rc;
+  if (a->layer < 0 || a->layer > 3 || (unpack ? (a->layer == 1 || a->layer == 2) : (a->layer == 0 || a->layer == 3)))
+    return set_err(IHDG_ERR_ARG, "halo layer: pack reads layer 1/2, unpack writes layer 0/3");
+  const int64_t total = layer_size(a->g) * a->n_idx;
+  int64_t grid = (total + 255) / 256;
+  if (grid > 4 * num_sms()) grid = 4 * num_sms();
+  k_halo_copy<<<(unsigned)grid, 256, 0, st>>>(*a, unpack);
+  return check_launch("k_halo_copy");
+}
+
+int ihdg_halo_pack(const ihdg_halo_args* a, void* stream) { return halo_copy(a, 0, (cudaStream_t)stream); }
+int ihdg_halo_unpack(const ihdg_halo_args* a, void* stream) { return halo_copy(a, 1, (cudaStream_t)stream); }
 
 int ihdg_extract_trace(const ihdg_trace_args* a, void* stream) {
   if (a == nullptr) return set_err(IHDG_ERR_ARG, "null args");

@@ -18,6 +18,11 @@ struct Pow<B, 0> {
 };
 
 constexpr int round_up(int x, int m) { return (x + m - 1) / m * m; }
+__host__ __device__ inline int ipow(int b, int e) {
+  int r = 1;
+  for (int i = 0; i < e; ++i) r *= b;
+  return r;
+}
 constexpr int cmin(int a, int b) { return a < b ? a : b; }
 constexpr int cmax(int a, int b) { return a > b ? a : b; }
 

@@ -11,25 +11,59 @@ namespace ihdg {
 
 constexpr long long NO_NBR = -(1LL << 62);
 
-// Fixed-order (rank-count independent) reduction of the tile partials and the
-// stopping / divergence logic of `run`.
-// 256 virtual lanes, lane v sums tiles v, v+256, ... in order, then a fixed
-// binary tree.  Must be executed by every thread of one CTA.
-__device__ inline void finalize_block(const double* parts, int64_t n, ihdg_iter_state* st,
-                                      double* hist) {
+// Sum of one row of tile partials by one warp: lane j sums the entries
+// j, j+32, ... in order, then an xor butterfly (every lane ends with the same
+// value: each stage adds a commutative pair).  Coalesced; the same code in
+// k_layer_sums gives a rank's layer sums bit-identically.
+__device__ __forceinline__ double warp_row_sum(const double* row, int64_t len, int lane) {
+  double s = 0.0;
+  for (int64_t i = lane; i < len; i += 32) s += __ldcg(row + i);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  return s;
+}
+
+// Fixed-order, partition-independent sum of tile partials laid out as rows
+// (one row per element layer of the slowest axis, row_len tiles each, in
+// tile order; a strip partition splits between rows, never inside one):
+// each row is summed by warp_row_sum, virtual lane v of 256 sums the row sums
+// v, v+256, ... in order, then a fixed binary tree -- an order independent of
+// the CTA size.  A rank's layer sums (k_layer_sums) therefore combine to
+// exactly the single-rank value (ihdg_finalize with row_len 1: a one-entry
+// row sums to itself).  Every thread of the CTA must call it; blockDim.x is a
+// multiple of 32.
+__device__ inline double rows_sum(const double* parts, int64_t n_rows, int64_t row_len) {
   __shared__ double red[256];
-  for (int v = threadIdx.x; v < 256; v += blockDim.x) {
+  __syncthreads();
+  const int lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  for (int v = threadIdx.x >> 5; v < 256; v += nw) {
     double s = 0.0;
-    for (int64_t i = v; i < n; i += 256) s += __ldcg(parts + i);
-    red[v] = s;
+    for (int64_t r = v; r < n_rows; r += 256) s += warp_row_sum(parts + r * row_len, row_len, lane);
+    if (lane == 0) red[v] = s;
   }
   __syncthreads();
   for (int w = 128; w > 0; w >>= 1) {
     for (int v = threadIdx.x; v < w; v += blockDim.x) red[v] += red[v + w];
     __syncthreads();
   }
+  return red[0];
+}
+
+// rows of the tile partials of a strip (see rows_sum): one per layer in 2D /
+// 3D, the whole strip in 1D
+__host__ __device__ inline void partial_rows(const Geo& g, int64_t& n_rows, int64_t& row_len) {
+  n_rows = g.D == 1 ? 1 : g.nlay;
+  row_len = g.D == 1 ? g.ntiles : g.segs;
+}
+
+// The stopping / divergence logic of `run` (
+// PAPER.md:1308-1311) on the fixed-order sum of the partials.  Must be
+// executed by every thread of one CTA.
+__device__ inline void finalize_block(const double* parts, int64_t n_rows, int64_t row_len, ihdg_iter_state* st,
+                                      double* hist) {
+  const double total = rows_sum(parts, n_rows, row_len);
   if (threadIdx.x == 0) {
-    const double norm = sqrt(red[0]);
+    const double norm = sqrt(total);
     const int it = st->iters + 1;
     st->iters = it;
     if (hist != nullptr && it <= st->max_iters) hist[it - 1] = norm;
@@ -286,7 +320,9 @@ __global__ void __launch_bounds__(Cfg<D, N1, M>::NT)
     __syncthreads();
     if (last_s) {
       __threadfence();
-      finalize_block(a.tile_partials, geo.ntiles, st, a.norm_hist);
+      int64_t n_rows, row_len;
+      partial_rows(geo, n_rows, row_len);
+      finalize_block(a.tile_partials, n_rows, row_len, st, a.norm_hist);
     }
   }
 }

@@ -343,7 +343,8 @@ __global__ void k_extract_trace(const ihdg_trace_args a) {
 
 __global__ void k_finalize(const ihdg_finalize_args a) {
   if (a.state->status != IHDG_RUNNING) return;  // later sweeps are no-ops
-  finalize_block(a.tile_partials, a.n_tiles, a.state, a.norm_hist);
+  const int64_t rl = a.row_len > 0 ? a.row_len : 1;
+  finalize_block(a.tile_partials, a.n_tiles / rl, rl, a.state, a.norm_hist);
 }
 
 // Fixed-order sum of n partials (256 virtual lanes, then a fixed tree), the
@@ -439,7 +440,9 @@ __global__ void k_error_norm(const ihdg_error_args a) {
     }
     return;
   }
-  const double norm = sqrt(fixed_sum(a.succ_partials, a.n_succ));
+  // the sweep's tile partials, in the rows of finalize_block
+  const int64_t srows = geo.D == 1 ? 1 : geo.nlay;
+  const double norm = sqrt(rows_sum(a.succ_partials, srows, a.n_succ / srows));
   if (threadIdx.x == 0) {
     const int it = st->iters + 1;
     st->iters = it;
@@ -578,6 +581,39 @@ __global__ void k_face_energy(const ihdg_face_energy_args a) {
 __global__ void k_fixed_total(const double* v, int64_t n, double* out) {
   const double s = fixed_sum(v, n);
   if (threadIdx.x == 0) *out = s;
+}
+
+// out[r] = sum of row r of the tile partials (warp_row_sum, the inner sums
+// of rows_sum): one warp per row
+__global__ void k_layer_sums(const double* parts, int64_t n_rows, int64_t row_len, double* out) {
+  const int lane = threadIdx.x & 31;
+  const int64_t w0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t r = w0; r < n_rows; r += nw) {
+    const double s = warp_row_sum(parts + r * row_len, row_len, lane);
+    if (lane == 0) out[r] = s;
+  }
+}
+
+// Halo pack / unpack: element-local DOF entries idx[0..n_idx) of every
+// element of one layer, between the ghost-padded state and a packed
+// [layer elems][n_idx] buffer.  layer: 0 = ghost_lo, 1 = first local,
+// 2 = last local, 3 = ghost_hi (rows of the padded buffer).
+__global__ void k_halo_copy(const ihdg_halo_args a, int unpack) {
+  Geo geo;
+  geo.init(a.g, 1);
+  const int64_t ls = geo.ls;
+  const int64_t nv = (int64_t)a.g.ncomp * ipow(a.g.order + 1, a.g.dim);
+  const int64_t row = a.layer == 0 ? 0 : (a.layer == 1 ? 1 : (a.layer == 2 ? geo.nlay : geo.nlay + 1));
+  double* base = a.buf + row * ls * nv;
+  const int64_t total = ls * a.n_idx;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t e = t / a.n_idx;
+    const int j = (int)(t - e * a.n_idx);
+    double* p = base + e * nv + a.idx[j];
+    if (unpack) *p = a.packed[t];
+    else a.packed[t] = *p;
+  }
 }
 
 }  // namespace ihdg

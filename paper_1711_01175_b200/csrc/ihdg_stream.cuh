@@ -686,7 +686,9 @@ __global__ void __launch_bounds__(SCfg<D, N1, M, NCF, NWC, E, NS, G>::NT, 1)
     __syncthreads();
     if (last_s) {
       __threadfence();
-      finalize_block(a.tile_partials, geo.ntiles, st, a.norm_hist);
+      int64_t n_rows, row_len;
+      partial_rows(geo, n_rows, row_len);
+      finalize_block(a.tile_partials, n_rows, row_len, st, a.norm_hist);
     }
   }
 }

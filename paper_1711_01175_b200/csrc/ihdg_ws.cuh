@@ -291,9 +291,12 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS>::NT, 1)
       __syncwarp();
       if (lane == 0) {
         const uint32_t bytes = (uint32_t)(nt * NV * sizeof(double));
-        mbar_arrive_expect_tx(&full_bar[stage], 2 * bytes);  // release: metadata above
+        constexpr uint32_t qbytes = (uint32_t)(C::QT * sizeof(double));
+        mbar_arrive_expect_tx(&full_bar[stage], 2 * bytes + (gram ? qbytes : 0u));  // release: metadata above
         bulk_g2s(sst, a.s + (int64_t)e0 * NV, bytes, &full_bar[stage]);
         bulk_g2s(ust, uo + (int64_t)e0 * NV, bytes, &full_bar[stage]);
+        // the stored q^{k-1} of the tile (consumer column order) into the dq slot
+        if (gram) bulk_g2s(ust + TILE + C::HALO + C::QT, a.q_store + (int64_t)tile * C::QT, qbytes, &full_bar[stage]);
       }
       if (IHDG_WS_PF > 0 && lane == 0 && it + IHDG_WS_PF < n_my) {
         // tile it+PF will be copied into a stage PF tiles from now: pull it into L2
@@ -320,8 +323,6 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS>::NT, 1)
     // out-of-tile neighbour face nodes of this warp's entries, loaded from
     // global (L2) into registers one tile ahead
     double gv[QM][NWC], gvn[QM][NWC];
-    // stored q^{k-1} of this warp's entries (Gram-form norm), one tile ahead
-    double qo[QM], qon[QM];
     int qs = 0, ql = 0, qsn = 0, qln = 0;
     // per-lane entry constants, hoisted out of the tile loop: entry m of this
     // lane is (element t, column k) with k's face f and its gather offsets
@@ -336,18 +337,12 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS>::NT, 1)
 #pragma unroll
       for (int j = 0; j < NWC; ++j) ent_q[m][j] = qt_s[k][j];
     }
-    auto gather = [&](int itg, double (&dst)[QM][NWC], double (&qdst)[QM], int& in_bits, int& ld_bits) {
+    auto gather = [&](int itg, double (&dst)[QM][NWC], int& in_bits, int& ld_bits) {
       in_bits = 0;
       ld_bits = 0;
       if (itg >= n_my) return;
       STile<D> tg;
-      const int tgi = (int)blockIdx.x + itg * (int)gridDim.x;
-      tg.init(a.g, tgi, E, nlay, lsi);
-      if (gram) {
-        const double* qsrc = a.q_store + (int64_t)tgi * C::QT + pw * HALF * KC + lane;
-#pragma unroll
-        for (int m = 0; m < QM; ++m) qdst[m] = ent_t[m] >= 0 ? __ldcs(qsrc + 32 * m) : 0.0;
-      }
+      tg.init(a.g, (int)blockIdx.x + itg * (int)gridDim.x, E, nlay, lsi);
       // missing neighbours: faces of axes >= 1 are tile-uniform, x faces only
       // at the tile ends
       int hm = 0;
@@ -383,10 +378,10 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS>::NT, 1)
         }
       }
     };
-    gather(0, gv, qo, qs, ql);
+    gather(0, gv, qs, ql);
     for (int it = 0; it < n_my; ++it) {
       const int stage = it % NS;
-      gather(it + 1, gvn, qon, qsn, qln);
+      gather(it + 1, gvn, qsn, qln);
       V3_T0(tp);
       mbar_wait(&full_bar[stage], (it / NS) & 1);
       V3_ACC(1, tp);
@@ -399,8 +394,8 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS>::NT, 1)
       const double* sst = sm + stage * C::STAGE;
       const double* ust = sst + TILE;
       double* qst = const_cast<double*>(ust) + TILE + C::HALO;
-      double* dqst = qst + C::QT;
-      double* qdst = qsave ? a.q_store + (int64_t)cur_tile * C::QT + pw * HALF * KC + lane : nullptr;
+      double* dqst = qst + C::QT;   // holds q^{k-1} (TMA), becomes dq in place
+      double* qdst = qsave ? a.q_store + (int64_t)cur_tile * C::QT : nullptr;
 #pragma unroll
       for (int m = 0; m < QM; ++m) {
         const int t = ent_t[m];
@@ -416,11 +411,13 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS>::NT, 1)
 #pragma unroll
             for (int j = 0; j < NWC; ++j) v = fma(w[j], gv[m][j], v);
           }
-          qst[ws_qcol<C::NEG>(t) * KC + k] = v;
-          if (gram) dqst[ws_qcol<C::NEG>(t) * KC + k] = v - qo[m];
-          if (qsave) __stcs(qdst + 32 * m, v);
+          const int qi = ws_qcol<C::NEG>(t) * KC + k;
+          qst[qi] = v;
+          if (gram) dqst[qi] = v - dqst[qi];
+          if (qsave) __stcs(qdst + qi, v);   // q store: the stage's column order
         }
       }
+      if (gram) fence_proxy_async();   // dq overwrote a TMA destination; the stage is refilled by TMA
       __syncwarp();
       V3_ACC(2, tq);
       if (lane == 0) mbar_arrive(&qready_bar[stage]);
@@ -448,11 +445,9 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS>::NT, 1)
       // the gathers of tile it+1 are consumed only here (a register move
       // waits on the load), i.e. after qready(it) and the done wait
 #pragma unroll
-      for (int m = 0; m < QM; ++m) {
+      for (int m = 0; m < QM; ++m)
 #pragma unroll
         for (int j = 0; j < NWC; ++j) gv[m][j] = gvn[m][j];
-        qo[m] = qon[m];
-      }
       qs = qsn;
       ql = qln;
     }
@@ -675,7 +670,9 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS>::NT, 1)
     __syncthreads();
     if (last_s) {
       __threadfence();
-      finalize_block(a.tile_partials, geo.ntiles, st, a.norm_hist);
+      int64_t n_rows, row_len;
+      partial_rows(geo, n_rows, row_len);
+      finalize_block(a.tile_partials, n_rows, row_len, st, a.norm_hist);
     }
   }
 }

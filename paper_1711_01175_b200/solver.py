@@ -775,50 +775,160 @@ class DeviceSolver:
 class DistributedSweeper:
     """Strip-partitioned iHDG-II over torch.distributed ranks (one GPU each).
 
-    Per sweep: halo exchange of the boundary layers (NCCL send/recv over
-    NVLink), the fused sweep kernel with finalize off, an all-gather of the
-    tile partials, and the fixed-order finalize on every rank, so every rank
-    derives the same device-side convergence flag.
+    Per sweep:
+      - halo: the face-node entries of the first / last local layer that the
+        neighbouring ranks read (partition.halo_entries) are packed on the
+        device, exchanged with NCCL send/recv (NVLink), and unpacked into the
+        ghost layers;
+      - the sweep kernel, finalize off.  With ``overlap`` the interior layers
+        (which read no ghost) are launched first and the halo runs on a side
+        stream meanwhile (local solves overlap the
+        communication); the two boundary layers follow it as one-layer strips;
+      - the layer sums of the tile partials (ihdg_layer_sums) are written into
+        this rank's slice of a zeroed global array and all-reduced (one
+        non-zero term per layer, so the sum is exact for any strip sizes),
+        then every rank applies the fixed-order finalize (ihdg_finalize), so
+        every rank derives the same device status and the norms are
+        bit-identical to one rank.
     """
 
     def __init__(self, solver: DeviceSolver, rank: int, world: int, group=None,
-                 host_staging: bool = False):
-        """``host_staging``: exchange halos and partials through host memory
+                 host_staging: bool = False, overlap: bool = True):
+        """``host_staging``: exchange halos and layer sums through host memory
         (gloo); used to test this path with several ranks on one GPU."""
+        from .partition import halo_entries
+
         self.sv, self.rank, self.world, self.group = solver, rank, world, group
         self.host_staging = host_staging
         torch = solver.torch
-        self.ntiles_rank = solver.ntiles
-        self.global_partials = torch.zeros(self.ntiles_rank * world, dtype=torch.float64,
-                                           device=solver.device)
-        self.periodic_last = bool(solver.mesh.periodic[solver.mesh.dim - 1])
-        self.nlay = solver.layers[1] - solver.layers[0]
+        sv = solver
+        d = sv.mesh.dim
+        if d < 2:
+            raise NotImplementedError("strip partitions are defined for 2D / 3D meshes (layers of the slowest axis)")
+        self.nlay = sv.layers[1] - sv.layers[0]
+        self.nlay_global = int(sv.mesh.cells[d - 1])
+        self.segs = sv.ntiles // self.nlay
+        self.layer_sums = torch.zeros(self.nlay_global, dtype=torch.float64, device=sv.device)
+        self.periodic_last = bool(sv.mesh.periodic[d - 1])
+        self.overlap = bool(overlap) and self.nlay >= 3
+        self.comm_stream = torch.cuda.Stream(sv.device) if self.overlap else None
+        self.idx, self.send, self.recv = {}, {}, {}
+        for direction in ("to_lower", "to_upper"):
+            ent = halo_entries(sv.spec, direction)
+            self.idx[direction] = torch.as_tensor(ent, dtype=torch.int32, device=sv.device) if ent else None
+            n = max(len(ent), 1)
+            self.send[direction] = torch.zeros((sv.ls, n), dtype=torch.float64, device=sv.device)
+            self.recv[direction] = torch.zeros((sv.ls, n), dtype=torch.float64, device=sv.device)
 
-    def _exchange(self):
-        from .partition import halo_exchange
+    # -- halo ----------------------------------------------------------------
+    def _halo_args(self, direction, layer, packed):
+        sv = self.sv
+        h = N.HaloArgs()
+        h.g = sv.geom
+        h.buf, h.packed = _ptr(sv.u[sv.cur]), _ptr(packed)
+        h.idx, h.n_idx, h.layer = _ptr(self.idx[direction]), int(self.idx[direction].numel()), layer
+        return h
+
+    def _exchange(self, stream=None):
+        """Ghost layers of the current iterate from the neighbouring ranks.
+        My first layer goes to the lower rank (entries "to_lower"), my last to
+        the upper rank ("to_upper"); I receive the lower rank's last layer into
+        ghost_lo and the upper rank's first layer into ghost_hi."""
+        import torch.distributed as dist
+        from .partition import halo_plan
 
         sv = self.sv
-        halo_exchange(sv.u[sv.cur], sv.ls, self.nlay, self.rank, self.world, self.periodic_last,
-                      self.group, host_staging=self.host_staging)
+        sp = C.c_void_p(stream.cuda_stream) if stream is not None else sv._sptr
+        plan = halo_plan(self.rank, self.world, self.periodic_last)
+        for _, sdir, _, _ in plan:
+            if self.idx[sdir] is not None:
+                layer = 1 if sdir == "to_lower" else 2
+                N.check(sv.L.ihdg_halo_pack(C.byref(self._halo_args(sdir, layer, self.send[sdir])), sp),
+                        "ihdg_halo_pack")
+        if self.host_staging:
+            (stream or sv.stream).synchronize()
+        ops = []
+        staged = {}
+        for peer, sdir, rdir, _ in plan:
+            if self.idx[sdir] is not None:
+                t = self.send[sdir].cpu() if self.host_staging else self.send[sdir]
+                ops.append(dist.P2POp(dist.isend, t, peer, self.group))
+            if self.idx[rdir] is not None:
+                t = torch_cpu_zeros_like(self.recv[rdir]) if self.host_staging else self.recv[rdir]
+                staged[rdir] = t
+                ops.append(dist.P2POp(dist.irecv, t, peer, self.group))
+        if ops:
+            for req in dist.batch_isend_irecv(ops):
+                req.wait()
+        for _, _, rdir, layer in plan:
+            if self.idx[rdir] is not None:
+                if self.host_staging:
+                    self.recv[rdir].copy_(staged[rdir])
+                N.check(sv.L.ihdg_halo_unpack(C.byref(self._halo_args(rdir, layer, self.recv[rdir])), sp),
+                        "ihdg_halo_unpack")
+
+    # -- one sweep -----------------------------------------------------------
+    def _sub_args(self, a: N.SweepArgs, l0: int, l1: int) -> N.SweepArgs:
+        """Sweep args of local layers [l0, l1) as a strip of its own: the
+        buffers shifted by l0 layers, so its ghost rows are the neighbouring
+        local layers (or the true ghosts at the strip ends)."""
+        sv = self.sv
+        b = N.SweepArgs.from_buffer_copy(a)
+        b.g.layer_begin, b.g.layer_end = sv.layers[0] + l0, sv.layers[0] + l1
+        lsz = sv.ls * sv.nv * 8
+        b.u_old, b.u_new = a.u_old + l0 * lsz, a.u_new + l0 * lsz
+        b.s = a.s + l0 * lsz
+        b.tile_partials = a.tile_partials + l0 * self.segs * 8
+        if a.q_store:
+            b.q_store = a.q_store + l0 * sv.ls * sv.gram_kc * 8
+        return b
 
     def sweep(self, a: N.SweepArgs) -> None:
         import torch.distributed as dist
 
         sv = self.sv
-        self._exchange()
+        torch = sv.torch
         a.u_old, a.u_new = _ptr(sv.u[sv.cur]), _ptr(sv.u[1 - sv.cur])
-        N.check(sv.L.ihdg_sweep(C.byref(a), sv._sptr), "ihdg_sweep")
-        if self.host_staging:
-            parts = [torch_cpu_zeros_like(sv.partials) for _ in range(self.world)]
-            dist.all_gather(parts, sv.partials.cpu(), group=self.group)
-            self.global_partials.copy_(sv.torch.cat(parts))
+        if self.overlap:
+            # interior layers first (no ghost reads), the halo meanwhile
+            main = sv.stream
+            inner = self._sub_args(a, 1, self.nlay - 1)
+            self.comm_stream.wait_stream(main)          # the previous sweep wrote u_old
+            N.check(sv.L.ihdg_sweep(C.byref(inner), sv._sptr), "ihdg_sweep (interior)")
+            with torch.cuda.stream(self.comm_stream):
+                self._exchange(self.comm_stream)
+            main.wait_stream(self.comm_stream)
+            for l0 in (0, self.nlay - 1):
+                b = self._sub_args(a, l0, l0 + 1)
+                N.check(sv.L.ihdg_sweep(C.byref(b), sv._sptr), "ihdg_sweep (boundary layer)")
         else:
-            dist.all_gather_into_tensor(self.global_partials, sv.partials, group=self.group)
+            self._exchange()
+            N.check(sv.L.ihdg_sweep(C.byref(a), sv._sptr), "ihdg_sweep")
+        lb = sv.layers[0]
+        self.layer_sums.zero_()
+        N.check(sv.L.ihdg_layer_sums(_ptr(sv.partials), self.nlay, self.segs,
+                                     _ptr(self.layer_sums) + lb * 8, sv._sptr), "ihdg_layer_sums")
+        if self.host_staging:
+            t = self.layer_sums.cpu()
+            dist.all_reduce(t, group=self.group)
+            self.layer_sums.copy_(t)
+        else:
+            dist.all_reduce(self.layer_sums, group=self.group)
         f = N.FinalizeArgs()
-        f.tile_partials, f.n_tiles = _ptr(self.global_partials), self.global_partials.numel()
+        f.tile_partials, f.n_tiles, f.row_len = _ptr(self.layer_sums), self.nlay_global, 1
         f.state, f.norm_hist = _ptr(sv.state_dev), _ptr(sv.norm_hist)
         N.check(sv.L.ihdg_finalize(C.byref(f), sv._sptr), "ihdg_finalize")
         sv.cur = 1 - sv.cur
+
+    def launches_per_sweep(self) -> int:
+        """Kernels of this library per sweep: the sweep (3 with overlap),
+        halo packs and unpacks, layer sums, finalize (NCCL's own not counted)."""
+        from .partition import halo_plan
+
+        n = 3 if self.overlap else 1
+        for _, sdir, rdir, _ in halo_plan(self.rank, self.world, self.periodic_last):
+            n += (self.idx[sdir] is not None) + (self.idx[rdir] is not None)
+        return n + 2
 
     def begin_step(self) -> None:
         self.sv.begin_step(exchange=self._exchange)
@@ -827,6 +937,8 @@ class DistributedSweeper:
         sv = self.sv
         sv.reset_state(tol, max_iters)
         a = sv.sweep_args(norm, finalize=0)
+        a.u_old, a.u_new = _ptr(sv.u[sv.cur]), _ptr(sv.u[1 - sv.cur])
+        kernel = N.sweep_kernel(a)
         start = sv.cur
         launched = 0
         t0 = time.perf_counter()
@@ -841,4 +953,4 @@ class DistributedSweeper:
         sv.cur = (start + st.iters) % 2
         norms = sv.norm_hist[: st.iters].cpu().numpy().copy()
         return IterResult(st.iters, N.STATUS_NAMES[st.status], norms, st.first_norm, st.last_norm,
-                          launched, sec)
+                          launched, sec, kernel=kernel)

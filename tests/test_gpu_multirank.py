@@ -1,12 +1,13 @@
 """The strip-partitioned device path (solver.DistributedSweeper) with two
 ranks sharing cuda:0.
 
-The ranks use the gloo backend with host staging of the halo layers and
-tile partials, so no kernel ever waits on another rank.  The NCCL variant
-differs only in the transport call.  The sweep kernels, the ghost-layer
-addressing, the all-gather of tile partials and the fixed-order finalize are
-the same.  For an even split the result must be bit-identical to one rank:
-same iteration count, same norms, same fields.
+The ranks use the gloo backend with host staging of the packed halo entries
+and the layer sums, so no kernel ever waits on another rank.  The NCCL
+variant differs only in the transport call.  The sweep kernels (interior
+layers first, boundary layers after the halo, or one launch), the halo
+pack / unpack kernels, the layer sums and the fixed-order finalize are the
+same.  For any split -- uneven ones included -- the result must be
+bit-identical to one rank: same iteration count, same norms, same fields.
 """
 
 import os
@@ -43,7 +44,7 @@ def _setup(wl, layers=None):
     return sv
 
 
-def _worker(rank, world, port, cfg, kw, q):
+def _worker(rank, world, port, cfg, kw, overlap, q):
     import torch
     import torch.distributed as dist
 
@@ -59,19 +60,24 @@ def _worker(rank, world, port, cfg, kw, q):
         wl = make_config(cfg, seed=1, **kw)
         layers = strip_range(wl.mesh.cells[-1], rank, world)
         sv = _setup(wl, layers)
-        ds = DistributedSweeper(sv, rank, world, host_staging=True)
+        ds = DistributedSweeper(sv, rank, world, host_staging=True, overlap=overlap)
+        assert ds.overlap == (overlap and sv.layers[1] - sv.layers[0] >= 3)
         res = ds.iterate(tol=1e-10, max_iters=5000, norm="volume", batch=8)
         q.put((rank, layers, res.iterations, res.status, res.norms, sv.get_state()))
     finally:
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("cfg,kw", [
-    (3, dict(cells=16, n_steps=1)),            # periodic shallow water (wrap across ranks)
-    (5, dict(cells=32, kappa=1e-1, n_steps=1)),  # convection-diffusion p=6, 9 operator classes
-    (4, dict(cells=8)),                        # 3D transport
+@pytest.mark.parametrize("cfg,kw,world,overlap", [
+    (3, dict(cells=16, n_steps=1), 2, True),             # periodic shallow water (wrap across ranks)
+    (3, dict(cells=16, n_steps=1), 3, False),            # uneven strips 6/5/5
+    (5, dict(cells=32, kappa=1e-1, n_steps=1), 2, True),  # convection-diffusion p=6, 9 operator classes
+    (5, dict(cells=32, kappa=1e-1, n_steps=1), 3, True),  # uneven strips 11/11/10
+    (5, dict(cells=32, kappa=1e-3, n_steps=1), 2, False),
+    (4, dict(cells=8), 2, True),                         # 3D transport (no data goes downstream)
+    (4, dict(cells=8), 3, False),                        # 3/3/2 layers
 ])
-def test_two_ranks_bit_identical_to_one(cfg, kw):
+def test_ranks_bit_identical_to_one(cfg, kw, world, overlap):
     import torch
     import torch.multiprocessing as mp
 
@@ -90,10 +96,10 @@ def test_two_ranks_bit_identical_to_one(cfg, kw):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, cfg, kw, q)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, cfg, kw, overlap, q)) for r in range(world)]
     for p in procs:
         p.start()
-    out = sorted([q.get(timeout=600) for _ in range(2)], key=lambda x: x[0])
+    out = sorted([q.get(timeout=600) for _ in range(world)], key=lambda x: x[0])
     for p in procs:
         p.join(timeout=120)
         assert p.exitcode == 0

@@ -1,7 +1,7 @@
 #!/usr/bin/env python
 """Time N sweeps of one BASELINE config (for ncu captures and A/B runs).
 
-    python tools/sweep_cfg.py <config 1-5> [n_sweeps] [warmup]
+    python tools/sweep_cfg.py <config 1-5> [n_sweeps] [warmup] [nogram]
 """
 import os
 import sys
@@ -19,6 +19,8 @@ def main():
     warm = int(sys.argv[3]) if len(sys.argv) > 3 else 3
     wl = make_config(cfg)
     sv = DeviceSolver(wl.mesh, wl.problem, wl.ops, dt=wl.dt, max_iters=100000)
+    if "nogram" in sys.argv[4:]:
+        sv.gram_kc = 0
     if getattr(wl.problem, "forcing", None) is not None:
         sv.set_forcing(wl.problem.forcing)
     sv.zero_state()

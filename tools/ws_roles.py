@@ -1,7 +1,8 @@
 #!/usr/bin/env python
 """Per-role cycle breakdown of the warp-specialised sweep (profiling build).
 
-    IHDG_LIB=paper_1711_01175_b200/libihdg_cuda_prof.so python tools/ws_roles.py [cells]
+    tools/build_flags.sh ablib/prof.so -DIHDG_WS_PROF
+    IHDG_LIB=ablib/prof.so python tools/ws_roles.py [config] [nogram]
 """
 import ctypes
 import os
@@ -25,6 +26,8 @@ def main():
     cfg = int(sys.argv[1]) if len(sys.argv) > 1 else 5
     wl = make_config(cfg)
     sv = DeviceSolver(wl.mesh, wl.problem, wl.ops, dt=wl.dt, max_iters=1000)
+    if "nogram" in sys.argv[2:]:
+        sv.gram_kc = 0
     if getattr(wl.problem, "forcing", None) is not None:
         sv.set_forcing(wl.problem.forcing)
     for name, fld in wl.initial.items():
