@@ -61,7 +61,7 @@ from typing import Optional
 import numpy as np
 
 from .basis import ElementOperators
-from .pde import ConvectionDiffusionProblem, ShallowWaterProblem, TransportProblem
+from .pde import ConvectionDiffusionProblem, ShallowWaterProblem, TransportProblem, stabilization
 
 __all__ = ["OperatorSpec", "build_spec", "OPS"]
 
@@ -329,8 +329,8 @@ def build_spec(mesh, problem, ops: ElementOperators, dt=None, norm="auto", schem
                 a, s = divmod(f, 2)
                 sgn = 1.0 if s else -1.0
                 bn = beta[a] * sgn
-                alpha = np.sqrt(bn * bn + 4.0)
-                tau = 0.5 * (alpha - bn)
+                st = stabilization(problem, bn)   # alpha, tau at this face
+                alpha, tau = float(st.alpha), float(st.tau)
                 cp = 0.5 * (alpha + bn)
                 if mk & (1 << f):
                     terms.vol(ci, A_T, U, a, sgn * Jf[a], axis=a, op=E(s))
