@@ -51,64 +51,21 @@ class IterResult:
     kernel: str = ""                      # sweep kernel ihdg_sweep dispatched to (ihdg_sweep_kernel)
 
 
-class DeviceSolver:
-    """Factor-once local operators + ping-pong iterate buffers on one GPU.
+class AssembledOperators:
+    """K1 (ihdg_assemble) for one OperatorSpec on one device: the factor-once
+    local systems of every operator class -- A, A^-1,
+    the lifted L = A^-1 B, P = A^-1 R, and the Crank-Nicolson / Dirichlet-data
+    lifted operators when the spec has them.  Shared by DeviceSolver (the
+    sweep) and local_solvers (the per-element API)."""
 
-    ``layers`` = (begin, end) range of the slowest axis owned by this rank
-    (strip partition, SURVEY.md 8e); default the whole mesh.
-    """
-
-    def __init__(self, mesh, problem, ops: ElementOperators, dt=None, layers=None,
-                 device=None, max_iters: int = 100000, spec: Optional[OperatorSpec] = None,
-                 scheme: str = "iHDG-II", time_scheme: str = "BE"):
+    def __init__(self, spec: OperatorSpec, device=None, stream=None):
         torch = _torch()
-        L = N.lib()
-        self.torch = torch
-        self.L = L
-        self.mesh, self.problem, self.ops, self.dt = mesh, problem, ops, dt
-        self.spec = spec if spec is not None else build_spec(mesh, problem, ops, dt, scheme=scheme,
-                                                             time_scheme=time_scheme)
-        sp = self.spec
-        d = mesh.dim
-        if not L.ihdg_supported(d, ops.p, sp.ncomp):
-            raise NotImplementedError(f"no sweep kernel for dim={d}, p={ops.p}, m={sp.ncomp}")
+        self.torch, self.L, self.spec = torch, N.lib(), spec
         self.device = torch.device("cuda", torch.cuda.current_device() if device is None else device)
-        nlay = mesh.cells[d - 1]
-        lb, le = (0, nlay) if layers is None else (int(layers[0]), int(layers[1]))
-        self.layers = (lb, le)
-        g = N.Geom()
-        g.dim, g.order, g.ncomp = d, ops.p, sp.ncomp
-        for a in range(3):
-            g.cells[a] = mesh.cells[a] if a < d else 1
-            g.periodic[a] = int(mesh.periodic[a]) if a < d else 0
-        g.layer_begin, g.layer_end = lb, le
-        self.geom = g
-        self.ls = int(np.prod(mesh.cells[: d - 1])) if d > 1 else 1
-        self.nloc = (le - lb) * self.ls
-        self.nv = sp.nv
-        self.np_ = sp.n_nodes
-        self.ntiles = int(L.ihdg_tile_count(C.byref(g)))
-        if self.ntiles < 1:
-            raise RuntimeError("ihdg_tile_count failed")
-        self.max_iters = int(max_iters)
-        dev = self.device
-        f64 = torch.float64
-        with torch.cuda.device(dev):
-            self.stream = torch.cuda.current_stream(dev)
+        with torch.cuda.device(self.device):
+            self.stream = stream if stream is not None else torch.cuda.current_stream(self.device)
             self._assemble()
-            npad = self.nloc + 2 * self.ls
-            self.u = [torch.zeros((npad, self.nv), dtype=f64, device=dev) for _ in range(2)]
-            self.cur = 0
-            self.s = torch.zeros((self.nloc, self.nv), dtype=f64, device=dev)
-            self.s_static = None
-            self.partials = torch.zeros(self.ntiles, dtype=f64, device=dev)
-            self.state_dev = torch.zeros(C.sizeof(N.IterState), dtype=torch.uint8, device=dev)
-            self.norm_hist = torch.zeros(self.max_iters, dtype=f64, device=dev)
-            self.chol = torch.as_tensor(ops.chol1d.copy(), dtype=f64, device=dev)
-            self.class_of_mask = torch.as_tensor(sp.class_of_mask, device=dev)
-            self._setup_gram()
 
-    # -- setup -------------------------------------------------------------
     @property
     def _sptr(self):
         return C.c_void_p(self.stream.cuda_stream)
@@ -192,6 +149,77 @@ class DeviceSolver:
         N.check(self.L.ihdg_assemble(C.byref(b), self._sptr), what)
         self.stream.synchronize()
         return LT
+
+
+
+class DeviceSolver:
+    """Factor-once local operators + ping-pong iterate buffers on one GPU.
+
+    ``layers`` = (begin, end) range of the slowest axis owned by this rank
+    (strip partition, SURVEY.md 8e); default the whole mesh.
+    """
+
+    def __init__(self, mesh, problem, ops: ElementOperators, dt=None, layers=None,
+                 device=None, max_iters: int = 100000, spec: Optional[OperatorSpec] = None,
+                 scheme: str = "iHDG-II", time_scheme: str = "BE"):
+        torch = _torch()
+        L = N.lib()
+        self.torch = torch
+        self.L = L
+        self.mesh, self.problem, self.ops, self.dt = mesh, problem, ops, dt
+        self.spec = spec if spec is not None else build_spec(mesh, problem, ops, dt, scheme=scheme,
+                                                             time_scheme=time_scheme)
+        sp = self.spec
+        d = mesh.dim
+        if not L.ihdg_supported(d, ops.p, sp.ncomp):
+            raise NotImplementedError(f"no sweep kernel for dim={d}, p={ops.p}, m={sp.ncomp}")
+        self.device = torch.device("cuda", torch.cuda.current_device() if device is None else device)
+        nlay = mesh.cells[d - 1]
+        lb, le = (0, nlay) if layers is None else (int(layers[0]), int(layers[1]))
+        self.layers = (lb, le)
+        g = N.Geom()
+        g.dim, g.order, g.ncomp = d, ops.p, sp.ncomp
+        for a in range(3):
+            g.cells[a] = mesh.cells[a] if a < d else 1
+            g.periodic[a] = int(mesh.periodic[a]) if a < d else 0
+        g.layer_begin, g.layer_end = lb, le
+        self.geom = g
+        self.ls = int(np.prod(mesh.cells[: d - 1])) if d > 1 else 1
+        self.nloc = (le - lb) * self.ls
+        self.nv = sp.nv
+        self.np_ = sp.n_nodes
+        self.ntiles = int(L.ihdg_tile_count(C.byref(g)))
+        if self.ntiles < 1:
+            raise RuntimeError("ihdg_tile_count failed")
+        self.max_iters = int(max_iters)
+        dev = self.device
+        f64 = torch.float64
+        with torch.cuda.device(dev):
+            self.stream = torch.cuda.current_stream(dev)
+            self._assemble()
+            npad = self.nloc + 2 * self.ls
+            self.u = [torch.zeros((npad, self.nv), dtype=f64, device=dev) for _ in range(2)]
+            self.cur = 0
+            self.s = torch.zeros((self.nloc, self.nv), dtype=f64, device=dev)
+            self.s_static = None
+            self.partials = torch.zeros(self.ntiles, dtype=f64, device=dev)
+            self.state_dev = torch.zeros(C.sizeof(N.IterState), dtype=torch.uint8, device=dev)
+            self.norm_hist = torch.zeros(self.max_iters, dtype=f64, device=dev)
+            self.chol = torch.as_tensor(ops.chol1d.copy(), dtype=f64, device=dev)
+            self.class_of_mask = torch.as_tensor(sp.class_of_mask, device=dev)
+            self._setup_gram()
+
+    # -- setup -------------------------------------------------------------
+    @property
+    def _sptr(self):
+        return C.c_void_p(self.stream.cuda_stream)
+
+    def _assemble(self):
+        """K1 through AssembledOperators; the class operators become attributes."""
+        ops = AssembledOperators(self.spec, self.device, self.stream)
+        self.assembled = ops
+        for name in ("A", "Ainv", "AinvT", "B", "R", "LT", "PT", "min_pivot", "LT_expl", "LT_dir", "LT_dir_expl"):
+            setattr(self, name, getattr(ops, name))
 
     def _setup_gram(self) -> None:
         """Gram-form stopping norm of the interior operator class (ihdg.h,
