@@ -233,6 +233,13 @@ typedef struct {
   const double* gram_R;       /* [gram_kc][gram_kc] row-major upper-triangular R of the interior class, kernel column order (coupled faces ascending, face nodes) */
   int32_t gram_kc;            /* ihdg_sweep_gram_kc(args), 0 = off */
   int32_t pad2;
+  /* Progressive layer sums (k_sweep_ws; both NULL = off): the CTA that
+   * writes the last tile partial of an element layer (per-layer arrival
+   * counter) reduces that layer's row of partials (the inner sums of
+   * ihdg_finalize's order) into layer_sums and resets the counter, so the
+   * fused finalize only sums the layer sums instead of every tile partial. */
+  double* layer_sums;         /* [n_layers_local] */
+  uint32_t* layer_cnt;        /* [n_layers_local], zero before the first sweep; left zero by every sweep */
 } ihdg_sweep_args;
 
 /* K5: ||u - u^e||_{L2(Omega)}^2 per tile by (p+2)^d Gauss quadrature

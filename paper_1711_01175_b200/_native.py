@@ -80,7 +80,8 @@ class SweepArgs(C.Structure):
                 ("coupled", _i32 * 6), ("out_face", _i32 * 6), ("norm_kind", _i32),
                 ("finalize", _i32), ("tile_offset", _i64), ("chol", _f64 * 64),
                 ("own_w", (_f64 * 4) * 6), ("scheme", _i32), ("pad1", _i32),
-                ("q_store", _p), ("gram_R", _p), ("gram_kc", _i32), ("pad2", _i32)]
+                ("q_store", _p), ("gram_R", _p), ("gram_kc", _i32), ("pad2", _i32),
+                ("layer_sums", _p), ("layer_cnt", _p)]
 
 
 class FinalizeArgs(C.Structure):

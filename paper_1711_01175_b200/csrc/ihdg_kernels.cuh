@@ -36,9 +36,32 @@ __device__ inline double rows_sum(const double* parts, int64_t n_rows, int64_t r
   __shared__ double red[256];
   __syncthreads();
   const int lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  constexpr int RB = 8;   // rows of one virtual lane loaded together (independent loads in flight)
   for (int v = threadIdx.x >> 5; v < 256; v += nw) {
     double s = 0.0;
-    for (int64_t r = v; r < n_rows; r += 256) s += warp_row_sum(parts + r * row_len, row_len, lane);
+    for (int64_t r0 = v; r0 < n_rows; r0 += 256 * RB) {
+      // warp_row_sum of rows r0, r0 + 256, ..., batched: same per-lane order
+      // and butterfly, so the value equals k_layer_sums' bit for bit
+      double rs[RB];
+#pragma unroll
+      for (int j = 0; j < RB; ++j) rs[j] = 0.0;
+      for (int64_t i = lane; i < row_len; i += 32) {
+        double x[RB];
+#pragma unroll
+        for (int j = 0; j < RB; ++j) {
+          const int64_t r = r0 + 256 * (int64_t)j;
+          x[j] = r < n_rows ? __ldcg(parts + r * row_len + i) : 0.0;
+        }
+#pragma unroll
+        for (int j = 0; j < RB; ++j) rs[j] += x[j];
+      }
+#pragma unroll
+      for (int j = 0; j < RB; ++j) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) rs[j] += __shfl_xor_sync(0xffffffffu, rs[j], o);
+        if (r0 + 256 * (int64_t)j < n_rows) s += rs[j];
+      }
+    }
     if (lane == 0) red[v] = s;
   }
   __syncthreads();

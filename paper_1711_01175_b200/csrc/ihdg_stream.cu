@@ -47,9 +47,13 @@ cudaError_t launch_stream_t(const ihdg_sweep_args* a, cudaStream_t st) {
 
 template <int N1, int M, int NCF, int NWC, int E, int NS>
 cudaError_t launch_ws_t(const ihdg_sweep_args* a, cudaStream_t st) {
-  using C = WCfg<N1, M, NCF, NWC, E, NS>;
   static_assert(E == Cfg<2, N1, M>::TE, "ws tile must equal the generic tile (tile partial count)");
-  return launch_persistent<k_sweep_ws<N1, M, NCF, NWC, E, NS>>(C::NT, C::BYTES, E, a, st);
+  if (a->q_store != nullptr && a->gram_kc == NCF * N1) {   // Gram-form norm instantiation
+    using C = WCfg<N1, M, NCF, NWC, E, NS, true>;
+    return launch_persistent<k_sweep_ws<N1, M, NCF, NWC, E, NS, true>>(C::NT, C::BYTES, E, a, st);
+  }
+  using C = WCfg<N1, M, NCF, NWC, E, NS, false>;
+  return launch_persistent<k_sweep_ws<N1, M, NCF, NWC, E, NS, false>>(C::NT, C::BYTES, E, a, st);
 }
 
 template <int D, int N1, int M, int NCF, int NWC, int NS, int NCW, int PF, int NQW>

@@ -90,7 +90,7 @@ __device__ __forceinline__ double norm_units_swz(const double* __restrict__ dbuf
   return acc;
 }
 
-template <int N1, int M, int NCF, int NWC, int E, int NS>
+template <int N1, int M, int NCF, int NWC, int E, int NS, bool GRAM = false>
 struct WCfg {
   static constexpr int D = 2;
   static constexpr int NP = N1 * N1;
@@ -118,7 +118,7 @@ struct WCfg {
   static constexpr int QT = E * KC;
   // stage: s tile, u^k tile, q (neighbour face scalars), dq = q^k - q^{k-1}
   // (Gram-form norm), the last two in the consumers' column order
-  static constexpr int STAGE = 2 * TILE + HALO + 2 * QT;
+  static constexpr int STAGE = 2 * TILE + HALO + (GRAM ? 2 : 1) * QT;
   // Gram-form norm ||R dq||^2: R is KC x KC upper triangular, so row tile rt
   // of R touches k-steps 2 rt .. KS-1; one (row tile, element group) item per
   // consumer warp, the heavy items on the last warps (lightest contraction)
@@ -153,10 +153,13 @@ struct WCfg {
   static_assert(BYTES + 4096 <= 232448, "shared memory (dynamic + static) over the sm_100a opt-in limit");
 };
 
-template <int N1, int M, int NCF, int NWC, int E, int NS>
-__global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS>::NT, 1)
+// GRAM: the instantiation that stores q and takes the Gram-form norm from the
+// second sweep of a solve on (ihdg.h, q_store); without it the code is the
+// direct-norm kernel only (no q stores, no dq slots in the stages).
+template <int N1, int M, int NCF, int NWC, int E, int NS, bool GRAM>
+__global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS, GRAM>::NT, 1)
     k_sweep_ws(const ihdg_sweep_args a) {
-  using C = WCfg<N1, M, NCF, NWC, E, NS>;
+  using C = WCfg<N1, M, NCF, NWC, E, NS, GRAM>;
   constexpr int D = 2, NP = C::NP, NV = C::NV, NF = C::NF, NFACE = 4, KC = C::KC;
   constexpr int NRT = C::NRT, KS = C::KS, NEG = C::NEG, NCW = C::NCW, RTW = C::RTW, UPW = C::UPW;
   constexpr int NQW = C::NQW, TILE = C::TILE;
@@ -245,8 +248,29 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS>::NT, 1)
   // the stored q^{k-1} is used from the second sweep of a solve on (the
   // last CTA's finalize of the previous launch wrote iters; no CTA of this
   // launch can finalize before every CTA has read it)
-  const bool qsave = a.q_store != nullptr && a.gram_kc == KC;
-  const bool gram = qsave && a.gram_R != nullptr && st->iters > 0;
+  constexpr bool qsave = GRAM;   // dispatch guarantees q_store / gram_kc
+  const bool lsum = a.layer_sums != nullptr && a.layer_cnt != nullptr;
+  const int segs = (int)geo.segs;
+  // tile partial written (one lane): count it against its layer; returns the
+  // layer if this was the layer's last tile (its row is now complete)
+  auto layer_arrive = [&](int tile) -> int {
+    if (!lsum) return -1;
+    __threadfence();
+    const int row = tile / segs;
+    const unsigned old = atomicAdd(&a.layer_cnt[row], 1u);
+    return old == (unsigned)(segs - 1) ? row : -1;
+  };
+  // the whole warp: reduce a complete layer row (warp_row_sum, the order of
+  // the fused finalize / k_layer_sums) and re-arm its counter
+  auto layer_reduce = [&](int row, int ln) {
+    __threadfence();
+    const double rs = warp_row_sum(a.tile_partials + (int64_t)row * segs, segs, ln);
+    if (ln == 0) {
+      a.layer_sums[row] = rs;
+      a.layer_cnt[row] = 0u;
+    }
+  };
+  const bool gram = GRAM && a.gram_R != nullptr && st->iters > 0;
   V3_T0(tk0);
   int n_my = 0;  // tiles of this CTA
   for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) ++n_my;
@@ -296,7 +320,8 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS>::NT, 1)
         bulk_g2s(sst, a.s + (int64_t)e0 * NV, bytes, &full_bar[stage]);
         bulk_g2s(ust, uo + (int64_t)e0 * NV, bytes, &full_bar[stage]);
         // the stored q^{k-1} of the tile (consumer column order) into the dq slot
-        if (gram) bulk_g2s(ust + TILE + C::HALO + C::QT, a.q_store + (int64_t)tile * C::QT, qbytes, &full_bar[stage]);
+        if constexpr (GRAM)
+          if (gram) bulk_g2s(ust + TILE + C::HALO + C::QT, a.q_store + (int64_t)tile * C::QT, qbytes, &full_bar[stage]);
       }
       if (IHDG_WS_PF > 0 && lane == 0 && it + IHDG_WS_PF < n_my) {
         // tile it+PF will be copied into a stage PF tiles from now: pull it into L2
@@ -413,30 +438,39 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS>::NT, 1)
           }
           const int qi = ws_qcol<C::NEG>(t) * KC + k;
           qst[qi] = v;
-          if (gram) dqst[qi] = v - dqst[qi];
-          if (qsave) __stcs(qdst + qi, v);   // q store: the stage's column order
+          if constexpr (GRAM) {
+            if (gram) dqst[qi] = v - dqst[qi];
+            __stcs(qdst + qi, v);   // q store: the stage's column order
+          }
         }
       }
-      if (gram) fence_proxy_async();   // dq overwrote a TMA destination; the stage is refilled by TMA
+      if constexpr (GRAM)
+        if (gram) fence_proxy_async();   // dq overwrote a TMA destination; the stage is refilled by TMA
       __syncwarp();
       V3_ACC(2, tq);
       if (lane == 0) mbar_arrive(&qready_bar[stage]);
       if (it >= 1) {
         const int pb = (it - 1) & 1;
         mbar_wait(&done_bar[pb], ((it - 1) >> 1) & 1);
-        if (pw == 0 && lane == 0) {
-          bulk_s2g(un + (int64_t)prev_e0 * NV, out_s + pb * TILE, (uint32_t)(prev_nt * NV * sizeof(double)));
-          bulk_commit();
-          const int jt = it - 1 - C::LAG;   // every warp has reduced tile jt by done(it-1)
-          if (jt >= 0) {
-            double s = 0.0;
-            for (int w = 0; w < NCW; ++w) s += red_s[(jt % C::NRED) * 32 + w];
-            a.tile_partials[hist[jt & 3]] = a.jac * s;
+        if (pw == 0) {
+          int row_done = -1;
+          if (lane == 0) {
+            bulk_s2g(un + (int64_t)prev_e0 * NV, out_s + pb * TILE, (uint32_t)(prev_nt * NV * sizeof(double)));
+            bulk_commit();
+            const int jt = it - 1 - C::LAG;   // every warp has reduced tile jt by done(it-1)
+            if (jt >= 0) {
+              double s = 0.0;
+              for (int w = 0; w < NCW; ++w) s += red_s[(jt % C::NRED) * 32 + w];
+              a.tile_partials[hist[jt & 3]] = a.jac * s;
+              row_done = layer_arrive(hist[jt & 3]);
+            }
+            if (it >= 2) {
+              bulk_wait_read<1>();                       // store of tile it-2 has read its buffer
+              mbar_arrive(&outfree_bar[it & 1]);
+            }
           }
-          if (it >= 2) {
-            bulk_wait_read<1>();                       // store of tile it-2 has read its buffer
-            mbar_arrive(&outfree_bar[it & 1]);
-          }
+          row_done = __shfl_sync(0xffffffffu, row_done, 0);
+          if (row_done >= 0) layer_reduce(row_done, lane);
         }
       }
       hist[it & 3] = cur_tile;
@@ -455,16 +489,22 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS>::NT, 1)
     if (n_my >= 1) {
       const int L = n_my - 1;
       mbar_wait(&done_bar[L & 1], (L >> 1) & 1);
-      if (pw == 0 && lane == 0) {
-        bulk_s2g(un + (int64_t)prev_e0 * NV, out_s + (L & 1) * TILE, (uint32_t)(prev_nt * NV * sizeof(double)));
-        bulk_commit();
-        const int jt = L - C::LAG;
-        if (jt >= 0) {
-          double s = 0.0;
-          for (int w = 0; w < NCW; ++w) s += red_s[(jt % C::NRED) * 32 + w];
-          a.tile_partials[hist[jt & 3]] = a.jac * s;
+      if (pw == 0) {
+        int row_done = -1;
+        if (lane == 0) {
+          bulk_s2g(un + (int64_t)prev_e0 * NV, out_s + (L & 1) * TILE, (uint32_t)(prev_nt * NV * sizeof(double)));
+          bulk_commit();
+          const int jt = L - C::LAG;
+          if (jt >= 0) {
+            double s = 0.0;
+            for (int w = 0; w < NCW; ++w) s += red_s[(jt % C::NRED) * 32 + w];
+            a.tile_partials[hist[jt & 3]] = a.jac * s;
+            row_done = layer_arrive(hist[jt & 3]);
+          }
+          bulk_wait<0>();
         }
-        bulk_wait<0>();
+        row_done = __shfl_sync(0xffffffffu, row_done, 0);
+        if (row_done >= 0) layer_reduce(row_done, lane);
       }
     }
   } else {
@@ -647,13 +687,19 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS>::NT, 1)
   }
 
   __syncthreads();
-  if (tid == 0) {
+  if (warp == 0) {
     // the last LAG tiles (the prep warp wrote the partials before them)
     for (int jn = n_my - C::LAG > 0 ? n_my - C::LAG : 0; jn < n_my; ++jn) {
       if (jn <= n_my - 1 - C::LAG) continue;
-      double s = 0.0;
-      for (int w = 0; w < NCW; ++w) s += red_s[(jn % C::NRED) * 32 + w];
-      a.tile_partials[blockIdx.x + jn * gridDim.x] = a.jac * s;
+      int row_done = -1;
+      if (lane == 0) {
+        double s = 0.0;
+        for (int w = 0; w < NCW; ++w) s += red_s[(jn % C::NRED) * 32 + w];
+        a.tile_partials[blockIdx.x + jn * gridDim.x] = a.jac * s;
+        row_done = layer_arrive(blockIdx.x + jn * gridDim.x);
+      }
+      row_done = __shfl_sync(0xffffffffu, row_done, 0);
+      if (row_done >= 0) layer_reduce(row_done, lane);
     }
   }
 #ifdef IHDG_WS_PROF
@@ -672,7 +718,10 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS>::NT, 1)
       __threadfence();
       int64_t n_rows, row_len;
       partial_rows(geo, n_rows, row_len);
-      finalize_block(a.tile_partials, n_rows, row_len, st, a.norm_hist);
+      if (lsum)   // the layer sums are the rows' inner sums: the same order, one value per row
+        finalize_block(a.layer_sums, n_rows, 1, st, a.norm_hist);
+      else
+        finalize_block(a.tile_partials, n_rows, row_len, st, a.norm_hist);
     }
   }
 }

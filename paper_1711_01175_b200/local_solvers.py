@@ -270,8 +270,15 @@ def apply_local(system: LocalSystem, snapshot: TraceSnapshot, forcing=None, prev
         um = np.asarray(prev_level, dtype=float).reshape(nv)[sp.time_comp0 * npn: sp.time_comp0 * npn + sp.nr]
         _apply_one(aops, sp, c, aops.PT[c], sp.nr, torch.as_tensor(np.ascontiguousarray(um), device=dev), out, acc)
         acc = 1
-    _apply_one(aops, sp, c, aops.LT[c], sp.kin, torch.as_tensor(q, device=dev), out, acc)
-    if aops.LT_dir is not None and np.any(qd != 0.0):
-        _apply_one(aops, sp, c, aops.LT_dir[c], sp.kin, torch.as_tensor(qd, device=dev), out, 1)
+    # the lifted couplings face by face (a column block of L per face: K4
+    # takes at most NV columns per call)
+    for LTc, qq in ((aops.LT[c], q), (aops.LT_dir[c] if aops.LT_dir is not None else None, qd)):
+        if LTc is None:
+            continue
+        for f in range(2 * d):
+            seg = qq[f * nf:(f + 1) * nf]
+            if np.any(seg != 0.0):     # out starts at zero: accumulating is exact
+                _apply_one(aops, sp, c, LTc.view(-1)[f * nf * nv:(f + 1) * nf * nv], nf,
+                           torch.as_tensor(np.ascontiguousarray(seg), device=dev), out, 1)
     aops.stream.synchronize()
     return out.cpu().numpy().reshape(sp.ncomp, npn)

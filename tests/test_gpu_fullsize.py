@@ -112,7 +112,7 @@ def test_config5_full_mesh_sweeps():
 
     K = 3
     wl = make_config(5)
-    sv = DeviceSolver(wl.mesh, wl.problem, wl.ops, dt=wl.dt, max_iters=K)
+    sv = DeviceSolver(wl.mesh, wl.problem, wl.ops, dt=wl.dt, max_iters=K, gram_norm=True)   # sweeps 2-3: Gram norm
     for name, fld in wl.initial.items():
         sv.set_state_component(fld, sv.spec.labels.index(name))
     u0_dev = sv.get_state()

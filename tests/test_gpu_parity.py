@@ -279,7 +279,7 @@ def test_gram_norm_matches_direct(cfg, cells, kw):
     try:
         out = []
         for gram in (True, False):
-            sv = DeviceSolver(wl.mesh, wl.problem, wl.ops, dt=wl.dt)
+            sv = DeviceSolver(wl.mesh, wl.problem, wl.ops, dt=wl.dt, gram_norm=True)
             assert sv.gram_kc == 4 * (wl.ops.p + 1)
             if not gram:
                 sv.gram_kc = 0

@@ -14,12 +14,12 @@ if [ "${2:-}" != "skip-tests" ]; then
 fi
 timeout 1200 python bench.py > $O/${TAG}_bench.json 2> $O/${TAG}_bench.err
 timeout 600 python bench.py --impl reference > $O/${TAG}_bench_reference.json 2> $O/${TAG}_bench_reference.err
-CMD="python bench.py --steps 20 --warmup 3 --ttc-steps 0 --no-e2e --no-cpu --no-others"
+CMD="python bench.py --steps 20 --warmup 3 --ttc --no-e2e --no-cpu --no-others"
 if timeout 300 $CMD > $O/${TAG}_bench_short.json 2>&1; then
   timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
     --log-file $O/${TAG}_launches.csv $CMD > $O/${TAG}_ncu_launches.log 2>&1
 fi
-CMD3="python bench.py --steps 3 --warmup 3 --ttc-steps 0 --no-e2e --no-cpu --no-others"
+CMD3="python bench.py --steps 3 --warmup 3 --ttc --no-e2e --no-cpu --no-others"
 if timeout 300 $CMD3 > $O/${TAG}_bench_short3.json 2>&1; then
   timeout 1200 ncu --set full --clock-control none --import-source on -k regex:^k_sweep_ws -s 2 -c 1 \
     -o $O/${TAG}_ws_full -f $CMD3 > $O/${TAG}_ncu_full.log 2>&1

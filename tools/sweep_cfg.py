@@ -1,7 +1,7 @@
 #!/usr/bin/env python
 """Time N sweeps of one BASELINE config (for ncu captures and A/B runs).
 
-    python tools/sweep_cfg.py <config 1-5> [n_sweeps] [warmup] [nogram]
+    python tools/sweep_cfg.py <config 1-5> [n_sweeps] [warmup] [gram] [nofin]
 """
 import os
 import sys
@@ -18,9 +18,7 @@ def main():
     n = int(sys.argv[2]) if len(sys.argv) > 2 else 20
     warm = int(sys.argv[3]) if len(sys.argv) > 3 else 3
     wl = make_config(cfg)
-    sv = DeviceSolver(wl.mesh, wl.problem, wl.ops, dt=wl.dt, max_iters=100000)
-    if "nogram" in sys.argv[4:]:
-        sv.gram_kc = 0
+    sv = DeviceSolver(wl.mesh, wl.problem, wl.ops, dt=wl.dt, max_iters=100000, gram_norm="gram" in sys.argv[4:])
     if getattr(wl.problem, "forcing", None) is not None:
         sv.set_forcing(wl.problem.forcing)
     sv.zero_state()
@@ -31,7 +29,7 @@ def main():
     else:
         sv.prepare_steady()
     sv.reset_state(0.0, 100000)
-    a = sv.sweep_args("volume", 1)
+    a = sv.sweep_args("volume", 0 if "nofin" in sys.argv[4:] else 1)
     for _ in range(warm):
         sv.sweep_once(a=a)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)

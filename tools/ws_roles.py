@@ -2,7 +2,7 @@
 """Per-role cycle breakdown of the warp-specialised sweep (profiling build).
 
     tools/build_flags.sh ablib/prof.so -DIHDG_WS_PROF
-    IHDG_LIB=ablib/prof.so python tools/ws_roles.py [config] [nogram]
+    IHDG_LIB=ablib/prof.so python tools/ws_roles.py [config] [gram]
 """
 import ctypes
 import os
@@ -25,9 +25,7 @@ NAMES = ["producer: wait (empty/done)", "prep: wait full", "prep: q compute", "c
 def main():
     cfg = int(sys.argv[1]) if len(sys.argv) > 1 else 5
     wl = make_config(cfg)
-    sv = DeviceSolver(wl.mesh, wl.problem, wl.ops, dt=wl.dt, max_iters=1000)
-    if "nogram" in sys.argv[2:]:
-        sv.gram_kc = 0
+    sv = DeviceSolver(wl.mesh, wl.problem, wl.ops, dt=wl.dt, max_iters=1000, gram_norm="gram" in sys.argv[2:])
     if getattr(wl.problem, "forcing", None) is not None:
         sv.set_forcing(wl.problem.forcing)
     for name, fld in wl.initial.items():
