@@ -35,6 +35,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 BYTES_PER_DOF = 24  # read u^k, read s, write u^{k+1} (fp64), SURVEY.md 8d
+FP64_DMMA_PEAK = 37.1  # TF/s, mma.sync m8n8k4 f64 on this pool's B200 (profiles/r01_fp64_peak_microbench.txt)
 
 
 def _peaks():
@@ -364,10 +365,17 @@ def run_ours(args):
             tms = eo0.elapsed_time(eo1) / nrep
             dofs_o = so.nloc * so.nv
             ach = BYTES_PER_DOF * dofs_o / (tms / 1e3) / 1e9
+            # fp64 tensor-pipe view (north_star: the shared-operator case is a
+            # dense contraction): 2 K_in flop per DOF (lifted solve, norm excluded)
+            kin = int(sum(so.spec.coupled[: 2 * wo.mesh.dim])) * so.spec.n1 ** (wo.mesh.dim - 1)
+            tfl = 2.0 * kin * dofs_o / (tms / 1e3) / 1e12
             others[f"config{cfg}"] = {
                 "workload": wo.name, "dofs": int(dofs_o), "ms_per_sweep": tms,
                 "dof_updates_per_s": dofs_o / (tms / 1e3), "roofline_frac": ach / _peaks()[0],
-                "kernel": "stream" if sv.L.ihdg_stream_variant(__import__("ctypes").byref(ao)) else "generic"}
+                "fp64_tensor": {"flop_per_dof": 2 * kin, "achieved_tflops": tfl, "peak_tflops": FP64_DMMA_PEAK,
+                                "frac": tfl / FP64_DMMA_PEAK,
+                                "peak_kind": "measured DMMA microbenchmark (profiles/r01_fp64_peak_microbench.txt)"},
+                "kernel": N.sweep_kernel(ao)}
             del so
             torch.cuda.empty_cache()
     cpu = None
@@ -395,8 +403,7 @@ def run_ours(args):
             "time_to_converge": ttc or None,
             "e2e": e2e,
             "cpu_baseline": cpu,
-            "kernel": "sm_100a warp-specialised TMA/DMMA sweep" if sv.L.ihdg_stream_variant(
-                __import__("ctypes").byref(a)) else "generic sweep",
+            "kernel": N.sweep_kernel(a),
             "other_configs": others or None,
         }
         print(json.dumps(line), flush=True)

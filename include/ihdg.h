@@ -120,7 +120,9 @@ typedef struct {
   int32_t n_ops;
   int32_t n_terms;
   int32_t nr;              /* R columns (n_time_comp * (p+1)^d), may be 0 */
-  int32_t pad0;
+  int32_t kin_blocks;      /* B column blocks per face (face nodes each): 0/1 = one neighbour
+                              scalar, 2 = raw neighbour values of 2 components (per-element
+                              operators), 4 = + the element's own 2 (iHDG-I) */
   const double* ops1d;     /* [n_ops][N1][N1] row-major (device) */
   const int32_t* op_ncols; /* [n_ops], N1 or 1 (column vector) (device) */
   const int32_t* terms;    /* [n_terms][8] = class,target,row_comp,col_block,op0,op1,op2,unused (device) */
@@ -149,7 +151,7 @@ typedef struct {
   int32_t in_ghost;           /* in is ghost-padded */
   int32_t out_ghost;          /* out is ghost-padded */
   int32_t accumulate;         /* out += ... instead of out = ... */
-  int32_t pad0;
+  int32_t per_element;        /* 1: operator class = local element index (per-element operators) */
 } ihdg_class_apply_args;
 
 /* Analytic fields evaluated at the tensor points of every local element:
@@ -233,13 +235,23 @@ typedef struct {
   const double* gram_R;       /* [gram_kc][gram_kc] row-major upper-triangular R of the interior class, kernel column order (coupled faces ascending, face nodes) */
   int32_t gram_kc;            /* ihdg_sweep_gram_kc(args), 0 = off */
   int32_t pad2;
-  /* Progressive layer sums (k_sweep_ws; both NULL = off): the CTA that
-   * writes the last tile partial of an element layer (per-layer arrival
-   * counter) reduces that layer's row of partials (the inner sums of
-   * ihdg_finalize's order) into layer_sums and resets the counter, so the
-   * fused finalize only sums the layer sums instead of every tile partial. */
+  /* Parallel finalize (k_sweep_ws with finalize = 1; both NULL = the
+   * single-CTA finalize): the kernel is launched cooperatively, every CTA
+   * reduces a share of the element-layer rows of the tile partials into
+   * layer_sums after a grid barrier on grid_bar, and the last CTA sums the
+   * layer sums -- the order of ihdg_finalize, so the norms are identical. */
   double* layer_sums;         /* [n_layers_local] */
-  uint32_t* layer_cnt;        /* [n_layers_local], zero before the first sweep; left zero by every sweep */
+  uint32_t* grid_bar;         /* [2] (arrival count, generation), zero before first use; left reusable */
+  /* Per-element operators ("GEMV mode", variable coefficients, SURVEY.md 8f
+   * row 1; generic kernel): the operator class of a local element is its
+   * index, and with raw_blocks > 0 the neighbour data are raw face-node
+   * values instead of weighted scalars: column (f, j, n) of LT holds
+   * u_src[raw_comp[f][j]][node n of the shared face] with src = the
+   * neighbour across f (j < 2) or the element itself (j >= 2, iHDG-I), so
+   * LT is [Nel_local][2d * raw_blocks * (p+1)^(d-1)][NV]. */
+  int32_t per_element;
+  int32_t raw_blocks;         /* 0 (weighted scalars), 2 or 4 */
+  int32_t raw_comp[IHDG_MAX_FACE][4];
 } ihdg_sweep_args;
 
 /* K5: ||u - u^e||_{L2(Omega)}^2 per tile by (p+2)^d Gauss quadrature

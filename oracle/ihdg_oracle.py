@@ -226,6 +226,30 @@ class _Element:
     def mass(self):
         return self.Phi.T @ (self.W[:, None] * self.Phi)
 
+    # physical points of an element with lower corner x0 (variable coefficients)
+    def _grid(self, x0, per_axis):
+        d = self.d
+        n = [len(v) for v in per_axis]
+        pts = np.zeros((int(np.prod(n)), d))
+        idx = np.indices(n[::-1]).reshape(d, -1)[::-1]     # axis 0 fastest
+        for a in range(d):
+            pts[:, a] = np.asarray(per_axis[a])[idx[a]]
+        return pts
+
+    def vol_points(self, x0):
+        return self._grid(x0, [x0[a] + 0.5 * self.h[a] * (self.b.qx + 1.0) for a in range(self.d)])
+
+    def face_points(self, x0, f, nodes=False):
+        a, s = divmod(f, 2)
+        ref = self.b.nodes if nodes else self.b.qx
+        axes = [np.array([x0[c] + (self.h[c] if s else 0.0)]) if c == a
+                else x0[c] + 0.5 * self.h[c] * (ref + 1.0) for c in range(self.d)]
+        return self._grid(x0, axes)
+
+    def Qw(self, a, w):
+        """Q with a pointwise weight at the volume quadrature points: (w phi_j, d_a phi_i)_K."""
+        return self.dPhi[a].T @ ((self.W * w)[:, None] * self.Phi)
+
     def Q(self, a):
         """Q[i, j] = (phi_j, d_a phi_i)_K."""
         return self.dPhi[a].T @ (self.W[:, None] * self.Phi)
@@ -239,7 +263,15 @@ def _blocks(m, npn):
     return [slice(c * npn, (c + 1) * npn) for c in range(m)]
 
 
-def local_operators(prob: OracleProblem, el: _Element, mask: int, dt=None, scheme: str = "II"):
+def _beta_at(prob, pts):
+    """beta at physical points: constant vector or callable beta(x) -> (n, d)."""
+    b = prob.beta
+    if callable(b):
+        return np.asarray(b(pts), dtype=float).reshape(len(pts), -1)
+    return np.broadcast_to(np.asarray(b, dtype=float), (len(pts), len(b)))
+
+
+def local_operators(prob: OracleProblem, el: _Element, mask: int, dt=None, scheme: str = "II", x0=None):
     """A (own, LHS), N[f] (neighbour iterate-k -> RHS), R (time level -> RHS),
     H_own[f], H_nbr[f] (trace at face NODES as maps of own / neighbour state),
     Own (own iterate-k -> RHS; zero for iHDG-II).
@@ -296,19 +328,23 @@ def local_operators(prob: OracleProblem, el: _Element, mask: int, dt=None, schem
                 T -= bn * el.fmass(f, P, P)
                 Hown[f] = el.Pn[f]
     elif prob.kind == "cd":
-        beta = prob.beta
+        # beta constant, or beta(x) (per-element operators, x0 = the element's
+        # lower corner): coefficients at the quadrature points
+        var = callable(prob.beta)
         U = d
+        bq = _beta_at(prob, el.vol_points(x0)) if var else None
         for a in range(d):
             A[sl[a], sl[a]] += M / prob.kappa
             A[sl[a], sl[U]] -= el.Q(a)
             A[sl[U], sl[a]] -= el.Q(a)
-            A[sl[U], sl[U]] -= beta[a] * el.Q(a)
+            A[sl[U], sl[U]] -= el.Qw(a, bq[:, a]) if var else prob.beta[a] * el.Q(a)
         A[sl[U], sl[U]] += (prob.nu + inv_dt) * M
         R[sl[U], sl[U]] = inv_dt * M
         for f in range(2 * d):
             a, s = divmod(f, 2)
             sgn = 1.0 if s else -1.0
-            bn = beta[a] * sgn
+            # beta.n at the face quadrature points (a column of row weights)
+            bn = (_beta_at(prob, el.face_points(x0, f))[:, a] * sgn)[:, None] if var else prob.beta[a] * sgn
             alpha = np.sqrt(bn * bn + 4.0)
             tm = 0.5 * (alpha - bn)          # tau^-
             tp = 0.5 * (alpha + bn)          # tau^+ (beta.n^+ = -bn)
@@ -322,10 +358,17 @@ def local_operators(prob: OracleProblem, el: _Element, mask: int, dt=None, schem
                 Ho[:, sl[U]] = (bn + tm) / alpha * P
                 Hn[:, sl[a]] = -sgn / alpha * Pn
                 Hn[:, sl[U]] = (-bn + tp) / alpha * Pn
-                Hown[f][:, sl[a]] = sgn / alpha * el.Pn[f]
-                Hown[f][:, sl[U]] = (bn + tm) / alpha * el.Pn[f]
-                Hnbr[f][:, sl[a]] = -sgn / alpha * el.Pn[fl(f)]
-                Hnbr[f][:, sl[U]] = (-bn + tp) / alpha * el.Pn[fl(f)]
+                # the same formula at the face NODES (returned trace)
+                if var:
+                    bnn = (_beta_at(prob, el.face_points(x0, f, nodes=True))[:, a] * sgn)[:, None]
+                else:
+                    bnn = bn
+                an = np.sqrt(bnn * bnn + 4.0)
+                tmn, tpn = 0.5 * (an - bnn), 0.5 * (an + bnn)
+                Hown[f][:, sl[a]] = sgn / an * el.Pn[f]
+                Hown[f][:, sl[U]] = (bnn + tmn) / an * el.Pn[f]
+                Hnbr[f][:, sl[a]] = -sgn / an * el.Pn[fl(f)]
+                Hnbr[f][:, sl[U]] = (-bnn + tpn) / an * el.Pn[fl(f)]
             # sigma_a rows: + <u_hat n_a, w>
             A[sl[a], :] += sgn * el.fmass(f, P, Ho)
             T[sl[a], :] += sgn * el.fmass(f, P, Ho)
@@ -336,8 +379,8 @@ def local_operators(prob: OracleProblem, el: _Element, mask: int, dt=None, schem
             own[:, sl[a]] += sgn * P
             own -= tm * Ho
             A[sl[U], :] += el.fmass(f, P, own)
-            T[sl[U], :] -= tm * el.fmass(f, P, Ho)
-            Nf[f][sl[U], :] += tm * el.fmass(f, P, Hn)
+            T[sl[U], :] -= el.fmass(f, P, tm * Ho)
+            Nf[f][sl[U], :] += el.fmass(f, P, tm * Hn)
     elif prob.kind == "sw":
         if d != 2:
             raise ValueError("sw is 2D")
@@ -463,13 +506,22 @@ class OracleSolver:
         self.classes = {}
         self.cls = np.zeros(self.nel, dtype=np.int32)
         masks = sorted(set(self.mask.tolist())) if prob.kind != "transport" else [0]
-        if prob.kind == "transport":
-            # the transport LHS does not depend on which faces are boundary
-            # except through inflow/outflow, which is the same on every element
-            pass
+        # variable coefficients (beta(x), convection-diffusion): one operator
+        # per element (the GEMV mode of the device); keys are element ids
+        self.per_element = callable(prob.beta)
+        if self.per_element and prob.kind != "cd":
+            raise NotImplementedError("variable beta: convection-diffusion")
+        if self.per_element:
+            e = np.arange(self.nel)
+            strides = [int(np.prod(self.cells[:a])) for a in range(d)]
+            self.x0 = np.stack([self.lo[a] + ((e // strides[a]) % self.cells[a]) * self.h[a] for a in range(d)], 1)
+            masks = list(range(self.nel))
         for ci, mk in enumerate(masks):
-            A, Nf, R, Ho, Hn, Own = local_operators(prob, self.el, mk if prob.kind != "transport" else 0, dt,
-                                                    scheme)
+            if self.per_element:
+                A, Nf, R, Ho, Hn, Own = local_operators(prob, self.el, int(self.mask[mk]), dt, scheme, x0=self.x0[mk])
+            else:
+                A, Nf, R, Ho, Hn, Own = local_operators(prob, self.el, mk if prob.kind != "transport" else 0, dt,
+                                                        scheme)
             Nx, Ownx = None, None
             if time_scheme == "CN":
                 th = np.ones(prob.m)
@@ -491,6 +543,9 @@ class OracleSolver:
             # boundary handling for transport uses the per-face masks (inflow u_ext = g = 0)
             _, _, _, Hob, _, _ = local_operators(prob, self.el, (1 << (2 * d)) - 1, dt)
             self._transport_bnd_H = Hob
+        elif self.per_element:
+            self.class_list = [self.classes[e] for e in masks]
+            self.cls = np.arange(self.nel, dtype=np.int32)
         else:
             self.class_list = [self.classes[mk] for mk in masks]
             lut = {mk: i for i, mk in enumerate(masks)}
@@ -597,8 +652,6 @@ class OracleSolver:
             if self.periodic[a]:
                 continue
             sgn = 1.0 if s else -1.0
-            bn = self.prob.beta[a] * sgn
-            tau = 0.5 * (np.sqrt(bn * bn + 4.0) - bn)
             on = np.flatnonzero(self.nbr[:, f] == BOUNDARY)
             ids = self._face_node_ids(f)
             gv = np.asarray(g(pts[on][:, ids, :].reshape(-1, d)), float).reshape(on.size, -1)
@@ -611,7 +664,18 @@ class OracleSolver:
                 g0 = np.asarray(g_old(pts[on][:, ids, :].reshape(-1, d)), float).reshape(on.size, -1)
                 val_u = 0.5 * (val + g0 @ M.T)
             self.b_inflow[on, a * self.npn:(a + 1) * self.npn] += -sgn * val
-            self.b_inflow[on, U * self.npn:(U + 1) * self.npn] += tau * val_u
+            if self.per_element:
+                # tau(x) at the face quadrature points of each boundary element
+                for i, e in enumerate(on):
+                    bq = _beta_at(self.prob, self.el.face_points(self.x0[e], f))[:, a] * sgn
+                    tq = 0.5 * (np.sqrt(bq * bq + 4.0) - bq)
+                    Mt = self.el.fmass(f, self.el.Pf[f], tq[:, None] * Vf)
+                    self.b_inflow[e, U * self.npn:(U + 1) * self.npn] += Mt @ (
+                        gv[i] if self.time_scheme != "CN" else 0.5 * (gv[i] + g0[i]))
+            else:
+                bn = self.prob.beta[a] * sgn
+                tau = 0.5 * (np.sqrt(bn * bn + 4.0) - bn)
+                self.b_inflow[on, U * self.npn:(U + 1) * self.npn] += tau * val_u
             self.inflow_nodes[f] = (on, gv)
 
     # -- sweep -------------------------------------------------------------

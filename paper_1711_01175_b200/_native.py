@@ -49,7 +49,7 @@ class IterState(C.Structure):
 
 class AssemblyArgs(C.Structure):
     _fields_ = [("dim", _i32), ("order", _i32), ("ncomp", _i32), ("n_class", _i32),
-                ("n_ops", _i32), ("n_terms", _i32), ("nr", _i32), ("pad0", _i32),
+                ("n_ops", _i32), ("n_terms", _i32), ("nr", _i32), ("kin_blocks", _i32),
                 ("ops1d", _p), ("op_ncols", _p), ("terms", _p), ("coefs", _p),
                 ("A", _p), ("Ainv", _p), ("AinvT", _p), ("B", _p), ("R", _p),
                 ("LT", _p), ("PT", _p), ("min_pivot", _p)]
@@ -58,7 +58,7 @@ class AssemblyArgs(C.Structure):
 class ClassApplyArgs(C.Structure):
     _fields_ = [("g", Geom), ("opT", _p), ("class_of_mask", _p), ("inp", _p), ("out", _p),
                 ("in_stride", _i64), ("in_offset", _i32), ("ncols", _i32), ("in_ghost", _i32),
-                ("out_ghost", _i32), ("accumulate", _i32), ("pad0", _i32)]
+                ("out_ghost", _i32), ("accumulate", _i32), ("per_element", _i32)]
 
 
 class FieldArgs(C.Structure):
@@ -81,7 +81,8 @@ class SweepArgs(C.Structure):
                 ("finalize", _i32), ("tile_offset", _i64), ("chol", _f64 * 64),
                 ("own_w", (_f64 * 4) * 6), ("scheme", _i32), ("pad1", _i32),
                 ("q_store", _p), ("gram_R", _p), ("gram_kc", _i32), ("pad2", _i32),
-                ("layer_sums", _p), ("layer_cnt", _p)]
+                ("layer_sums", _p), ("grid_bar", _p),
+                ("per_element", _i32), ("raw_blocks", _i32), ("raw_comp", (_i32 * 4) * 6)]
 
 
 class FinalizeArgs(C.Structure):

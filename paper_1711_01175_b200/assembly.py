@@ -109,6 +109,16 @@ class OperatorSpec:
     coefs_dir: Optional[np.ndarray] = None
     terms_dir_expl: Optional[np.ndarray] = None   # CN: A terms + (1 - theta) B_D terms (old-level data)
     coefs_dir_expl: Optional[np.ndarray] = None
+    # per-element operators (variable coefficients, the GEMV mode): class =
+    # element, B columns = raw face-node values of raw_comp (kin_blocks per face)
+    per_element: bool = False
+    kin_blocks: int = 1
+    raw_comp: Optional[np.ndarray] = None       # (6, 4) int32
+
+    @property
+    def kin_base(self):
+        """neighbour face scalars per element (one per face node)"""
+        return 2 * self.dim * self.n1 ** (self.dim - 1)
 
     @property
     def n1(self):
@@ -124,7 +134,7 @@ class OperatorSpec:
 
     @property
     def kin(self):
-        return 2 * self.dim * self.n1 ** (self.dim - 1)
+        return 2 * self.dim * self.n1 ** (self.dim - 1) * max(1, self.kin_blocks)
 
 
 class _Terms:
@@ -308,7 +318,7 @@ def build_spec(mesh, problem, ops: ElementOperators, dt=None, norm="auto", schem
     elif isinstance(problem, ConvectionDiffusionProblem):
         beta = problem.beta_const(d)
         if beta is None:
-            raise NotImplementedError("device path needs a constant beta (shared operator)")
+            return build_spec_variable(mesh, problem, ops, dt, scheme=scheme, time_scheme=time_scheme)
         dterms = _Terms(d) if problem.dirichlet is not None else None
         m = d + 1
         U = d
@@ -571,3 +581,185 @@ def neighbor_coupling(spec: OperatorSpec, B: np.ndarray, f: int) -> np.ndarray:
     for c in range(spec.ncomp):
         W[np.arange(nf), c * npn + idx] = spec.face_w[f, c]
     return B[:, f * nf:(f + 1) * nf] @ W
+
+
+def beta_dependence(beta, dim, lo, hi, rng_seed=0) -> list:
+    """For a callable velocity beta(x) -> (n, dim): the coordinate each
+    component depends on (None = constant), checked on random points.  The
+    per-element term lists need every component to vary along at most one
+    axis, different from its own (so div beta = 0 and the face coefficients
+    of an a-face vary along one tangential axis) -- e.g. the cdr_manufactured
+    velocity (1 + z, 1 + x, 1 + y) of PAPER.md:1664-1666."""
+    rng = np.random.default_rng(rng_seed)
+    lo, hi = np.asarray(lo, float), np.asarray(hi, float)
+    x = lo + (hi - lo) * rng.uniform(size=(64, dim))
+    b0 = np.asarray(beta(x), float).reshape(64, dim)
+    dep = []
+    for a in range(dim):
+        axes = []
+        for c in range(dim):
+            y = x.copy()
+            y[:, c] = lo[c] + (hi[c] - lo[c]) * rng.uniform(size=64)
+            if not np.allclose(np.asarray(beta(y), float).reshape(64, dim)[:, a], b0[:, a], rtol=1e-13, atol=1e-13):
+                axes.append(c)
+        if len(axes) > 1 or (axes and axes[0] == a):
+            raise NotImplementedError(f"beta component {a} depends on axes {axes}: the per-element term lists "
+                                      "need each component to vary along one axis other than its own")
+        dep.append(axes[0] if axes else None)
+    return dep
+
+
+def build_spec_variable(mesh, problem, ops: ElementOperators, dt=None, scheme: str = "iHDG-II",
+                        time_scheme: str = "BE") -> OperatorSpec:
+    """Per-element operators of convection-diffusion with a variable velocity
+    beta(x) (the GEMV mode; Table 7):
+    the same substituted local equations as the constant case
+    (ErrorDDMCD + uhatCDR, PAPER.md:1067-1077) with beta.n, alpha, tau
+    evaluated at the (p+2) Gauss points -- as weighted 1D mass matrices along
+    the axis the coefficient varies on.  Every element is its own operator
+    class; the neighbour enters through raw face-node values (sigma_a^+ and
+    u^+, 2 blocks per face; iHDG-I adds the element's own 2), because the
+    trace weights vary along the face."""
+    if time_scheme != "BE":
+        raise NotImplementedError("per-element operators: steady or backward Euler")
+    one = scheme == "iHDG-I"
+    d = mesh.dim
+    m, U = d + 1, d
+    h = mesh.h
+    J = float(np.prod(h / 2.0))
+    Jf = np.array([float(np.prod([h[b] / 2.0 for b in range(d) if b != a])) for a in range(d)])
+    jac_face = np.zeros(3)
+    jac_face[:d] = Jf
+    T0, nc0 = _ops_table(ops)
+    dep = beta_dependence(problem.beta, d, mesh.lo, mesh.hi)
+    center = 0.5 * (np.asarray(mesh.lo, float) + np.asarray(mesh.hi, float))
+    qx, qw, V = ops.quad_points, ops.quad_weights, ops.interp     # V[q, i] = l_i(x_q)
+    extra, cache = [], {}
+
+    def beta_1d(a, b, xs):
+        pts = np.tile(center, (len(xs), 1))
+        if b is not None:
+            pts[:, b] = xs
+        return np.asarray(problem.beta(pts), float).reshape(len(xs), d)[:, a]
+
+    def wop(key, wq):
+        """1D mass weighted by wq at the Gauss points: sum_q w_q wq l_i l_j."""
+        if key not in cache:
+            cache[key] = len(T0) + len(extra)
+            extra.append((V * (qw * wq)[:, None]).T @ V)
+        return cache[key]
+
+    BOUND = -1
+    nel = mesh.n_elements
+    strides = [int(np.prod(mesh.cells[:a])) for a in range(d)]
+    terms = _Terms(d)
+    dterms = _Terms(d) if problem.dirichlet is not None else None
+    blocks = 4 if one else 2
+    kinv = 1.0 / problem.kappa
+    inv_dt = 0.0 if dt is None else 1.0 / float(dt)
+
+    def E(s):
+        return E1 if s else E0
+
+    def Cc(s):
+        return C1 if s else C0
+
+    for e in range(nel):
+        idx = [(e // strides[a]) % mesh.cells[a] for a in range(d)]
+
+        def xq(b):
+            return mesh.lo[b] + (idx[b] + 0.5 * (qx + 1.0)) * h[b]
+
+        for a in range(d):
+            terms.vol(e, A_T, a, a, kinv * J)
+            terms.vol(e, A_T, a, U, -Jf[a], axis=a, op=CONVT)
+            terms.vol(e, A_T, U, a, -Jf[a], axis=a, op=CONVT)
+            b = dep[a]
+            if b is None:
+                terms.vol(e, A_T, U, U, -float(beta_1d(a, None, np.array([0.0]))[0]) * Jf[a], axis=a, op=CONVT)
+            else:
+                ops_ = [MASS] * d
+                ops_[a] = CONVT
+                ops_[b] = wop(("beta", a, b, idx[b]), beta_1d(a, b, xq(b)))
+                terms.add(e, A_T, U, U, ops_, -Jf[a])
+        terms.vol(e, A_T, U, U, problem.nu * J)
+        terms.vol(e, A_T, U, U, inv_dt * J, time=True)
+        for f in range(2 * d):
+            a, s = divmod(f, 2)
+            sgn = 1.0 if s else -1.0
+            b = dep[a]
+            boundary = (idx[a] == 0 and not s or idx[a] == mesh.cells[a] - 1 and s) and not mesh.periodic[a]
+
+            def coeffs(xs):
+                bn = sgn * beta_1d(a, b, xs)
+                al = np.sqrt(bn * bn + 4.0)
+                tau = 0.5 * (al - bn)
+                cp = 0.5 * (al + bn)
+                return bn, al, tau, cp
+
+            def face(target, rc, cb, op_a, fn, tag):
+                ops_ = [MASS] * d
+                ops_[a] = op_a
+                if b is None:
+                    val = float(fn(*coeffs(np.array([0.0])))[0])
+                    (dterms if target == "D" else terms).add(e, B_T if target in ("B", "D") else A_T, rc, cb,
+                                                             ops_, val * Jf[a])
+                else:
+                    ops_[b] = wop((tag, f, b, idx[b]), fn(*coeffs(xq(b))))
+                    (dterms if target == "D" else terms).add(e, B_T if target in ("B", "D") else A_T, rc, cb,
+                                                             ops_, Jf[a])
+
+            if boundary:
+                terms.add(e, A_T, U, a, [E(s) if c == a else MASS for c in range(d)], sgn * Jf[a])
+                face("A", U, U, E(s), lambda bn, al, tau, cp: bn + tau, "A_uu_bnd")
+                if dterms is not None:
+                    dterms.add(e, B_T, a, f, [Cc(s) if c == a else MASS for c in range(d)], -sgn * Jf[a])
+                    face("D", U, f, Cc(s), lambda bn, al, tau, cp: tau, "D_u")
+                continue
+            cb0 = f * blocks
+            if one:
+                terms.add(e, A_T, U, a, [E(s) if c == a else MASS for c in range(d)], sgn * Jf[a])
+                face("A", U, U, E(s), lambda bn, al, tau, cp: bn + tau, "A1_uu")
+            else:
+                face("A", a, a, E(s), lambda bn, al, tau, cp: 1.0 / al, "A_ss")
+                face("A", a, U, E(s), lambda bn, al, tau, cp: sgn * cp / al, "A_su")
+                face("A", U, a, E(s), lambda bn, al, tau, cp: sgn * (1.0 - tau / al), "A_us")
+                face("A", U, U, E(s), lambda bn, al, tau, cp: bn + tau - tau * cp / al, "A_uu")
+            # neighbour raw values sigma_a^+ (block 0) and u^+ (block 1):
+            # q_nbr = -sgn sigma_a^+ + tau u^+, sigma rows -sgn/alpha q, u row tau/alpha q
+            face("B", a, cb0 + 0, Cc(s), lambda bn, al, tau, cp: 1.0 / al, "B_s0")
+            face("B", a, cb0 + 1, Cc(s), lambda bn, al, tau, cp: -sgn * tau / al, "B_s1")
+            face("B", U, cb0 + 0, Cc(s), lambda bn, al, tau, cp: -sgn * tau / al, "B_u0")
+            face("B", U, cb0 + 1, Cc(s), lambda bn, al, tau, cp: tau * tau / al, "B_u1")
+            if one:
+                # iHDG-I: the element's own iterate-k trace part, q_own = sgn sigma_a + cp u
+                face("B", a, cb0 + 2, Cc(s), lambda bn, al, tau, cp: -1.0 / al, "B_s2")
+                face("B", a, cb0 + 3, Cc(s), lambda bn, al, tau, cp: -sgn * cp / al, "B_s3")
+                face("B", U, cb0 + 2, Cc(s), lambda bn, al, tau, cp: sgn * tau / al, "B_u2")
+                face("B", U, cb0 + 3, Cc(s), lambda bn, al, tau, cp: tau * cp / al, "B_u3")
+        if dt is not None:
+            terms.vol(e, R_T, U, 0, J * inv_dt)
+    T = np.concatenate([T0, np.asarray(extra).reshape(-1, ops.n1, ops.n1)]) if extra else T0
+    ncols = np.concatenate([nc0, np.full(len(extra), ops.n1, dtype=np.int32)]).astype(np.int32)
+    raw_comp = np.zeros((6, 4), dtype=np.int32)
+    coupled = np.zeros(6, dtype=np.int32)
+    for f in range(2 * d):
+        raw_comp[f] = [f // 2, U, f // 2, U]
+        coupled[f] = 1
+    comp_w = np.zeros(4)
+    comp_w[:m] = 1.0
+    terms_dir = coefs_dir = None
+    if dterms is not None:
+        keep = [i for i, r in enumerate(terms.rows) if r[1] == A_T]
+        terms_dir = np.asarray([terms.rows[i] for i in keep] + dterms.rows, dtype=np.int32).reshape(-1, 8)
+        coefs_dir = np.asarray([terms.coefs[i] for i in keep] + dterms.coefs, dtype=float)
+    tw = {k: np.zeros((3, 4)) for k in ("int_own", "int_nbr", "lo", "hi")}
+    return OperatorSpec(
+        dim=d, order=ops.p, ncomp=m, labels=problem.labels(d), n_class=nel,
+        class_masks=[], class_of_mask=np.zeros(64, dtype=np.int32), ops1d=T, op_ncols=ncols,
+        terms=np.asarray(terms.rows, dtype=np.int32).reshape(-1, 8), coefs=np.asarray(terms.coefs, dtype=float),
+        nr=ops.n_nodes if dt is not None else 0, time_comp0=U, n_time_comp=1, forcing_comp=U,
+        face_w=np.zeros((6, 4)), coupled=coupled, out_face=np.zeros(6, dtype=np.int32), out_w=np.zeros((6, 4)),
+        own_w=np.zeros((6, 4)), comp_w=comp_w, trace_w=tw, jac=J, jac_face=jac_face,
+        periodic=tuple(mesh.periodic), scheme=scheme, time_scheme=time_scheme,
+        terms_dir=terms_dir, coefs_dir=coefs_dir, per_element=True, kin_blocks=blocks, raw_comp=raw_comp)

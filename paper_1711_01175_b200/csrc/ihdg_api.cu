@@ -122,7 +122,7 @@ const Entry kEntries[] = {
     IHDG_ENTRY(2, 2, 3) IHDG_ENTRY(2, 3, 3) IHDG_ENTRY(2, 4, 3) IHDG_ENTRY(2, 5, 3) IHDG_ENTRY(2, 6, 3)
     IHDG_ENTRY(2, 7, 3)
     IHDG_ENTRY(3, 2, 1) IHDG_ENTRY(3, 3, 1) IHDG_ENTRY(3, 4, 1) IHDG_ENTRY(3, 5, 1)
-    IHDG_ENTRY(3, 2, 4) IHDG_ENTRY(3, 3, 4) IHDG_ENTRY(3, 4, 4)
+    IHDG_ENTRY(3, 2, 4) IHDG_ENTRY(3, 3, 4) IHDG_ENTRY(3, 4, 4) IHDG_ENTRY(3, 5, 4)
 };
 
 const Entry* find_entry(int D, int order, int M) {
@@ -205,7 +205,7 @@ int ihdg_assemble(const ihdg_assembly_args* a, void* stream) {
   for (int i = 0; i < dm.D; ++i) dm.NP *= dm.N1;
   dm.NF = dm.NP / dm.N1;
   dm.NV = a->ncomp * dm.NP;
-  dm.KIN = 2 * dm.D * dm.NF;
+  dm.KIN = 2 * dm.D * dm.NF * (a->kin_blocks > 1 ? a->kin_blocks : 1);
   dm.nr = a->nr;
   int* perm = nullptr;
   IHDG_CUDA_TRY(cudaMallocAsync((void**)&perm, sizeof(int) * dm.NV * a->n_class, st));

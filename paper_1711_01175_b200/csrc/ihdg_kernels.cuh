@@ -36,7 +36,10 @@ __device__ inline double rows_sum(const double* parts, int64_t n_rows, int64_t r
   __shared__ double red[256];
   __syncthreads();
   const int lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-  constexpr int RB = 8;   // rows of one virtual lane loaded together (independent loads in flight)
+#ifndef IHDG_ROWS_RB
+#define IHDG_ROWS_RB 8
+#endif
+  constexpr int RB = IHDG_ROWS_RB;   // rows of one virtual lane loaded together (independent loads in flight)
   for (int v = threadIdx.x >> 5; v < 256; v += nw) {
     double s = 0.0;
     for (int64_t r0 = v; r0 < n_rows; r0 += 256 * RB) {
@@ -106,7 +109,8 @@ __device__ inline void finalize_block(const double* parts, int64_t n_rows, int64
 template <int D, int N1, int M>
 struct SweepSmem {
   using C = Cfg<D, N1, M>;
-  static constexpr size_t doubles = (size_t)C::KIN * C::TE + 2 * (size_t)C::TE * C::NV +
+  // q: up to 4 raw blocks per face node (per-element operators, iHDG-I)
+  static constexpr size_t doubles = 4 * (size_t)C::KIN * C::TE + 2 * (size_t)C::TE * C::NV +
                                     N1 * N1 + C::TE * (2 * D + 1);
   static constexpr size_t bytes = doubles * sizeof(double);
 };
@@ -128,8 +132,11 @@ __global__ void __launch_bounds__(Cfg<D, N1, M>::NT)
   constexpr int NFACE = 2 * D;
 
   extern __shared__ __align__(16) double sm[];
-  double* q_s = sm;                 // [KIN][TE]
-  double* d_s = q_s + KIN * TE;     // [TE][NV]
+  // per-element operators with raw neighbour values (ihdg.h): kin columns
+  const int rb = a.raw_blocks > 0 ? a.raw_blocks : 1;
+  const int kin = KIN * rb;
+  double* q_s = sm;                 // [kin][TE]
+  double* d_s = q_s + 4 * KIN * TE; // [TE][NV]
   double* t_s = d_s + TE * NV;      // [TE][NV]
   double* c_s = t_s + TE * NV;      // [N1][N1]
   double* pf_s = c_s + N1 * N1;     // [TE][NFACE+1]
@@ -174,18 +181,36 @@ __global__ void __launch_bounds__(Cfg<D, N1, M>::NT)
             mask |= 1 << f;
           }
         }
-        cls_s[t] = a.class_of_mask[mask];
+        cls_s[t] = a.per_element ? (int)e : a.class_of_mask[mask];
       } else {
         cls_s[t] = -1;
       }
     }
     __syncthreads();
     if (tid == 0) {
-      int u = 1;
+      int u = !a.per_element;
       for (int t = 1; t < nt; ++t) u &= (cls_s[t] == cls_s[0]);
       uni_s = u;
     }
     // -- gather neighbour face scalars (iterate k) --------------------------
+    if (a.raw_blocks > 0) {
+      // raw face-node values (per-element operators): column (f, j, n)
+      for (int i = tid; i < kin * TE; i += NT) {
+        const int k = i / TE, t = i % TE;
+        const int f = k / (rb * NF), j = (k / NF) % rb, n = k % NF;
+        double v = 0.0;
+        if (t < nt) {
+          const int c = a.raw_comp[f][j];
+          if (j < 2) {
+            const long long nb = nb_s[t][f];
+            if (nb != NO_NBR && a.coupled[f]) v = __ldg(uo + nb * NV + c * NP + fv_s[f ^ 1][n]);
+          } else {
+            v = __ldg(uo + (e0 + t) * NV + c * NP + fv_s[f][n]);
+          }
+        }
+        q_s[i] = v;
+      }
+    } else
     for (int i = tid; i < KIN * TE; i += NT) {
       const int k = i / TE, t = i % TE;
       const int f = k / NF, n = k % NF;
@@ -227,13 +252,16 @@ __global__ void __launch_bounds__(Cfg<D, N1, M>::NT)
           for (int j = 0; j < J; ++j) acc[j] = fma(l, q_s[k * TE + gi + j * G], acc[j]);
         }
       } else if (rv) {
+        // per element (mixed classes at the boundary; every element its own
+        // operator in GEMV mode: a memory-bound stream of L)
 #pragma unroll
         for (int j = 0; j < J; ++j) {
           const int t = gi + j * G;
           if (t < nt) {
-            const double* __restrict__ Lc = a.LT + (size_t)cls_s[t] * KIN * NV + rr;
+            const double* __restrict__ Lc = a.LT + (size_t)cls_s[t] * kin * NV + rr;
             double s = acc[j];
-            for (int k = 0; k < KIN; ++k) s = fma(__ldg(Lc + (size_t)k * NV), q_s[k * TE + t], s);
+#pragma unroll 4
+            for (int k = 0; k < kin; ++k) s = fma(__ldg(Lc + (size_t)k * NV), q_s[k * TE + t], s);
             acc[j] = s;
           }
         }
@@ -389,7 +417,7 @@ __global__ void __launch_bounds__(Cfg<D, N1, M>::NT)
           int64_t nb;
           if (!geo.neighbor(e, idx, f, nb)) mask |= 1 << f;
         }
-        cls_s[t] = a.class_of_mask[mask];
+        cls_s[t] = a.per_element ? (int)e : a.class_of_mask[mask];
       } else {
         cls_s[t] = -1;
       }
@@ -400,7 +428,7 @@ __global__ void __launch_bounds__(Cfg<D, N1, M>::NT)
     }
     __syncthreads();
     if (tid == 0) {
-      int u = 1;
+      int u = !a.per_element;
       for (int t = 1; t < nt; ++t) u &= (cls_s[t] == cls_s[0]);
       uni_s = u;
     }

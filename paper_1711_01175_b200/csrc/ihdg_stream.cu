@@ -16,7 +16,8 @@ namespace ihdg {
 // Launch one persistent grid (one CTA per SM) of kernel K with BYTES of
 // dynamic shared memory; the attribute is set once per device.
 template <auto kernel>
-cudaError_t launch_persistent(int nt, size_t bytes, int tile_elems, const ihdg_sweep_args* a, cudaStream_t st) {
+cudaError_t launch_persistent(int nt, size_t bytes, int tile_elems, const ihdg_sweep_args* a, cudaStream_t st,
+                              bool cooperative = false) {
   static std::atomic<unsigned> configured{0u};   // per kernel: bit per device ordinal (< 32)
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
@@ -34,6 +35,21 @@ cudaError_t launch_persistent(int nt, size_t bytes, int tile_elems, const ihdg_s
   geo.init(a->g, tile_elems);
   int64_t grid = geo.ntiles < sms ? geo.ntiles : sms;
   if (grid < 1) grid = 1;
+  if (cooperative) {
+    // co-residency of the whole grid is guaranteed (or the launch fails):
+    // the kernel's grid barrier cannot deadlock
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)grid);
+    cfg.blockDim = dim3(nt);
+    cfg.dynamicSmemBytes = bytes;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeCooperative;
+    attr[0].val.cooperative = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kernel, *a);
+  }
   kernel<<<(unsigned)grid, nt, bytes, st>>>(*a);
   return cudaGetLastError();
 }
@@ -48,12 +64,13 @@ cudaError_t launch_stream_t(const ihdg_sweep_args* a, cudaStream_t st) {
 template <int N1, int M, int NCF, int NWC, int E, int NS>
 cudaError_t launch_ws_t(const ihdg_sweep_args* a, cudaStream_t st) {
   static_assert(E == Cfg<2, N1, M>::TE, "ws tile must equal the generic tile (tile partial count)");
+  const bool coop = a->finalize && a->layer_sums != nullptr && a->grid_bar != nullptr;   // parallel finalize
   if (a->q_store != nullptr && a->gram_kc == NCF * N1) {   // Gram-form norm instantiation
     using C = WCfg<N1, M, NCF, NWC, E, NS, true>;
-    return launch_persistent<k_sweep_ws<N1, M, NCF, NWC, E, NS, true>>(C::NT, C::BYTES, E, a, st);
+    return launch_persistent<k_sweep_ws<N1, M, NCF, NWC, E, NS, true>>(C::NT, C::BYTES, E, a, st, coop);
   }
   using C = WCfg<N1, M, NCF, NWC, E, NS, false>;
-  return launch_persistent<k_sweep_ws<N1, M, NCF, NWC, E, NS, false>>(C::NT, C::BYTES, E, a, st);
+  return launch_persistent<k_sweep_ws<N1, M, NCF, NWC, E, NS, false>>(C::NT, C::BYTES, E, a, st, coop);
 }
 
 template <int D, int N1, int M, int NCF, int NWC, int NS, int NCW, int PF, int NQW>
@@ -141,6 +158,7 @@ const StreamEntry* stream_entry(const ihdg_sweep_args* a) {
   const int impl = current_impl();
   if (impl == IMPL_GENERIC) return nullptr;
   if (a->norm_kind != IHDG_NORM_VOLUME) return nullptr;
+  if (a->per_element || a->raw_blocks > 0) return nullptr;   // per-element operators: generic kernel
   if (a->scheme != IHDG_SCHEME_II) return nullptr;   // iHDG-I: generic kernel
   const ihdg_geom& g = a->g;
   int ncf = 0, maxw = 0;

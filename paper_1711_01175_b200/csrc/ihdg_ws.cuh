@@ -249,27 +249,6 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS, GRAM>::NT, 1)
   // last CTA's finalize of the previous launch wrote iters; no CTA of this
   // launch can finalize before every CTA has read it)
   constexpr bool qsave = GRAM;   // dispatch guarantees q_store / gram_kc
-  const bool lsum = a.layer_sums != nullptr && a.layer_cnt != nullptr;
-  const int segs = (int)geo.segs;
-  // tile partial written (one lane): count it against its layer; returns the
-  // layer if this was the layer's last tile (its row is now complete)
-  auto layer_arrive = [&](int tile) -> int {
-    if (!lsum) return -1;
-    __threadfence();
-    const int row = tile / segs;
-    const unsigned old = atomicAdd(&a.layer_cnt[row], 1u);
-    return old == (unsigned)(segs - 1) ? row : -1;
-  };
-  // the whole warp: reduce a complete layer row (warp_row_sum, the order of
-  // the fused finalize / k_layer_sums) and re-arm its counter
-  auto layer_reduce = [&](int row, int ln) {
-    __threadfence();
-    const double rs = warp_row_sum(a.tile_partials + (int64_t)row * segs, segs, ln);
-    if (ln == 0) {
-      a.layer_sums[row] = rs;
-      a.layer_cnt[row] = 0u;
-    }
-  };
   const bool gram = GRAM && a.gram_R != nullptr && st->iters > 0;
   V3_T0(tk0);
   int n_my = 0;  // tiles of this CTA
@@ -452,25 +431,21 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS, GRAM>::NT, 1)
       if (it >= 1) {
         const int pb = (it - 1) & 1;
         mbar_wait(&done_bar[pb], ((it - 1) >> 1) & 1);
-        if (pw == 0) {
-          int row_done = -1;
-          if (lane == 0) {
-            bulk_s2g(un + (int64_t)prev_e0 * NV, out_s + pb * TILE, (uint32_t)(prev_nt * NV * sizeof(double)));
-            bulk_commit();
-            const int jt = it - 1 - C::LAG;   // every warp has reduced tile jt by done(it-1)
-            if (jt >= 0) {
-              double s = 0.0;
-              for (int w = 0; w < NCW; ++w) s += red_s[(jt % C::NRED) * 32 + w];
-              a.tile_partials[hist[jt & 3]] = a.jac * s;
-              row_done = layer_arrive(hist[jt & 3]);
-            }
-            if (it >= 2) {
-              bulk_wait_read<1>();                       // store of tile it-2 has read its buffer
-              mbar_arrive(&outfree_bar[it & 1]);
-            }
+        if (pw == 0 && lane == 0) {
+          bulk_s2g(un + (int64_t)prev_e0 * NV, out_s + pb * TILE, (uint32_t)(prev_nt * NV * sizeof(double)));
+          bulk_commit();
+          if (it >= 2) {
+            bulk_wait_read<1>();                       // store of tile it-2 has read its buffer
+            mbar_arrive(&outfree_bar[it & 1]);
           }
-          row_done = __shfl_sync(0xffffffffu, row_done, 0);
-          if (row_done >= 0) layer_reduce(row_done, lane);
+        }
+        if (pw == 0 && lane == 1) {
+          const int jt = it - 1 - C::LAG;   // every warp has reduced tile jt by done(it-1)
+          if (jt >= 0) {
+            double s = 0.0;
+            for (int w = 0; w < NCW; ++w) s += red_s[(jt % C::NRED) * 32 + w];
+            a.tile_partials[hist[jt & 3]] = a.jac * s;
+          }
         }
       }
       hist[it & 3] = cur_tile;
@@ -489,22 +464,16 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS, GRAM>::NT, 1)
     if (n_my >= 1) {
       const int L = n_my - 1;
       mbar_wait(&done_bar[L & 1], (L >> 1) & 1);
-      if (pw == 0) {
-        int row_done = -1;
-        if (lane == 0) {
-          bulk_s2g(un + (int64_t)prev_e0 * NV, out_s + (L & 1) * TILE, (uint32_t)(prev_nt * NV * sizeof(double)));
-          bulk_commit();
-          const int jt = L - C::LAG;
-          if (jt >= 0) {
-            double s = 0.0;
-            for (int w = 0; w < NCW; ++w) s += red_s[(jt % C::NRED) * 32 + w];
-            a.tile_partials[hist[jt & 3]] = a.jac * s;
-            row_done = layer_arrive(hist[jt & 3]);
-          }
-          bulk_wait<0>();
+      if (pw == 0 && lane == 0) {
+        bulk_s2g(un + (int64_t)prev_e0 * NV, out_s + (L & 1) * TILE, (uint32_t)(prev_nt * NV * sizeof(double)));
+        bulk_commit();
+        const int jt = L - C::LAG;
+        if (jt >= 0) {
+          double s = 0.0;
+          for (int w = 0; w < NCW; ++w) s += red_s[(jt % C::NRED) * 32 + w];
+          a.tile_partials[hist[jt & 3]] = a.jac * s;
         }
-        row_done = __shfl_sync(0xffffffffu, row_done, 0);
-        if (row_done >= 0) layer_reduce(row_done, lane);
+        bulk_wait<0>();
       }
     }
   } else {
@@ -687,19 +656,13 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS, GRAM>::NT, 1)
   }
 
   __syncthreads();
-  if (warp == 0) {
+  if (tid == 0) {
     // the last LAG tiles (the prep warp wrote the partials before them)
     for (int jn = n_my - C::LAG > 0 ? n_my - C::LAG : 0; jn < n_my; ++jn) {
       if (jn <= n_my - 1 - C::LAG) continue;
-      int row_done = -1;
-      if (lane == 0) {
-        double s = 0.0;
-        for (int w = 0; w < NCW; ++w) s += red_s[(jn % C::NRED) * 32 + w];
-        a.tile_partials[blockIdx.x + jn * gridDim.x] = a.jac * s;
-        row_done = layer_arrive(blockIdx.x + jn * gridDim.x);
-      }
-      row_done = __shfl_sync(0xffffffffu, row_done, 0);
-      if (row_done >= 0) layer_reduce(row_done, lane);
+      double s = 0.0;
+      for (int w = 0; w < NCW; ++w) s += red_s[(jn % C::NRED) * 32 + w];
+      a.tile_partials[blockIdx.x + jn * gridDim.x] = a.jac * s;
     }
   }
 #ifdef IHDG_WS_PROF
@@ -707,6 +670,50 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS, GRAM>::NT, 1)
   V3_FLUSH;
 #endif
   if (a.finalize) {
+#ifndef IHDG_WS_SIMPLE_FIN
+    if (a.layer_sums != nullptr && a.grid_bar != nullptr) {
+      // Parallel finalize (launched cooperatively: every CTA is resident).
+      // Phase 1: grid barrier on grid_bar once every tile partial is
+      // written; phase 2: CTA b reduces the rows b, b + grid, ... (warp_row_sum,
+      // one warp per row) into layer_sums; phase 3: the last CTA (ticket) sums
+      // the layer sums in the fixed order -- bit-identical to finalize_block
+      // over the tile partials.
+      int64_t n_rows, row_len;
+      partial_rows(geo, n_rows, row_len);
+      __threadfence();
+      __syncthreads();
+      if (tid == 0) {
+        volatile unsigned* bar = a.grid_bar;
+        const unsigned gen = bar[1];
+        if (atomicAdd(a.grid_bar, 1u) == gridDim.x - 1) {
+          a.grid_bar[0] = 0u;
+          __threadfence();
+          atomicAdd(a.grid_bar + 1, 1u);      // release the barrier (generation)
+        } else {
+          while (bar[1] == gen) __nanosleep(64);
+        }
+        __threadfence();
+      }
+      __syncthreads();
+      const int nw = blockDim.x >> 5;
+      for (int64_t r = (int64_t)blockIdx.x * nw + warp; r < n_rows; r += (int64_t)gridDim.x * nw) {
+        const double rs = warp_row_sum(a.tile_partials + r * row_len, row_len, lane);
+        if (lane == 0) a.layer_sums[r] = rs;
+      }
+      __threadfence();
+      __syncthreads();
+      if (tid == 0) {
+        const unsigned tk = atomicAdd(&st->ticket, 1u);
+        last_s = (tk == gridDim.x - 1);
+      }
+      __syncthreads();
+      if (last_s) {
+        __threadfence();
+        finalize_block(a.layer_sums, n_rows, 1, st, a.norm_hist);
+      }
+      return;
+    }
+#endif
     __threadfence();
     __syncthreads();
     if (tid == 0) {
@@ -718,10 +725,7 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS, GRAM>::NT, 1)
       __threadfence();
       int64_t n_rows, row_len;
       partial_rows(geo, n_rows, row_len);
-      if (lsum)   // the layer sums are the rows' inner sums: the same order, one value per row
-        finalize_block(a.layer_sums, n_rows, 1, st, a.norm_hist);
-      else
-        finalize_block(a.tile_partials, n_rows, row_len, st, a.norm_hist);
+      finalize_block(a.tile_partials, n_rows, row_len, st, a.norm_hist);
     }
   }
 }

@@ -270,7 +270,7 @@ def run(mesh, problem, ops: ElementOperators, cfg: Optional[IterationConfig] = N
     res = solver.iterate(tol=cfg.tol, max_iters=cfg.max_iters or default_max_iters(mesh),
                          norm=_norm_name(cfg, problem), batch=cfg.check_every)
     state = FieldState(solver.get_state(), solver.spec.labels, k=res.iterations) if return_state else None
-    tr = solver.trace() if (return_trace and solver.layers[0] == 0
+    tr = solver.trace() if (return_trace and not solver.spec.per_element and solver.layers[0] == 0
                             and solver.layers[1] == mesh.cells[-1]) else None
     return IterationReport(res.iterations, res.status, res.norms, time.perf_counter() - t0,
                            state, tr, res.first_norm, res.last_norm, res.launched,
@@ -382,7 +382,7 @@ def run_time_dependent(mesh, problem, ops: ElementOperators, cfg: Optional[Itera
         st = (FieldState(solver.get_state(), solver.spec.labels, k=res.iterations, m=m + 1)
               if keep else None)
         # the step's single-valued trace with every state returned
-        tr = solver.trace() if (keep and return_trace and solver.layers[0] == 0
+        tr = solver.trace() if (keep and return_trace and not solver.spec.per_element and solver.layers[0] == 0
                                 and solver.layers[1] == mesh.cells[-1]) else None
         reports.append(IterationReport(res.iterations, res.status, res.norms,
                                        time.perf_counter() - t0, st, tr, res.first_norm,

@@ -213,6 +213,34 @@ def _gauss_timedep(x, t):
     return np.exp(-5.0 * np.sum((x - 0.35 * t) ** 2, axis=1))
 
 
+def cdr_manufactured(kappa: float = 1e-2) -> "ConvectionDiffusionProblem":
+    """SPEC.md:198 / PAPER.md:1661-1666: u^e = sin(pi x) cos(pi y) sin(pi z) / pi,
+    beta = (1 + z, 1 + x, 1 + y) (div beta = 0), nu = 1, forcing
+    f = -kappa Lap u^e + beta . grad u^e + nu u^e, Dirichlet data u^e on [0,1]^3."""
+    pi = np.pi
+
+    def ue(x):
+        x = np.asarray(x, dtype=float)
+        return np.sin(pi * x[:, 0]) * np.cos(pi * x[:, 1]) * np.sin(pi * x[:, 2]) / pi
+
+    def beta(x):
+        x = np.asarray(x, dtype=float)
+        return np.stack([1.0 + x[:, 2], 1.0 + x[:, 0], 1.0 + x[:, 1]], axis=1)
+
+    def forcing(x):
+        x = np.asarray(x, dtype=float)
+        X, Y, Z = x[:, 0], x[:, 1], x[:, 2]
+        ux = np.cos(pi * X) * np.cos(pi * Y) * np.sin(pi * Z)
+        uy = -np.sin(pi * X) * np.sin(pi * Y) * np.sin(pi * Z)
+        uz = np.sin(pi * X) * np.cos(pi * Y) * np.cos(pi * Z)
+        b = beta(x)
+        u = ue(x)
+        return kappa * 3.0 * pi * pi * u + b[:, 0] * ux + b[:, 1] * uy + b[:, 2] * uz + 1.0 * u
+
+    return ConvectionDiffusionProblem(kappa=kappa, beta=beta, nu=1.0, forcing=forcing, dirichlet=ue, lam=1.0,
+                                      exact=ue)
+
+
 def preset_problems():
     """Named presets usable through the same API."""
     s2 = np.sqrt(2.0)
@@ -234,5 +262,6 @@ def preset_problems():
                 np.cos(np.pi * x[:, 0]) * np.sin(np.pi * x[:, 1]) * np.sin(s2 * np.pi * t) / s2],
                 axis=1)),
         "elliptic": ConvectionDiffusionProblem(kappa=1.0, beta=np.zeros(3), nu=1.0, lam=1.0),
+        "cdr_manufactured": cdr_manufactured(1e-2),
     }
     return cat

@@ -91,6 +91,7 @@ class AssembledOperators:
         a = N.AssemblyArgs()
         a.dim, a.order, a.ncomp, a.n_class = sp.dim, sp.order, sp.ncomp, nc
         a.n_ops, a.n_terms, a.nr = sp.ops1d.shape[0], sp.terms.shape[0], nr
+        a.kin_blocks = sp.kin_blocks
         a.ops1d, a.op_ncols = _ptr(self._ops1d), _ptr(self._opn)
         a.terms, a.coefs = _ptr(self._terms), _ptr(self._coefs)
         a.A, a.Ainv, a.AinvT, a.B = _ptr(self.A), _ptr(self.Ainv), _ptr(self.AinvT), _ptr(self.B)
@@ -139,8 +140,10 @@ class AssembledOperators:
         tt = torch.as_tensor(terms, device=self.device).contiguous()
         cc = torch.as_tensor(coefs, dtype=torch.float64, device=self.device)
         A2, Ai2, AiT2 = torch.zeros_like(self.A), torch.zeros_like(self.A), torch.zeros_like(self.A)
-        B2 = torch.zeros_like(self.B)
-        LT = torch.zeros_like(self.LT)
+        # the data couplings: one column per face node (g), whatever the main B's blocks
+        kb = sp.kin_base
+        B2 = torch.zeros((sp.n_class, sp.nv, kb), dtype=torch.float64, device=self.device)
+        LT = torch.zeros((sp.n_class, kb, sp.nv), dtype=torch.float64, device=self.device)
         mp2 = torch.zeros_like(self.min_pivot)
         b = N.AssemblyArgs()
         b.dim, b.order, b.ncomp, b.n_class = sp.dim, sp.order, sp.ncomp, sp.n_class
@@ -210,9 +213,9 @@ class DeviceSolver:
             self.norm_hist = torch.zeros(self.max_iters, dtype=f64, device=dev)
             self.chol = torch.as_tensor(ops.chol1d.copy(), dtype=f64, device=dev)
             self.class_of_mask = torch.as_tensor(sp.class_of_mask, device=dev)
-            # progressive per-layer sums of the tile partials (ihdg_sweep_args.layer_sums)
+            # parallel finalize of k_sweep_ws (ihdg_sweep_args.layer_sums / grid_bar)
             self.layer_sums = torch.zeros(max(le - lb, 1), dtype=f64, device=dev)
-            self.layer_cnt = torch.zeros(max(le - lb, 1), dtype=torch.int32, device=dev)
+            self.grid_bar = torch.zeros(2, dtype=torch.int32, device=dev)
             self.gram_kc = 0
             if gram_norm:
                 self._setup_gram()
@@ -356,6 +359,7 @@ class DeviceSolver:
         a.opT, a.class_of_mask, a.inp, a.out = _ptr(opT), _ptr(self.class_of_mask), _ptr(inp), _ptr(out)
         a.in_stride, a.in_offset, a.ncols = in_stride, in_offset, ncols
         a.in_ghost, a.out_ghost, a.accumulate = in_ghost, 0, accumulate
+        a.per_element = int(self.spec.per_element)
         N.check(self.L.ihdg_class_apply(C.byref(a), self._sptr), "ihdg_class_apply")
 
     def set_inflow(self, g, g_explicit=None) -> None:
@@ -438,7 +442,7 @@ class DeviceSolver:
         sp = self.spec
         q, faces = self._boundary_face_data(g, lambda f: True)
         nfc = q.shape[1]
-        assert sp.kin == nfc, "Dirichlet data: every face slot is coupled for convection-diffusion"
+        assert sp.kin_base == nfc, "Dirichlet data: every face slot is coupled for convection-diffusion"
         self.s_bdata = self.torch.zeros((self.nloc, self.nv), dtype=self.torch.float64, device=self.device)
         self._apply(self.LT_dir, nfc, q, nfc, 0, 0, self.s_bdata, 0)
         if self.LT_dir_expl is not None:
@@ -522,10 +526,18 @@ class DeviceSolver:
         a.finalize = finalize
         a.tile_offset = 0
         a.scheme = N.SCHEME_I if sp.scheme == "iHDG-I" else N.SCHEME_II
+        if sp.per_element:
+            # per-element operators: raw neighbour (and, iHDG-I, own) face values;
+            # the own part is a column of L, not the own_w scalar trick
+            a.per_element, a.raw_blocks = 1, int(sp.kin_blocks)
+            for f in range(6):
+                for j in range(4):
+                    a.raw_comp[f][j] = int(sp.raw_comp[f, j])
+            a.scheme = N.SCHEME_II
         if gram and getattr(self, "gram_kc", 0) > 0:
             a.q_store, a.gram_R, a.gram_kc = _ptr(self.q_store), _ptr(self.gram_R), self.gram_kc
-        if getattr(self, "layer_cnt", None) is not None and self.mesh.dim > 1:
-            a.layer_sums, a.layer_cnt = _ptr(self.layer_sums), _ptr(self.layer_cnt)
+        if getattr(self, "grid_bar", None) is not None and self.mesh.dim > 1:
+            a.layer_sums, a.grid_bar = _ptr(self.layer_sums), _ptr(self.grid_bar)
         return a
 
     def reset_state(self, tol: float, max_iters: int, diverge_factor: float = 1e6) -> None:
@@ -728,6 +740,9 @@ class DeviceSolver:
     def trace(self) -> np.ndarray:
         """Single-valued trace (n_faces, 1, N_f) in mesh.py face order; on
         inflow boundary faces with data it is g at the face nodes."""
+        if self.spec.per_element:
+            raise NotImplementedError("the single-valued trace of per-element (variable-coefficient) operators "
+                                      "varies along the face weights; not extracted on the device")
         t = self.trace_of()
         for f, (on, vals) in (getattr(self, "_bdata_faces", None) or {}).items():
             t[self.torch.as_tensor(self._face_ids(on, f), device=self.device)] = self.torch.as_tensor(
@@ -925,8 +940,7 @@ class DistributedSweeper:
         b.tile_partials = a.tile_partials + l0 * self.segs * 8
         if a.q_store:
             b.q_store = a.q_store + l0 * sv.ls * sv.gram_kc * 8
-        if a.layer_sums:
-            b.layer_sums, b.layer_cnt = a.layer_sums + l0 * 8, a.layer_cnt + l0 * 4
+        b.layer_sums = b.grid_bar = None   # sub-strips run with finalize = 0
         return b
 
     def sweep(self, a: N.SweepArgs) -> None:

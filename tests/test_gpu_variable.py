@@ -1,0 +1,115 @@
+"""Per-element operators on the device (variable coefficients, the GEMV mode;
+SURVEY.md 8f row 1): parity with the CPU oracle on cdr_manufactured (SPEC.md:198,
+beta = (1+z, 1+x, 1+y)) under iHDG-II and iHDG-I, and Table 7's iteration
+counts (SPEC.md acceptance 7)."""
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+TOL_FIELD = 1e-10
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _gpu():
+    import torch
+
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    torch.cuda.set_device(0)
+
+
+def _device(n, p, kappa, scheme, max_iters=3000):
+    from paper_1711_01175_b200.basis import build_operators
+    from paper_1711_01175_b200.iteration import IterationConfig, run
+    from paper_1711_01175_b200.mesh import build_mesh
+    from paper_1711_01175_b200.pde import cdr_manufactured
+
+    mesh = build_mesh(3, [n] * 3)
+    return run(mesh, cdr_manufactured(kappa), build_operators(p, 3, mesh.h),
+               IterationConfig(scheme=scheme, stop="exact", tol=1e-10, max_iters=max_iters))
+
+
+def _oracle(n, p, kappa, scheme, max_iters=3000):
+    from oracle.ihdg_oracle import OracleProblem, OracleSolver
+    from paper_1711_01175_b200.pde import cdr_manufactured
+
+    pr = cdr_manufactured(kappa)
+    S = OracleSolver(OracleProblem("cd", 3, beta=pr.beta, kappa=kappa, nu=pr.nu), [n] * 3, p,
+                     scheme="I" if scheme == "iHDG-I" else "II")
+    S.set_forcing(pr.forcing)
+    S.set_dirichlet(pr.dirichlet)
+    S.set_exact(pr.exact)
+    return S, S.run(tol=1e-10, norm="exact", max_iters=max_iters)
+
+
+@pytest.mark.parametrize("n,p,kappa,scheme", [(4, 2, 1e-2, "iHDG-II"), (4, 1, 1e-3, "iHDG-I"),
+                                              (2, 3, 1e-6, "iHDG-II"), (2, 2, 1e-2, "iHDG-I")])
+def test_cdr_manufactured_parity(n, p, kappa, scheme):
+    from tests.oracle_bridge import rel_l2
+
+    rep = _device(n, p, kappa, scheme)
+    S, ref = _oracle(n, p, kappa, scheme)
+    assert rep.extra["kernel"] == "k_sweep"
+    assert rep.status == ref["status"] == "converged"
+    assert rep.iterations == ref["iterations"]
+    assert rel_l2(rep.state.data.reshape(S.nel, -1), ref["u"]) < TOL_FIELD
+    assert np.allclose(rep.extra["l2_errors"], ref["errors"], rtol=1e-8, atol=0)
+
+
+def test_variable_beta_time_step_parity():
+    """2D, a variable velocity in both components, one backward-Euler step
+    (successive rule) against the oracle."""
+    from oracle.ihdg_oracle import OracleProblem, OracleSolver
+    from paper_1711_01175_b200.basis import build_operators
+    from paper_1711_01175_b200.iteration import IterationConfig, run_time_dependent
+    from paper_1711_01175_b200.mesh import build_mesh
+    from paper_1711_01175_b200.pde import ConvectionDiffusionProblem
+    from paper_1711_01175_b200.workloads import fourier_modes
+    from tests.oracle_bridge import rel_l2
+
+    def beta(x):
+        return np.stack([1 + 0.5 * np.sin(3 * x[:, 1]), -0.3 + x[:, 0] ** 2], 1)
+
+    mesh = build_mesh(2, [12, 12])
+    ops = build_operators(3, 2, mesh.h)
+    prob = ConvectionDiffusionProblem(kappa=1e-2, beta=beta, nu=0.5)
+    u0 = fourier_modes(np.random.default_rng(2), 2)
+    rep = run_time_dependent(mesh, prob, ops, IterationConfig(tol=1e-10), 0.02, n_steps=2, initial={"u": u0},
+                             keep_states=True)
+    S = OracleSolver(OracleProblem("cd", 2, beta=beta, kappa=1e-2, nu=0.5), [12, 12], 3, dt=0.02)
+    init = np.zeros((S.nel, S.m, S.npn))
+    init[:, 2, :] = S.interpolate(u0)
+    _, refs = S.run_time_dependent(init.reshape(S.nel, -1), 2, tol=1e-10)
+    assert [r.iterations for r in rep] == [r["iterations"] for r in refs]
+    for r, o in zip(rep, refs):
+        assert rel_l2(r.state.data.reshape(S.nel, -1), o["u"]) < TOL_FIELD
+
+
+# PAPER.md:1709-1739 (Table 7): (h, p) -> iHDG-II counts at kappa = 1e-2, 1e-3, 1e-6
+TABLE7_II = {(0.5, 1): (17, 17, 17), (0.25, 1): (25, 25, 26), (0.125, 1): (35, 37, 38),
+             (0.5, 2): (17, 19, 19), (0.25, 2): (27, 27, 27), (0.125, 2): (42, 43, 43),
+             (0.5, 3): (19, 19, 19), (0.25, 3): (24, 26, 27)}
+
+
+@pytest.mark.parametrize("h,p", sorted(TABLE7_II), ids=[f"h{h}_p{p}" for h, p in sorted(TABLE7_II)])
+def test_table7_ihdg2_counts(h, p):
+    """iHDG-II within +-3 of Table 7 and independent of kappa (spread <= 3)."""
+    n = int(round(1.0 / h))
+    counts = []
+    for kappa, paper in zip((1e-2, 1e-3, 1e-6), TABLE7_II[(h, p)]):
+        rep = _device(n, p, kappa, "iHDG-II")
+        assert rep.status == "converged"
+        assert abs(rep.iterations - paper) <= 3, (kappa, rep.iterations, paper)
+        counts.append(rep.iterations)
+    assert max(counts) - min(counts) <= 3
+
+
+def test_table7_ihdg1_divergence():
+    """Table 7 marks iHDG-I diverged ('*') at h = 0.125, p = 3, kappa = 1e-2,
+    and convergent at the same (h, p) for kappa = 1e-3."""
+    rep = _device(8, 3, 1e-2, "iHDG-I")
+    assert rep.status == "diverged"
+    ok = _device(8, 3, 1e-3, "iHDG-I")
+    assert ok.status == "converged"

@@ -76,3 +76,20 @@ def test_timedep_transport_forcing_is_manufactured():
                      for i in range(3)], axis=1)
     res = ut + grad @ np.asarray(tr.beta) - tr.forcing(x, t)
     assert np.max(np.abs(res)) < 1e-6
+
+
+def test_cdr_manufactured_preset():
+    """div beta = 0 (so lambda = nu = 1); the forcing is
+    kappa (-Lap u^e) + beta . grad u^e + nu u^e at sample points (central differences)."""
+    cdr = preset_problems()["cdr_manufactured"]
+    rng = np.random.default_rng(3)
+    x = rng.uniform(size=(40, 3))
+    h = 1e-4
+    div = sum((cdr.beta(x + h * np.eye(3)[i])[:, i] - cdr.beta(x - h * np.eye(3)[i])[:, i]) / (2 * h) for i in range(3))
+    assert np.max(np.abs(div)) < 1e-9 and cdr.nu == 1.0
+    lap = sum((cdr.exact(x + h * np.eye(3)[i]) - 2 * cdr.exact(x) + cdr.exact(x - h * np.eye(3)[i])) / h ** 2
+              for i in range(3))
+    grad = np.stack([(cdr.exact(x + h * np.eye(3)[i]) - cdr.exact(x - h * np.eye(3)[i])) / (2 * h)
+                     for i in range(3)], 1)
+    res = -cdr.kappa * lap + np.sum(cdr.beta(x) * grad, 1) + cdr.nu * cdr.exact(x) - cdr.forcing(x)
+    assert np.max(np.abs(res)) < 1e-5

@@ -1,7 +1,7 @@
 #!/usr/bin/env python
 """Time N sweeps of one BASELINE config (for ncu captures and A/B runs).
 
-    python tools/sweep_cfg.py <config 1-5> [n_sweeps] [warmup] [gram] [nofin]
+    python tools/sweep_cfg.py <config 1-5> [n_sweeps] [warmup] [gram] [nofin] [nolsum]
 """
 import os
 import sys
@@ -30,6 +30,8 @@ def main():
         sv.prepare_steady()
     sv.reset_state(0.0, 100000)
     a = sv.sweep_args("volume", 0 if "nofin" in sys.argv[4:] else 1)
+    if "nolsum" in sys.argv[4:]:
+        a.layer_sums = a.grid_bar = None
     for _ in range(warm):
         sv.sweep_once(a=a)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
