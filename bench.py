@@ -378,6 +378,45 @@ def run_ours(args):
                 "kernel": N.sweep_kernel(ao)}
             del so
             torch.cuda.empty_cache()
+    # ---- per-element operators (GEMV mode): Table 7's
+    # cdr_manufactured at 16^3, p=2 -- every element streams its own lifted
+    # operator L_e (NV x K_raw), the memory-bound GEMV of north_star ----
+    if args.other_configs and world == 1:
+        from paper_1711_01175_b200.basis import build_operators as _bo
+        from paper_1711_01175_b200.mesh import build_mesh as _bm
+        from paper_1711_01175_b200.pde import cdr_manufactured
+
+        gm = _bm(3, [16, 16, 16])
+        gp = cdr_manufactured(1e-3)
+        t_set = time.perf_counter()
+        sg = DeviceSolver(gm, gp, _bo(2, 3, gm.h), max_iters=1000)
+        sg.set_forcing(gp.forcing)
+        sg.set_dirichlet(gp.dirichlet)
+        sg.prepare_steady()
+        torch.cuda.synchronize()
+        setup_g = time.perf_counter() - t_set
+        sg.reset_state(tol=0.0, max_iters=1000)
+        ag = sg.sweep_args("volume", finalize=1)
+        for _ in range(3):
+            sg.sweep_once(a=ag)
+        eg0, eg1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        eg0.record(sg.stream)
+        for _ in range(20):
+            sg.sweep_once(a=ag)
+        eg1.record(sg.stream)
+        torch.cuda.synchronize()
+        tg = eg0.elapsed_time(eg1) / 20
+        kraw = sg.spec.kin
+        bpd = 8 * (kraw + 3)   # L_e row (K_raw doubles) + u^k, s, u^{k+1}: SURVEY.md 8d "8 (K_in + 3) B/DOF"
+        dofs_g = sg.nloc * sg.nv
+        others["gemv_cdr_manufactured_16^3_p2"] = {
+            "workload": "cdr_manufactured (beta=(1+z,1+x,1+y)), 16^3 hexes, p=2, per-element operators",
+            "dofs": int(dofs_g), "ms_per_sweep": tg, "dof_updates_per_s": dofs_g / (tg / 1e3),
+            "bytes_per_dof": bpd, "roofline_frac": bpd * dofs_g / (tg / 1e3) / 1e9 / _peaks()[0],
+            "setup_seconds": setup_g, "kernel": N.sweep_kernel(ag)}
+        del sg
+        torch.cuda.empty_cache()
     cpu = None
     if rank == 0 and world == 1 and args.cpu_baseline:
         threads = len(os.sched_getaffinity(0))

@@ -32,14 +32,14 @@ __device__ __forceinline__ double warp_row_sum(const double* row, int64_t len, i
 // exactly the single-rank value (ihdg_finalize with row_len 1: a one-entry
 // row sums to itself).  Every thread of the CTA must call it; blockDim.x is a
 // multiple of 32.
+// RB rows of one virtual lane are loaded together (independent loads in
+// flight); any RB gives the same value.  Small RB keeps the code small where
+// the reduction is off the hot path's instruction cache footprint (k_sweep_ws).
+template <int RB = 8>
 __device__ inline double rows_sum(const double* parts, int64_t n_rows, int64_t row_len) {
   __shared__ double red[256];
   __syncthreads();
   const int lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-#ifndef IHDG_ROWS_RB
-#define IHDG_ROWS_RB 8
-#endif
-  constexpr int RB = IHDG_ROWS_RB;   // rows of one virtual lane loaded together (independent loads in flight)
   for (int v = threadIdx.x >> 5; v < 256; v += nw) {
     double s = 0.0;
     for (int64_t r0 = v; r0 < n_rows; r0 += 256 * RB) {
@@ -85,9 +85,10 @@ __host__ __device__ inline void partial_rows(const Geo& g, int64_t& n_rows, int6
 // The stopping / divergence logic of `run` (
 // PAPER.md:1308-1311) on the fixed-order sum of the partials.  Must be
 // executed by every thread of one CTA.
+template <int RB = 8>
 __device__ inline void finalize_block(const double* parts, int64_t n_rows, int64_t row_len, ihdg_iter_state* st,
                                       double* hist) {
-  const double total = rows_sum(parts, n_rows, row_len);
+  const double total = rows_sum<RB>(parts, n_rows, row_len);
   if (threadIdx.x == 0) {
     const double norm = sqrt(total);
     const int it = st->iters + 1;

@@ -508,13 +508,16 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS, GRAM>::NT, 1)
     const int gi = NCW - 1 - warp;
     const bool has_gi = gi >= 0 && gi < C::NGI;
     const int grt = has_gi ? gi / NEG : 0, geg = has_gi ? gi - (gi / NEG) * NEG : 0;
-    double Rf[KS];
+    double Rf[GRAM ? KS : 1];
+    if constexpr (GRAM) {
 #pragma unroll
-    for (int ks = 0; ks < KS; ++ks) {
-      const int row = grt * 8 + (lane >> 2), col = 4 * ks + (lane & 3);
-      Rf[ks] = (gram && has_gi && row < KC) ? __ldg(a.gram_R + row * KC + col) : 0.0;
+      for (int ks = 0; ks < KS; ++ks) {
+        const int row = grt * 8 + (lane >> 2), col = 4 * ks + (lane & 3);
+        Rf[ks] = (gram && has_gi && row < KC) ? __ldg(a.gram_R + row * KC + col) : 0.0;
+      }
     }
-    int prev_direct = 0;   // tile it-1 took the direct norm (its delta is in d_s)
+    // tile it-1 took the direct norm (its delta is in d_s); always, without GRAM
+    int prev_direct = GRAM ? 0 : 1;
     for (int it = 0; it < n_my; ++it) {
       const int stage = it % NS;
       const int ob = it & 1;
@@ -522,13 +525,13 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS, GRAM>::NT, 1)
       mbar_wait(&qready_bar[stage], (it / NS) & 1);
       V3_ACC(3, tc);
       const int fast = mfast_s[stage];
-      const bool gtile = gram && fast;   // tile it: Gram-form norm
+      const bool gtile = GRAM && gram && fast;   // tile it: Gram-form norm
       const double* sst = sm + stage * C::STAGE;
       const double* ust = sst + TILE;
       const double* qst = ust + TILE + C::HALO;
       // direct norm of the previous tile (needs every warp's delta of tile it-1)
       double nprev = 0.0;
-      if (it >= 1 && prev_direct) {
+      if (it >= 1 && (!GRAM || prev_direct)) {
         const int jn = it - 1;
         V3_T0(td);
         mbar_wait(&done_bar[jn & 1], (jn >> 1) & 1);
@@ -590,18 +593,20 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS, GRAM>::NT, 1)
       // (comp_w and the reference mass are inside R, the Jacobian is applied
       // with the tile partial)
       double ng = 0.0;
-      if (gtile && has_gi) {
-        const double* dqb = qst + C::QT + (lane >> 2) * KC + (lane & 3) + geg * 8 * KC;
-        double y0 = 0.0, y1 = 0.0;
+      if constexpr (GRAM) {
+        if (gtile && has_gi) {
+          const double* dqb = qst + C::QT + (lane >> 2) * KC + (lane & 3) + geg * 8 * KC;
+          double y0 = 0.0, y1 = 0.0;
 #pragma unroll
-        for (int ks = 0; ks < KS; ++ks)
-          if (ks >= 2 * grt) dmma_8x8x4(y0, y1, Rf[ks], dqb[4 * ks]);
-        ng = fma(y0, y0, y1 * y1);
+          for (int ks = 0; ks < KS; ++ks)
+            if (ks >= 2 * grt) dmma_8x8x4(y0, y1, Rf[ks], dqb[4 * ks]);
+          ng = fma(y0, y0, y1 * y1);
+        }
       }
       V3_ACC(4, tm);
       // a direct tile rewrites the d_s slot of tile it-2: every warp finished
       // that tile's norm by done(it-1)
-      if (!gtile && it >= 1 && !prev_direct) mbar_wait(&done_bar[(it - 1) & 1], ((it - 1) >> 1) & 1);
+      if (GRAM && !gtile && it >= 1 && !prev_direct) mbar_wait(&done_bar[(it - 1) & 1], ((it - 1) >> 1) & 1);
       V3_T0(to);
       if (it >= 2) mbar_wait(&outfree_bar[ob], ((it - 2) >> 1) & 1);
       V3_ACC(5, to);
@@ -625,12 +630,12 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS, GRAM>::NT, 1)
         }
       }
       V3_ACC(10, te);
-      if (it >= 1 && prev_direct) {
+      if (it >= 1 && (!GRAM || prev_direct)) {
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) nprev += __shfl_xor_sync(0xffffffffu, nprev, o);
         if (lane == 0) red_s[((it - 1) % C::NRED) * 32 + warp] = nprev;
       }
-      if (gtile) {
+      if (GRAM && gtile) {
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) ng += __shfl_xor_sync(0xffffffffu, ng, o);
         if (lane == 0) red_s[(it % C::NRED) * 32 + warp] = ng;
@@ -641,10 +646,10 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS, GRAM>::NT, 1)
         mbar_arrive(&empty_bar[stage]);
         mbar_arrive(&done_bar[ob]);
       }
-      prev_direct = gtile ? 0 : 1;
+      if constexpr (GRAM) prev_direct = gtile ? 0 : 1;
     }
     // drain: direct norm of the last tile
-    if (n_my >= 1 && prev_direct) {
+    if (n_my >= 1 && (!GRAM || prev_direct)) {
       const int jn = n_my - 1;
       mbar_wait(&done_bar[jn & 1], (jn >> 1) & 1);
       double nsum = norm_units_swz<N1, M, E, NCW, UPW, C::DUE, C::DUC>(d_s + (jn % C::NDB) * C::DT, warp, lane, cfr,
@@ -709,7 +714,7 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS, GRAM>::NT, 1)
       __syncthreads();
       if (last_s) {
         __threadfence();
-        finalize_block(a.layer_sums, n_rows, 1, st, a.norm_hist);
+        finalize_block<1>(a.layer_sums, n_rows, 1, st, a.norm_hist);
       }
       return;
     }
@@ -725,7 +730,7 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS, GRAM>::NT, 1)
       __threadfence();
       int64_t n_rows, row_len;
       partial_rows(geo, n_rows, row_len);
-      finalize_block(a.tile_partials, n_rows, row_len, st, a.norm_hist);
+      finalize_block<1>(a.tile_partials, n_rows, row_len, st, a.norm_hist);
     }
   }
 }

@@ -282,7 +282,11 @@ def cfl_number(problem, mesh, p: int, dt: float) -> float:
     """CFL = |beta|_max dt (p+1)^2 / h (the DG estimate of
     PAPER.md section 4.4); |beta| is the Euclidean speed, h the smallest
     element size.  Shallow water uses the gravity-wave speed sqrt(Phi)."""
-    if hasattr(problem, "beta"):
+    if hasattr(problem, "beta") and callable(problem.beta):
+        # variable velocity: the largest speed at the element centres
+        c = np.asarray(mesh.all_element_points([np.zeros(1)] * mesh.dim), float).reshape(-1, mesh.dim)
+        speed = float(np.max(np.linalg.norm(np.asarray(problem.beta(c), float).reshape(len(c), -1), axis=1)))
+    elif hasattr(problem, "beta"):
         speed = float(np.linalg.norm(np.asarray(problem.beta, float)))
     elif hasattr(problem, "Phi"):
         speed = float(np.sqrt(problem.Phi))
