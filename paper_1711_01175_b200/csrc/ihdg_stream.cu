@@ -10,6 +10,7 @@
 #include "ihdg_stream.cuh"
 #include "ihdg_ws.cuh"
 #include "ihdg_v3.cuh"
+#include "ihdg_v4.cuh"
 
 namespace ihdg {
 
@@ -17,7 +18,7 @@ namespace ihdg {
 // dynamic shared memory; the attribute is set once per device.
 template <auto kernel>
 cudaError_t launch_persistent(int nt, size_t bytes, int tile_elems, const ihdg_sweep_args* a, cudaStream_t st,
-                              bool cooperative = false) {
+                              bool cooperative = false, int ctas_per_sm = 1) {
   static std::atomic<unsigned> configured{0u};   // per kernel: bit per device ordinal (< 32)
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
@@ -33,6 +34,7 @@ cudaError_t launch_persistent(int nt, size_t bytes, int tile_elems, const ihdg_s
   if (e != cudaSuccess) return e;
   Geo geo;
   geo.init(a->g, tile_elems);
+  sms *= ctas_per_sm;
   int64_t grid = geo.ntiles < sms ? geo.ntiles : sms;
   if (grid < 1) grid = 1;
   if (cooperative) {
@@ -80,17 +82,26 @@ cudaError_t launch_v3_t(const ihdg_sweep_args* a, cudaStream_t st) {
   return launch_persistent<k_sweep_v3<D, N1, M, NCF, NWC, NS, NCW, PF, NQW>>(C::NT, C::BYTES, 8 * PF, a, st);
 }
 
-enum Kind { KIND_V3 = 0, KIND_WS = 1, KIND_STREAM = 2 };
-const char* const kKindName[] = {"k_sweep_v3", "k_sweep_ws", "k_sweep_stream"};
+template <int FMASK, int NW, int MINB>
+cudaError_t launch_v4_t(const ihdg_sweep_args* a, cudaStream_t st) {
+  using C = V4Cfg<FMASK, NW, MINB>;
+  static_assert(8 * C::PF == Cfg<3, 4, 1>::TE, "v4 logical tile must equal the generic tile (tile partial count)");
+  return launch_persistent<k_sweep_v4<FMASK, NW, MINB>>(C::NT, C::BYTES, 8 * C::PF, a, st, false, MINB);
+}
+
+enum Kind { KIND_V3 = 0, KIND_WS = 1, KIND_STREAM = 2, KIND_V4 = 3 };
+const char* const kKindName[] = {"k_sweep_v3", "k_sweep_ws", "k_sweep_stream", "k_sweep_v4"};
 
 struct StreamEntry {
   int D, N1, M, NCF, NWC, E, NV;
   cudaError_t (*launch)(const ihdg_sweep_args*, cudaStream_t);
   int kind;
+  int fmask = -1;   // >= 0: the entry needs exactly this set of coupled faces
 };
 
 #define IHDG_V3(D, N1, M, NCF, NWC, NS, NCW, PF, NQW) \
   {D, N1, M, NCF, NWC, 8 * PF, M * Pow<N1, D>::v, launch_v3_t<D, N1, M, NCF, NWC, NS, NCW, PF, NQW>, KIND_V3},
+#define IHDG_V4(FMASK, NW, MINB) {3, 4, 1, v4_popc(FMASK), 1, 32, 64, launch_v4_t<FMASK, NW, MINB>, KIND_V4, FMASK},
 #define IHDG_WS(N1, M, NCF, NWC, E, NS) \
   {2, N1, M, NCF, NWC, E, M * N1 * N1, launch_ws_t<N1, M, NCF, NWC, E, NS>, KIND_WS},
 #define IHDG_STREAM(D, N1, M, NCF, NWC, E, NS, G) \
@@ -120,8 +131,22 @@ struct StreamEntry {
 #define IHDG_C23_NQW 8
 #endif
 
-// First match wins: v3 before ws/stream for the same (D, N1, M).
+// config-4 v4 shape (A/B builds override it): warps per CTA, CTAs per SM
+#ifndef IHDG_C4_V4_NW
+#define IHDG_C4_V4_NW 16
+#endif
+#ifndef IHDG_C4_V4_MINB
+#define IHDG_C4_V4_MINB 1
+#endif
+
+// First match wins: v4 before v3 before ws/stream for the same (D, N1, M).
 const StreamEntry kStream[] = {
+    // config 4: transport 3D p=3; one instantiation per inflow-face set (the
+    // sign pattern of beta; config 4 itself is faces 0, 2, 4 = 0x15)
+    IHDG_V4(0x15, IHDG_C4_V4_NW, IHDG_C4_V4_MINB) IHDG_V4(0x16, IHDG_C4_V4_NW, IHDG_C4_V4_MINB)
+    IHDG_V4(0x19, IHDG_C4_V4_NW, IHDG_C4_V4_MINB) IHDG_V4(0x1a, IHDG_C4_V4_NW, IHDG_C4_V4_MINB)
+    IHDG_V4(0x25, IHDG_C4_V4_NW, IHDG_C4_V4_MINB) IHDG_V4(0x26, IHDG_C4_V4_NW, IHDG_C4_V4_MINB)
+    IHDG_V4(0x29, IHDG_C4_V4_NW, IHDG_C4_V4_MINB) IHDG_V4(0x2a, IHDG_C4_V4_NW, IHDG_C4_V4_MINB)
     IHDG_V3(2, 5, 3, 4, 2, IHDG_C23_NS, IHDG_C23_NCW, 2, IHDG_C23_NQW)  // configs 2/3: CD / SW 2D p=4
     IHDG_V3(3, 4, 1, 3, 1, IHDG_C4_NS, IHDG_C4_NCW, 4, IHDG_C4_NQW)  // config 4: transport 3D p=3
     IHDG_WS(7, 3, 4, 2, 16, IHDG_WS5_NS)   // config 5: CD 2D p=6 (warp-specialised)
@@ -131,13 +156,14 @@ const StreamEntry kStream[] = {
 
 // Process-wide kernel selector (ihdg_set_sweep_impl); the initial value comes
 // from IHDG_SWEEP_IMPL so A/B tools keep working.
-enum Impl { IMPL_AUTO = 0, IMPL_NO_V3 = 1, IMPL_GENERIC = 2 };
+enum Impl { IMPL_AUTO = 0, IMPL_NO_V3 = 1, IMPL_GENERIC = 2, IMPL_V3 = 3 };
 std::atomic<int> g_impl{-1};
 
 int parse_impl(const char* s) {
   if (s == nullptr || s[0] == '\0' || std::strcmp(s, "auto") == 0) return IMPL_AUTO;
   if (std::strcmp(s, "ws") == 0 || std::strcmp(s, "stream") == 0) return IMPL_NO_V3;
   if (std::strcmp(s, "generic") == 0) return IMPL_GENERIC;
+  if (std::strcmp(s, "v3") == 0) return IMPL_V3;   // skip v4
   return -1;
 }
 
@@ -161,10 +187,11 @@ const StreamEntry* stream_entry(const ihdg_sweep_args* a) {
   if (a->per_element || a->raw_blocks > 0) return nullptr;   // per-element operators: generic kernel
   if (a->scheme != IHDG_SCHEME_II) return nullptr;   // iHDG-I: generic kernel
   const ihdg_geom& g = a->g;
-  int ncf = 0, maxw = 0;
+  int ncf = 0, maxw = 0, fmask = 0;
   for (int f = 0; f < 2 * g.dim; ++f) {
     if (!a->coupled[f]) continue;
     ++ncf;
+    fmask |= 1 << f;
     int w = 0;
     for (int c = 0; c < g.ncomp; ++c) w += a->face_w[f][c] != 0.0;
     maxw = w > maxw ? w : maxw;
@@ -172,11 +199,13 @@ const StreamEntry* stream_entry(const ihdg_sweep_args* a) {
   for (const StreamEntry& e : kStream) {
     if (e.D != g.dim || e.N1 != g.order + 1 || e.M != g.ncomp) continue;
     if (e.NCF != ncf || maxw > e.NWC) continue;
-    if (e.kind == KIND_V3 && impl == IMPL_NO_V3) continue;
+    if (e.fmask >= 0 && e.fmask != fmask) continue;
+    if ((e.kind == KIND_V3 || e.kind == KIND_V4) && impl == IMPL_NO_V3) continue;
+    if (e.kind == KIND_V4 && impl == IMPL_V3) continue;
     Geo geo;
     geo.init(g, e.E);
     if (geo.tile_len % e.E != 0) continue;                       // full tiles only
-    if (g.cells[0] % (e.kind == KIND_V3 ? 8 : e.E) != 0) continue;  // tiles inside one axis-0 row
+    if (g.cells[0] % ((e.kind == KIND_V3 || e.kind == KIND_V4) ? 8 : e.E) != 0) continue;  // tiles inside one axis-0 row
     if (geo.nloc + 2 * geo.ls >= (1LL << 31) || geo.ntiles >= (1LL << 31)) continue;  // 32-bit indices
     if ((geo.ls * e.NV * 8) % 16 != 0) continue;                  // ghost offset
     if (((uintptr_t)a->u_old | (uintptr_t)a->u_new | (uintptr_t)a->s) % 16 != 0) continue;

@@ -129,6 +129,19 @@ __device__ __forceinline__ void consumer_bar(int n) { asm volatile("bar.sync 1, 
 // element and tile counts < 2^31 and cells[0] % E == 0).  Tile = E
 // consecutive elements of one axis-0 row.  Neighbour offsets across faces of
 // axes >= 1 are the same for every element of the tile.
+// Exact unsigned division by a runtime-invariant divisor (round-up method:
+// q = (mulhi(n, m) + n) >> s for every 32-bit n); init once per kernel.
+struct FastDiv {
+  uint32_t m, s;
+  __device__ __forceinline__ void init(uint32_t d) {
+    s = d <= 1 ? 0 : 32 - __clz(d - 1);
+    m = (uint32_t)(((1ull << 32) * ((1ull << s) - d)) / d + 1ull);
+  }
+  __device__ __forceinline__ int div(int n) const {
+    return (int)(((unsigned long long)__umulhi((uint32_t)n, m) + (uint32_t)n) >> s);
+  }
+};
+
 template <int D>
 struct STile {
   int e0, nt, i0;
@@ -139,13 +152,24 @@ struct STile {
     const int c0 = (int)g.cells[0];
     const int segs0 = c0 / E;
     const int xrow = tile / segs0;
+    init_row(g, tile, xrow, D == 3 ? xrow / (int)g.cells[1] : xrow, segs0, E, nlay, ls);
+  }
+  // the same with the two divisions done by precomputed FastDiv (segs0 = c0 / E, c1)
+  __device__ __forceinline__ void init(const ihdg_geom& g, int tile, int E, int nlay, int ls, int segs0,
+                                       const FastDiv& dsegs0, const FastDiv& dc1) {
+    const int xrow = dsegs0.div(tile);
+    init_row(g, tile, xrow, D == 3 ? dc1.div(xrow) : xrow, segs0, E, nlay, ls);
+  }
+  __device__ __forceinline__ void init_row(const ihdg_geom& g, int tile, int xrow, int lay3, int segs0, int E, int nlay,
+                                           int ls) {
+    const int c0 = (int)g.cells[0];
     i0 = (tile - xrow * segs0) * E;
     e0 = xrow * c0 + i0;
     nt = E;
     int lay = xrow;      // local layer (D == 2)
     if (D == 3) {
       const int c1 = (int)g.cells[1];
-      lay = xrow / c1;
+      lay = lay3;
       const int i1 = xrow - lay * c1;
       // axis 1 (inside the layer)
       has[2] = (i1 > 0) || g.periodic[1];

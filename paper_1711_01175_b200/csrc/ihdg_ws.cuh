@@ -49,9 +49,14 @@ __device__ __forceinline__ int ws_dnode(int kk, int nn) { return kk * 8 + (nn ^ 
 
 // tensor-core norm over the swizzled delta tile: units u = warp + m NCW,
 // (element, component); sum of w_c |C^T Delta C|_F^2
+// The second product Y = R C contracts over the columns of R in the order the
+// D fragment holds them (k slot (ks, c) = column 2 c + ks, with C's rows
+// permuted alike in cfp), so R feeds the A operand straight from the
+// accumulator registers: no shuffles between the two DMMAs.
 template <int N1, int M, int E, int NCW, int UPW, int DUE, int DUC>
 __device__ __forceinline__ double norm_units_swz(const double* __restrict__ dbuf, int warp, int lane,
-                                                 const double (&cfr)[2], const double* comp_w) {
+                                                 const double (&cfr)[2], const double (&cfp)[2],
+                                                 const double* comp_w) {
   double acc = 0.0;
   double r0[UPW], r1[UPW];
 #pragma unroll
@@ -75,14 +80,8 @@ __device__ __forceinline__ double norm_units_swz(const double* __restrict__ dbuf
     const int u = warp + m * NCW;
     const int c = (u < E * M ? u : 0) % M;
     double y0 = 0.0, y1 = 0.0;
-#pragma unroll
-    for (int ks = 0; ks < 2; ++ks) {
-      const int col = 4 * ks + (lane & 3);
-      const int src = (lane & ~3) | (col >> 1);
-      const double x0 = __shfl_sync(0xffffffffu, r0[m], src);
-      const double x1 = __shfl_sync(0xffffffffu, r1[m], src);
-      dmma_8x8x4(y0, y1, (col & 1) ? x1 : x0, cfr[ks]);  // Y = R C
-    }
+    dmma_8x8x4(y0, y1, r0[m], cfp[0]);  // Y = R C, columns 2c of R
+    dmma_8x8x4(y0, y1, r1[m], cfp[1]);  // columns 2c + 1
     const double w = comp_w[c];
     acc = fma(w * y0, y0, acc);
     acc = fma(w * y1, y1, acc);
@@ -503,6 +502,12 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS, GRAM>::NT, 1)
       const int kk = 4 * ks + (lane & 3), nn = lane >> 2;
       cfr[ks] = (kk < N1 && nn < N1) ? chol_s[kk * N1 + nn] : 0.0;
     }
+    double cfp[2];   // C rows in the D-fragment column order: B[k slot c][n] = C[2 c + ks][n]
+#pragma unroll
+    for (int ks = 0; ks < 2; ++ks) {
+      const int kk = 2 * (lane & 3) + ks, nn = lane >> 2;
+      cfp[ks] = (kk < N1 && nn < N1) ? chol_s[kk * N1 + nn] : 0.0;
+    }
     // Gram-form norm item of this warp: R row tile grt x element group geg
     static_assert(C::LAG == 1, "the Gram / direct norm schedule assumes LAG = 1");
     const int gi = NCW - 1 - warp;
@@ -538,7 +543,7 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS, GRAM>::NT, 1)
         V3_ACC(8, td);
         V3_T0(tn);
         nprev = norm_units_swz<N1, M, E, NCW, UPW, C::DUE, C::DUC>(d_s + (jn % C::NDB) * C::DT, warp, lane, cfr,
-                                                                   a.comp_w);
+                                                                   cfp, a.comp_w);
         V3_ACC(7, tn);
       }
       V3_T0(tm);
@@ -653,7 +658,7 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS, GRAM>::NT, 1)
       const int jn = n_my - 1;
       mbar_wait(&done_bar[jn & 1], (jn >> 1) & 1);
       double nsum = norm_units_swz<N1, M, E, NCW, UPW, C::DUE, C::DUC>(d_s + (jn % C::NDB) * C::DT, warp, lane, cfr,
-                                                                       a.comp_w);
+                                                                       cfp, a.comp_w);
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) nsum += __shfl_xor_sync(0xffffffffu, nsum, o);
       if (lane == 0) red_s[(jn % C::NRED) * 32 + warp] = nsum;

@@ -83,7 +83,7 @@ def test_config4_full_size():
     rep = run(wl.mesh, wl.problem, wl.ops, IterationConfig(tol=1e-10))
     S = oracle_solver(wl)
     ref = S.run(tol=1e-10, engine="c", threads=THREADS)
-    assert rep.extra["kernel"] == "k_sweep_v3"
+    assert rep.extra["kernel"] == "k_sweep_v4"
     assert rep.status == ref["status"] == "converged"
     assert rep.iterations == ref["iterations"]
     assert rel_l2(rep.state.data.reshape(S.nel, -1), ref["u"]) < TOL_FIELD

@@ -96,12 +96,42 @@ def test_config3_reduced_parity():
         assert rel_l2(r.state.data.reshape(S.nel, -1), o["u"]) < TOL_FIELD
 
 
+@pytest.mark.parametrize("beta,impl,kernel", [
+    ((1.0, 0.7, 0.4), "v3", "k_sweep_v3"), ((-1.0, 0.7, -0.4), "auto", "k_sweep_v4"),
+    ((1.0, -0.7, 0.4), "auto", "k_sweep_v4"), ((-0.3, -0.7, 1.0), "auto", "k_sweep_v4"),
+    ((1.0, 0.0, 0.4), "auto", "k_sweep")])
+def test_config4_kernels_by_inflow_faces(beta, impl, kernel):
+    """3D p=3 transport: k_sweep_v4 has one instantiation per inflow-face set
+    (sign pattern of beta); the v3 selector and a beta with a zero component
+    (two coupled faces: generic kernel) are checked alike, all against the
+    oracle on a 16^3 mesh."""
+    import dataclasses
+
+    from paper_1711_01175_b200 import _native as N
+    from paper_1711_01175_b200.pde import TransportProblem
+    from tests.oracle_bridge import rel_l2
+
+    wl = _wl(4, cells=16)
+    prob = TransportProblem(beta=np.array(beta), forcing=wl.problem.forcing)
+    wl = dataclasses.replace(wl, problem=prob, params={**wl.params, "beta": list(beta)})
+    N.set_sweep_impl(impl)
+    try:
+        rep, S, ref = _steady(wl, "successive")
+    finally:
+        N.set_sweep_impl("auto")
+    assert rep.extra["kernel"] == kernel
+    assert rep.status == ref["status"] == "converged"
+    assert rep.iterations == ref["iterations"]
+    assert rel_l2(rep.state.data.reshape(S.nel, -1), ref["u"]) < TOL_FIELD
+    assert np.allclose(rep.successive_norms, ref["norms"], rtol=1e-7, atol=1e-300)
+
+
 def test_config4_reduced_parity():
     from tests.oracle_bridge import rel_l2
 
     wl = _wl(4, cells=8)
     rep, S, ref = _steady(wl, "successive")
-    assert rep.extra["kernel"] == "k_sweep_v3"
+    assert rep.extra["kernel"] == "k_sweep_v4"
     assert rep.iterations == ref["iterations"] == 3 * 7 + 1 + 1
     assert rel_l2(rep.state.data.reshape(S.nel, -1), ref["u"]) < TOL_FIELD
     assert rel_l2(rep.trace, S.trace(ref["u"])) < TOL_FIELD
