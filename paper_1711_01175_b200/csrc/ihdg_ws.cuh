@@ -47,44 +47,78 @@ __device__ __forceinline__ int ws_qcol(int t) {
 // swizzled offset of node (kk, nn) inside a delta unit
 __device__ __forceinline__ int ws_dnode(int kk, int nn) { return kk * 8 + (nn ^ (4 * ((kk >> 1) & 1))); }
 
-// tensor-core norm over the swizzled delta tile: units u = warp + m NCW,
-// (element, component); sum of w_c |C^T Delta C|_F^2
+// Norm units (element, component) of consumer warp w: units [first, first +
+// cnt).  The warps of one SM sub-partition (warp % 4) share one fp64 tensor
+// pipe (16 clk per DMMA, tools/microbench/dmma_smsp.cu), 10 consumer warps sit
+// 3/3/2/2 on them, and the consumers run the norm of a tile in lockstep (it
+// needs every warp's delta): the phase lasts as long as the busiest
+// sub-partition, so the units are dealt evenly per sub-partition (12 each for
+// 48 units), not per warp.
+template <int NCW, int NRT, int KS, int NEG, int NU>
+__host__ __device__ constexpr void ws_units(int w, int& first, int& cnt) {
+  int load[4] = {0, 0, 0, 0};
+  int uc[NCW] = {};
+  for (int u = 0; u < NU; ++u) {
+    int best = 0;
+    for (int i = 1; i < NCW; ++i)
+      if (load[i % 4] < load[best % 4] || (load[i % 4] == load[best % 4] && uc[i] < uc[best])) best = i;
+    ++uc[best];
+    ++load[best % 4];
+  }
+  first = 0;
+  for (int i = 0; i < w; ++i) first += uc[i];
+  cnt = uc[w];
+}
+template <int NCW, int NRT, int KS, int NEG, int NU>
+__host__ __device__ constexpr int ws_max_units() {
+  int mx = 0;
+  for (int w = 0; w < NCW; ++w) {
+    int f = 0, c = 0;
+    ws_units<NCW, NRT, KS, NEG, NU>(w, f, c);
+    mx = c > mx ? c : mx;
+  }
+  return mx;
+}
+
+// tensor-core norm over the swizzled delta tile: units u0 .. u0 + ucnt - 1 of
+// this warp, (element, component); sum of w_c |C^T Delta C|_F^2
 // The second product Y = R C contracts over the columns of R in the order the
 // D fragment holds them (k slot (ks, c) = column 2 c + ks, with C's rows
 // permuted alike in cfp), so R feeds the A operand straight from the
 // accumulator registers: no shuffles between the two DMMAs.
-template <int N1, int M, int E, int NCW, int UPW, int DUE, int DUC>
-__device__ __forceinline__ double norm_units_swz(const double* __restrict__ dbuf, int warp, int lane,
+template <int N1, int M, int E, int UPW, int DUE, int DUC>
+__device__ __forceinline__ double norm_units_swz(const double* __restrict__ dbuf, int u0, int ucnt, int lane,
                                                  const double (&cfr)[2], const double (&cfp)[2],
                                                  const double* comp_w) {
   double acc = 0.0;
   double r0[UPW], r1[UPW];
 #pragma unroll
   for (int m = 0; m < UPW; ++m) {
-    const int u = warp + m * NCW;
-    const bool valid = u < E * M;
-    const int uu = valid ? u : 0;
-    const int t = uu / M, c = uu - (uu / M) * M;
-    const double* base = dbuf + t * DUE + c * DUC;
     r0[m] = 0.0;
     r1[m] = 0.0;
+    if (m < ucnt) {   // warp-uniform
+      const int u = u0 + m;
+      const int t = u / M, c = u - (u / M) * M;
+      const double* base = dbuf + t * DUE + c * DUC;
 #pragma unroll
-    for (int ks = 0; ks < 2; ++ks) {
-      const int kk = 4 * ks + (lane & 3), nn = lane >> 2;
-      const double b = (valid && kk < N1 && nn < N1) ? base[ws_dnode(kk, nn)] : 0.0;
-      dmma_8x8x4(r0[m], r1[m], cfr[ks], b);   // R = C^T Delta
+      for (int ks = 0; ks < 2; ++ks) {
+        const int kk = 4 * ks + (lane & 3), nn = lane >> 2;
+        const double b = (kk < N1 && nn < N1) ? base[ws_dnode(kk, nn)] : 0.0;
+        dmma_8x8x4(r0[m], r1[m], cfr[ks], b);   // R = C^T Delta
+      }
     }
   }
 #pragma unroll
   for (int m = 0; m < UPW; ++m) {
-    const int u = warp + m * NCW;
-    const int c = (u < E * M ? u : 0) % M;
-    double y0 = 0.0, y1 = 0.0;
-    dmma_8x8x4(y0, y1, r0[m], cfp[0]);  // Y = R C, columns 2c of R
-    dmma_8x8x4(y0, y1, r1[m], cfp[1]);  // columns 2c + 1
-    const double w = comp_w[c];
-    acc = fma(w * y0, y0, acc);
-    acc = fma(w * y1, y1, acc);
+    if (m < ucnt) {
+      const int c = (u0 + m) % M;
+      double y0 = 0.0, y1 = 0.0;
+      dmma_8x8x4(y0, y1, r0[m], cfp[0]);  // Y = R C, columns 2c of R
+      dmma_8x8x4(y0, y1, r1[m], cfp[1]);  // columns 2c + 1
+      const double w = comp_w[c];
+      acc = fma(w * y0, y0, acc);
+      acc = fma(w * y1, y1, acc);
+    }
   }
   return acc;
 }
@@ -105,7 +139,7 @@ struct WCfg {
   static constexpr int NCW = NRT >= 16 ? 10 : (NRT >= 8 ? 8 : 4);  // consumer warps
 #endif
   static constexpr int RTW = (NRT + NCW - 1) / NCW;
-  static constexpr int UPW = (E * M + NCW - 1) / NCW;
+  static constexpr int UPW = ws_max_units<NCW, NRT, KS, NEG, E * M>();   // most norm units of one warp
 #ifdef IHDG_WS_NQW
   static constexpr int NQW = IHDG_WS_NQW;                          // A/B builds
 #else
@@ -508,6 +542,8 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS, GRAM>::NT, 1)
       const int kk = 2 * (lane & 3) + ks, nn = lane >> 2;
       cfp[ks] = (kk < N1 && nn < N1) ? chol_s[kk * N1 + nn] : 0.0;
     }
+    int nu0 = 0, nucnt = 0;   // this warp's norm units
+    ws_units<NCW, NRT, KS, NEG, E * M>(warp, nu0, nucnt);
     // Gram-form norm item of this warp: R row tile grt x element group geg
     static_assert(C::LAG == 1, "the Gram / direct norm schedule assumes LAG = 1");
     const int gi = NCW - 1 - warp;
@@ -542,7 +578,7 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS, GRAM>::NT, 1)
         mbar_wait(&done_bar[jn & 1], (jn >> 1) & 1);
         V3_ACC(8, td);
         V3_T0(tn);
-        nprev = norm_units_swz<N1, M, E, NCW, UPW, C::DUE, C::DUC>(d_s + (jn % C::NDB) * C::DT, warp, lane, cfr,
+        nprev = norm_units_swz<N1, M, E, UPW, C::DUE, C::DUC>(d_s + (jn % C::NDB) * C::DT, nu0, nucnt, lane, cfr,
                                                                    cfp, a.comp_w);
         V3_ACC(7, tn);
       }
@@ -657,7 +693,7 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS, GRAM>::NT, 1)
     if (n_my >= 1 && (!GRAM || prev_direct)) {
       const int jn = n_my - 1;
       mbar_wait(&done_bar[jn & 1], (jn >> 1) & 1);
-      double nsum = norm_units_swz<N1, M, E, NCW, UPW, C::DUE, C::DUC>(d_s + (jn % C::NDB) * C::DT, warp, lane, cfr,
+      double nsum = norm_units_swz<N1, M, E, UPW, C::DUE, C::DUC>(d_s + (jn % C::NDB) * C::DT, nu0, nucnt, lane, cfr,
                                                                        cfp, a.comp_w);
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) nsum += __shfl_xor_sync(0xffffffffu, nsum, o);
