@@ -354,15 +354,26 @@ def run_ours(args):
             ao = so.sweep_args("volume", finalize=1)
             for _ in range(3):
                 so.sweep_once(a=ao)
+            # these sweeps last 30-130 us, the order of a Python launch, so the
+            # 20 timed sweeps are replayed from one CUDA graph (as ihdg_iterate
+            # replays its batches in production) instead of launched one by one
             nrep = 20
             eo0, eo1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             torch.cuda.synchronize()
-            eo0.record(so.stream)
-            for _ in range(nrep):
-                so.sweep_once(a=ao)
-            eo1.record(so.stream)
+            gr, cap = torch.cuda.CUDAGraph(), torch.cuda.Stream()
+            so.stream = cap          # the solver launches on its stream attribute
+            with torch.cuda.graph(gr, stream=cap):
+                for _ in range(nrep):
+                    so.sweep_once(a=ao)
+            torch.cuda.synchronize()
+            with torch.cuda.stream(cap):
+                gr.replay()          # warm replay
+                eo0.record(cap)
+                gr.replay()
+                eo1.record(cap)
             torch.cuda.synchronize()
             tms = eo0.elapsed_time(eo1) / nrep
+            del gr
             dofs_o = so.nloc * so.nv
             ach = BYTES_PER_DOF * dofs_o / (tms / 1e3) / 1e9
             # fp64 tensor-pipe view (north_star: the shared-operator case is a

@@ -32,7 +32,7 @@ __device__ __forceinline__ double warp_row_sum(const double* row, int64_t len, i
 // exactly the single-rank value (ihdg_finalize with row_len 1: a one-entry
 // row sums to itself).  Every thread of the CTA must call it; blockDim.x is a
 // multiple of 32.
-// RB rows of one virtual lane are loaded together (independent loads in
+// RB virtual lanes of one warp are walked together (independent loads in
 // flight); any RB gives the same value.  Small RB keeps the code small where
 // the reduction is off the hot path's instruction cache footprint (k_sweep_ws).
 template <int RB = 8>
@@ -40,32 +40,61 @@ __device__ inline double rows_sum(const double* parts, int64_t n_rows, int64_t r
   __shared__ double red[256];
   __syncthreads();
   const int lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-  for (int v = threadIdx.x >> 5; v < 256; v += nw) {
-    double s = 0.0;
-    for (int64_t r0 = v; r0 < n_rows; r0 += 256 * RB) {
-      // warp_row_sum of rows r0, r0 + 256, ..., batched: same per-lane order
-      // and butterfly, so the value equals k_layer_sums' bit for bit
-      double rs[RB];
+  if (row_len == 1) {
+    // one-entry rows (layer sums): warp_row_sum of a row is the entry itself
+    // (the butterfly only adds zeros), so one thread per virtual lane adds
+    // its rows v, v + 256, ... in order -- the same value bit for bit, without
+    // a dependent load and five shuffles per row
+    for (int v = threadIdx.x; v < 256; v += blockDim.x) {
+      double s = 0.0;
+      for (int64_t r0 = v; r0 < n_rows; r0 += 256 * 8) {
+        double x[8];
 #pragma unroll
-      for (int j = 0; j < RB; ++j) rs[j] = 0.0;
-      for (int64_t i = lane; i < row_len; i += 32) {
-        double x[RB];
-#pragma unroll
-        for (int j = 0; j < RB; ++j) {
+        for (int j = 0; j < 8; ++j) {
           const int64_t r = r0 + 256 * (int64_t)j;
-          x[j] = r < n_rows ? __ldcg(parts + r * row_len + i) : 0.0;
+          x[j] = r < n_rows ? __ldcg(parts + r) : 0.0;
         }
 #pragma unroll
-        for (int j = 0; j < RB; ++j) rs[j] += x[j];
+        for (int j = 0; j < 8; ++j)
+          if (r0 + 256 * (int64_t)j < n_rows) s += x[j];
       }
-#pragma unroll
-      for (int j = 0; j < RB; ++j) {
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) rs[j] += __shfl_xor_sync(0xffffffffu, rs[j], o);
-        if (r0 + 256 * (int64_t)j < n_rows) s += rs[j];
-      }
+      red[v] = s;
     }
-    if (lane == 0) red[v] = s;
+  } else {
+    // a warp takes RB virtual lanes at a time (v = vb + j nw) and walks their
+    // rows v, v + 256, ... together: RB independent row loads in flight, each
+    // row still summed by warp_row_sum's per-lane order and butterfly and each
+    // virtual lane still adding its rows in order -- the same bits for any RB
+    for (int vb = threadIdx.x >> 5; vb < 256; vb += nw * RB) {
+      double s[RB];
+#pragma unroll
+      for (int j = 0; j < RB; ++j) s[j] = 0.0;
+      for (int64_t k = 0; 256 * k < n_rows; ++k) {
+        double rs[RB];
+#pragma unroll
+        for (int j = 0; j < RB; ++j) rs[j] = 0.0;
+        for (int64_t i = lane; i < row_len; i += 32) {
+          double x[RB];
+#pragma unroll
+          for (int j = 0; j < RB; ++j) {
+            const int v = vb + j * nw;
+            const int64_t r = v + 256 * k;
+            x[j] = (v < 256 && r < n_rows) ? __ldcg(parts + r * row_len + i) : 0.0;
+          }
+#pragma unroll
+          for (int j = 0; j < RB; ++j) rs[j] += x[j];
+        }
+#pragma unroll
+        for (int j = 0; j < RB; ++j) {
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) rs[j] += __shfl_xor_sync(0xffffffffu, rs[j], o);
+          if (vb + j * nw + 256 * k < n_rows) s[j] += rs[j];
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < RB; ++j)
+        if (lane == 0 && vb + j * nw < 256) red[vb + j * nw] = s[j];
+    }
   }
   __syncthreads();
   for (int w = 128; w > 0; w >>= 1) {

@@ -1,7 +1,7 @@
 #!/usr/bin/env python
 """Time N sweeps of one BASELINE config (for ncu captures and A/B runs).
 
-    python tools/sweep_cfg.py <config 1-5> [n_sweeps] [warmup] [gram] [nofin] [nolsum]
+    python tools/sweep_cfg.py <config 1-5> [n_sweeps] [warmup] [gram] [nofin] [nolsum] [graph]
 """
 import os
 import sys
@@ -36,10 +36,25 @@ def main():
         sv.sweep_once(a=a)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()
-    e0.record(sv.stream)
-    for _ in range(n):
-        sv.sweep_once(a=a)
-    e1.record(sv.stream)
+    if "graph" in sys.argv[4:]:
+        # replay the n sweeps from one CUDA graph (no host launch gaps between short sweeps)
+        n += n % 2
+        gr, cap = torch.cuda.CUDAGraph(), torch.cuda.Stream()
+        sv.stream = cap
+        with torch.cuda.graph(gr, stream=cap):
+            for _ in range(n):
+                sv.sweep_once(a=a)
+        torch.cuda.synchronize()
+        with torch.cuda.stream(cap):
+            gr.replay()
+            e0.record(cap)
+            gr.replay()
+            e1.record(cap)
+    else:
+        e0.record(sv.stream)
+        for _ in range(n):
+            sv.sweep_once(a=a)
+        e1.record(sv.stream)
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / n
     dofs = sv.nloc * sv.nv
