@@ -25,7 +25,7 @@ if timeout 300 $CMD3 > $O/${TAG}_bench_short3.json 2>&1; then
     -o $O/${TAG}_ws_full -f $CMD3 > $O/${TAG}_ncu_full.log 2>&1
 fi
 if timeout 300 python tools/sweep_cfg.py 4 20 3 > $O/${TAG}_cfg4_plain.txt 2>&1; then
-  timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_sweep_v3 -s 3 -c 1 \
-    -o $O/${TAG}_cfg4_v3_full -f python tools/sweep_cfg.py 4 5 3 > $O/${TAG}_cfg4_ncu.log 2>&1
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_sweep_v4 -s 3 -c 1 \
+    -o $O/${TAG}_cfg4_v4_full -f python tools/sweep_cfg.py 4 5 3 > $O/${TAG}_cfg4_ncu.log 2>&1
 fi
 echo done
