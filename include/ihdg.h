@@ -380,14 +380,13 @@ int ihdg_class_apply(const ihdg_class_apply_args* a, void* stream);
 int ihdg_eval_field(const ihdg_field_args* a, void* stream);
 int ihdg_quad_project(const ihdg_quad_args* a, void* stream);
 int ihdg_sweep(const ihdg_sweep_args* a, void* stream);
-/* 1 if ihdg_sweep would use the streaming (TMA bulk-copy) kernel for these
- * args, 0 if it falls back to the generic kernel */
+/* 1 if ihdg_sweep would use one of the streaming kernels (ws / v3 / v4) for
+ * these args, 0 if it falls back to the generic kernel */
 int ihdg_stream_variant(const ihdg_sweep_args* a);
 /* Name of the kernel ihdg_sweep launches for these args under the current
  * selector: "k_sweep_ws" (2D warp-specialised, config 5), "k_sweep_v4"
  * (register-tiled, 3D p=3 scalar: config 4), "k_sweep_v3" (warp-owned tiles
- * behind a staged ring, configs 2-3), "k_sweep_stream" (TMA ring), "k_sweep"
- * (generic), or NULL if no kernel is instantiated (static string). */
+ * behind a staged ring, configs 2-3), "k_sweep" (generic), or NULL if no kernel is instantiated (static string). */
 const char* ihdg_sweep_kernel(const ihdg_sweep_args* a);
 /* Process-wide sweep-kernel selector: "auto" (default; the initial value is
  * read from the environment variable IHDG_SWEEP_IMPL), "v3" (skip v4),

@@ -1,5 +1,5 @@
 // Instantiations + dispatch of the streaming sweep kernels (k_sweep_ws,
-// k_sweep_v3, k_sweep_stream).  Which kernel a call uses is decided here from
+// k_sweep_v3, k_sweep_v4).  Which kernel a call uses is decided here from
 // the args (stream_entry) and the process-wide selector set by
 // ihdg_set_sweep_impl; ihdg_sweep_kernel reports the decision by name.
 #include <atomic>
@@ -11,6 +11,7 @@
 #include "ihdg_ws.cuh"
 #include "ihdg_v3.cuh"
 #include "ihdg_v4.cuh"
+#include "ihdg_gemv.cuh"
 
 namespace ihdg {
 
@@ -56,13 +57,6 @@ cudaError_t launch_persistent(int nt, size_t bytes, int tile_elems, const ihdg_s
   return cudaGetLastError();
 }
 
-template <int D, int N1, int M, int NCF, int NWC, int E, int NS, int G>
-cudaError_t launch_stream_t(const ihdg_sweep_args* a, cudaStream_t st) {
-  using C = SCfg<D, N1, M, NCF, NWC, E, NS, G>;
-  static_assert(E == Cfg<D, N1, M>::TE, "stream tile must equal the generic tile (tile partial count)");
-  return launch_persistent<k_sweep_stream<D, N1, M, NCF, NWC, E, NS, G>>(C::NT, C::BYTES, E, a, st);
-}
-
 template <int N1, int M, int NCF, int NWC, int E, int NS>
 cudaError_t launch_ws_t(const ihdg_sweep_args* a, cudaStream_t st) {
   static_assert(E == Cfg<2, N1, M>::TE, "ws tile must equal the generic tile (tile partial count)");
@@ -89,8 +83,25 @@ cudaError_t launch_v4_t(const ihdg_sweep_args* a, cudaStream_t st) {
   return launch_persistent<k_sweep_v4<FMASK, NW, MINB>>(C::NT, C::BYTES, 8 * C::PF, a, st, false, MINB);
 }
 
-enum Kind { KIND_V3 = 0, KIND_WS = 1, KIND_STREAM = 2, KIND_V4 = 3 };
-const char* const kKindName[] = {"k_sweep_v3", "k_sweep_ws", "k_sweep_stream", "k_sweep_v4"};
+// per-element operators (GEMV mode): as many CTAs per SM as fit, one tile each
+template <int D, int N1, int M>
+cudaError_t launch_gemv_t(const ihdg_sweep_args* a, cudaStream_t st) {
+  using G = GCfg<D, N1, M>;
+  static std::atomic<int> cps{0};   // resident CTAs per SM (same for every device of one model)
+  int c = cps.load();
+  if (c == 0) {
+    cudaError_t e = cudaFuncSetAttribute(k_sweep_gemv<D, N1, M>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G::BYTES);
+    if (e != cudaSuccess) return e;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c, k_sweep_gemv<D, N1, M>, G::NT, G::BYTES);
+    if (e != cudaSuccess) return e;
+    if (c < 1) c = 1;
+    cps.store(c);
+  }
+  return launch_persistent<k_sweep_gemv<D, N1, M>>(G::NT, G::BYTES, G::TE, a, st, false, c);
+}
+
+enum Kind { KIND_V3 = 0, KIND_WS = 1, KIND_V4 = 2, KIND_GEMV = 3 };
+const char* const kKindName[] = {"k_sweep_v3", "k_sweep_ws", "k_sweep_v4", "k_sweep_gemv"};
 
 struct StreamEntry {
   int D, N1, M, NCF, NWC, E, NV;
@@ -104,8 +115,6 @@ struct StreamEntry {
 #define IHDG_V4(FMASK, NW, MINB) {3, 4, 1, v4_popc(FMASK), 1, 32, 64, launch_v4_t<FMASK, NW, MINB>, KIND_V4, FMASK},
 #define IHDG_WS(N1, M, NCF, NWC, E, NS) \
   {2, N1, M, NCF, NWC, E, M * N1 * N1, launch_ws_t<N1, M, NCF, NWC, E, NS>, KIND_WS},
-#define IHDG_STREAM(D, N1, M, NCF, NWC, E, NS, G) \
-  {D, N1, M, NCF, NWC, E, M * Pow<N1, D>::v, launch_stream_t<D, N1, M, NCF, NWC, E, NS, G>, KIND_STREAM},
 
 #ifndef IHDG_WS5_NS
 #define IHDG_WS5_NS 3   // stage count of the config-5 ring (A/B builds override it)
@@ -139,7 +148,7 @@ struct StreamEntry {
 #define IHDG_C4_V4_MINB 1
 #endif
 
-// First match wins: v4 before v3 before ws/stream for the same (D, N1, M).
+// First match wins: v4 before v3 before ws for the same (D, N1, M).
 const StreamEntry kStream[] = {
     // config 4: transport 3D p=3; one instantiation per inflow-face set (the
     // sign pattern of beta; config 4 itself is faces 0, 2, 4 = 0x15)
@@ -151,7 +160,16 @@ const StreamEntry kStream[] = {
     IHDG_V3(3, 4, 1, 3, 1, IHDG_C4_NS, IHDG_C4_NCW, 4, IHDG_C4_NQW)  // config 4: transport 3D p=3
     IHDG_WS(7, 3, 4, 2, 16, IHDG_WS5_NS)   // config 5: CD 2D p=6 (warp-specialised)
     IHDG_WS(5, 3, 4, 2, 16, 4)             // configs 2/3 without v3
-    IHDG_STREAM(3, 4, 1, 3, 1, 32, 3, 4)   // config 4 without v3
+};
+
+// Per-element operators with raw neighbour values (GEMV mode), by (D, N1, M):
+// the elements large enough to keep a CTA of row threads busy (NV >= 108;
+// measured on B200, cdr_manufactured: 16^3 p=2 0.267 -> 0.105 ms, 8^3 p=3
+// 0.244 -> 0.083 ms, but 16^3 p=1 (NV = 32, one consumer warp) 0.068 -> 0.225 ms,
+// so the small ones stay on the generic kernel).
+#define IHDG_GEMV(D, N1, M) {D, N1, M, 0, 0, Cfg<D, N1, M>::TE, M * Pow<N1, D>::v, launch_gemv_t<D, N1, M>, KIND_GEMV},
+const StreamEntry kGemv[] = {
+    IHDG_GEMV(3, 3, 4) IHDG_GEMV(3, 4, 4) IHDG_GEMV(3, 5, 4)   // cdr_manufactured (3D, variable beta) p = 2..4
 };
 
 // Process-wide kernel selector (ihdg_set_sweep_impl); the initial value comes
@@ -184,7 +202,16 @@ const StreamEntry* stream_entry(const ihdg_sweep_args* a) {
   const int impl = current_impl();
   if (impl == IMPL_GENERIC) return nullptr;
   if (a->norm_kind != IHDG_NORM_VOLUME) return nullptr;
-  if (a->per_element || a->raw_blocks > 0) return nullptr;   // per-element operators: generic kernel
+  if (a->per_element && (a->raw_blocks == 2 || a->raw_blocks == 4)) {   // per-element operators: GEMV kernel
+    const ihdg_geom& gg = a->g;
+    for (const StreamEntry& e : kGemv) {
+      if (e.D != gg.dim || e.N1 != gg.order + 1 || e.M != gg.ncomp) continue;
+      if (((uintptr_t)a->LT) % 16 != 0) continue;   // bulk copies of the operator chunks
+      return &e;
+    }
+    return nullptr;
+  }
+  if (a->per_element || a->raw_blocks > 0) return nullptr;   // other per-element layouts: generic kernel
   if (a->scheme != IHDG_SCHEME_II) return nullptr;   // iHDG-I: generic kernel
   const ihdg_geom& g = a->g;
   int ncf = 0, maxw = 0, fmask = 0;

@@ -1,7 +1,6 @@
 // Warp-specialised iHDG-II sweep for 2D configurations (production path for
-// BASELINE configs 2, 3 and 5).  Same algorithm and HBM traffic as
-// k_sweep_stream; the roles run asynchronously and hand tiles over through
-// mbarriers only (no CTA-wide barrier in the steady state):
+// BASELINE configs 2, 3 and 5).  The roles run asynchronously and hand tiles
+// over through mbarriers only (no CTA-wide barrier in the steady state):
 //
 //   producer warp  : per tile, metadata + TMA bulk copies of the s and u^k
 //                    tiles + cp.async gathers of out-of-tile neighbour faces

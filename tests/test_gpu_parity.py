@@ -249,26 +249,6 @@ def test_sweep_impl_parity(impl, graphs, cfg, cells, kernel):
         assert rel_l2(r.state.data.reshape(S.nel, -1), o["u"]) < TOL_FIELD
 
 
-def test_config4_stream_kernel_parity():
-    """Config 4 reduced through k_sweep_stream (the 3D kernel without v3)."""
-    from paper_1711_01175_b200 import _native as N
-    from tests.oracle_bridge import rel_l2
-
-    from paper_1711_01175_b200.iteration import IterationConfig, run
-    from tests.oracle_bridge import oracle_solver
-
-    wl = _wl(4, cells=32)   # k_sweep_stream tiles are 32 elements of one axis-0 row
-    N.set_sweep_impl("stream")
-    try:
-        rep = run(wl.mesh, wl.problem, wl.ops, IterationConfig(tol=1e-10))
-    finally:
-        N.set_sweep_impl("auto")
-    S = oracle_solver(wl)
-    ref = S.run(tol=1e-10, engine="c")
-    assert rep.extra["kernel"] == "k_sweep_stream"
-    assert rep.iterations == ref["iterations"]
-    assert rel_l2(rep.state.data.reshape(S.nel, -1), ref["u"]) < TOL_FIELD
-
 
 # PAPER.md:1349-1395 (Table 2) / SPEC.md acceptance 1: 2D N x N -> {9, 17, 33, 65} for N = 4..32,
 # 3D N^3 -> {6, 12, 23, 47} for N = 2..16, within +-2 (any p)
