@@ -26,6 +26,8 @@
 // HBM per element-DOF: 8 (kin + 3) B (L_e, s, u^k, u^{k+1}).
 #pragma once
 
+#include <climits>
+
 #include "ihdg_stream.cuh"
 
 namespace ihdg {
@@ -42,7 +44,10 @@ struct GCfg {
   // columns per chunk: about 16 KB, even (16-byte multiples for odd NV)
   static constexpr int CH0 = 16384 / (NV * 8);
   static constexpr int CH = CH0 < 2 ? 2 : (CH0 > 32 ? 32 : CH0 / 2 * 2);
-  static constexpr int NS = 4;                      // ring stages
+#ifndef IHDG_GEMV_NS
+#define IHDG_GEMV_NS 4
+#endif
+  static constexpr int NS = IHDG_GEMV_NS;           // ring stages
   static constexpr int STAGE = CH * NV;             // doubles
   static constexpr int QM = (KMAX + NCT - 1) / NCT; // gathered q entries per consumer thread
   static constexpr int OFF_Q = NS * STAGE;          // q[2][KMAX]
@@ -119,28 +124,63 @@ __global__ void __launch_bounds__(GCfg<D, N1, M>::NT) k_sweep_gemv(const ihdg_sw
     // ============================ consumer warps ===========================
     const int row = tid;
     const bool rv = row < NV;
+    // 32-bit element geometry (the dispatch guarantees local counts < 2^31):
+    // multi-index by two FastDiv divisions per element, neighbours as in
+    // Geo::neighbor (ghost layers beyond the strip on the last axis)
+    const int c0 = (int)geo.c[0], c1 = (int)geo.c[1];
+    const int lsi = (int)ls, nlay = (int)geo.nlay, lb = (int)geo.lb;
+    FastDiv dc0, dc1;
+    dc0.init((uint32_t)c0);
+    dc1.init((uint32_t)c1);
+    constexpr int NONE = INT_MIN;
+    auto neighbour = [&](int e, int f) -> int {
+      int idx[3];
+      const int r = dc0.div(e);
+      idx[0] = e - r * c0;
+      if (D == 3) {
+        const int l = dc1.div(r);
+        idx[1] = r - l * c1;
+        idx[2] = lb + l;
+      } else {
+        idx[1] = lb + r;
+        idx[2] = 0;
+      }
+      const int ax = f >> 1, sd = f & 1;
+      const int cn = (int)geo.c[ax];
+      int j = idx[ax] + (sd ? 1 : -1);
+      if (j < 0) {
+        if (!geo.per[ax]) return NONE;
+        j = cn - 1;
+      } else if (j >= cn) {
+        if (!geo.per[ax]) return NONE;
+        j = 0;
+      }
+      if (ax < D - 1) return e + (j - idx[ax]) * (ax == 0 ? 1 : c0);
+      const int lay = idx[D - 1] - lb, in_layer = e - lay * lsi;
+      const int l = j - lb;
+      return ((l >= 0 && l < nlay) ? l : (sd ? nlay : -1)) * lsi + in_layer;
+    };
     // gather of one q entry: raw face-node value of the neighbour across face
     // f (blocks 0, 1) or of the element itself (blocks 2, 3: iHDG-I)
-    auto gather = [&](int64_t e, int k) -> double {
+    auto gather = [&](int e, int k) -> double {
       const int f = k / (rb * NF), j = (k / NF) % rb, n = k % NF;
       const int c = a.raw_comp[f][j];
-      if (j >= 2) return __ldg(uo + e * NV + c * NP + fv_s[f][n]);
+      if (j >= 2) return __ldg(uo + (int64_t)e * NV + c * NP + fv_s[f][n]);
       if (!a.coupled[f]) return 0.0;
-      int64_t idx[3], nb;
-      geo.multi_index(e, idx);
-      if (!geo.neighbor(e, idx, f, nb)) return 0.0;
-      return __ldg(uo + nb * NV + c * NP + fv_s[f ^ 1][n]);
+      const int nb = neighbour(e, f);
+      if (nb == NONE) return 0.0;
+      return __ldg(uo + (int64_t)nb * NV + c * NP + fv_s[f ^ 1][n]);
     };
     // operands of one element, loaded one element ahead
     double qn[QM], sn = 0.0, ukn = 0.0;
-    auto prefetch = [&](int64_t e) {
+    auto prefetch = [&](int e) {
 #pragma unroll
       for (int m = 0; m < QM; ++m) {
         const int k = tid + m * NCT;
         qn[m] = k < kin ? gather(e, k) : 0.0;
       }
-      sn = rv ? __ldg(a.s + e * NV + row) : 0.0;
-      ukn = rv ? __ldg(uo + e * NV + row) : 0.0;
+      sn = rv ? __ldg(a.s + (int64_t)e * NV + row) : 0.0;
+      ukn = rv ? __ldg(uo + (int64_t)e * NV + row) : 0.0;
     };
     int cnt = 0, cur = 0;
     bool first = true;
@@ -149,7 +189,7 @@ __global__ void __launch_bounds__(GCfg<D, N1, M>::NT) k_sweep_gemv(const ihdg_sw
       int nt;
       geo.tile_range(tile, TE, e0, nt);
       if (first) {
-        prefetch(e0);
+        prefetch((int)e0);
         first = false;
       }
       double tile_sum = 0.0;   // warp 0, lane 0: the tile partial, its elements in order
@@ -174,7 +214,7 @@ __global__ void __launch_bounds__(GCfg<D, N1, M>::NT) k_sweep_gemv(const ihdg_sw
             int ntn;
             geo.tile_range(tile + gridDim.x, TE, en, ntn);
           }
-          if (en >= 0) prefetch(en);
+          if (en >= 0) prefetch((int)en);
         }
         // stream L_e through the ring: one FMA chain per row, columns in order
         for (int c = 0; c < nch; ++c, ++cnt) {
@@ -225,7 +265,7 @@ __global__ void __launch_bounds__(GCfg<D, N1, M>::NT) k_sweep_gemv(const ihdg_sw
           }
 #pragma unroll
           for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-          tile_sum += a.jac * s;
+          tile_sum = __dadd_rn(tile_sum, __dmul_rn(a.jac, s));   // product rounded first, as the generic kernel stores it
         }
         cur ^= 1;
       }

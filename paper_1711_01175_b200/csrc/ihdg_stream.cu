@@ -207,6 +207,9 @@ const StreamEntry* stream_entry(const ihdg_sweep_args* a) {
     for (const StreamEntry& e : kGemv) {
       if (e.D != gg.dim || e.N1 != gg.order + 1 || e.M != gg.ncomp) continue;
       if (((uintptr_t)a->LT) % 16 != 0) continue;   // bulk copies of the operator chunks
+      Geo geo;
+      geo.init(gg, e.E);
+      if (geo.nloc + 2 * geo.ls >= (1LL << 31)) continue;   // 32-bit element indices
       return &e;
     }
     return nullptr;
