@@ -102,3 +102,27 @@ def test_dispatch_names(cfg, cells, auto, no_v3):
         N.set_sweep_impl("auto")
     with pytest.raises(RuntimeError):
         N.set_sweep_impl("ws9")
+
+
+@pytest.mark.parametrize("order,blocks,kernel", [(2, 2, "k_sweep_gemv"), (3, 4, "k_sweep_gemv"), (1, 2, "k_sweep")])
+def test_dispatch_per_element_operators(order, blocks, kernel):
+    """Per-element operators with raw neighbour values (the GEMV mode) go to
+    k_sweep_gemv when the element is large enough for a CTA of row threads
+    (N_vol >= 108), otherwise to the generic kernel; "generic" always wins."""
+    if not os.path.exists(N.LIB_PATH):
+        pytest.skip("libihdg_cuda.so not built")
+    a = N.SweepArgs()
+    a.g.dim, a.g.order, a.g.ncomp = 3, order, 4
+    for i in range(3):
+        a.g.cells[i] = 16
+        a.g.periodic[i] = 0
+    a.g.layer_begin, a.g.layer_end = 0, 16
+    a.norm_kind = N.NORM_VOLUME
+    a.scheme = N.SCHEME_II if blocks == 2 else N.SCHEME_I
+    a.per_element, a.raw_blocks = 1, blocks
+    try:
+        assert N.sweep_kernel(a) == kernel
+        N.set_sweep_impl("generic")
+        assert N.sweep_kernel(a) == "k_sweep"
+    finally:
+        N.set_sweep_impl("auto")
