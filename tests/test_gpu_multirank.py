@@ -109,3 +109,38 @@ def test_ranks_bit_identical_to_one(cfg, kw, world, overlap):
         assert iters == ref.iterations
         np.testing.assert_array_equal(norms, ref.norms)
         np.testing.assert_array_equal(state, ref_state[lb * ls:le * ls])
+
+
+def test_bench_multirank_line_host_staging():
+    """bench.py's N > 1 path (strips, DistributedSweeper, e2e and time to
+    converge at N ranks) in its test mode: two ranks share the GPU and exchange
+    through host memory.  The line must carry the contract's keys and the same
+    sweep counts as one rank."""
+    import json
+    import os
+    import subprocess
+    import sys
+
+    import torch
+
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    common = ["--cells", "64", "--steps", "3", "--warmup", "3", "--no-cpu", "--no-others", "--ttc", "1e-3:2"]
+
+    def line(cmd):
+        out = subprocess.run(cmd, cwd=root, capture_output=True, text=True, timeout=600)
+        assert out.returncode == 0, out.stderr[-2000:]
+        return json.loads([ln for ln in out.stdout.splitlines() if ln.startswith("{")][-1])
+
+    one = line([sys.executable, "bench.py"] + common)
+    two = line([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+                "--master-addr", "127.0.0.1", f"--master-port={_free_port()}", "bench.py", "--gpus", "2",
+                "--host-staging", "--scaling", "strong"] + common)
+    assert two["n_gpus"] == 2 and two["scaling"] == "strong" and two["config"]["parallelism"] == "strip2"
+    for key in ("roofline", "clocks", "e2e", "gpu_launches", "time_to_converge"):
+        assert two.get(key), key
+    t1, t2 = one["time_to_converge"]["kappa=0.001"], two["time_to_converge"]["kappa=0.001"]
+    assert t2["status"] == t1["status"] == "converged"
+    assert t2["sweeps_per_step"] == t1["sweeps_per_step"]
+    assert two["e2e"]["sweeps"] == one["e2e"]["sweeps"]
