@@ -75,7 +75,7 @@ __global__ void __launch_bounds__(GCfg<D, N1, M>::NT) k_sweep_gemv(const ihdg_sw
   __shared__ int last_s;
 
   ihdg_iter_state* st = a.state;
-  if (st->status != IHDG_RUNNING) return;
+  pdl_launch_dependents();   // the next launch may start its own prologue
 
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
@@ -98,6 +98,10 @@ __global__ void __launch_bounds__(GCfg<D, N1, M>::NT) k_sweep_gemv(const ihdg_sw
     fence_mbar_init();
   }
   __syncthreads();
+  // everything above reads only launch-invariant data; the operators' stream,
+  // the iterate and the iteration state wait for the previous launches
+  pdl_wait();
+  if (st->status != IHDG_RUNNING) return;
 
   if (warp == NCW) {
     // ============================ producer warp ============================

@@ -105,6 +105,13 @@ __device__ __forceinline__ void dmma_8x8x4(double& d0, double& d1, double a, dou
       : "+d"(d0), "+d"(d1)
       : "d"(a), "d"(b));
 }
+// Programmatic dependent launch (launch attribute
+// cudaLaunchAttributeProgrammaticStreamSerialization): a sweep lets the next
+// launch in the stream start its prologue early, and every sweep waits for
+// the previous grid to complete (and flush) before it reads anything the
+// previous grid wrote.  Both are no-ops without the launch attribute.
+__device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void consumer_bar(int n) { asm volatile("bar.sync 1, %0;" ::"r"(n) : "memory"); }
 
 // 32-bit tile geometry for the streaming kernel (host guarantees local

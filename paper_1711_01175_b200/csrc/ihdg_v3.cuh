@@ -101,7 +101,7 @@ __global__ void __launch_bounds__(V3Cfg<D, N1, M, NCF, NWC, NS, NCW, PF, NQW_>::
   __shared__ int last_s;
 
   ihdg_iter_state* st = a.state;
-  if (st->status != IHDG_RUNNING) return;
+  pdl_launch_dependents();   // the next launch may start its own prologue
   V3_DECL
 
   const int tid = threadIdx.x;
@@ -162,6 +162,10 @@ __global__ void __launch_bounds__(V3Cfg<D, N1, M, NCF, NWC, NS, NCW, PF, NQW_>::
     sm[C::OFF_L + idx] = (row < NV) ? a.LT[((size_t)fast_class * (NFACE * NF) + col) * NV + row] : 0.0;
   }
   __syncthreads();
+  // everything above reads only launch-invariant data (operators, tables);
+  // the iterate, s and the iteration state belong to the previous launches
+  pdl_wait();
+  if (st->status != IHDG_RUNNING) return;
 
   V3_T0(tk0);
   const int nlog = (int)geo.ntiles;

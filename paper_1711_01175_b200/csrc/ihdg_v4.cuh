@@ -102,7 +102,7 @@ __global__ void __launch_bounds__(V4Cfg<FMASK, NW, MINB_>::NT, MINB_) k_sweep_v4
   __shared__ __align__(8) uint64_t ubar[NW];   // per warp: u^k tile landed
 
   ihdg_iter_state* st = a.state;
-  if (st->status != IHDG_RUNNING) return;
+  pdl_launch_dependents();   // the next launch may start its own prologue
 
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
@@ -132,6 +132,11 @@ __global__ void __launch_bounds__(V4Cfg<FMASK, NW, MINB_>::NT, MINB_) k_sweep_v4
     sm[idx] = a.LT[((size_t)fast_class * (NFACE * NF) + col) * NV + row];
   }
   __syncthreads();
+
+  // everything above reads only launch-invariant data (operators, tables);
+  // the iterate, s and the iteration state belong to the previous launches
+  pdl_wait();
+  if (st->status != IHDG_RUNNING) return;
 
   const int grp = warp / PF, sub = warp - grp * PF;
   const int nlog = (int)geo.ntiles;
