@@ -6,7 +6,7 @@
 // for 3D p=2) exactly once per sweep, so the kernel is a bandwidth pump:
 //
 //   producer warp  : TMA bulk copies (cp.async.bulk) of LT_e in chunks of CH
-//                    columns (~16 KB, contiguous in memory) into an NS-stage
+//                    columns (~24 KB, contiguous in memory) into an NS-stage
 //                    shared-memory ring, across element and tile boundaries
 //                    (full / empty mbarriers);
 //   consumer warps : thread = row of L_e.  q_e (raw neighbour face-node values
@@ -41,11 +41,14 @@ struct GCfg {
   static constexpr int NCT = 32 * NCW;
   static constexpr int NT = NCT + 32;               // + producer warp
   static constexpr int KMAX = 4 * KIN;              // raw_blocks <= 4
-  // columns per chunk: about 16 KB, even (16-byte multiples for odd NV)
-  static constexpr int CH0 = 16384 / (NV * 8);
-  static constexpr int CH = CH0 < 2 ? 2 : (CH0 > 32 ? 32 : CH0 / 2 * 2);
+  // columns per chunk: about 24 KB, even (16-byte multiples for odd NV)
+#ifndef IHDG_GEMV_CHB
+#define IHDG_GEMV_CHB 24576   // chunk bytes (A/B: 8 / 12 / 16 / 24 / 32 / 48 KB; 24 KB x 3 stages measured best)
+#endif
+  static constexpr int CH0 = IHDG_GEMV_CHB / (NV * 8);
+  static constexpr int CH = CH0 < 2 ? 2 : (CH0 > 64 ? 64 : CH0 / 2 * 2);
 #ifndef IHDG_GEMV_NS
-#define IHDG_GEMV_NS 4
+#define IHDG_GEMV_NS 3
 #endif
   static constexpr int NS = IHDG_GEMV_NS;           // ring stages
   static constexpr int STAGE = CH * NV;             // doubles
