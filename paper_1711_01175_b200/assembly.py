@@ -643,10 +643,14 @@ def build_spec_variable(mesh, problem, ops: ElementOperators, dt=None, scheme: s
         return np.asarray(problem.beta(pts), float).reshape(len(xs), d)[:, a]
 
     def wop(key, wq):
-        """1D mass weighted by wq at the Gauss points: sum_q w_q wq l_i l_j."""
+        """1D mass weighted by wq() at the Gauss points: sum_q w_q wq l_i l_j.
+        The weights depend on the element only through its index along the
+        axis the coefficient varies on (part of the key), so they are
+        evaluated on a cache miss only (cells x faces x tags operators, not
+        elements x faces x tags evaluations of beta)."""
         if key not in cache:
             cache[key] = len(T0) + len(extra)
-            extra.append((V * (qw * wq)[:, None]).T @ V)
+            extra.append((V * (qw * wq())[:, None]).T @ V)
         return cache[key]
 
     BOUND = -1
@@ -680,7 +684,7 @@ def build_spec_variable(mesh, problem, ops: ElementOperators, dt=None, scheme: s
             else:
                 ops_ = [MASS] * d
                 ops_[a] = CONVT
-                ops_[b] = wop(("beta", a, b, idx[b]), beta_1d(a, b, xq(b)))
+                ops_[b] = wop(("beta", a, b, idx[b]), lambda: beta_1d(a, b, xq(b)))
                 terms.add(e, A_T, U, U, ops_, -Jf[a])
         terms.vol(e, A_T, U, U, problem.nu * J)
         terms.vol(e, A_T, U, U, inv_dt * J, time=True)
@@ -705,7 +709,7 @@ def build_spec_variable(mesh, problem, ops: ElementOperators, dt=None, scheme: s
                     (dterms if target == "D" else terms).add(e, B_T if target in ("B", "D") else A_T, rc, cb,
                                                              ops_, val * Jf[a])
                 else:
-                    ops_[b] = wop((tag, f, b, idx[b]), fn(*coeffs(xq(b))))
+                    ops_[b] = wop((tag, f, b, idx[b]), lambda: fn(*coeffs(xq(b))))
                     (dterms if target == "D" else terms).add(e, B_T if target in ("B", "D") else A_T, rc, cb,
                                                              ops_, Jf[a])
 
