@@ -112,16 +112,6 @@ __device__ __forceinline__ void dmma_8x8x4(double& d0, double& d1, double a, dou
 // previous grid wrote.  Both are no-ops without the launch attribute.
 __device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
-// the same, issued only if on != 0 (warp-uniform): a predicated DMMA, no branch
-__device__ __forceinline__ void dmma_8x8x4_if(double& d0, double& d1, double a, double b, int on) {
-  asm("{\n"
-      " .reg .pred p;\n"
-      " setp.ne.s32 p, %4, 0;\n"
-      " @p mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
-      "}\n"
-      : "+d"(d0), "+d"(d1)
-      : "d"(a), "d"(b), "r"(on));
-}
 __device__ __forceinline__ void consumer_bar(int n) { asm volatile("bar.sync 1, %0;" ::"r"(n) : "memory"); }
 
 // 32-bit tile geometry for the streaming kernel (host guarantees local

@@ -521,7 +521,6 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS, GRAM>::NT, 1)
         Lf[j][ks] = (row < NV) ? __ldg(a.LT + ((size_t)fast_class * (NFACE * NF) + col) * NV + row) : 0.0;
       }
     }
-    const int last_slot = (warp + (RTW - 1) * NCW) < NRT ? 1 : 0;   // this warp's last row-tile slot is real
     int doff[RTW];   // swizzled delta offset of this lane's row in each row tile
 #pragma unroll
     for (int j = 0; j < RTW; ++j) {
@@ -605,14 +604,7 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS, GRAM>::NT, 1)
 #pragma unroll
           for (int eg = 0; eg < NEG; ++eg)
 #pragma unroll
-            for (int j = 0; j < RTW; ++j) {
-#ifdef IHDG_WS_PRED
-              // the last slot is empty on the warps past NRT - (RTW-1) NCW: predicated off
-              if (j == RTW - 1 && RTW > 1) dmma_8x8x4_if(acc[eg][j][0], acc[eg][j][1], Lf[j][ks], b[eg], last_slot);
-              else
-#endif
-              dmma_8x8x4(acc[eg][j][0], acc[eg][j][1], Lf[j][ks], b[eg]);
-            }
+            for (int j = 0; j < RTW; ++j) dmma_8x8x4(acc[eg][j][0], acc[eg][j][1], Lf[j][ks], b[eg]);
         }
       } else if (!IHDG_MEMONLY_ON) {
         const unsigned cset = mcset_s[stage];
