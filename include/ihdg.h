@@ -385,12 +385,13 @@ int ihdg_sweep(const ihdg_sweep_args* a, void* stream);
 int ihdg_stream_variant(const ihdg_sweep_args* a);
 /* Name of the kernel ihdg_sweep launches for these args under the current
  * selector: "k_sweep_ws" (2D warp-specialised, config 5), "k_sweep_v4"
- * (register-tiled, 3D p=3 scalar: config 4), "k_sweep_v3" (warp-owned tiles
- * behind a staged ring, configs 2-3), "k_sweep" (generic), or NULL if no kernel is instantiated (static string). */
+ * (register-tiled, 3D p=3 scalar: config 4), "k_sweep_v5" (register-tiled, 2D
+ * p=4: config 2), "k_sweep_v3" (warp-owned tiles behind a staged ring, config
+ * 3), "k_sweep_gemv" (per-element operators), "k_sweep" (generic), or NULL if no kernel is instantiated (static string). */
 const char* ihdg_sweep_kernel(const ihdg_sweep_args* a);
 /* Process-wide sweep-kernel selector: "auto" (default; the initial value is
- * read from the environment variable IHDG_SWEEP_IMPL), "v3" (skip v4),
- * "ws" / "stream" (skip v4 and v3), "generic" (generic kernel only).
+ * read from the environment variable IHDG_SWEEP_IMPL), "v3" (skip v4 / v5),
+ * "ws" / "stream" (skip v3, v4 and v5), "generic" (generic kernel only).
  * IHDG_ERR_ARG for other names. */
 int ihdg_set_sweep_impl(const char* name);
 /* Columns of the Gram factor R the dispatched kernel takes for these args

@@ -183,7 +183,7 @@ def lib():
 
 def sweep_kernel(args: "SweepArgs") -> str:
     """Name of the kernel ihdg_sweep dispatches these args to (k_sweep_ws,
-    k_sweep_v4, k_sweep_v3 or k_sweep)."""
+    k_sweep_v4, k_sweep_v5, k_sweep_v3, k_sweep_gemv or k_sweep)."""
     s = lib().ihdg_sweep_kernel(C.byref(args))
     if s is None:
         raise RuntimeError("no sweep kernel instantiated for these args")

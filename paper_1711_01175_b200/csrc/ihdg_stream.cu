@@ -3,6 +3,7 @@
 // the args (stream_entry) and the process-wide selector set by
 // ihdg_set_sweep_impl; ihdg_sweep_kernel reports the decision by name.
 #include <atomic>
+#include <cmath>
 #include <cstdlib>
 #include <cstring>
 #include <string>
@@ -12,6 +13,7 @@
 #include "ihdg_v3.cuh"
 #include "ihdg_v4.cuh"
 #include "ihdg_gemv.cuh"
+#include "ihdg_v5.cuh"
 
 namespace ihdg {
 
@@ -128,8 +130,15 @@ cudaError_t launch_gemv_t(const ihdg_sweep_args* a, cudaStream_t st) {
   return launch_persistent<k_sweep_gemv<D, N1, M>>(G::NT, G::BYTES, G::TE, a, st, false, c, false);
 }
 
-enum Kind { KIND_V3 = 0, KIND_WS = 1, KIND_V4 = 2, KIND_GEMV = 3 };
-const char* const kKindName[] = {"k_sweep_v3", "k_sweep_ws", "k_sweep_v4", "k_sweep_gemv"};
+template <int N1, int M, int NWC, int NW, int PF>
+cudaError_t launch_v5_t(const ihdg_sweep_args* a, cudaStream_t st) {
+  using C = V5Cfg<N1, M, NWC, NW, PF>;
+  static_assert(8 * PF == Cfg<2, N1, M>::TE, "v5 logical tile must equal the generic tile (tile partial count)");
+  return launch_persistent<k_sweep_v5<N1, M, NWC, NW, PF>>(C::NT, C::BYTES, 8 * PF, a, st);
+}
+
+enum Kind { KIND_V3 = 0, KIND_WS = 1, KIND_V4 = 2, KIND_GEMV = 3, KIND_V5 = 4 };
+const char* const kKindName[] = {"k_sweep_v3", "k_sweep_ws", "k_sweep_v4", "k_sweep_gemv", "k_sweep_v5"};
 
 struct StreamEntry {
   int D, N1, M, NCF, NWC, E, NV;
@@ -141,6 +150,7 @@ struct StreamEntry {
 #define IHDG_V3(D, N1, M, NCF, NWC, NS, NCW, PF, NQW) \
   {D, N1, M, NCF, NWC, 8 * PF, M * Pow<N1, D>::v, launch_v3_t<D, N1, M, NCF, NWC, NS, NCW, PF, NQW>, KIND_V3},
 #define IHDG_V4(FMASK, NW, MINB) {3, 4, 1, v4_popc(FMASK), 1, 32, 64, launch_v4_t<FMASK, NW, MINB>, KIND_V4, FMASK},
+#define IHDG_V5(N1, M, NWC, NW, PF) {2, N1, M, 4, NWC, 8 * PF, M * N1 * N1, launch_v5_t<N1, M, NWC, NW, PF>, KIND_V5},
 #define IHDG_WS(N1, M, NCF, NWC, E, NS) \
   {2, N1, M, NCF, NWC, E, M * N1 * N1, launch_ws_t<N1, M, NCF, NWC, E, NS>, KIND_WS},
 
@@ -178,6 +188,9 @@ struct StreamEntry {
 
 // First match wins: v4 before v3 before ws for the same (D, N1, M).
 const StreamEntry kStream[] = {
+#ifndef IHDG_NO_V5
+    IHDG_V5(5, 3, 2, 16, 2)   // configs 2/3: CD / SW 2D p=4, register-tiled
+#endif
     // config 4: transport 3D p=3; one instantiation per inflow-face set (the
     // sign pattern of beta; config 4 itself is faces 0, 2, 4 = 0x15)
     IHDG_V4(0x15, IHDG_C4_V4_NW, IHDG_C4_V4_MINB) IHDG_V4(0x16, IHDG_C4_V4_NW, IHDG_C4_V4_MINB)
@@ -225,6 +238,22 @@ int current_impl() {
   return v;
 }
 
+// k_sweep_v5 or k_sweep_v3 for a 2D p=4 strip?  Both walk 8-element tiles in
+// rounds (v5: 16 warps per SM, one tile each; v3: 7 consumer warps per SM), so
+// the sweep time is a fixed part plus rounds x time per round.  Measured on
+// B200 (us; profiles/r02_v5_ab.txt): v5 9.2 + 9.3 rounds, v3 15.6 + 3.4 rounds:
+// v5 wins where its rounds are well filled (config 2: 2048 tiles, one round),
+// v3 on config 3 (8192 tiles: 3.46 -> 4 rounds of v5 against 7.9 -> 8 of v3).
+bool v5_cheaper(const ihdg_geom& g) {
+  int dev = 0, sms = 148;
+  if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  Geo geo;
+  geo.init(g, 8);
+  const double tiles = (double)geo.ntiles;
+  const double r5 = std::ceil(tiles / (16.0 * sms)), r3 = std::ceil(tiles / (7.0 * sms));
+  return 9.2 + 9.3 * r5 < 15.6 + 3.4 * r3;
+}
+
 // Returns the entry usable for these args, or nullptr (generic kernel).
 const StreamEntry* stream_entry(const ihdg_sweep_args* a) {
   const int impl = current_impl();
@@ -258,12 +287,13 @@ const StreamEntry* stream_entry(const ihdg_sweep_args* a) {
     if (e.D != g.dim || e.N1 != g.order + 1 || e.M != g.ncomp) continue;
     if (e.NCF != ncf || maxw > e.NWC) continue;
     if (e.fmask >= 0 && e.fmask != fmask) continue;
-    if ((e.kind == KIND_V3 || e.kind == KIND_V4) && impl == IMPL_NO_V3) continue;
-    if (e.kind == KIND_V4 && impl == IMPL_V3) continue;
+    if ((e.kind == KIND_V3 || e.kind == KIND_V4 || e.kind == KIND_V5) && impl == IMPL_NO_V3) continue;
+    if ((e.kind == KIND_V4 || e.kind == KIND_V5) && impl == IMPL_V3) continue;
+    if (e.kind == KIND_V5 && !v5_cheaper(g)) continue;
     Geo geo;
     geo.init(g, e.E);
     if (geo.tile_len % e.E != 0) continue;                       // full tiles only
-    if (g.cells[0] % ((e.kind == KIND_V3 || e.kind == KIND_V4) ? 8 : e.E) != 0) continue;  // tiles inside one axis-0 row
+    if (g.cells[0] % ((e.kind == KIND_V3 || e.kind == KIND_V4 || e.kind == KIND_V5) ? 8 : e.E) != 0) continue;  // tiles inside one axis-0 row
     if (geo.nloc + 2 * geo.ls >= (1LL << 31) || geo.ntiles >= (1LL << 31)) continue;  // 32-bit indices
     if ((geo.ls * e.NV * 8) % 16 != 0) continue;                  // ghost offset
     if (((uintptr_t)a->u_old | (uintptr_t)a->u_new | (uintptr_t)a->s) % 16 != 0) continue;

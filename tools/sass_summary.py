@@ -46,7 +46,7 @@ def main() -> None:
         kernels[cur]["total"] += 1
         if op in CLASSES:
             kernels[cur][op] += 1
-    prod = [k for k in kernels if re.search(r"k_sweep_ws|k_sweep_v4|k_sweep_v3|k_sweep[^_]|k_finalize|k_layer_sums", k)]
+    prod = [k for k in kernels if re.search(r"k_sweep_ws|k_sweep_v4|k_sweep_v5|k_sweep_gemv|k_sweep_v3|k_sweep[^_]|k_finalize|k_layer_sums", k)]
     print(f"# static SASS instruction counts, {os.path.relpath(lib, ROOT)} (cuobjdump -sass)")
     hdr = ["kernel", "total"] + CLASSES
     print("\t".join(hdr))

@@ -17,7 +17,8 @@ def main():
     cfg = int(sys.argv[1])
     n = int(sys.argv[2]) if len(sys.argv) > 2 else 20
     warm = int(sys.argv[3]) if len(sys.argv) > 3 else 3
-    wl = make_config(cfg)
+    cells = int(os.environ["CELLS"]) if os.environ.get("CELLS") else None   # reduced / enlarged mesh
+    wl = make_config(cfg, cells=cells)
     sv = DeviceSolver(wl.mesh, wl.problem, wl.ops, dt=wl.dt, max_iters=100000, gram_norm="gram" in sys.argv[4:])
     if getattr(wl.problem, "forcing", None) is not None:
         sv.set_forcing(wl.problem.forcing)
