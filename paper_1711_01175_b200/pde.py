@@ -241,6 +241,25 @@ def cdr_manufactured(kappa: float = 1e-2) -> "ConvectionDiffusionProblem":
                                       exact=ue)
 
 
+def elliptic_manufactured(kappa: float = 1.0) -> "ConvectionDiffusionProblem":
+    """The elliptic regime of PAPER.md section 6.3 ("elliptic with
+    kappa = 1 and beta = 0") on the manufactured solution of cdr_manufactured:
+    -kappa Lap u + nu u = f with u^e = sin(pi x) cos(pi y) sin(pi z) / pi,
+    nu = 1, f = (3 pi^2 kappa + nu) u^e, Dirichlet data u^e on [0,1]^3.  The
+    velocity is constant (zero), so the operators are shared per class."""
+    pi = np.pi
+
+    def ue(x):
+        x = np.asarray(x, dtype=float)
+        return np.sin(pi * x[:, 0]) * np.cos(pi * x[:, 1]) * np.sin(pi * x[:, 2]) / pi
+
+    def forcing(x):
+        return (3.0 * pi * pi * kappa + 1.0) * ue(x)
+
+    return ConvectionDiffusionProblem(kappa=kappa, beta=np.zeros(3), nu=1.0, forcing=forcing, dirichlet=ue, lam=1.0,
+                                      exact=ue)
+
+
 def preset_problems():
     """Named presets usable through the same API."""
     s2 = np.sqrt(2.0)
@@ -262,6 +281,7 @@ def preset_problems():
                 np.cos(np.pi * x[:, 0]) * np.sin(np.pi * x[:, 1]) * np.sin(s2 * np.pi * t) / s2],
                 axis=1)),
         "elliptic": ConvectionDiffusionProblem(kappa=1.0, beta=np.zeros(3), nu=1.0, lam=1.0),
+        "elliptic_manufactured": elliptic_manufactured(1.0),
         "cdr_manufactured": cdr_manufactured(1e-2),
     }
     return cat
