@@ -316,6 +316,13 @@ extern "C" int ihdg_ws_prof(unsigned long long* out, int reset) {
 }
 #endif
 
+#ifdef IHDG_WS_TRACE
+// trace build only: the phase timestamps of CTA 0 (tools/ws_trace.py)
+extern "C" int ihdg_ws_trace(long long* out) {
+  return (int)cudaMemcpyFromSymbol(out, ihdg::g_ws_trace, sizeof(long long) * 16 * 8 * 12);
+}
+#endif
+
 // 1 if the streaming kernel is used for these args, 0 for the generic one.
 int ihdg_stream_variant(const ihdg_sweep_args* a) { return ihdg::stream_entry(a) != nullptr ? 1 : 0; }
 

@@ -32,6 +32,23 @@ __device__ unsigned long long g_ws_prof[16];
 #define V3_FLUSH
 #endif
 
+// Timeline trace of CTA 0 (trace build, -DIHDG_WS_TRACE; tools/ws_trace.py):
+// lane 0 of every warp stamps clock64 at its phase boundaries for iterations
+// IHDG_TRACE_IT0 .. +7
+#ifdef IHDG_WS_TRACE
+#ifndef IHDG_TRACE_IT0
+#define IHDG_TRACE_IT0 400
+#endif
+__device__ long long g_ws_trace[16][8][12];
+#define WS_STAMP(warp, it, slot)                                                              \
+  do {                                                                                        \
+    if (blockIdx.x == 0 && (threadIdx.x & 31) == 0 && (it) >= IHDG_TRACE_IT0 && (it) < IHDG_TRACE_IT0 + 8) \
+      g_ws_trace[warp][(it) - IHDG_TRACE_IT0][slot] = clock64();                              \
+  } while (0)
+#else
+#define WS_STAMP(warp, it, slot)
+#endif
+
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }

@@ -296,7 +296,9 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS, GRAM>::NT, 1)
       const int tile = blockIdx.x + it * gridDim.x;
       const int stage = it % NS;
       V3_T0(tw);
+      WS_STAMP(warp, it, 0);
       if (it >= NS) mbar_wait(&empty_bar[stage], ((it / NS) - 1) & 1);
+      WS_STAMP(warp, it, 1);
       V3_ACC(0, tw);
       V3_T0(tl);
       double* sst = sm + stage * C::STAGE;
@@ -343,6 +345,7 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS, GRAM>::NT, 1)
         bulk_prefetch_l2(uo + (int64_t)tp.e0 * NV, pb);
       }
       V3_ACC(9, tl);
+      WS_STAMP(warp, it, 2);
     }
   } else if (warp >= NCW) {
     // ============================ prep warps ===============================
@@ -419,7 +422,9 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS, GRAM>::NT, 1)
       const int stage = it % NS;
       gather(it + 1, gvn, qsn, qln);
       V3_T0(tp);
+      WS_STAMP(warp, it, 0);
       mbar_wait(&full_bar[stage], (it / NS) & 1);
+      WS_STAMP(warp, it, 1);
       V3_ACC(1, tp);
       V3_T0(tq);
       // stage metadata is read now: the stage can be refilled once the
@@ -459,10 +464,12 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS, GRAM>::NT, 1)
         if (gram) fence_proxy_async();   // dq overwrote a TMA destination; the stage is refilled by TMA
       __syncwarp();
       V3_ACC(2, tq);
+      WS_STAMP(warp, it, 2);
       if (lane == 0) mbar_arrive(&qready_bar[stage]);
       if (it >= 1) {
         const int pb = (it - 1) & 1;
         mbar_wait(&done_bar[pb], ((it - 1) >> 1) & 1);
+        WS_STAMP(warp, it, 3);
         if (pw == 0 && lane == 0) {
           bulk_s2g(un + (int64_t)prev_e0 * NV, out_s + pb * TILE, (uint32_t)(prev_nt * NV * sizeof(double)));
           bulk_commit();
@@ -562,7 +569,9 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS, GRAM>::NT, 1)
       const int stage = it % NS;
       const int ob = it & 1;
       V3_T0(tc);
+      WS_STAMP(warp, it, 0);
       mbar_wait(&qready_bar[stage], (it / NS) & 1);
+      WS_STAMP(warp, it, 1);
       V3_ACC(3, tc);
       const int fast = mfast_s[stage];
       const bool gtile = GRAM && gram && fast;   // tile it: Gram-form norm
@@ -576,11 +585,13 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS, GRAM>::NT, 1)
         V3_T0(td);
         mbar_wait(&done_bar[jn & 1], (jn >> 1) & 1);
         V3_ACC(8, td);
+        WS_STAMP(warp, it, 2);
         V3_T0(tn);
         nprev = norm_units_swz<N1, M, E, UPW, C::DUE, C::DUC>(d_s + (jn % C::NDB) * C::DT, nu0, nucnt, lane, cfr,
                                                                    cfp, a.comp_w);
         V3_ACC(7, tn);
       }
+      WS_STAMP(warp, it, 3);
       V3_T0(tm);
       double acc[NEG][RTW][2];
 #pragma unroll
@@ -595,6 +606,7 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS, GRAM>::NT, 1)
         }
       }
       const double* qb = qst + (lane >> 2) * KC + (lane & 3);
+      WS_STAMP(warp, it, 4);
       if (fast && !IHDG_MEMONLY_ON) {
 #pragma unroll
         for (int ks = 0; ks < KS; ++ks) {
@@ -644,12 +656,14 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS, GRAM>::NT, 1)
         }
       }
       V3_ACC(4, tm);
+      WS_STAMP(warp, it, 5);
       // a direct tile rewrites the d_s slot of tile it-2: every warp finished
       // that tile's norm by done(it-1)
       if (GRAM && !gtile && it >= 1 && !prev_direct) mbar_wait(&done_bar[(it - 1) & 1], ((it - 1) >> 1) & 1);
       V3_T0(to);
       if (it >= 2) mbar_wait(&outfree_bar[ob], ((it - 2) >> 1) & 1);
       V3_ACC(5, to);
+      WS_STAMP(warp, it, 6);
       V3_T0(te);
       double* outb = out_s + ob * TILE;
       double* dcur = d_s + (it % C::NDB) * C::DT;
@@ -670,6 +684,7 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS, GRAM>::NT, 1)
         }
       }
       V3_ACC(10, te);
+      WS_STAMP(warp, it, 7);
       if (it >= 1 && (!GRAM || prev_direct)) {
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) nprev += __shfl_xor_sync(0xffffffffu, nprev, o);
@@ -680,8 +695,10 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS, GRAM>::NT, 1)
         for (int o = 16; o > 0; o >>= 1) ng += __shfl_xor_sync(0xffffffffu, ng, o);
         if (lane == 0) red_s[(it % C::NRED) * 32 + warp] = ng;
       }
+      WS_STAMP(warp, it, 8);
       fence_proxy_async();
       __syncwarp();
+      WS_STAMP(warp, it, 9);
       if (lane == 0) {
         mbar_arrive(&empty_bar[stage]);
         mbar_arrive(&done_bar[ob]);
