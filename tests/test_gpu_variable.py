@@ -138,3 +138,17 @@ def test_table7_ihdg1_divergence():
     assert rep.status == "diverged"
     ok = _device(8, 3, 1e-3, "iHDG-I")
     assert ok.status == "converged"
+
+
+def test_gemv_persistent_multi_tile_path_bitwise():
+    """20^3 elements, p = 2: 500 tiles, more than the resident CTAs, so every
+    CTA of k_sweep_gemv walks several tiles (ring and operand prefetch across
+    tile boundaries); 18^3 has partial tiles.  Sweeps and norms bitwise equal
+    to the generic kernel."""
+    from tools.sweep_gemv import run
+
+    for cells in (20, 18):
+        ua, na = run(cells, 2, 3, "auto")
+        ug, ng = run(cells, 2, 3, "generic")
+        assert np.array_equal(na, ng)
+        assert np.array_equal(ua, ug)
