@@ -223,7 +223,7 @@ def run_ours(args):
     dofs_rank = sv.nloc * sv.nv
     dofs_total = mesh.n_elements * sv.nv
     dsw = DistributedSweeper(sv, rank, world, group, host_staging=args.host_staging,
-                             overlap=not args.no_overlap) if world > 1 else None
+                             overlap=(False if args.no_overlap else (True if args.overlap else None))) if world > 1 else None
     # a large tolerance-free run: status stays RUNNING for K+W sweeps
     sv.reset_state(tol=0.0, max_iters=args.steps + args.warmup + 10)
     a = sv.sweep_args("volume", finalize=1 if world == 1 else 0)
@@ -560,6 +560,8 @@ def main():
     ap.add_argument("--cpu-reps", type=int, default=3)
     ap.add_argument("--host-staging", action="store_true",
                     help="test mode: ranks share GPUs and exchange through host memory (gloo) instead of NCCL")
+    ap.add_argument("--overlap", action="store_true",
+                    help="multi-GPU: force the interior-first split launch (default: by strip height)")
     ap.add_argument("--no-overlap", action="store_true",
                     help="multi-GPU: halo before the whole sweep instead of under the interior layers")
     args = ap.parse_args()

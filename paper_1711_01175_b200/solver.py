@@ -851,10 +851,16 @@ class DistributedSweeper:
         bit-identical to one rank.
     """
 
+    # the split launch of the overlap path costs ~80 us per sweep on B200 (two
+    # one-layer strips; profiles/r02_strip_overhead.txt: +2% on 2048 layers of
+    # config 5, +29% on 512), so it is the default only for tall strips
+    OVERLAP_MIN_LAYERS = 1024
+
     def __init__(self, solver: DeviceSolver, rank: int, world: int, group=None,
-                 host_staging: bool = False, overlap: bool = True):
+                 host_staging: bool = False, overlap=None):
         """``host_staging``: exchange halos and layer sums through host memory
-        (gloo); used to test this path with several ranks on one GPU."""
+        (gloo); used to test this path with several ranks on one GPU.
+        ``overlap``: True / False, or None = by strip height (OVERLAP_MIN_LAYERS)."""
         from .partition import halo_entries
 
         self.sv, self.rank, self.world, self.group = solver, rank, world, group
@@ -869,6 +875,8 @@ class DistributedSweeper:
         self.segs = sv.ntiles // self.nlay
         self.layer_sums = torch.zeros(self.nlay_global, dtype=torch.float64, device=sv.device)
         self.periodic_last = bool(sv.mesh.periodic[d - 1])
+        if overlap is None:
+            overlap = self.nlay >= self.OVERLAP_MIN_LAYERS
         self.overlap = bool(overlap) and self.nlay >= 3
         self.comm_stream = torch.cuda.Stream(sv.device) if self.overlap else None
         self.idx, self.send, self.recv = {}, {}, {}
