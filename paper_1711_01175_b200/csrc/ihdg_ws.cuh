@@ -68,6 +68,18 @@ __host__ __device__ constexpr void ws_units(int w, int& first, int& cnt) {
   for (int i = 0; i < w; ++i) first += uc[i];
   cnt = uc[w];
 }
+// the deal as a compile-time table (the greedy loop costs ~10 us per launch
+// when every consumer thread runs it)
+template <int NCW>
+struct WsUnitTable {
+  int first[NCW], cnt[NCW];
+};
+template <int NCW, int NRT, int KS, int NEG, int NU>
+__host__ __device__ constexpr WsUnitTable<NCW> ws_unit_table() {
+  WsUnitTable<NCW> t{};
+  for (int w = 0; w < NCW; ++w) ws_units<NCW, NRT, KS, NEG, NU>(w, t.first[w], t.cnt[w]);
+  return t;
+}
 template <int NCW, int NRT, int KS, int NEG, int NU>
 __host__ __device__ constexpr int ws_max_units() {
   int mx = 0;
@@ -255,12 +267,6 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS, GRAM>::NT, 1)
       }
       ++n;
     }
-    for (int k = 0; k < KC; ++k) {
-      const int ci = k / NF, nn = k % NF, f = cf_s[ci];
-      qf_s[k] = f;
-      for (int j = 0; j < NWC; ++j) qt_s[k][j] = wc_s[ci][j] * NP + face_node_vidx(D, N1, f ^ 1, nn);
-      qh_s[k] = ci * NWC * NF + nn;
-    }
     for (int s = 0; s < NS; ++s) {
       mbar_init(&full_bar[s], 1);
       mbar_init(&qready_bar[s], NQW);
@@ -271,6 +277,14 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS, GRAM>::NT, 1)
       mbar_init(&outfree_bar[b], 1);
     }
     fence_mbar_init();
+  }
+  __syncthreads();
+  if (tid < KC) {   // one thread per neighbour scalar (was a serial loop of thread 0)
+    const int k = tid;
+    const int ci = k / NF, nn = k % NF, f = cf_s[ci];
+    qf_s[k] = f;
+    for (int j = 0; j < NWC; ++j) qt_s[k][j] = wc_s[ci][j] * NP + face_node_vidx(D, N1, f ^ 1, nn);
+    qh_s[k] = ci * NWC * NF + nn;
   }
   __syncthreads();
 
@@ -549,7 +563,15 @@ __global__ void __launch_bounds__(WCfg<N1, M, NCF, NWC, E, NS, GRAM>::NT, 1)
       cfp[ks] = (kk < N1 && nn < N1) ? chol_s[kk * N1 + nn] : 0.0;
     }
     int nu0 = 0, nucnt = 0;   // this warp's norm units
-    ws_units<NCW, NRT, KS, NEG, E * M>(warp, nu0, nucnt);
+    {
+      constexpr WsUnitTable<NCW> UT = ws_unit_table<NCW, NRT, KS, NEG, E * M>();
+#pragma unroll
+      for (int w = 0; w < NCW; ++w)
+        if (warp == w) {
+          nu0 = UT.first[w];
+          nucnt = UT.cnt[w];
+        }
+    }
     // Gram-form norm item of this warp: R row tile grt x element group geg
     static_assert(C::LAG == 1, "the Gram / direct norm schedule assumes LAG = 1");
     const int gi = NCW - 1 - warp;

@@ -851,10 +851,12 @@ class DistributedSweeper:
         bit-identical to one rank.
     """
 
-    # the split launch of the overlap path costs ~80 us per sweep on B200 (two
-    # one-layer strips; profiles/r02_strip_overhead.txt: +2% on 2048 layers of
-    # config 5, +29% on 512), so it is the default only for tall strips
-    OVERLAP_MIN_LAYERS = 1024
+    # the split launch of the overlap path costs ~25 us per sweep on B200 (two
+    # one-layer strips at ~11 us each; profiles/r02_strip_overhead.txt: +0.6%
+    # on the 2048 layers of config 5), about what an exposed packed-halo
+    # exchange costs, so it is the default only for strips tall enough to make
+    # it a small fraction of the sweep
+    OVERLAP_MIN_LAYERS = 512
 
     def __init__(self, solver: DeviceSolver, rank: int, world: int, group=None,
                  host_staging: bool = False, overlap=None):
