@@ -391,7 +391,8 @@ int ihdg_stream_variant(const ihdg_sweep_args* a);
 const char* ihdg_sweep_kernel(const ihdg_sweep_args* a);
 /* Process-wide sweep-kernel selector: "auto" (default; the initial value is
  * read from the environment variable IHDG_SWEEP_IMPL), "v3" (skip v4 / v5),
- * "ws" / "stream" (skip v3, v4 and v5), "generic" (generic kernel only).
+ * "v5" (v5 wherever it applies, without the round model), "ws" / "stream"
+ * (skip v3, v4 and v5), "generic" (generic kernel only).
  * IHDG_ERR_ARG for other names. */
 int ihdg_set_sweep_impl(const char* name);
 /* Columns of the Gram factor R the dispatched kernel takes for these args

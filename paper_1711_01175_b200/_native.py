@@ -191,7 +191,7 @@ def sweep_kernel(args: "SweepArgs") -> str:
 
 
 def set_sweep_impl(name: str) -> None:
-    """Process-wide kernel selector: auto / v3 / ws / stream / generic."""
+    """Process-wide kernel selector: auto / v3 / v5 / ws / stream / generic."""
     check(lib().ihdg_set_sweep_impl(name.encode()), "ihdg_set_sweep_impl")
 
 

@@ -296,7 +296,7 @@ int ihdg_sweep_gram_kc(const ihdg_sweep_args* a) {
 int ihdg_set_sweep_impl(const char* name) {
   if (ihdg_stream_set_impl(name) != 0)
     return set_err(IHDG_ERR_ARG, std::string("unknown sweep impl '") + (name ? name : "(null)") +
-                                     "' (auto, v3, ws, stream, generic)");
+                                     "' (auto, v3, v5, ws, stream, generic)");
   return IHDG_OK;
 }
 

@@ -215,14 +215,15 @@ const StreamEntry kGemv[] = {
 
 // Process-wide kernel selector (ihdg_set_sweep_impl); the initial value comes
 // from IHDG_SWEEP_IMPL so A/B tools keep working.
-enum Impl { IMPL_AUTO = 0, IMPL_NO_V3 = 1, IMPL_GENERIC = 2, IMPL_V3 = 3 };
+enum Impl { IMPL_AUTO = 0, IMPL_NO_V3 = 1, IMPL_GENERIC = 2, IMPL_V3 = 3, IMPL_V5 = 4 };
 std::atomic<int> g_impl{-1};
 
 int parse_impl(const char* s) {
   if (s == nullptr || s[0] == '\0' || std::strcmp(s, "auto") == 0) return IMPL_AUTO;
   if (std::strcmp(s, "ws") == 0 || std::strcmp(s, "stream") == 0) return IMPL_NO_V3;
   if (std::strcmp(s, "generic") == 0) return IMPL_GENERIC;
-  if (std::strcmp(s, "v3") == 0) return IMPL_V3;   // skip v4
+  if (std::strcmp(s, "v3") == 0) return IMPL_V3;   // skip v4 / v5
+  if (std::strcmp(s, "v5") == 0) return IMPL_V5;   // v5 wherever it applies (no round model)
   return -1;
 }
 
@@ -251,6 +252,7 @@ bool v5_cheaper(const ihdg_geom& g) {
   geo.init(g, 8);
   const double tiles = (double)geo.ntiles;
   const double r5 = std::ceil(tiles / (16.0 * sms)), r3 = std::ceil(tiles / (7.0 * sms));
+  if (r3 < 2.0) return false;   // one round of v3 (up to ~96^2): its floor is lower (16^2: 9-12 us against 14-17 us)
   return 9.2 + 9.3 * r5 < 15.6 + 3.4 * r3;
 }
 
@@ -289,7 +291,7 @@ const StreamEntry* stream_entry(const ihdg_sweep_args* a) {
     if (e.fmask >= 0 && e.fmask != fmask) continue;
     if ((e.kind == KIND_V3 || e.kind == KIND_V4 || e.kind == KIND_V5) && impl == IMPL_NO_V3) continue;
     if ((e.kind == KIND_V4 || e.kind == KIND_V5) && impl == IMPL_V3) continue;
-    if (e.kind == KIND_V5 && !v5_cheaper(g)) continue;
+    if (e.kind == KIND_V5 && impl != IMPL_V5 && !v5_cheaper(g)) continue;
     Geo geo;
     geo.init(g, e.E);
     if (geo.tile_len % e.E != 0) continue;                       // full tiles only

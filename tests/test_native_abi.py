@@ -82,7 +82,7 @@ def _cpu_sweep_args(cfg, cells=None):
 
 @pytest.mark.parametrize("cfg,cells,auto,no_v3", [
     (5, None, "k_sweep_ws", "k_sweep_ws"), (4, None, "k_sweep_v4", "k_sweep"),
-    (3, None, "k_sweep_v3", "k_sweep_ws"), (2, None, "k_sweep_v5", "k_sweep_ws"), (3, 64, "k_sweep_v5", "k_sweep_ws"),
+    (3, None, "k_sweep_v3", "k_sweep_ws"), (2, None, "k_sweep_v5", "k_sweep_ws"), (3, 64, "k_sweep_v3", "k_sweep_ws"), (3, 192, "k_sweep_v5", "k_sweep_ws"),
     (2, 20, "k_sweep", "k_sweep"), (1, None, "k_sweep", "k_sweep")])
 def test_dispatch_names(cfg, cells, auto, no_v3):
     """ihdg_sweep_kernel names the kernel each BASELINE config runs on; the
